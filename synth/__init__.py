@@ -1,0 +1,133 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU parity tests and bench.py.
+
+This module holds NONE of LASP's arithmetic: it only draws numbers. Both sides of every
+parity check (the fp64 CPU oracle under ``oracle/`` and the CUDA path behind
+``include/lasp.h``) receive exactly the bits produced here, so neither side generates
+its own inputs.
+
+Generator:
+  u   = splitmix64(seed XOR tensor_id * 2**56 XOR flat_index) -> top 53 bits -> [0, 1)
+  x   = (2u - 1) * sqrt(3) * scale          (unit variance times ``scale``)
+  out = x rounded to fp32, then (for bf16 tensors) rounded to-nearest-even to bf16.
+
+``flat_index`` is the element's index in the GLOBAL [B][N][H][D] tensor, so a rank that
+owns tokens [r*C, (r+1)*C) can draw its shard without drawing the whole sequence.
+
+Scales follow SURVEY.md §8(d): Q and K use D**-0.25 (q.k has unit variance), V and dO
+use 1. Per-head decay for TNL-shaped workloads: lambda_h = 1 - 2**-(1 + 14 h/(H-1)),
+which spans [0.5, 0.99997] (the paper gives no lambda values; the recipe exercises both the
+fast-decay/underflow end and the long-memory end).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+__all__ = [
+    "TENSOR_IDS", "splitmix64", "uniform", "draw", "round_bf16", "bf16_bits",
+    "bits_to_f32", "head_lambdas", "problem",
+]
+
+# Fixed tensor ids (part of the recipe: changing them changes every fixture).
+TENSOR_IDS = {"q": 1, "k": 2, "v": 3, "do": 4}
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    """SplitMix64 finaliser applied elementwise to a uint64 array (counter-based)."""
+    x = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = x + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return z
+
+
+def uniform(seed: int, tensor_id: int, flat_index: np.ndarray) -> np.ndarray:
+    """u in [0, 1) as float64 from the top 53 bits of splitmix64(seed ^ id<<56 ^ idx)."""
+    key = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) ^ (np.uint64(tensor_id) << np.uint64(56))
+    z = splitmix64(np.asarray(flat_index, dtype=np.uint64) ^ key)
+    return (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+
+
+def round_bf16(x: np.ndarray) -> np.ndarray:
+    """Round float32 values to the nearest bf16 (ties to even); returned as float32."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    u = (u + np.uint64(0x7FFF) + ((u >> np.uint64(16)) & np.uint64(1))) & np.uint64(0xFFFF0000)
+    out = u.astype(np.uint32).view(np.float32)
+    # NaN/inf never occur in the recipe (|x| <= sqrt(3)); keep them untouched anyway.
+    bad = ~np.isfinite(x)
+    if bad.any():
+        out = out.copy()
+        out[bad] = x[bad]
+    return out
+
+
+def bf16_bits(x_bf16_valued_f32: np.ndarray) -> np.ndarray:
+    """uint16 bf16 bit patterns of float32 values that are already bf16-representable."""
+    x = np.ascontiguousarray(x_bf16_valued_f32, dtype=np.float32)
+    return (x.view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+
+
+def bits_to_f32(bits: np.ndarray) -> np.ndarray:
+    """Inverse of bf16_bits."""
+    return (np.asarray(bits, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)
+
+
+def draw(name: str, seed: int, batch: int, n_global: int, heads: int, head_dim: int,
+         dtype: str = "bf16", token_lo: int = 0, token_hi: int | None = None,
+         scale: float | None = None) -> np.ndarray:
+    """Draw tensor ``name`` ("q","k","v","do") as float32 with layout [B][tokens][H][D].
+
+    Only tokens [token_lo, token_hi) of the global sequence of length ``n_global`` are drawn
+    (a rank's shard). ``dtype`` "bf16" rounds to bf16 values; "fp32" keeps fp32.
+    """
+    if token_hi is None:
+        token_hi = n_global
+    if not (0 <= token_lo <= token_hi <= n_global):
+        raise ValueError("bad token range")
+    if scale is None:
+        scale = head_dim ** -0.25 if name in ("q", "k") else 1.0
+    tid = TENSOR_IDS[name]
+    n = token_hi - token_lo
+    out = np.empty((batch, n, heads, head_dim), dtype=np.float32)
+    inner = heads * head_dim
+    # chunk over (b, tokens) rows to bound temporary memory
+    rows_per = max(1, (1 << 22) // max(inner, 1))
+    for b in range(batch):
+        for s0 in range(0, n, rows_per):
+            s1 = min(n, s0 + rows_per)
+            base = (b * n_global + token_lo + s0) * inner
+            idx = np.arange(base, base + (s1 - s0) * inner, dtype=np.uint64)
+            u = uniform(seed, tid, idx)
+            x = ((2.0 * u - 1.0) * (math.sqrt(3.0) * scale)).astype(np.float32)
+            out[b, s0:s1] = x.reshape(s1 - s0, heads, head_dim)
+    if dtype == "bf16":
+        out = round_bf16(out).reshape(out.shape)
+    elif dtype != "fp32":
+        raise ValueError(dtype)
+    return out
+
+
+def head_lambdas(heads: int, scalar: float | None = None) -> np.ndarray:
+    """Per-head decay lambda_h as float32 (the boundary's precision, reading A8)."""
+    if scalar is not None:
+        return np.full(heads, scalar, dtype=np.float32)
+    if heads == 1:
+        return np.array([0.99], dtype=np.float32)
+    h = np.arange(heads, dtype=np.float64)
+    return (1.0 - 2.0 ** -(1.0 + 14.0 * h / (heads - 1))).astype(np.float32)
+
+
+def problem(seed: int, batch: int, n_global: int, heads: int, head_dim: int,
+            dtype: str = "bf16", lam: float | None = None, token_lo: int = 0,
+            token_hi: int | None = None, with_do: bool = True) -> dict:
+    """Convenience: q, k, v (and do) shards plus the float32 per-head lambda vector."""
+    t = {nm: draw(nm, seed, batch, n_global, heads, head_dim, dtype, token_lo, token_hi)
+         for nm in (("q", "k", "v", "do") if with_do else ("q", "k", "v"))}
+    t["lam"] = head_lambdas(heads, lam)
+    return t

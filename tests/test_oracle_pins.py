@@ -1,0 +1,364 @@
+"""Pins for the fp64 oracle (oracle/) against things other than itself.
+
+Each test states what pins what. Citations: P:n = PAPER.md line n,
+S:n = SPEC.md line n. All CPU-only.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def rand_problem(seed, B, N, H, D, lam=None):
+    p = synth.problem(seed, B, N, H, D, dtype="fp32", lam=lam)
+    return {k: p[k].astype(np.float64) if k != "lam" else p[k] for k in p}
+
+
+def dense_mask(N, lam):
+    """M_ij = lam^(i-j) for i>=j (Alg. 2) built with numpy power (not the oracle's
+    repeated multiplication)."""
+    i = np.arange(N)[:, None]
+    j = np.arange(N)[None, :]
+    e = np.where(i >= j, i - j, 0).astype(np.float64)
+    return np.where(i >= j, np.power(np.float64(lam), e), 0.0)
+
+
+def dense_fwd(q, k, v, lam):
+    """Eq. 2 without Norm: O = [(Q K^T) (.) M] V, per (b, h), numpy fp64."""
+    B, N, H, D = q.shape
+    o = np.zeros_like(q)
+    for b in range(B):
+        for h in range(H):
+            M = dense_mask(N, float(np.float64(np.float32(lam[h]))))
+            o[b, :, h] = ((q[b, :, h] @ k[b, :, h].T) * M) @ v[b, :, h]
+    return o
+
+
+def dense_torch_grads(q, k, v, lam, do):
+    """torch fp64 autograd of L = sum(O * dO) on the dense masked form (pin 2)."""
+    tq, tk, tv = (torch.tensor(x, dtype=torch.float64, requires_grad=True) for x in (q, k, v))
+    B, N, H, D = q.shape
+    outs = []
+    for h in range(H):
+        M = torch.tensor(dense_mask(N, float(np.float64(np.float32(lam[h])))))
+        s = torch.einsum("bid,bjd->bij", tq[:, :, h], tk[:, :, h]) * M
+        outs.append(torch.einsum("bij,bjd->bid", s, tv[:, :, h]))
+    o = torch.stack(outs, dim=2)
+    (o * torch.tensor(do)).sum().backward()
+    return tq.grad.numpy(), tk.grad.numpy(), tv.grad.numpy()
+
+
+def rel(x, ref):
+    den = np.max(np.abs(ref))
+    return float(np.max(np.abs(x - ref)) / den) if den > 0 else float(np.max(np.abs(x)))
+
+
+# ---------------------------------------------------------------------------------------------
+# pin 1: dense masked form (Eq. 2 without Norm) -- oracle forward, S:694 criterion 1
+@pytest.mark.parametrize("lam", [1.0, 0.99, 0.9, 0.5])
+@pytest.mark.parametrize("N,D", [(16, 4), (64, 16), (256, 32)])
+def test_fwd_matches_dense_masked_form(oracle_mod, lam, N, D):
+    for seed in range(2):
+        p = rand_problem(seed, 1, N, 2, D, lam=lam)
+        o = oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])
+        ref = dense_fwd(p["q"], p["k"], p["v"], p["lam"])
+        assert rel(o, ref) <= 1e-12
+
+
+def test_fwd_per_head_lambdas_batch(oracle_mod):
+    p = rand_problem(3, 2, 96, 4, 8)  # per-head TNL recipe, B=2
+    o = oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])
+    assert rel(o, dense_fwd(p["q"], p["k"], p["v"], p["lam"])) <= 1e-12
+
+
+# pin 2: fp64 autograd of the dense form -- oracle backward
+@pytest.mark.parametrize("lam", [1.0, 0.95, 0.5])
+def test_bwd_matches_torch_autograd(oracle_mod, lam):
+    p = rand_problem(7, 2, 48, 2, 8, lam=lam)
+    dq, dk, dv = oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"])
+    rq, rk, rv = dense_torch_grads(p["q"], p["k"], p["v"], p["lam"], p["do"])
+    for x, r in ((dq, rq), (dk, rk), (dv, rv)):
+        assert rel(x, r) <= 1e-12
+
+
+# pin 2b: the paper's masked closed forms via numpy, full sequence T=1
+def test_bwd_matches_paper_masked_products(oracle_mod):
+    p = rand_problem(11, 1, 40, 1, 6, lam=0.8)
+    q, k, v, do = (p[x][0, :, 0] for x in ("q", "k", "v", "do"))
+    M = dense_mask(40, float(np.float64(np.float32(0.8))))
+    dq_ref = ((do @ v.T) * M) @ k
+    dk_ref = ((do @ v.T) * M).T @ q
+    dv_ref = ((q @ k.T) * M).T @ do
+    dq, dk, dv = oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"])
+    assert rel(dq[0, :, 0], dq_ref) <= 1e-12
+    assert rel(dk[0, :, 0], dk_ref) <= 1e-12
+    assert rel(dv[0, :, 0], dv_ref) <= 1e-12
+
+
+# pin 3: central finite differences of L = sum(O * dO)
+def test_bwd_matches_finite_differences(oracle_mod):
+    p = rand_problem(5, 1, 12, 1, 3, lam=0.9)
+    dq, dk, dv = oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"])
+    eps = 1e-6
+
+    def loss(q, k, v):
+        return float(np.sum(oracle_mod.fwd(q, k, v, p["lam"]) * p["do"]))
+
+    for name, g in (("q", dq), ("k", dk), ("v", dv)):
+        fd = np.zeros_like(g)
+        base = {x: p[x].copy() for x in ("q", "k", "v")}
+        it = np.nditer(base[name], flags=["multi_index"])
+        for _ in it:
+            idx = it.multi_index
+            plus = {x: base[x].copy() for x in base}
+            minus = {x: base[x].copy() for x in base}
+            plus[name][idx] += eps
+            minus[name][idx] -= eps
+            fd[idx] = (loss(plus["q"], plus["k"], plus["v"]) - loss(minus["q"], minus["k"], minus["v"])) / (2 * eps)
+        assert rel(g, fd) <= 1e-5
+
+
+# pin 4: SPEC worked examples (tests/golden/spec_examples.json, each with its citation)
+def _arr(x):
+    a = np.asarray(x, dtype=np.float64)
+    return a.reshape(1, a.shape[0], 1, a.shape[1])
+
+
+@pytest.mark.parametrize("key", ["fwd_n1", "fwd_lambda1_n2", "fwd_lambda_half_n3"])
+def test_golden_forward(oracle_mod, key):
+    g = GOLD[key]
+    o = oracle_mod.fwd(_arr(g["q"]), _arr(g["k"]), _arr(g["v"]), [g["lam"]])
+    np.testing.assert_allclose(o[0, :, 0], np.asarray(g["o"]), rtol=0, atol=1e-15)
+
+
+def test_golden_backward_n1(oracle_mod):
+    g = GOLD["bwd_n1"]
+    dq, dk, dv = oracle_mod.bwd(_arr(g["q"]), _arr(g["k"]), _arr(g["v"]), [g["lam"]], _arr(g["do"]))
+    np.testing.assert_allclose(dq[0, :, 0], g["dq"], atol=1e-15)
+    np.testing.assert_allclose(dk[0, :, 0], g["dk"], atol=1e-15)
+    np.testing.assert_allclose(dv[0, :, 0], g["dv"], atol=1e-15)
+
+
+def test_golden_build_decay(oracle_mod):
+    g = GOLD["build_decay_half_c3"]
+    mask, lf, lr, lc = oracle_mod.build_decay(g["C"], g["lam"])
+    np.testing.assert_array_equal(mask, g["mask"])
+    np.testing.assert_array_equal(lf, g["lam_fwd"])
+    np.testing.assert_array_equal(lr, g["lam_rev"])
+    assert lc == g["lam_C"]
+
+
+def test_golden_dkv_update_c1(oracle_mod):
+    g = GOLD["dkv_update_c1"]
+    _, lf, _, lc = oracle_mod.build_decay(1, g["lam"])
+    out = oracle_mod.dkv_update(np.array(g["dkv_next"]), np.array(g["q"]), np.array(g["do"]), lf, lc)
+    np.testing.assert_array_equal(out, g["dkv"])
+
+
+def test_golden_table1_volume(oracle_mod):
+    g = GOLD["table1_lasp_volume"]
+    # one hop of the ring carries B*H*D*D elements with D = d/h
+    H, D = g["h"], g["d"] // g["h"]
+    N, T = 1024, 4
+    p = rand_problem(0, g["B"], N, 1, 2)
+    q = np.zeros((g["B"], N, H, D))
+    _, _, hops, elems = oracle_mod.lasp_fwd_sim(q[:, :, :1, :2], q[:, :, :1, :2], q[:, :, :1, :2], [0.9], T)
+    assert hops == T - 1
+    assert g["B"] * H * D * D == g["elements"]
+    del p
+
+
+# pin 5: closed forms for constant inputs (derived from Eq. 4), any N
+@pytest.mark.parametrize("lam", [1.0, 0.999, 0.9, 0.5])
+def test_constant_input_closed_forms(oracle_mod, lam):
+    N, D = 4096, 3
+    rng = np.random.default_rng(0)
+    qv, kv_, vv, dov = (rng.standard_normal(D) for _ in range(4))
+    q = np.broadcast_to(qv, (1, N, 1, D)).copy()
+    k = np.broadcast_to(kv_, (1, N, 1, D)).copy()
+    v = np.broadcast_to(vv, (1, N, 1, D)).copy()
+    do = np.broadcast_to(dov, (1, N, 1, D)).copy()
+    l64 = float(np.float64(np.float32(lam)))
+    s = np.arange(1, N + 1, dtype=np.float64)  # 1-based position
+    geo = (lambda n: n) if l64 == 1.0 else (lambda n: (1.0 - l64 ** n) / (1.0 - l64))
+    o = oracle_mod.fwd(q, k, v, [lam])
+    o_ref = (qv @ kv_) * np.outer(geo(s), vv)
+    assert rel(o[0, :, 0], o_ref) <= 1e-12
+    dq, dk, dv = oracle_mod.bwd(q, k, v, [lam], do)
+    assert rel(dq[0, :, 0], (vv @ dov) * np.outer(geo(s), kv_)) <= 1e-12
+    assert rel(dk[0, :, 0], (vv @ dov) * np.outer(geo(N - s + 1), qv)) <= 1e-12
+    assert rel(dv[0, :, 0], (qv @ kv_) * np.outer(geo(N - s + 1), dov)) <= 1e-12
+
+
+# pin 6: Euler identity -- L is linear in each of Q, K, V, so <X, dX> = L for X in {Q,K,V}
+def test_euler_identity(oracle_mod):
+    p = rand_problem(2, 1, 512, 3, 16)
+    o = oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])
+    dq, dk, dv = oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"])
+    L = np.sum(o * p["do"])
+    for x, g in ((p["q"], dq), (p["k"], dk), (p["v"], dv)):
+        assert abs(np.sum(x * g) - L) <= 1e-11 * max(1.0, abs(L))
+
+
+# pin 7: causality
+def test_causality(oracle_mod):
+    p = rand_problem(4, 1, 128, 2, 8)
+    o = oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])
+    for cut in (0, 17, 64, 127):
+        k2, v2 = p["k"].copy(), p["v"].copy()
+        k2[:, cut + 1:] = 0
+        v2[:, cut + 1:] = 0
+        o2 = oracle_mod.fwd(p["q"], k2, v2, p["lam"])
+        np.testing.assert_array_equal(o2[:, :cut + 1], o[:, :cut + 1])
+
+
+# pin 8: chunk-size / rank-count invariance of Alg. 2/3 in the rank-simulated mode
+@pytest.mark.parametrize("lam", [1.0, 0.99, 0.9, 0.5])
+def test_rank_simulated_matches_definition(oracle_mod, lam):
+    N = 256
+    p = rand_problem(9, 2, N, 2, 8, lam=lam)
+    o_ref = oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])
+    g_ref = oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"])
+    for T in (1, 2, 4, 8, 16, 64, 256):
+        o, cache, hops, elems = oracle_mod.lasp_fwd_sim(p["q"], p["k"], p["v"], p["lam"], T)
+        assert rel(o, o_ref) <= 1e-10
+        assert hops == T - 1 and elems == 2 * 2 * 8 * 8
+        dq, dk, dv, bh, be = oracle_mod.lasp_bwd_sim(p["q"], p["k"], p["v"], p["lam"], p["do"], cache, T)
+        assert bh == T - 1 and be == elems
+        for x, r in zip((dq, dk, dv), g_ref):
+            assert rel(x, r) <= 1e-10
+
+
+def test_cache_holds_state_entering_each_rank(oracle_mod):
+    """cache[t] = KV_in(t) = sum_{g < tC} lam^(tC-1-g) k_g v_g^T (reading A4), by brute force."""
+    N, T, D = 64, 4, 5
+    p = rand_problem(13, 1, N, 1, D, lam=0.9)
+    _, cache, _, _ = oracle_mod.lasp_fwd_sim(p["q"], p["k"], p["v"], p["lam"], T)
+    l64 = float(np.float64(np.float32(0.9)))
+    C = N // T
+    k, v = p["k"][0, :, 0], p["v"][0, :, 0]
+    for t in range(T):
+        ref = np.zeros((D, D))
+        for g in range(t * C):
+            ref += l64 ** (t * C - 1 - g) * np.outer(k[g], v[g])
+        np.testing.assert_allclose(cache[t, 0, 0], ref, rtol=1e-12, atol=1e-12)
+
+
+def test_partition_and_domain_errors(oracle_mod):
+    p = rand_problem(0, 1, 30, 1, 4)
+    with pytest.raises(oracle_mod.OracleError):
+        oracle_mod.lasp_fwd_sim(p["q"], p["k"], p["v"], p["lam"], 4)  # 4 does not divide 30
+    with pytest.raises(oracle_mod.OracleError):
+        oracle_mod.fwd(p["q"], p["k"], p["v"], [1.5])  # lambda outside (0, 1]
+    with pytest.raises(oracle_mod.OracleError):
+        oracle_mod.fwd(p["q"], p["k"], p["v"], [0.0])
+
+
+# pin 9: lambda = 1, T = 1 -> torch.tril(Q K^T) V (plain linear attention)
+def test_lambda_one_is_tril_linear_attention(oracle_mod):
+    p = rand_problem(1, 1, 200, 1, 16, lam=1.0)
+    q, k, v = (torch.tensor(p[x][0, :, 0]) for x in ("q", "k", "v"))
+    ref = (torch.tril(q @ k.T) @ v).numpy()
+    o = oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])
+    assert rel(o[0, :, 0], ref) <= 1e-12
+
+
+# pin 10: protocol -- T-1 hops of B*H*D*D elements per direction, independent of N
+def test_protocol_independent_of_n(oracle_mod):
+    T, B, H, D = 4, 1, 2, 4
+    seen = set()
+    for N in (256, 1024, 4096):
+        p = rand_problem(0, B, N, H, D)
+        o, cache, hops, elems = oracle_mod.lasp_fwd_sim(p["q"], p["k"], p["v"], p["lam"], T)
+        _, _, _, bh, be = oracle_mod.lasp_bwd_sim(p["q"], p["k"], p["v"], p["lam"], p["do"], cache, T)
+        seen.add((hops, elems, bh, be))
+    assert seen == {(T - 1, B * H * D * D, T - 1, B * H * D * D)}
+
+
+# pin 12: head independence -- h heads equal h single-head runs, bitwise
+def test_head_independence_bitwise(oracle_mod):
+    p = rand_problem(6, 1, 100, 4, 8)
+    o = oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])
+    g = oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"])
+    for h in range(4):
+        sl = (slice(None), slice(None), slice(h, h + 1))
+        o1 = oracle_mod.fwd(p["q"][sl], p["k"][sl], p["v"][sl], p["lam"][h:h + 1])
+        np.testing.assert_array_equal(o1, o[sl])
+        g1 = oracle_mod.bwd(p["q"][sl], p["k"][sl], p["v"][sl], p["lam"][h:h + 1], p["do"][sl])
+        for a, b in zip(g1, g):
+            np.testing.assert_array_equal(a, b[sl])
+
+
+# ---- single-chunk ops vs brute-force sums of their defining equations ----------------------
+def _chunk(seed, C, D):
+    rng = np.random.default_rng(seed)
+    return [rng.standard_normal((C, D)) for _ in range(4)] + [rng.standard_normal((D, D))]
+
+
+def test_chunk_intra_fwd_is_dense_on_isolated_chunk(oracle_mod):
+    Q, K, V, _, _ = _chunk(1, 8, 3)
+    mask, _, _, _ = oracle_mod.build_decay(8, 0.7)
+    ref = dense_fwd(Q[None, :, None], K[None, :, None], V[None, :, None], [np.float32(0.7)])[0, :, 0]
+    assert rel(oracle_mod.intra_fwd(Q, K, V, mask), ref) <= 1e-13
+
+
+def test_chunk_inter_terms_brute_force(oracle_mod):
+    """Second summands of Eq. 8, Eq. 16, Eq. 19, Eq. 22."""
+    C, D, lam = 6, 3, 0.8
+    l64 = float(np.float64(np.float32(lam)))
+    Q, K, V, dO, S = _chunk(2, C, D)
+    _, lf, lr, lc = oracle_mod.build_decay(C, lam)
+    # O_inter row s: lam^(s+1) q_s^T KV_{t-1}   (s 0-based)
+    ref = np.stack([l64 ** (s + 1) * (Q[s] @ S) for s in range(C)])
+    assert rel(oracle_mod.inter_fwd(Q, S, lf), ref) <= 1e-14
+    ref = np.stack([l64 ** (s + 1) * (S @ dO[s]) for s in range(C)])
+    assert rel(oracle_mod.inter_bwd_q(dO, S, lf), ref) <= 1e-14
+    ref = np.stack([l64 ** (C - 1 - s) * (S @ V[s]) for s in range(C)])
+    assert rel(oracle_mod.inter_bwd_k(V, S, lr), ref) <= 1e-14
+    ref = np.stack([l64 ** (C - 1 - s) * (K[s] @ S) for s in range(C)])
+    assert rel(oracle_mod.inter_bwd_v(K, S, lr), ref) <= 1e-14
+
+
+def test_chunk_state_updates_brute_force(oracle_mod):
+    """Eq. 12 and Eq. 21 as defining sums: KV_t = sum lam^(C-1-s) k v^T + lam^C KV_{t-1};
+    dKV_t = sum lam^(s+1) q do^T + lam^C dKV_{t+1}."""
+    C, D, lam = 7, 4, 0.6
+    l64 = float(np.float64(np.float32(lam)))
+    Q, K, V, dO, S = _chunk(3, C, D)
+    _, lf, lr, lc = oracle_mod.build_decay(C, lam)
+    ref = l64 ** C * S + sum(l64 ** (C - 1 - s) * np.outer(K[s], V[s]) for s in range(C))
+    assert rel(oracle_mod.kv_update(S, K, V, lr, lc), ref) <= 1e-14
+    ref = l64 ** C * S + sum(l64 ** (s + 1) * np.outer(Q[s], dO[s]) for s in range(C))
+    assert rel(oracle_mod.dkv_update(S, Q, dO, lf, lc), ref) <= 1e-14
+
+
+def test_chunk_intra_bwd_matches_autograd(oracle_mod):
+    C, D = 9, 4
+    Q, K, V, dO, _ = _chunk(4, C, D)
+    mask, _, _, _ = oracle_mod.build_decay(C, 0.75)
+    dq, dk, dv = oracle_mod.intra_bwd(Q, K, V, dO, mask)
+    rq, rk, rv = dense_torch_grads(Q[None, :, None], K[None, :, None], V[None, :, None], [np.float32(0.75)],
+                                   dO[None, :, None])
+    for a, r in ((dq, rq), (dk, rk), (dv, rv)):
+        assert rel(a, r[0, :, 0]) <= 1e-13
+
+
+def test_dkv_chain_matches_definition(oracle_mod):
+    """Iterating Eq. 21 from the last chunk reproduces dKV_t = sum_{s > tC} lam^(s-tC) q_s do_s^T
+    with the 0-based reading A3 (exponent starts at 1)."""
+    N, C, D, lam = 24, 6, 3, 0.85
+    l64 = float(np.float64(np.float32(lam)))
+    rng = np.random.default_rng(8)
+    Q, dO = rng.standard_normal((N, D)), rng.standard_normal((N, D))
+    _, lf, _, lc = oracle_mod.build_decay(C, lam)
+    dkv = np.zeros((D, D))
+    for t in range(N // C - 1, -1, -1):
+        dkv = oracle_mod.dkv_update(dkv, Q[t * C:(t + 1) * C], dO[t * C:(t + 1) * C], lf, lc)
+        ref = sum(l64 ** (g - t * C + 1) * np.outer(Q[g], dO[g]) for g in range(t * C, N))
+        assert rel(dkv, ref) <= 1e-13
