@@ -1,0 +1,152 @@
+/*
+ * lasp.h -- C ABI of the B200-native LASP hot path (Linear Attention Sequence Parallelism,
+ * arXiv 2404.02882): chunked causal linear attention with per-head decay lambda, sequence
+ * split across ranks, one d x d KV state per head passed forward around a P2P ring and a
+ * dKV state passed backward.
+ *
+ * Citations: "P:n" = line n of the paper text; "S:n" = line n of SPEC.md.
+ *
+ * ------------------------------------------------------------------------------------------
+ * What is computed (per batch row b, head h; rank r owns tokens [r*C, (r+1)*C), C = n_local,
+ * P:106-111 with T = W):
+ *
+ *   O    : o_s^T = q_s^T sum_{i<=s} lambda_h^(s-i) k_i v_i^T          (Eq. 4)
+ *          evaluated per rank as Alg. 2:
+ *            O_r = [(Q_r K_r^T) (.) M] V_r + Lambda Q_r KV_in(r)        (Eq. 7, 9)
+ *            KV_out(r) = lambda^C KV_in(r) + (lambda^C Lambda^-1 K_r)^T V_r   (Eq. 12)
+ *          M_ij = lambda^(i-j) (i >= j), Lambda = diag(lambda^1..lambda^C). No Norm(.)
+ *          and no 1/sqrt(d).
+ *   dQ, dK, dV : gradients of L = sum(O (.) dO) (Eq. 13-14), evaluated per rank as
+ *          Alg. 3:
+ *            dQ_r = [(dO V^T) (.) M] K + Lambda dO KV_in(r)^T
+ *            dK_r = [(dO V^T) (.) M]^T Q + lambda^C Lambda^-1 V dKV_in(r)^T
+ *            dV_r = [(Q K^T) (.) M]^T dO + lambda^C Lambda^-1 K dKV_in(r)
+ *            dKV_out(r) = lambda^C dKV_in(r) + (Lambda Q_r)^T dO_r
+ *          where dKV_in(r) = sum_{g >= (r+1)C} lambda^(g-(r+1)C+1) q_g do_g^T (exponent starts at
+ *          1; reading A3) arrives from rank r+1 and dKV_out(r) goes to r-1 (reading A2).
+ *
+ * KV-state caching: lasp_fwd* writes into a caller-owned cache the state
+ * ENTERING the rank, KV_in(r) (reading A4), plus the in-rank segment states derived from it;
+ * lasp_bwd* reads them and never re-communicates KV.
+ *
+ * ------------------------------------------------------------------------------------------
+ * Conventions
+ *   Layout   : every sequence tensor is [batch][n_local][heads][head_dim], contiguous, row-major,
+ *              device memory owned by the caller, base address 16-byte aligned. Element type is
+ *              bf16 (LASP_BF16) or fp32 (LASP_FP32) for q, k, v, o, d_o, dq, dk, dv alike.
+ *   States   : kv_in / kv_out / dkv_in / dkv_out are fp32 [batch][heads][head_dim][head_dim],
+ *              row index = the first factor's dimension (KV = sum k v^T: rows index k, columns v;
+ *              dKV = sum q do^T: rows index q, columns do). Device memory, caller-owned.
+ *   lambda   : HOST pointer to `heads` fp32 decay rates, each in (0, 1] (P:145 gives a single
+ *              lambda, heads are independent, P:18 -- reading A7). lambda = 1 is plain linear
+ *              attention.
+ *   Streams  : all device work is enqueued on the caller's stream; calls return after enqueue.
+ *   Errors   : argument validation is synchronous and enqueues nothing. On a non-OK status
+ *              lasp_last_error() returns a thread-local message. LASP_ERR_CUDA / LASP_ERR_COMM
+ *              report launch / NCCL failures (with rank and peer for COMM).
+ *   Sizes    : n_local may be any value >= 0 (a ragged last GPU block is zero-padded on load and
+ *              clipped on store); n_local = 0 is a no-op that forwards the state (kv_out = kv_in).
+ *              head_dim must be 32, 64 or 128 (else LASP_ERR_UNSUPPORTED).
+ *   Determinism: results are bitwise reproducible run to run for fixed inputs and shape (no
+ *              order-dependent atomics; segment states are folded in a fixed order).
+ *   Protocol : per direction and per call exactly world-1 messages of batch*heads*head_dim^2 fp32
+ *              elements cross the ring, independent of n_local (Table 1 LASP row).
+ *              Forward goes r -> r+1, backward r+1 -> r.
+ */
+#ifndef LASP_H_
+#define LASP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LASP_OK = 0,
+  LASP_ERR_SHAPE = 1,       /* null/misaligned pointer, negative or inconsistent sizes          */
+  LASP_ERR_DOMAIN = 2,      /* lambda outside (0, 1]                                    */
+  LASP_ERR_PARTITION = 3,   /* world/rank inconsistent (rank outside [0, world))                */
+  LASP_ERR_STATE = 4,       /* cache not written by a matching lasp_fwd*                 */
+  LASP_ERR_COMM = 5,        /* NCCL failure or NCCL unavailable                                  */
+  LASP_ERR_CUDA = 6,        /* CUDA launch / driver failure                                      */
+  LASP_ERR_UNSUPPORTED = 7  /* head_dim not in {32, 64, 128} or device is not sm_100            */
+} lasp_status_t;
+
+typedef enum { LASP_BF16 = 0, LASP_FP32 = 1 } lasp_dtype_t;
+
+typedef struct {
+  int64_t batch;     /* B >= 1                                   */
+  int64_t n_local;   /* C = tokens owned by this rank, >= 0       */
+  int64_t heads;     /* H >= 1                                   */
+  int64_t head_dim;  /* D = d_k = d_v, one of 32, 64, 128 */
+  lasp_dtype_t dtype;
+} lasp_shape_t;
+
+/* Opaque ring context: owns the NCCL communicator and nothing else. */
+typedef struct lasp_ctx* lasp_ctx_t;
+
+/* Message for the last non-OK status on the calling thread ("" if none). */
+const char* lasp_last_error(void);
+
+/* Library version string and whether the tcgen05 (sm_100a) path is compiled in. */
+const char* lasp_version(void);
+
+/* Bytes of the caller-owned per-layer KV cache for `shape` (fp32 segment states: the state entering
+ * the rank, KV_in(r), and the states entering each in-rank segment). 256-byte aligned base required. */
+size_t lasp_cache_bytes(const lasp_shape_t* shape);
+
+/* Bytes of the caller-owned scratch workspace used by lasp_fwd, lasp_fwd_local, lasp_bwd and lasp_bwd_local (reusable across
+ * calls on the same stream; contents are not preserved). */
+size_t lasp_workspace_bytes(const lasp_shape_t* shape);
+
+/* In-rank segment length (tokens) the library uses for `shape` (reported for tests/bench). */
+int64_t lasp_segment_len(const lasp_shape_t* shape);
+
+/* ---- communication-free halves (one rank's compute; a ring can be simulated on one GPU by
+ *      chaining kv_out -> kv_in, exactly the Recv/Send of Alg. 2/3 without a transport) ---- */
+
+/* Alg. 2 for one rank. kv_in: state entering the rank (NULL = zero, rank 0). kv_out
+ * (nullable): KV_out(r) = lambda^C KV_in + (lambda^C Lambda^-1 K)^T V. Writes o and cache. */
+lasp_status_t lasp_fwd_local(const lasp_shape_t* shape, const void* q, const void* k, const void* v,
+                             const float* lambda, const float* kv_in, void* o, float* kv_out,
+                             void* cache, void* workspace, void* stream /* cudaStream_t */);
+
+/* Alg. 3 for one rank. dkv_in: dKV_in(r) from rank r+1 (NULL = zero, last rank).
+ * dkv_out (nullable): lambda^C dKV_in + (Lambda Q)^T dO. `cache` must come from lasp_fwd_local or
+ * lasp_fwd with the same shape, lambda and (rank, world); otherwise LASP_ERR_STATE. */
+lasp_status_t lasp_bwd_local(const lasp_shape_t* shape, const void* q, const void* k, const void* v,
+                             const float* lambda, const void* d_o, const void* cache,
+                             const float* dkv_in, void* dq, void* dk, void* dv, float* dkv_out,
+                             void* workspace, void* stream);
+
+/* ---- the ring (NCCL point-to-point over NVLink; one process per GPU) ---- */
+
+/* Writes a 128-byte NCCL unique id (rank 0 calls it; broadcast it with torch.distributed). */
+lasp_status_t lasp_unique_id(uint8_t id[128]);
+
+/* Creates the ring context for (rank, world) on CUDA device `device` (collective over the world). */
+lasp_status_t lasp_ctx_create(int rank, int world, const uint8_t id[128], int device, lasp_ctx_t* out);
+lasp_status_t lasp_ctx_destroy(lasp_ctx_t ctx);
+
+/* Messages and fp32 elements per message this ctx will send per direction per call (protocol
+ * introspection for tests: world-1 hops in total, this rank sends 0 or 1). */
+lasp_status_t lasp_ctx_protocol(lasp_ctx_t ctx, const lasp_shape_t* shape, int64_t* sends_fwd,
+                                int64_t* sends_bwd, int64_t* elems_per_msg);
+
+/* Alg. 2 across the ring: every rank calls it with identical shape and lambda. Rank r receives
+ * KV_in(r) from r-1, stores it in its cache, sends KV_out(r) to r+1, and writes O_r. */
+lasp_status_t lasp_fwd(lasp_ctx_t ctx, const lasp_shape_t* shape, const void* q, const void* k,
+                       const void* v, const float* lambda, void* o, void* cache, void* workspace,
+                       void* stream);
+
+/* Alg. 3 across the ring: receives dKV_in(r) from r+1, sends dKV_out(r) to r-1, writes dQ, dK, dV. */
+lasp_status_t lasp_bwd(lasp_ctx_t ctx, const lasp_shape_t* shape, const void* q, const void* k,
+                       const void* v, const float* lambda, const void* d_o, const void* cache,
+                       void* dq, void* dk, void* dv, void* workspace, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LASP_H_ */

@@ -1,0 +1,9 @@
+"""B200-native LASP hot path (arXiv 2404.02882): chunked causal linear attention with per-head
+decay, sequence-parallel over a KV-state P2P ring. The compute lives in liblasp.so (CUDA, sm_100a,
+C ABI in include/lasp.h); this package only marshals arguments."""
+from . import _native
+from .api import (LaspAttention, Ring, alloc_cache, alloc_workspace, bwd_local, cache_bytes, fwd_local,
+                  lasp_attention, segment_len, workspace_bytes)
+
+__all__ = ["LaspAttention", "Ring", "alloc_cache", "alloc_workspace", "bwd_local", "cache_bytes", "fwd_local",
+           "lasp_attention", "segment_len", "workspace_bytes", "_native"]

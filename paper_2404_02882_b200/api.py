@@ -1,0 +1,197 @@
+"""Torch-facing wrappers of the LASP C ABI (marshalling only; all compute is in liblasp.so).
+
+PyTorch is used for device memory, streams and process groups. Tensors use the boundary layout
+[batch][n_local][heads][head_dim] (include/lasp.h); states are fp32 [batch][heads][D][D].
+
+* ``fwd_local`` / ``bwd_local`` -- one rank's Alg. 2 / Alg. 3 compute without transport.
+* ``Ring``                        -- Alg. 2 / Alg. 3 across a torch.distributed world (NCCL P2P).
+* ``LaspAttention``               -- torch.autograd.Function over ``Ring`` or the local path.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+_DT = {torch.bfloat16: N.LASP_BF16, torch.float32: N.LASP_FP32}
+
+
+def _shape(q: torch.Tensor) -> N.lasp_shape_t:
+    if q.dim() != 4:
+        raise ValueError("expected [batch][n_local][heads][head_dim]")
+    if q.dtype not in _DT:
+        raise TypeError("dtype must be bfloat16 or float32")
+    B, C, H, D = q.shape
+    return N.shape(B, C, H, D, _DT[q.dtype])
+
+
+def _lam(lam, heads: int):
+    arr = np.ascontiguousarray(np.broadcast_to(np.asarray(
+        lam.detach().cpu().numpy() if isinstance(lam, torch.Tensor) else lam, dtype=np.float32), (heads,)))
+    return arr, arr.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _check_seq(*ts):
+    ref = ts[0]
+    for t in ts:
+        if t is None:
+            continue
+        if not t.is_cuda or t.shape != ref.shape or t.dtype != ref.dtype or not t.is_contiguous():
+            raise ValueError("sequence tensors must be contiguous CUDA tensors of equal shape and dtype")
+
+
+def cache_bytes(shape: N.lasp_shape_t) -> int:
+    return int(N.lib().lasp_cache_bytes(ctypes.byref(shape)))
+
+
+def workspace_bytes(shape: N.lasp_shape_t) -> int:
+    return int(N.lib().lasp_workspace_bytes(ctypes.byref(shape)))
+
+
+def segment_len(shape: N.lasp_shape_t) -> int:
+    return int(N.lib().lasp_segment_len(ctypes.byref(shape)))
+
+
+def alloc_cache(q: torch.Tensor) -> torch.Tensor:
+    """Caller-owned KV cache for q's shape (one per layer)."""
+    return torch.empty(max(cache_bytes(_shape(q)), 16), dtype=torch.uint8, device=q.device)
+
+
+def alloc_workspace(q: torch.Tensor) -> torch.Tensor:
+    return torch.empty(max(workspace_bytes(_shape(q)), 16), dtype=torch.uint8, device=q.device)
+
+
+def _state_like(q: torch.Tensor) -> torch.Tensor:
+    B, _, H, D = q.shape
+    return torch.empty((B, H, D, D), dtype=torch.float32, device=q.device)
+
+
+def fwd_local(q, k, v, lam, kv_in=None, *, o=None, kv_out=True, cache=None, workspace=None):
+    """Alg. 2 for one rank -> (o, kv_out or None, cache)."""
+    _check_seq(q, k, v)
+    s = _shape(q)
+    o = torch.empty_like(q) if o is None else o
+    kv_out_t = _state_like(q) if kv_out is True else (kv_out if isinstance(kv_out, torch.Tensor) else None)
+    cache = alloc_cache(q) if cache is None else cache
+    workspace = alloc_workspace(q) if workspace is None else workspace
+    _, lp = _lam(lam, s.heads)
+    N.check(N.lib().lasp_fwd_local(ctypes.byref(s), _p(q), _p(k), _p(v), lp, _p(kv_in), _p(o), _p(kv_out_t),
+                                   _p(cache), _p(workspace), _stream(q.device)))
+    return o, kv_out_t, cache
+
+
+def bwd_local(q, k, v, lam, do, cache, dkv_in=None, *, dq=None, dk=None, dv=None, dkv_out=True, workspace=None):
+    """Alg. 3 for one rank -> (dq, dk, dv, dkv_out or None)."""
+    _check_seq(q, k, v, do)
+    s = _shape(q)
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(q) if dk is None else dk
+    dv = torch.empty_like(q) if dv is None else dv
+    dkv_out_t = _state_like(q) if dkv_out is True else (dkv_out if isinstance(dkv_out, torch.Tensor) else None)
+    workspace = alloc_workspace(q) if workspace is None else workspace
+    _, lp = _lam(lam, s.heads)
+    N.check(N.lib().lasp_bwd_local(ctypes.byref(s), _p(q), _p(k), _p(v), lp, _p(do), _p(cache), _p(dkv_in),
+                                   _p(dq), _p(dk), _p(dv), _p(dkv_out_t), _p(workspace), _stream(q.device)))
+    return dq, dk, dv, dkv_out_t
+
+
+class Ring:
+    """The LASP ring over the default torch.distributed group: rank r owns tokens [rC, (r+1)C)
+    (Alg. 1 with T = W). Rank 0 creates the NCCL id; torch broadcasts it."""
+
+    def __init__(self, device=None, group=None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        idbuf = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            N.check(N.lib().lasp_unique_id(idbuf))
+        obj = [bytes(idbuf.raw)]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        self._ctx = ctypes.c_void_p()
+        N.check(N.lib().lasp_ctx_create(self.rank, self.world, obj[0], self.device.index or 0,
+                                        ctypes.byref(self._ctx)))
+
+    def close(self):
+        if self._ctx:
+            N.lib().lasp_ctx_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def protocol(self, q) -> tuple[int, int, int]:
+        s = _shape(q)
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        N.check(N.lib().lasp_ctx_protocol(self._ctx, ctypes.byref(s), ctypes.byref(a), ctypes.byref(b),
+                                          ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    def fwd(self, q, k, v, lam, *, o=None, cache=None, workspace=None):
+        _check_seq(q, k, v)
+        s = _shape(q)
+        o = torch.empty_like(q) if o is None else o
+        cache = alloc_cache(q) if cache is None else cache
+        workspace = alloc_workspace(q) if workspace is None else workspace
+        _, lp = _lam(lam, s.heads)
+        N.check(N.lib().lasp_fwd(self._ctx, ctypes.byref(s), _p(q), _p(k), _p(v), lp, _p(o), _p(cache),
+                                 _p(workspace), _stream(q.device)))
+        return o, cache
+
+    def bwd(self, q, k, v, lam, do, cache, *, dq=None, dk=None, dv=None, workspace=None):
+        _check_seq(q, k, v, do)
+        s = _shape(q)
+        dq = torch.empty_like(q) if dq is None else dq
+        dk = torch.empty_like(q) if dk is None else dk
+        dv = torch.empty_like(q) if dv is None else dv
+        workspace = alloc_workspace(q) if workspace is None else workspace
+        _, lp = _lam(lam, s.heads)
+        N.check(N.lib().lasp_bwd(self._ctx, ctypes.byref(s), _p(q), _p(k), _p(v), lp, _p(do), _p(cache), _p(dq),
+                                 _p(dk), _p(dv), _p(workspace), _stream(q.device)))
+        return dq, dk, dv
+
+
+class LaspAttention(torch.autograd.Function):
+    """O = LASP(Q, K, V; lambda) with the KV-state cache saved for backward.
+    ``ring`` None runs the single-rank path (world size 1)."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, lam, ring=None):
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        if ring is None:
+            o, _, cache = fwd_local(q, k, v, lam, kv_out=False)
+        else:
+            o, cache = ring.fwd(q, k, v, lam)
+        ctx.save_for_backward(q, k, v, cache)
+        ctx.lam = lam
+        ctx.ring = ring
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, cache = ctx.saved_tensors
+        do = do.contiguous()
+        if ctx.ring is None:
+            dq, dk, dv, _ = bwd_local(q, k, v, ctx.lam, do, cache, dkv_out=False)
+        else:
+            dq, dk, dv = ctx.ring.bwd(q, k, v, ctx.lam, do, cache)
+        return dq, dk, dv, None, None
+
+
+def lasp_attention(q, k, v, lam, ring=None):
+    return LaspAttention.apply(q, k, v, lam, ring)

@@ -1,0 +1,282 @@
+// kernels_simt.cu -- CUDA-core (FFMA) kernels of the LASP path.
+//
+// These serve the fp32 path (LASP_FP32, parity tolerance 1e-5: TF32 tensor cores cannot meet it,
+// SURVEY.md V3) and any (dtype, head_dim) the tcgen05 kernels do not cover. They implement the
+// same three stages as the tensor-core path (see lasp_common.cuh):
+//   seg_state : decayed outer-product accumulation over one segment (F1 / B1, Eq. 12 / Eq. 21)
+//   prefix    : fold of segment states along the rank, seeded with the received state (F2 / B2)
+//   core      : fused intra + inter chunk pass with the running state (F3 / B3, Eq. 7-9, 15-22)
+#include "lasp_common.cuh"
+
+#include <cmath>
+
+namespace lasp {
+namespace {
+
+template <typename T> __device__ __forceinline__ float ld(const T* p);
+template <> __device__ __forceinline__ float ld<float>(const float* p) { return *p; }
+template <> __device__ __forceinline__ float ld<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat162float(*p);
+}
+template <typename T> __device__ __forceinline__ void st(T* p, float v);
+template <> __device__ __forceinline__ void st<float>(float* p, float v) { *p = v; }
+template <> __device__ __forceinline__ void st<__nv_bfloat16>(__nv_bfloat16* p, float v) {
+  *p = __float2bfloat16_rn(v);
+}
+
+// lambda^k in fp64, rounded once to fp32 (reading A9: powers are never inverted).
+__device__ __forceinline__ float powk(float lam, double k) { return (float)pow((double)lam, k); }
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------------------------
+// seg_state: out[b][h][p] = sum_{pos in seg p} w_pos x_pos y_pos^T  (D x D, fp32)
+//   FWD: w = lam^(end-1-pos)  (Eq. 12's lambda^C Lambda^-1 weights, relative to the segment end)
+//   REV: w = lam^(pos-begin+1) (Eq. 21's Lambda weights, relative to the segment begin)
+template <typename T, int D, Dir DIR>
+__global__ void __launch_bounds__(kThreads) seg_state_simt_kernel(Plan p, const T* __restrict__ x,
+                                                                  const T* __restrict__ y,
+                                                                  float* __restrict__ out) {
+  constexpr int TT = 32;        // tokens per smem tile
+  constexpr int R = D / 16;     // per-thread register tile R x R
+  __shared__ float xs[TT][D + 1];
+  __shared__ float ys[TT][D + 1];
+  const int64_t seg = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const float lam = p.lam[h];
+  const int64_t beg = seg_begin(DIR, seg, p.seg_len, p.C), end = seg_end(DIR, seg, p.seg_len, p.C);
+  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
+  float acc[R][R];
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < R; ++j) acc[i][j] = 0.f;
+  const int64_t rs = p.H * D;  // row stride (elements) between consecutive tokens
+  for (int64_t t0 = beg; t0 < end; t0 += TT) {
+    for (int idx = threadIdx.x; idx < TT * D; idx += kThreads) {
+      const int s = idx / D, d = idx % D;
+      const int64_t pos = t0 + s;
+      float xv = 0.f, yv = 0.f;
+      if (pos < end) {
+        const int64_t off = (b * p.C + pos) * rs + h * D + d;
+        const double k = (DIR == Dir::FWD) ? double(end - 1 - pos) : double(pos - beg + 1);
+        xv = ld(x + off) * powk(lam, k);
+        yv = ld(y + off);
+      }
+      xs[s][d] = xv;
+      ys[s][d] = yv;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int s = 0; s < TT; ++s) {
+      float xr[R], yr[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) xr[i] = xs[s][tr + 16 * i];
+#pragma unroll
+      for (int j = 0; j < R; ++j) yr[j] = ys[s][tc + 16 * j];
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int j = 0; j < R; ++j) acc[i][j] = fmaf(xr[i], yr[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* o = out + ((b * p.H + h) * p.nseg + seg) * D * D;
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < R; ++j) o[(tr + 16 * i) * D + tc + 16 * j] = acc[i][j];
+}
+
+// ---------------------------------------------------------------------------------------------
+// prefix: per element, cur = init; for p: prefix[p] = cur; cur = lam^len_p cur + seg[p]; final = cur
+// (Alg. 2 P:171 / Alg. 3 P:648 applied between segments). `prefix` may alias `seg_states`.
+__global__ void prefix_kernel(Plan p, Dir dir, const float* __restrict__ init, const float* seg_states,
+                              float* prefix, float* __restrict__ final_out) {
+  const int64_t DD = p.D * p.D;
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over B*H*D*D
+  if (idx >= p.B * p.H * DD) return;
+  const int64_t bh = idx / DD, e = idx % DD, h = bh % p.H;
+  const float lam = p.lam[h];
+  float cur = init ? init[idx] : 0.f;
+  for (int64_t s = 0; s < p.nseg; ++s) {
+    const int64_t len = seg_end(dir, s, p.seg_len, p.C) - seg_begin(dir, s, p.seg_len, p.C);
+    const int64_t off = (bh * p.nseg + s) * DD + e;
+    const float v = seg_states ? seg_states[off] : 0.f;
+    if (prefix) prefix[off] = cur;
+    cur = fmaf(powk(lam, double(len)), cur, v);
+  }
+  if (final_out) final_out[idx] = cur;
+}
+
+// kv_out = lam^C kv_in + local (the ring's combine step, Alg. 2 P:171 with the local part hoisted)
+__global__ void combine_kernel(Plan p, const float* __restrict__ kv_in,
+                               const float* __restrict__ local, float* __restrict__ kv_out) {
+  const int64_t DD = p.D * p.D;
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= p.B * p.H * DD) return;
+  const int64_t h = (idx / DD) % p.H;
+  const float in = kv_in ? kv_in[idx] : 0.f;
+  kv_out[idx] = fmaf(powk(p.lam[h], double(p.C)), in, local[idx]);
+}
+
+// ---------------------------------------------------------------------------------------------
+// core: one CTA per (segment, head, batch); blocks of BT tokens in direction order with the running
+// state S in shared memory (fp32).
+template <typename T, int D, Dir DIR>
+__global__ void __launch_bounds__(kThreads) core_simt_kernel(Plan p, SeqArgs a) {
+  constexpr int BT = 32;
+  extern __shared__ float smem[];
+  float* sa = smem;                  // [BT][D+1]
+  float* sb = sa + BT * (D + 1);     // [BT][D+1]
+  float* sc = sb + BT * (D + 1);     // [BT][D+1]
+  float* S = sc + BT * (D + 1);      // [D][D+1]
+  float* A = S + D * (D + 1);        // [BT][BT+1]
+  float* pw = A + BT * (BT + 1);     // [BT+1]
+  const int64_t seg = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const float lam = p.lam[h];
+  const int64_t beg = seg_begin(DIR, seg, p.seg_len, p.C), end = seg_end(DIR, seg, p.seg_len, p.C);
+  const int tid = threadIdx.x;
+  for (int k = tid; k <= BT; k += kThreads) pw[k] = powk(lam, double(k));
+  const float* st0 = a.state + ((b * p.H + h) * p.nseg + seg) * D * D;
+  for (int idx = tid; idx < D * D; idx += kThreads) {
+    const int d = idx / D, e = idx % D;
+    S[d * (D + 1) + e] = a.trans_state ? st0[e * D + d] : st0[idx];
+  }
+  const T* ga = static_cast<const T*>(a.a);
+  const T* gb = static_cast<const T*>(a.b);
+  const T* gc = static_cast<const T*>(a.c);
+  T* go = static_cast<T*>(a.out);
+  const int64_t rs = p.H * D;
+  const int64_t nblk = (end - beg + BT - 1) / BT;
+  __syncthreads();
+  for (int64_t j = 0; j < nblk; ++j) {
+    // block rows [t0, t0 + BT): FWD ascending from beg; REV descending, aligned to end
+    const int64_t t0 = (DIR == Dir::FWD) ? beg + j * BT : end - (j + 1) * BT;
+    for (int idx = tid; idx < BT * D; idx += kThreads) {
+      const int s = idx / D, d = idx % D;
+      const int64_t pos = t0 + s;
+      float va = 0.f, vb = 0.f, vc = 0.f;
+      if (pos >= beg && pos < end) {
+        const int64_t off = (b * p.C + pos) * rs + h * D + d;
+        va = ld(ga + off); vb = ld(gb + off); vc = ld(gc + off);
+      }
+      sa[s * (D + 1) + d] = va; sb[s * (D + 1) + d] = vb; sc[s * (D + 1) + d] = vc;
+    }
+    __syncthreads();
+    // A_ij = (a_i . b_j) * M_ij
+    for (int idx = tid; idx < BT * BT; idx += kThreads) {
+      const int i = idx / BT, jj = idx % BT;
+      const bool live = (DIR == Dir::FWD) ? (jj <= i) : (jj >= i);
+      float s = 0.f;
+      if (live) {
+#pragma unroll 8
+        for (int d = 0; d < D; ++d) s = fmaf(sa[i * (D + 1) + d], sb[jj * (D + 1) + d], s);
+        s *= pw[(DIR == Dir::FWD) ? (i - jj) : (jj - i)];
+      }
+      A[i * (BT + 1) + jj] = s;
+    }
+    __syncthreads();
+    // out_i = sum_j A_ij c_j + r_i a_i^T S
+    for (int idx = tid; idx < BT * D; idx += kThreads) {
+      const int i = idx / D, e = idx % D;
+      const int64_t pos = t0 + i;
+      float intra = 0.f, inter = 0.f;
+#pragma unroll 8
+      for (int jj = 0; jj < BT; ++jj) intra = fmaf(A[i * (BT + 1) + jj], sc[jj * (D + 1) + e], intra);
+#pragma unroll 8
+      for (int d = 0; d < D; ++d) inter = fmaf(sa[i * (D + 1) + d], S[d * (D + 1) + e], inter);
+      const float r = (DIR == Dir::FWD) ? pw[i + 1] : pw[BT - 1 - i];
+      if (pos >= beg && pos < end) st(go + (b * p.C + pos) * rs + h * D + e, fmaf(r, inter, intra));
+    }
+    __syncthreads();
+    // S = lam^BT S + sum_s u_s b_s c_s^T
+    if (j + 1 < nblk) {
+      for (int idx = tid; idx < D * D; idx += kThreads) {
+        const int d = idx / D, e = idx % D;
+        float acc = 0.f;
+#pragma unroll 8
+        for (int s = 0; s < BT; ++s) {
+          const float u = (DIR == Dir::FWD) ? pw[BT - 1 - s] : pw[s + 1];
+          acc = fmaf(u * sb[s * (D + 1) + d], sc[s * (D + 1) + e], acc);
+        }
+        S[d * (D + 1) + e] = fmaf(pw[BT], S[d * (D + 1) + e], acc);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T, int D>
+cudaError_t seg_state_dispatch_dir(const Plan& p, Dir dir, const void* x, const void* y, float* out,
+                                   cudaStream_t st) {
+  dim3 grid((unsigned)p.nseg, (unsigned)p.H, (unsigned)p.B);
+  if (dir == Dir::FWD)
+    seg_state_simt_kernel<T, D, Dir::FWD><<<grid, kThreads, 0, st>>>(p, (const T*)x, (const T*)y, out);
+  else
+    seg_state_simt_kernel<T, D, Dir::REV><<<grid, kThreads, 0, st>>>(p, (const T*)x, (const T*)y, out);
+  return cudaGetLastError();
+}
+
+template <typename T, int D, Dir DIR>
+cudaError_t core_launch(const Plan& p, const SeqArgs& a, cudaStream_t st) {
+  constexpr int BT = 32;
+  const size_t smem = sizeof(float) * (3 * BT * (D + 1) + D * (D + 1) + BT * (BT + 1) + BT + 1);
+  auto kern = core_simt_kernel<T, D, DIR>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)p.nseg, (unsigned)p.H, (unsigned)p.B);
+  kern<<<grid, kThreads, smem, st>>>(p, a);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t seg_state_dispatch(const Plan& p, Dir dir, const void* x, const void* y, float* out,
+                               cudaStream_t st) {
+  switch (p.D) {
+    case 32: return seg_state_dispatch_dir<T, 32>(p, dir, x, y, out, st);
+    case 64: return seg_state_dispatch_dir<T, 64>(p, dir, x, y, out, st);
+    case 128: return seg_state_dispatch_dir<T, 128>(p, dir, x, y, out, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+cudaError_t core_dispatch(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st) {
+  const bool f = dir == Dir::FWD;
+  switch (p.D) {
+    case 32: return f ? core_launch<T, 32, Dir::FWD>(p, a, st) : core_launch<T, 32, Dir::REV>(p, a, st);
+    case 64: return f ? core_launch<T, 64, Dir::FWD>(p, a, st) : core_launch<T, 64, Dir::REV>(p, a, st);
+    case 128: return f ? core_launch<T, 128, Dir::FWD>(p, a, st) : core_launch<T, 128, Dir::REV>(p, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+cudaError_t launch_seg_state_simt(const Plan& p, Dir dir, const void* x, const void* y, float* out,
+                                  cudaStream_t st) {
+  return p.dtype == 0 ? seg_state_dispatch<__nv_bfloat16>(p, dir, x, y, out, st)
+                      : seg_state_dispatch<float>(p, dir, x, y, out, st);
+}
+
+cudaError_t launch_core_simt(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st) {
+  return p.dtype == 0 ? core_dispatch<__nv_bfloat16>(p, dir, a, st) : core_dispatch<float>(p, dir, a, st);
+}
+
+cudaError_t launch_prefix(const Plan& p, Dir dir, const float* init, const float* seg_states, float* prefix_out,
+                          float* final_out, cudaStream_t st) {
+  const int64_t n = p.B * p.H * p.D * p.D;
+  const int threads = 256;
+  prefix_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, st>>>(p, dir, init, seg_states,
+                                                                            prefix_out, final_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local, float* kv_out, cudaStream_t st) {
+  const int64_t n = p.B * p.H * p.D * p.D;
+  const int threads = 256;
+  combine_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, st>>>(p, kv_in, local, kv_out);
+  return cudaGetLastError();
+}
+
+}  // namespace lasp

@@ -1,0 +1,470 @@
+// lasp_api.cu -- the C ABI declared in include/lasp.h: validation, planning, the KV-cache tag
+// registry, stage orchestration (Alg. 2 / Alg. 3 per rank) and the NCCL P2P ring.
+//
+// Stage order per rank:
+//   forward : F1 seg_state(K,V) -> [ring: recv KV_in, combine, send] -> F2 prefix(KV_in) -> F3 core
+//   backward: B1 seg_state(Q,dO) -> [ring: recv dKV_in, combine, send] || B3a core(dQ, cache)
+//             -> B2 prefix(dKV_in) -> B3b core(dV), core(dK)
+// The KV-independent local parts (F1/B1) are hoisted in front of the ring hop, so the hop carries
+// lambda^C * received + local (Alg. 2, Alg. 3), and dQ overlaps the dKV ring.
+#include "../../include/lasp.h"
+#include "lasp_common.cuh"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+using namespace lasp;
+
+namespace {
+
+thread_local std::string g_err;
+
+lasp_status_t fail(lasp_status_t st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+lasp_status_t cuda_fail(cudaError_t e, const char* where) {
+  return fail(LASP_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define LASP_CUDA(call)                                       \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);       \
+  } while (0)
+
+// ---- planning --------------------------------------------------------------------------------
+int64_t env_i64(const char* name, int64_t dflt) {
+  const char* s = std::getenv(name);
+  if (!s || !*s) return dflt;
+  return std::atoll(s);
+}
+
+int64_t choose_seg_len(int64_t B, int64_t C, int64_t H) {
+  const int64_t q = kSegQuantum;
+  const int64_t forced = env_i64("LASP_SEG_LEN", 0);
+  if (forced > 0) return ((forced + q - 1) / q) * q;
+  if (C <= 0) return q;
+  const int64_t nb = (C + q - 1) / q;
+  const int64_t target = env_i64("LASP_TARGET_CTAS", 4 * 148);
+  int64_t nseg_t = (target + B * H - 1) / (B * H);
+  if (nseg_t < 1) nseg_t = 1;
+  if (nseg_t > nb) nseg_t = nb;
+  const int64_t seg_blocks = (nb + nseg_t - 1) / nseg_t;
+  return seg_blocks * q;
+}
+
+lasp_status_t validate_shape(const lasp_shape_t* s) {
+  if (!s) return fail(LASP_ERR_SHAPE, "shape is NULL");
+  if (s->batch < 1 || s->n_local < 0 || s->heads < 1)
+    return fail(LASP_ERR_SHAPE, "need batch >= 1, n_local >= 0, heads >= 1");
+  if (s->heads > kMaxHeads) return fail(LASP_ERR_UNSUPPORTED, "heads > 256 not supported");
+  if (s->head_dim != 32 && s->head_dim != 64 && s->head_dim != 128)
+    return fail(LASP_ERR_UNSUPPORTED, "head_dim must be 32, 64 or 128");
+  if (s->dtype != LASP_BF16 && s->dtype != LASP_FP32) return fail(LASP_ERR_SHAPE, "bad dtype");
+  return LASP_OK;
+}
+
+Plan make_plan(const lasp_shape_t* s) {
+  Plan p{};
+  p.B = s->batch; p.C = s->n_local; p.H = s->heads; p.D = s->head_dim;
+  p.dtype = s->dtype == LASP_BF16 ? 0 : 1;
+  p.seg_len = choose_seg_len(p.B, p.C, p.H);
+  p.nseg = p.C > 0 ? (p.C + p.seg_len - 1) / p.seg_len : 1;
+  return p;
+}
+
+lasp_status_t load_lambda(Plan& p, const float* lambda) {
+  if (!lambda) return fail(LASP_ERR_SHAPE, "lambda is NULL");
+  for (int64_t h = 0; h < p.H; ++h) {
+    const float l = lambda[h];
+    if (!(l > 0.f && l <= 1.f)) {
+      char buf[96];
+      std::snprintf(buf, sizeof buf, "lambda[%lld] = %g outside (0, 1]", (long long)h, (double)l);
+      return fail(LASP_ERR_DOMAIN, buf);
+    }
+    p.lam[h] = l;
+  }
+  return LASP_OK;
+}
+
+size_t state_elems(const Plan& p) { return size_t(p.B * p.H * p.D * p.D); }
+size_t seg_state_elems(const Plan& p) { return size_t(p.B * p.H * p.nseg * p.D * p.D); }
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Workspace {
+  float* seg;     // [B][H][nseg][D][D]
+  float* local;   // [B][H][D][D] local total (ring)
+  float* in;      // received state
+  float* out;     // state to send
+};
+
+Workspace carve(const Plan& p, void* ws) {
+  char* c = static_cast<char*>(ws);
+  Workspace w;
+  w.seg = reinterpret_cast<float*>(c);
+  c += align256(seg_state_elems(p) * 4);
+  w.local = reinterpret_cast<float*>(c);
+  c += align256(state_elems(p) * 4);
+  w.in = reinterpret_cast<float*>(c);
+  c += align256(state_elems(p) * 4);
+  w.out = reinterpret_cast<float*>(c);
+  return w;
+}
+
+size_t workspace_bytes(const Plan& p) {
+  return align256(seg_state_elems(p) * 4) + 3 * align256(state_elems(p) * 4);
+}
+
+bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
+
+lasp_status_t check_ptrs(const Plan& p, std::initializer_list<const void*> seq, const void* cache,
+                         const void* ws) {
+  if (p.C > 0)
+    for (const void* x : seq)
+      if (!x || !aligned16(x)) return fail(LASP_ERR_SHAPE, "sequence tensor NULL or not 16-byte aligned");
+  if (!cache || !aligned16(cache)) return fail(LASP_ERR_SHAPE, "cache NULL or not 16-byte aligned");
+  if (!ws || !aligned16(ws)) return fail(LASP_ERR_SHAPE, "workspace NULL or not 16-byte aligned");
+  return LASP_OK;
+}
+
+// ---- device check: the kernels are compiled for sm_100a only -----------------------------------
+lasp_status_t check_device() {
+  static std::mutex mu;
+  static std::unordered_map<int, bool> ok;
+  int dev = 0;
+  LASP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  auto it = ok.find(dev);
+  if (it == ok.end()) {
+    int maj = 0, min = 0;
+    LASP_CUDA(cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, dev));
+    LASP_CUDA(cudaDeviceGetAttribute(&min, cudaDevAttrComputeCapabilityMinor, dev));
+    it = ok.emplace(dev, maj == 10 && min == 0).first;
+  }
+  if (!it->second) return fail(LASP_ERR_UNSUPPORTED, "device is not sm_100 (B200); kernels are sm_100a only");
+  return LASP_OK;
+}
+
+// ---- KV-cache tag registry (backward before/without a matching forward -> STATE) -------
+struct CacheTag {
+  int64_t B, C, H, D, seg_len;
+  int dtype, rank, world;
+  uint64_t lam_hash;
+};
+
+uint64_t hash_lam(const Plan& p) {
+  uint64_t h = 1469598103934665603ull;
+  for (int64_t i = 0; i < p.H; ++i) {
+    uint32_t bits;
+    std::memcpy(&bits, &p.lam[i], 4);
+    h = (h ^ bits) * 1099511628211ull;
+  }
+  return h;
+}
+
+std::mutex g_tag_mu;
+std::unordered_map<const void*, CacheTag> g_tags;
+
+void register_cache(const Plan& p, const void* cache, int rank, int world) {
+  std::lock_guard<std::mutex> g(g_tag_mu);
+  g_tags[cache] = CacheTag{p.B, p.C, p.H, p.D, p.seg_len, p.dtype, rank, world, hash_lam(p)};
+}
+
+lasp_status_t check_cache(const Plan& p, const void* cache, int rank, int world, bool check_rank) {
+  std::lock_guard<std::mutex> g(g_tag_mu);
+  auto it = g_tags.find(cache);
+  if (it == g_tags.end()) return fail(LASP_ERR_STATE, "cache was not written by lasp_fwd/lasp_fwd_local");
+  const CacheTag& t = it->second;
+  if (t.B != p.B || t.C != p.C || t.H != p.H || t.D != p.D || t.seg_len != p.seg_len || t.dtype != p.dtype)
+    return fail(LASP_ERR_STATE, "cache shape does not match the backward call");
+  if (t.lam_hash != hash_lam(p)) return fail(LASP_ERR_STATE, "cache lambda does not match the backward call");
+  if (check_rank && (t.rank != rank || t.world != world))
+    return fail(LASP_ERR_STATE, "cache (rank, world) does not match the ring context");
+  return LASP_OK;
+}
+
+// ---- stage dispatch: tcgen05 for covered bf16 shapes, CUDA cores otherwise ---------------------
+cudaError_t seg_state(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st) {
+  if (tc_supported(p)) return launch_seg_state_tc(p, dir, x, y, out, st);
+  return launch_seg_state_simt(p, dir, x, y, out, st);
+}
+
+cudaError_t core(const Plan& p, Dir dir, const void* a, const void* b, const void* c, void* out,
+                 const float* state, int trans, cudaStream_t st) {
+  SeqArgs args{a, b, c, out, state, trans};
+  if (tc_supported(p)) return launch_core_tc(p, dir, args, st);
+  return launch_core_simt(p, dir, args, st);
+}
+
+// ---- common prologue -------------------------------------------------------------------------
+lasp_status_t prologue(const lasp_shape_t* shape, const float* lambda, Plan& p) {
+  lasp_status_t s = validate_shape(shape);
+  if (s != LASP_OK) return s;
+  p = make_plan(shape);
+  return load_lambda(p, lambda);
+}
+
+// Forward compute after KV_in is known (F2 prefix + F3 core). `seg` already holds F1's states.
+lasp_status_t fwd_tail(const Plan& p, const void* q, const void* k, const void* v, const float* kv_in,
+                       void* o, float* kv_out, void* cache, float* seg, cudaStream_t st) {
+  float* P = static_cast<float*>(cache);
+  if (p.C == 0) {
+    LASP_CUDA(launch_prefix(p, Dir::FWD, kv_in, nullptr, P, kv_out, st));
+    return LASP_OK;
+  }
+  LASP_CUDA(launch_prefix(p, Dir::FWD, kv_in, seg, P, kv_out, st));
+  LASP_CUDA(core(p, Dir::FWD, q, k, v, o, P, 0, st));
+  return LASP_OK;
+}
+
+// ---- NCCL, loaded lazily so that the library works without it (local path) -------------------
+struct NcclApi {
+  bool loaded = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* cands[] = {std::getenv("LASP_NCCL_LIB"), "libnccl.so.2",
+                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+    void* h = nullptr;
+    for (const char* c : cands)
+      if (c && (h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) { api.why = "libnccl.so.2 not found (set LASP_NCCL_LIB)"; return; }
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+    api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.loaded = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
+                 api.GetErrorString;
+    if (!api.loaded) api.why = "libnccl.so.2 lacks the point-to-point API";
+  });
+  return api;
+}
+
+lasp_status_t nccl_fail(ncclResult_t r, const char* what, int rank, int peer) {
+  char buf[256];
+  std::snprintf(buf, sizeof buf, "%s failed on rank %d (peer %d): %s", what, rank, peer,
+                nccl().GetErrorString ? nccl().GetErrorString(r) : "?");
+  return fail(LASP_ERR_COMM, buf);
+}
+
+}  // namespace
+
+struct lasp_ctx {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1, device = 0;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+};
+
+extern "C" {
+
+const char* lasp_last_error(void) { return g_err.c_str(); }
+
+const char* lasp_version(void) { return "lasp-b200 0.1 (sm_100a; tcgen05 + CUDA-core paths)"; }
+
+size_t lasp_cache_bytes(const lasp_shape_t* shape) {
+  if (validate_shape(shape) != LASP_OK) return 0;
+  const Plan p = make_plan(shape);
+  return seg_state_elems(p) * sizeof(float);
+}
+
+size_t lasp_workspace_bytes(const lasp_shape_t* shape) {
+  if (validate_shape(shape) != LASP_OK) return 0;
+  return workspace_bytes(make_plan(shape));
+}
+
+int64_t lasp_segment_len(const lasp_shape_t* shape) {
+  if (validate_shape(shape) != LASP_OK) return 0;
+  return make_plan(shape).seg_len;
+}
+
+lasp_status_t lasp_fwd_local(const lasp_shape_t* shape, const void* q, const void* k, const void* v,
+                             const float* lambda, const float* kv_in, void* o, float* kv_out, void* cache,
+                             void* workspace, void* stream) {
+  Plan p;
+  lasp_status_t s = prologue(shape, lambda, p);
+  if (s != LASP_OK) return s;
+  if ((s = check_ptrs(p, {q, k, v, o}, cache, workspace)) != LASP_OK) return s;
+  if ((s = check_device()) != LASP_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Workspace w = carve(p, workspace);
+  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st));
+  if ((s = fwd_tail(p, q, k, v, kv_in, o, kv_out, cache, w.seg, st)) != LASP_OK) return s;
+  register_cache(p, cache, -1, -1);
+  return LASP_OK;
+}
+
+lasp_status_t lasp_bwd_local(const lasp_shape_t* shape, const void* q, const void* k, const void* v,
+                             const float* lambda, const void* d_o, const void* cache, const float* dkv_in,
+                             void* dq, void* dk, void* dv, float* dkv_out, void* workspace, void* stream) {
+  Plan p;
+  lasp_status_t s = prologue(shape, lambda, p);
+  if (s != LASP_OK) return s;
+  if ((s = check_ptrs(p, {q, k, v, d_o, dq, dk, dv}, cache, workspace)) != LASP_OK) return s;
+  if ((s = check_cache(p, cache, -1, -1, false)) != LASP_OK) return s;
+  if ((s = check_device()) != LASP_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Workspace w = carve(p, workspace);
+  const float* P = static_cast<const float*>(cache);
+  if (p.C == 0) {
+    LASP_CUDA(launch_prefix(p, Dir::REV, dkv_in, nullptr, nullptr, dkv_out, st));
+    return LASP_OK;
+  }
+  LASP_CUDA(core(p, Dir::FWD, d_o, v, k, dq, P, 1, st));                     // dQ (cache only)
+  LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st));                      // B1
+  LASP_CUDA(launch_prefix(p, Dir::REV, dkv_in, w.seg, w.seg, dkv_out, st));  // B2 (in place)
+  LASP_CUDA(core(p, Dir::REV, k, q, d_o, dv, w.seg, 0, st));                 // dV
+  LASP_CUDA(core(p, Dir::REV, v, d_o, q, dk, w.seg, 1, st));                 // dK
+  return LASP_OK;
+}
+
+lasp_status_t lasp_unique_id(uint8_t id[128]) {
+  if (!id) return fail(LASP_ERR_SHAPE, "id is NULL");
+  NcclApi& n = nccl();
+  if (!n.loaded) return fail(LASP_ERR_COMM, n.why);
+  ncclUniqueId uid;
+  ncclResult_t r = n.GetUniqueId(&uid);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId", -1, -1);
+  static_assert(sizeof(uid.internal) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id, uid.internal, 128);
+  return LASP_OK;
+}
+
+lasp_status_t lasp_ctx_create(int rank, int world, const uint8_t id[128], int device, lasp_ctx_t* out) {
+  if (!out || !id) return fail(LASP_ERR_SHAPE, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(LASP_ERR_PARTITION, "rank outside [0, world)");
+  NcclApi& n = nccl();
+  if (!n.loaded) return fail(LASP_ERR_COMM, n.why);
+  LASP_CUDA(cudaSetDevice(device));
+  lasp_ctx* c = new lasp_ctx;
+  c->rank = rank; c->world = world; c->device = device;
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id, 128);
+  ncclResult_t r = n.CommInitRank(&c->comm, world, uid, rank);
+  if (r != ncclSuccess) { delete c; return nccl_fail(r, "ncclCommInitRank", rank, -1); }
+  cudaError_t e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming);
+  if (e != cudaSuccess) { n.CommDestroy(c->comm); delete c; return cuda_fail(e, "ctx stream/event"); }
+  *out = c;
+  return LASP_OK;
+}
+
+lasp_status_t lasp_ctx_destroy(lasp_ctx_t c) {
+  if (!c) return LASP_OK;
+  if (c->comm) nccl().CommDestroy(c->comm);
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  delete c;
+  return LASP_OK;
+}
+
+lasp_status_t lasp_ctx_protocol(lasp_ctx_t c, const lasp_shape_t* shape, int64_t* sends_fwd, int64_t* sends_bwd,
+                                int64_t* elems_per_msg) {
+  if (!c) return fail(LASP_ERR_SHAPE, "ctx is NULL");
+  lasp_status_t s = validate_shape(shape);
+  if (s != LASP_OK) return s;
+  if (sends_fwd) *sends_fwd = c->rank < c->world - 1 ? 1 : 0;  // Alg. 2: send to i+1
+  if (sends_bwd) *sends_bwd = c->rank > 0 ? 1 : 0;             // Alg. 3 P:649 (reading A2): to i-1
+  if (elems_per_msg) *elems_per_msg = shape->batch * shape->heads * shape->head_dim * shape->head_dim;
+  return LASP_OK;
+}
+
+lasp_status_t lasp_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, const void* k, const void* v,
+                       const float* lambda, void* o, void* cache, void* workspace, void* stream) {
+  if (!c) return fail(LASP_ERR_SHAPE, "ctx is NULL");
+  Plan p;
+  lasp_status_t s = prologue(shape, lambda, p);
+  if (s != LASP_OK) return s;
+  if ((s = check_ptrs(p, {q, k, v, o}, cache, workspace)) != LASP_OK) return s;
+  if ((s = check_device()) != LASP_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Workspace w = carve(p, workspace);
+  const size_t n = state_elems(p);
+  NcclApi& nc = nccl();
+  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st));                     // F1
+  LASP_CUDA(launch_prefix(p, Dir::FWD, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
+  // F2 ring hop: Recv KV_in from r-1 (Alg. 2), combine, Send to r+1
+  if (c->rank > 0) {
+    ncclResult_t r = nc.Recv(w.in, n, ncclFloat32, c->rank - 1, c->comm, st);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclRecv(KV)", c->rank, c->rank - 1);
+  } else {
+    LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), st));
+  }
+  if (c->rank < c->world - 1) {
+    LASP_CUDA(launch_combine(p, w.in, w.local, w.out, st));
+    ncclResult_t r = nc.Send(w.out, n, ncclFloat32, c->rank + 1, c->comm, st);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclSend(KV)", c->rank, c->rank + 1);
+  }
+  if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, st)) != LASP_OK) return s;  // F2 + F3
+  register_cache(p, cache, c->rank, c->world);
+  return LASP_OK;
+}
+
+lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, const void* k, const void* v,
+                       const float* lambda, const void* d_o, const void* cache, void* dq, void* dk, void* dv,
+                       void* workspace, void* stream) {
+  if (!c) return fail(LASP_ERR_SHAPE, "ctx is NULL");
+  Plan p;
+  lasp_status_t s = prologue(shape, lambda, p);
+  if (s != LASP_OK) return s;
+  if ((s = check_ptrs(p, {q, k, v, d_o, dq, dk, dv}, cache, workspace)) != LASP_OK) return s;
+  if ((s = check_cache(p, cache, c->rank, c->world, true)) != LASP_OK) return s;
+  if ((s = check_device()) != LASP_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Workspace w = carve(p, workspace);
+  const size_t n = state_elems(p);
+  NcclApi& nc = nccl();
+  const float* P = static_cast<const float*>(cache);
+  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st));                    // B1
+  LASP_CUDA(launch_prefix(p, Dir::REV, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
+  // B2 ring hop on the comm stream: Recv dKV_in from r+1 (Alg. 3), combine, Send to r-1
+  LASP_CUDA(cudaEventRecord(c->ev_ready, st));
+  LASP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+  if (c->rank < c->world - 1) {
+    ncclResult_t r = nc.Recv(w.in, n, ncclFloat32, c->rank + 1, c->comm, c->comm_stream);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclRecv(dKV)", c->rank, c->rank + 1);
+  } else {
+    LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), c->comm_stream));
+  }
+  if (c->rank > 0) {
+    LASP_CUDA(launch_combine(p, w.in, w.local, w.out, c->comm_stream));
+    ncclResult_t r = nc.Send(w.out, n, ncclFloat32, c->rank - 1, c->comm, c->comm_stream);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclSend(dKV)", c->rank, c->rank - 1);
+  }
+  LASP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
+  // dQ needs only the cache: it runs while the dKV hop is in flight
+  if (p.C > 0) LASP_CUDA(core(p, Dir::FWD, d_o, v, k, dq, P, 1, st));
+  LASP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
+  if (p.C == 0) return LASP_OK;
+  LASP_CUDA(launch_prefix(p, Dir::REV, w.in, w.seg, w.seg, nullptr, st));               // B2
+  LASP_CUDA(core(p, Dir::REV, k, q, d_o, dv, w.seg, 0, st));                            // dV
+  LASP_CUDA(core(p, Dir::REV, v, d_o, q, dk, w.seg, 1, st));                            // dK
+  return LASP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+// lasp_common.cuh -- shared definitions of the LASP CUDA path (plan, launch interfaces).
+//
+// Notation (0-based, one (batch, head)):
+//   C = n_local tokens of this rank, split into segments of Lseg tokens; segments are split into
+//   GPU blocks of BT tokens. Every level applies the same LASP identity (Eq. 12):
+//     FWD direction (O, dQ):   out_i = sum_{j<=i} lam^(i-j) (a_i.b_j) c_j + lam^(i+1) a_i^T S
+//                              S'    = lam^BT S + sum_s lam^(BT-1-s) b_s c_s^T
+//     REV direction (dK, dV):  out_i = sum_{j>=i} lam^(j-i) (a_i.b_j) c_j + lam^(BT-1-i) a_i^T S
+//                              S'    = lam^BT S + sum_s lam^(s+1) b_s c_s^T
+//   with (a,b,c,S) = (Q,K,V,KV) for O, (dO,V,K,KV^T) for dQ, (K,Q,dO,dKV) for dV and
+//   (V,dO,Q,dKV^T) for dK (Eq. 4 and Eq. 13 rewritten; the REV state has exponent starting at 1,
+//   reading A3). FWD segments are aligned to the rank start, REV segments to the rank end, so a
+//   ragged block only ever sits where no state leaves it.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace lasp {
+
+enum class Dir : int { FWD = 0, REV = 1 };
+
+struct Plan {
+  int64_t B, C, H, D;  // batch, n_local, heads, head_dim
+  int dtype;           // 0 = bf16, 1 = fp32
+  int64_t seg_len;     // multiple of kSegQuantum
+  int64_t nseg;        // >= 1
+  float lam[256];      // per-head decay (fp32, the boundary's precision; reading A8), by value
+};
+constexpr int64_t kMaxHeads = 256;
+
+constexpr int64_t kSegQuantum = 128;  // every kernel's block size divides this
+
+// Segment p geometry. FWD: [p*L, min((p+1)*L, C)). REV (end-aligned): [max(0, C-(p+1)L), C-p*L).
+__host__ __device__ inline int64_t seg_begin(Dir dir, int64_t p, int64_t L, int64_t C) {
+  if (dir == Dir::FWD) return p * L;
+  int64_t b = C - (p + 1) * L;
+  return b < 0 ? 0 : b;
+}
+__host__ __device__ inline int64_t seg_end(Dir dir, int64_t p, int64_t L, int64_t C) {
+  if (dir == Dir::FWD) { int64_t e = (p + 1) * L; return e > C ? C : e; }
+  return C - p * L;
+}
+
+// Kernel launch interfaces (kernels_simt.cu, kernels_tc.cu). All return cudaGetLastError().
+// Sequence tensors are [B][C][H][D]; state arrays are [B][H][nseg][D][D] fp32.
+struct SeqArgs {
+  const void* a; const void* b; const void* c;  // core: out rows from a, keys b, values c
+  void* out;
+  const float* state;     // device [B][H][nseg][D][D] (state entering each segment)
+  int trans_state;        // use S^T of the stored state
+};
+
+cudaError_t launch_seg_state_simt(const Plan& p, Dir dir, const void* x, const void* y,
+                                  float* out, cudaStream_t st);
+cudaError_t launch_prefix(const Plan& p, Dir dir, const float* init, const float* seg_states,
+                          float* prefix_out, float* final_out, cudaStream_t st);
+cudaError_t launch_core_simt(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st);
+cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local, float* kv_out,
+                           cudaStream_t st);
+
+// tcgen05 path (bf16 only); returns cudaErrorNotSupported when the shape is not covered.
+bool tc_supported(const Plan& p);
+cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out,
+                                cudaStream_t st);
+cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st);
+
+}  // namespace lasp
