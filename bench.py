@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""bench.py -- LASP forward+backward tokens/s per layer on B200 (BASELINE.json metric).
+
+One step = one pass of the whole hot path over one batch: lasp forward (F1 seg states, F2 prefix /
+ring hop, F3 fused intra+inter core) and lasp backward (B3 dQ core, B1 seg states, B2 prefix / ring
+hop, B3 dV and dK cores) for one attention layer, inputs resident in HBM.
+
+Workload (N=1: BASELINE configs[1], the TNL-0.4B layer): 16 heads x 64, batch 1, 32K tokens per GPU,
+bf16, per-head lambda_h = 1 - 2^-(1 + 14h/15). N>1 keeps 32K tokens per GPU (weak scaling) and runs the
+NCCL KV/dKV ring (one process per GPU, launched by torchrun). Synthetic inputs from synth/ (seeded).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lasp|reference] [--config tnl04b|tnl1b|tnl7b]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (heads, head_dim, tokens per GPU, description)
+    "tnl04b": (16, 64, 32768, "TNL-0.4B layer (BASELINE configs[1]): 16 heads x 64, batch 1, 32K tokens/GPU"),
+    "tnl1b": (16, 128, 32768, "TNL-1B layer (BASELINE configs[2] per-GPU shard): 16 heads x 128, 32K tokens/GPU"),
+    "tnl7b": (32, 128, 131072, "TNL-7B layer (BASELINE configs[3] per-GPU shard): 32 heads x 128, 128K tokens/GPU"),
+}
+METRIC = "LASP fwd+bwd tokens/sec per layer"
+FLOP_BLOCK = 64  # algorithmic flops fixed at b = 64
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", 0)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def alg_flops_per_token_head(D):
+    return 7 * (FLOP_BLOCK + 1) * D + 12 * D * D
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            names = {
+                "hw_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+                "sw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                "hw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                "sw_power_cap": getattr(pynvml, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                        for n, bit in names.items():
+                            if r & bit:
+                                self.reasons.add(n)
+                    except Exception:
+                        pass
+                    self._stop.wait(0.02)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception as e:  # NVML unavailable: report it instead of inventing clocks
+            self.reasons.add(f"nvml_unavailable:{type(e).__name__}")
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------------------------------
+def run_reference(args):
+    """The oracle as it stands (fp64 C, host cores) on a bounded token sample of the same workload."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+    import synth
+    H, D, C, desc = CONFIGS[args.config]
+    oracle.build()
+    threads = os.cpu_count() or 1
+    cores = min(threads, H)  # one work item per (batch, head)
+
+    def step(p):
+        oracle.fwd(p["q"], p["k"], p["v"], p["lam"], nthreads=threads)
+        oracle.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"], nthreads=threads)
+
+    cal = synth.problem(0, 1, 256, H, D, dtype="bf16", token_hi=256)
+    t = time.perf_counter()
+    step(cal)
+    per_tok = (time.perf_counter() - t) / 256
+    budget = float(os.environ.get("LASP_REF_BUDGET_S", "90"))
+    S = int(max(128, min(C, budget / max(1, args.steps + args.warmup) / max(per_tok, 1e-9))))
+    p = synth.problem(0, 1, C * world, H, D, dtype="bf16", token_lo=0, token_hi=S)
+    for _ in range(args.warmup):
+        step(p)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(p)
+    el = time.perf_counter() - t0
+    value = S * args.steps / el
+    sample = f"first {S} tokens of the {desc} sequence, fwd+bwd, fp64 oracle, {args.steps} steps"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (synth/, seed 0)",
+            "config": {"workload": desc, "global_batch": 1, "seq_len": C * world, "n_local": C, "heads": H,
+                       "head_dim": D, "parallelism": f"sp{world}"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(H, D, C, desc):
+    import oracle
+    import synth
+    oracle.build()
+    threads = os.cpu_count() or 1
+    p = synth.problem(0, 1, C, H, D, dtype="bf16")
+    reps, el = 0, 0.0
+    t0 = time.perf_counter()
+    while reps < 3 and (el < 10.0 or reps == 0):
+        oracle.fwd(p["q"], p["k"], p["v"], p["lam"], nthreads=threads)
+        oracle.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"], nthreads=threads)
+        reps += 1
+        el = time.perf_counter() - t0
+    return {"value": C * reps / el, "unit": "tokens/s", "cores": min(threads, H), "kind": "oracle",
+            "sample": f"full {desc} layer, fwd+bwd in fp64, {reps} rep(s), {el:.1f} s on {min(threads, H)} threads"}
+
+
+# ----------------------------------------------------------------------------------------------------
+def run_lasp(args):
+    import ctypes
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2404_02882_b200 as lasp
+    from paper_2404_02882_b200 import _native as N
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    H, D, C, desc = CONFIGS[args.config]
+    B = 1
+    lib = N.lib()
+
+    # inputs: this rank's shard [r*C, (r+1)*C) of the global sequence
+    p = synth.problem(0, B, C * world, H, D, dtype="bf16", token_lo=rank * C, token_hi=(rank + 1) * C)
+    lam = p["lam"]
+    host = {k: torch.from_numpy(p[k]) for k in ("q", "k", "v", "do")}
+    d_in = {k: v.to(dev, torch.bfloat16) for k, v in host.items()}
+    q, k, v, do = d_in["q"], d_in["k"], d_in["v"], d_in["do"]
+    o, dq, dk, dv = (torch.empty_like(q) for _ in range(4))
+    cache, ws = lasp.alloc_cache(q), lasp.alloc_workspace(q)
+    ring = lasp.Ring(dev) if world > 1 else None
+
+    def step():
+        if ring is None:
+            lasp.fwd_local(q, k, v, lam, o=o, kv_out=False, cache=cache, workspace=ws)
+            lasp.bwd_local(q, k, v, lam, do, cache, dq=dq, dk=dk, dv=dv, dkv_out=False, workspace=ws)
+        else:
+            ring.fwd(q, k, v, lam, o=o, cache=cache, workspace=ws)
+            ring.bwd(q, k, v, lam, do, cache, dq=dq, dk=dk, dv=dv, workspace=ws)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = lib.lasp_launch_count()
+    lib.lasp_profile_enable(1)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()                       # L2 flushed between timed steps (outside the events)
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    lib.lasp_profile_enable(0)
+    launches = lib.lasp_launch_count() - launches0
+    buf = ctypes.create_string_buffer(1 << 16)
+    lib.lasp_profile_read(buf, len(buf))
+    stages = json.loads(buf.value.decode() or "{}")
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    value = world * B * C * args.steps / (total_ms / 1e3)
+
+    # e2e through the public API with pinned host buffers: H2D inputs + fwd + bwd + D2H outputs
+    e2e = None
+    if not args.no_e2e:
+        pin = {kk: vv.to(torch.bfloat16).pin_memory() for kk, vv in host.items()}
+        outs_h = [torch.empty(q.shape, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
+        n_e2e = max(3, min(args.steps, 20))
+        h2d = sum(int(x.numel()) * 2 for x in pin.values())
+        d2h = sum(int(x.numel()) * 2 for x in outs_h)
+
+        def e2e_step():
+            for kk in ("q", "k", "v", "do"):
+                d_in[kk].copy_(pin[kk], non_blocking=True)
+            step()
+            for hbuf, dbuf in zip(outs_h, (o, dq, dk, dv)):
+                hbuf.copy_(dbuf, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * B * C * n_e2e / (float(et.item()) / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e}
+
+    # roofline of the dominant kernel, from the live per-stage CUDA events
+    hbm, tflops, tflops_sus, peak_src = peaks()
+    dom_name, (dom_n, dom_ms) = max(stages.items(), key=lambda kv: kv[1][1]) if stages else ("none", (1, 0.0))
+    per_launch_ms = dom_ms / max(dom_n, 1)
+    if dom_name.startswith("core"):
+        bytes_per_launch = 4 * 2 * D * B * C * H          # reads a, b, c and writes out (bf16): 8D B/token-head
+        unit_note = "8*D bytes per token-head (3 bf16 reads + 1 bf16 write)"
+    elif dom_name.startswith("seg_state"):
+        bytes_per_launch = 2 * 2 * D * B * C * H          # reads two bf16 tensors: 4D B/token-head
+        unit_note = "4*D bytes per token-head (2 bf16 reads)"
+    else:
+        bytes_per_launch = 0
+        unit_note = "n/a"
+    achieved = bytes_per_launch / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{args.config}:{dom_name}")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic, "kernel": dom_name, "launches_per_step": dom_n / args.steps,
+                "bytes_per_launch": bytes_per_launch, "bytes_rule": unit_note, "peak_source": peak_src}
+    path_bytes = 22 * D * B * C * H
+    path = {"bytes_per_step": path_bytes, "achieved_gbs": path_bytes / (ms_step / 1e3) / 1e9,
+            "frac_of_hbm": path_bytes / (ms_step / 1e3) / 1e9 / hbm,
+            "tc_peak_frac": B * C * H * alg_flops_per_token_head(D) / (ms_step / 1e3) / (tflops * 1e12),
+            "stages_ms_per_step": {kk: vv[1] / args.steps for kk, vv in stages.items()}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(H, D, C, desc)
+
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (synth/, seed 0; bf16 inputs)",
+            "config": {"workload": desc, "global_batch": B, "seq_len": C * world, "n_local": C, "heads": H,
+                       "head_dim": D, "lambda": "per-head 1-2^-(1+14h/(H-1))",
+                       "segment_len": lasp.segment_len(N.shape(B, C, H, D, N.LASP_BF16)),
+                       "l2": "flushed between timed steps (256 MiB write outside the step events); inputs 4x"
+                             f" {B * C * H * D * 2 >> 20} MiB", "parallelism": f"sp{world}"},
+            "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e, "roofline": roofline,
+            "path": path, "cpu_baseline": cpu}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ring is not None:
+        ring.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["lasp", "reference"], default="lasp")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="tnl04b")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_lasp(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

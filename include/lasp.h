@@ -93,6 +93,16 @@ const char* lasp_last_error(void);
 /* Library version string and whether the tcgen05 (sm_100a) path is compiled in. */
 const char* lasp_version(void);
 
+/* Number of CUDA kernels this library has launched since it was loaded (all entry points). */
+uint64_t lasp_launch_count(void);
+
+/* Measurement hooks (bench.py): when enabled, every kernel launch is bracketed by CUDA events
+ * recorded on the launching stream. lasp_profile_read synchronizes on them, writes a JSON object
+ * {"stage": [launches, total_ms], ...} into buf (NUL-terminated, truncated to cap) and clears the
+ * records; returns the JSON length, or -1 if an event could not be read. */
+void lasp_profile_enable(int on);
+int lasp_profile_read(char* buf, size_t cap);
+
 /* Bytes of the caller-owned per-layer KV cache for `shape` (fp32 segment states: the state entering
  * the rank, KV_in(r), and the states entering each in-rank segment). 256-byte aligned base required. */
 size_t lasp_cache_bytes(const lasp_shape_t* shape);

@@ -39,6 +39,9 @@ _SIGS = {
     "lasp_last_error": ([], ctypes.c_char_p),
     "lasp_version": ([], ctypes.c_char_p),
     "lasp_cache_bytes": ([_sp], ctypes.c_size_t),
+    "lasp_launch_count": ([], ctypes.c_uint64),
+    "lasp_profile_enable": ([ctypes.c_int], None),
+    "lasp_profile_read": ([ctypes.c_char_p, ctypes.c_size_t], ctypes.c_int),
     "lasp_workspace_bytes": ([_sp], ctypes.c_size_t),
     "lasp_segment_len": ([_sp], ctypes.c_int64),
     "lasp_fwd_local": ([_sp, _vp, _vp, _vp, _fp, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),

@@ -21,6 +21,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 using namespace lasp;
 
@@ -194,17 +195,66 @@ lasp_status_t check_cache(const Plan& p, const void* cache, int rank, int world,
   return LASP_OK;
 }
 
+// ---- launch accounting and optional per-stage CUDA-event profiling -----------------------------
+std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_profile{0};
+struct ProfRec { const char* name; cudaEvent_t a, b; };
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof_recs;
+std::vector<cudaEvent_t> g_prof_pool;
+
+cudaEvent_t prof_event() {
+  cudaEvent_t e = nullptr;
+  if (!g_prof_pool.empty()) { e = g_prof_pool.back(); g_prof_pool.pop_back(); return e; }
+  cudaEventCreate(&e);
+  return e;
+}
+
+template <class F>
+cudaError_t staged(const char* name, cudaStream_t st, F&& launch) {
+  ProfRec rec{name, nullptr, nullptr};
+  const bool prof = g_profile.load(std::memory_order_relaxed) != 0;
+  if (prof) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    rec.a = prof_event();
+    rec.b = prof_event();
+  }
+  if (prof) cudaEventRecord(rec.a, st);
+  cudaError_t e = launch();
+  if (prof) {
+    cudaEventRecord(rec.b, st);
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_prof_recs.push_back(rec);
+  }
+  if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
+  return e;
+}
+
 // ---- stage dispatch: tcgen05 for covered bf16 shapes, CUDA cores otherwise ---------------------
 cudaError_t seg_state(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st) {
-  if (tc_supported(p)) return launch_seg_state_tc(p, dir, x, y, out, st);
-  return launch_seg_state_simt(p, dir, x, y, out, st);
+  const bool tc = tc_supported(p);
+  return staged(dir == Dir::FWD ? (tc ? "seg_state_fwd_tc" : "seg_state_fwd_simt")
+                                : (tc ? "seg_state_rev_tc" : "seg_state_rev_simt"), st, [&] {
+    return tc ? launch_seg_state_tc(p, dir, x, y, out, st) : launch_seg_state_simt(p, dir, x, y, out, st);
+  });
 }
 
 cudaError_t core(const Plan& p, Dir dir, const void* a, const void* b, const void* c, void* out,
                  const float* state, int trans, cudaStream_t st) {
   SeqArgs args{a, b, c, out, state, trans};
-  if (tc_supported(p)) return launch_core_tc(p, dir, args, st);
-  return launch_core_simt(p, dir, args, st);
+  const bool tc = tc_supported(p);
+  return staged(dir == Dir::FWD ? (tc ? "core_fwd_tc" : "core_fwd_simt") : (tc ? "core_rev_tc" : "core_rev_simt"),
+                st, [&] { return tc ? launch_core_tc(p, dir, args, st) : launch_core_simt(p, dir, args, st); });
+}
+
+cudaError_t prefix(const Plan& p, Dir dir, const float* init, const float* seg, float* out, float* fin,
+                   cudaStream_t st) {
+  return staged(dir == Dir::FWD ? "prefix_fwd" : "prefix_rev", st,
+                [&] { return launch_prefix(p, dir, init, seg, out, fin, st); });
+}
+
+cudaError_t combine(const Plan& p, const float* in, const float* local, float* out, cudaStream_t st) {
+  return staged("combine", st, [&] { return launch_combine(p, in, local, out, st); });
 }
 
 // ---- common prologue -------------------------------------------------------------------------
@@ -220,10 +270,10 @@ lasp_status_t fwd_tail(const Plan& p, const void* q, const void* k, const void* 
                        void* o, float* kv_out, void* cache, float* seg, cudaStream_t st) {
   float* P = static_cast<float*>(cache);
   if (p.C == 0) {
-    LASP_CUDA(launch_prefix(p, Dir::FWD, kv_in, nullptr, P, kv_out, st));
+    LASP_CUDA(prefix(p, Dir::FWD, kv_in, nullptr, P, kv_out, st));
     return LASP_OK;
   }
-  LASP_CUDA(launch_prefix(p, Dir::FWD, kv_in, seg, P, kv_out, st));
+  LASP_CUDA(prefix(p, Dir::FWD, kv_in, seg, P, kv_out, st));
   LASP_CUDA(core(p, Dir::FWD, q, k, v, o, P, 0, st));
   return LASP_OK;
 }
@@ -283,6 +333,39 @@ extern "C" {
 
 const char* lasp_last_error(void) { return g_err.c_str(); }
 
+uint64_t lasp_launch_count(void) { return g_launches.load(); }
+
+void lasp_profile_enable(int on) { g_profile.store(on ? 1 : 0); }
+
+int lasp_profile_read(char* buf, size_t cap) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  struct Acc { int64_t n = 0; double ms = 0; };
+  std::vector<std::pair<std::string, Acc>> acc;
+  int rc = 0;
+  for (ProfRec& r : g_prof_recs) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) rc = -1;
+    auto it = acc.begin();
+    for (; it != acc.end(); ++it) if (it->first == r.name) break;
+    if (it == acc.end()) { acc.emplace_back(r.name, Acc{}); it = acc.end() - 1; }
+    it->second.n += 1;
+    it->second.ms += ms;
+    g_prof_pool.push_back(r.a);
+    g_prof_pool.push_back(r.b);
+  }
+  g_prof_recs.clear();
+  std::string js = "{";
+  for (size_t i = 0; i < acc.size(); ++i) {
+    char item[160];
+    std::snprintf(item, sizeof item, "%s\"%s\": [%lld, %.6f]", i ? ", " : "", acc[i].first.c_str(),
+                  (long long)acc[i].second.n, acc[i].second.ms);
+    js += item;
+  }
+  js += "}";
+  if (buf && cap) { std::strncpy(buf, js.c_str(), cap - 1); buf[cap - 1] = 0; }
+  return rc != 0 ? rc : (int)js.size();
+}
+
 const char* lasp_version(void) { return "lasp-b200 0.1 (sm_100a; tcgen05 + CUDA-core paths)"; }
 
 size_t lasp_cache_bytes(const lasp_shape_t* shape) {
@@ -330,12 +413,12 @@ lasp_status_t lasp_bwd_local(const lasp_shape_t* shape, const void* q, const voi
   Workspace w = carve(p, workspace);
   const float* P = static_cast<const float*>(cache);
   if (p.C == 0) {
-    LASP_CUDA(launch_prefix(p, Dir::REV, dkv_in, nullptr, nullptr, dkv_out, st));
+    LASP_CUDA(prefix(p, Dir::REV, dkv_in, nullptr, nullptr, dkv_out, st));
     return LASP_OK;
   }
   LASP_CUDA(core(p, Dir::FWD, d_o, v, k, dq, P, 1, st));                     // dQ (cache only)
   LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st));                      // B1
-  LASP_CUDA(launch_prefix(p, Dir::REV, dkv_in, w.seg, w.seg, dkv_out, st));  // B2 (in place)
+  LASP_CUDA(prefix(p, Dir::REV, dkv_in, w.seg, w.seg, dkv_out, st));  // B2 (in place)
   LASP_CUDA(core(p, Dir::REV, k, q, d_o, dv, w.seg, 0, st));                 // dV
   LASP_CUDA(core(p, Dir::REV, v, d_o, q, dk, w.seg, 1, st));                 // dK
   return LASP_OK;
@@ -407,7 +490,7 @@ lasp_status_t lasp_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   const size_t n = state_elems(p);
   NcclApi& nc = nccl();
   if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st));                     // F1
-  LASP_CUDA(launch_prefix(p, Dir::FWD, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
+  LASP_CUDA(prefix(p, Dir::FWD, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
   // F2 ring hop: Recv KV_in from r-1 (Alg. 2), combine, Send to r+1
   if (c->rank > 0) {
     ncclResult_t r = nc.Recv(w.in, n, ncclFloat32, c->rank - 1, c->comm, st);
@@ -416,7 +499,7 @@ lasp_status_t lasp_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
     LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), st));
   }
   if (c->rank < c->world - 1) {
-    LASP_CUDA(launch_combine(p, w.in, w.local, w.out, st));
+    LASP_CUDA(combine(p, w.in, w.local, w.out, st));
     ncclResult_t r = nc.Send(w.out, n, ncclFloat32, c->rank + 1, c->comm, st);
     if (r != ncclSuccess) return nccl_fail(r, "ncclSend(KV)", c->rank, c->rank + 1);
   }
@@ -441,7 +524,7 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   NcclApi& nc = nccl();
   const float* P = static_cast<const float*>(cache);
   if (p.C > 0) LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st));                    // B1
-  LASP_CUDA(launch_prefix(p, Dir::REV, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
+  LASP_CUDA(prefix(p, Dir::REV, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
   // B2 ring hop on the comm stream: Recv dKV_in from r+1 (Alg. 3), combine, Send to r-1
   LASP_CUDA(cudaEventRecord(c->ev_ready, st));
   LASP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
@@ -452,7 +535,7 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
     LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), c->comm_stream));
   }
   if (c->rank > 0) {
-    LASP_CUDA(launch_combine(p, w.in, w.local, w.out, c->comm_stream));
+    LASP_CUDA(combine(p, w.in, w.local, w.out, c->comm_stream));
     ncclResult_t r = nc.Send(w.out, n, ncclFloat32, c->rank - 1, c->comm, c->comm_stream);
     if (r != ncclSuccess) return nccl_fail(r, "ncclSend(dKV)", c->rank, c->rank - 1);
   }
@@ -461,7 +544,7 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   if (p.C > 0) LASP_CUDA(core(p, Dir::FWD, d_o, v, k, dq, P, 1, st));
   LASP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
   if (p.C == 0) return LASP_OK;
-  LASP_CUDA(launch_prefix(p, Dir::REV, w.in, w.seg, w.seg, nullptr, st));               // B2
+  LASP_CUDA(prefix(p, Dir::REV, w.in, w.seg, w.seg, nullptr, st));               // B2
   LASP_CUDA(core(p, Dir::REV, k, q, d_o, dv, w.seg, 0, st));                            // dV
   LASP_CUDA(core(p, Dir::REV, v, d_o, q, dk, w.seg, 1, st));                            // dK
   return LASP_OK;
