@@ -1,13 +1,619 @@
-// kernels_tc.cu -- tcgen05 / TMEM / TMA kernels (sm_100a) of the LASP path (bf16).
+// kernels_tc.cu -- tcgen05 / TMEM / TMA kernels (sm_100a) of the LASP path, bf16 in / fp32 accumulate.
+//
+// Two kernels (see lasp_common.cuh for the FWD/REV formulas):
+//
+//  seg_state_tc  (F1 / B1): L = sum_pos w_pos x_pos y_pos^T over one segment. Per 128-token block:
+//                TMA loads X, Y tiles -> 4 scaler warps multiply X rows by w in place -> one thread
+//                issues UMMA (M = N = D, K = 128, both operands MN-major) accumulating in TMEM.
+//                Eq. 12 for the forward, Eq. 21 for the backward.
+//
+//  core_tc       (F3 / B3): per segment, blocks of 128 tokens in direction order, with warp roles
+//                  warp 0       TMA producer (a, b, c tiles; 2-stage ring)
+//                  warp 1       UMMA issuer:  S = a b^T            (M=128, N=128, K=D)   [Eq. 7]
+//                                             dS = (u.b)^T c        (M=D,   N=D,   K=128) [Eq. 12]
+//                                             O_intra = P c         (M=128, N=D,   K=128) [Eq. 7]
+//                                             O_inter = a S_j       (M=128, N=D,   K=D)   [Eq. 9]
+//                  warps 4-7    mask: S (TMEM) -> (.) M_lambda -> bf16 P (smem, 128B-swizzled)
+//                  warps 8-11   state: u.b (smem), S_{j+1} = lambda^128 S_j + dS in fp32 registers,
+//                               bf16 copy of S_{j+1} for the next block's inter MMA
+//                  warps 12-15  epilogue: out = O_intra + r (.) O_inter -> bf16 -> TMA store
+//                The running state is the paper's KV (dKV) state applied between GPU blocks; the
+//                segment's initial state comes from the prefix kernel (KV_in of the ring included).
 #include "lasp_common.cuh"
+#include "sm100.cuh"
+
+#include <cudaTypedefs.h>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
 
 namespace lasp {
+using namespace sm100;
 
-bool tc_supported(const Plan&) { return false; }
+namespace {
 
-cudaError_t launch_seg_state_tc(const Plan&, Dir, const void*, const void*, float*, cudaStream_t) {
+constexpr int BT = 128;                 // tokens per block (UMMA M of the query side)
+constexpr uint32_t BOX = BT * 128;      // one [128 rows][64 bf16] 128B-swizzled box = 16 KB
+
+// ------------------------------------------------------------------------------------------------
+// host: TMA tensor maps over the [B][C][H][D] bf16 layout (4-D: D, H, C, B), box [64][1][128][1]
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+thread_local char g_tc_err[256];
+
+cudaError_t make_seq_map(CUtensorMap* m, const void* base, const Plan& p) {
+  auto fn = encode_fn();
+  if (!fn) {
+    snprintf(g_tc_err, sizeof g_tc_err, "cuTensorMapEncodeTiled entry point unavailable");
+    return cudaErrorNotSupported;
+  }
+  cuuint64_t dims[4] = {cuuint64_t(p.D), cuuint64_t(p.H), cuuint64_t(p.C), cuuint64_t(p.B)};
+  cuuint64_t strides[3] = {cuuint64_t(p.D * 2), cuuint64_t(p.H * p.D * 2), cuuint64_t(p.C * p.H * p.D * 2)};
+  cuuint32_t box[4] = {64, 1, BT, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(g_tc_err, sizeof g_tc_err, "cuTensorMapEncodeTiled failed (CUresult %d) for ptr=%p dims=[%lld,%lld,%lld,%lld]",
+             int(r), base, (long long)p.D, (long long)p.H, (long long)p.C, (long long)p.B);
+    return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
+}
+
+__device__ __forceinline__ float powk(float lam, double k) { return (float)pow((double)lam, k); }
+
+// scale the 8 bf16 of a 16-byte chunk by w
+__device__ __forceinline__ uint4 scale_chunk(uint4 v, float w) {
+  uint32_t* u = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float lo = __uint_as_float(u[i] << 16) * w;
+    const float hi = __uint_as_float(u[i] & 0xFFFF0000u) * w;
+    u[i] = pack_bf16(lo, hi);
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint64_t desc_k(uint32_t addr) { return smem_desc(addr, 16, 1024); }
+__device__ __forceinline__ uint64_t desc_mn(uint32_t addr, uint32_t lbo) { return smem_desc(addr, lbo, 1024); }
+
+// ================================================================================================
+// seg_state_tc
+// ================================================================================================
+template <int D>
+struct SegLayout {
+  static constexpr int NBOX = D / 64;
+  static constexpr uint32_t TILE = NBOX * BOX;
+  static constexpr int STAGES = D == 64 ? 3 : 2;
+  static constexpr uint32_t X(int s) { return uint32_t(s) * 2 * TILE; }
+  static constexpr uint32_t Y(int s) { return uint32_t(s) * 2 * TILE + TILE; }
+  static constexpr uint32_t BARS = STAGES * 2 * TILE;
+  static constexpr uint32_t BYTES = BARS + 256 + 1024;  // barriers + tmem slot + alignment slack
+};
+
+struct SegParams {
+  CUtensorMap mx, my;
+  Plan p;
+  float* out;
+};
+
+template <int D, Dir DIR>
+__global__ void __launch_bounds__(192, 1) seg_state_tc_kernel(const __grid_constant__ SegParams prm) {
+  using L = SegLayout<D>;
+  constexpr int ST = L::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::BARS);
+  uint64_t* scaled = full + ST;
+  uint64_t* empty = scaled + ST;
+  uint64_t* done = empty + ST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const uint32_t sbase = smem_u32(sm);
+
+  const Plan& p = prm.p;
+  const int64_t seg = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int64_t beg = seg_begin(DIR, seg, p.seg_len, p.C), end = seg_end(DIR, seg, p.seg_len, p.C);
+  const int nblk = int((end - beg + BT - 1) / BT);
+  const float lam = p.lam[h];
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&prm.mx);
+    tma_prefetch(&prm.my);
+    for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&scaled[s], 128); mbar_init(&empty[s], 1); }
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<(D < 64 ? 64 : D)>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto row0 = [&](int j) -> int64_t { return DIR == Dir::FWD ? beg + int64_t(j) * BT : end - int64_t(j + 1) * BT; };
+
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % ST;
+        mbar_wait(&empty[s], ((j / ST) & 1) ^ 1);
+        mbar_expect_tx(&full[s], 2 * L::TILE);
+        const int t0 = int(row0(j));
+#pragma unroll
+        for (int x = 0; x < L::NBOX; ++x) {
+          tma_load_4d(sm + L::X(s) + x * BOX, &prm.mx, &full[s], x * 64, int(h), t0, int(b));
+          tma_load_4d(sm + L::Y(s) + x * BOX, &prm.my, &full[s], x * 64, int(h), t0, int(b));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_bf16(D, D, 1, 1);
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % ST;
+        mbar_wait(&scaled[s], (j / ST) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BT / 16; ++kk)
+          mma_bf16(tmem, desc_mn(sbase + L::X(s) + kk * 2048, BOX), desc_mn(sbase + L::Y(s) + kk * 2048, BOX), idesc,
+                   (j | kk) != 0);
+        mma_commit(&empty[s]);
+      }
+      mma_commit(done);
+    }
+  } else {
+    // warps 2..5: scale X rows by the decay weight, then drain the accumulator
+    const int g = int(threadIdx.x) - 64;  // row of the tile
+    for (int j = 0; j < nblk; ++j) {
+      const int s = j % ST;
+      mbar_wait(&full[s], (j / ST) & 1);
+      const int64_t pos = row0(j) + g;
+      float w = 0.f;
+      if (pos >= beg && pos < end) w = powk(lam, DIR == Dir::FWD ? double(end - 1 - pos) : double(pos - beg + 1));
+#pragma unroll
+      for (int x = 0; x < L::NBOX; ++x)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t a = sbase + L::X(s) + x * BOX + uint32_t(g) * 128 + c * 16;
+          sts128(a, scale_chunk(lds128(a), w));
+        }
+      fence_async_smem();
+      mbar_arrive(&scaled[s]);
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const uint32_t q4 = warp & 3;
+    const bool valid = D == 128 || lane < 16;
+    const int row = D == 128 ? int(q4 * 32 + lane) : int(q4 * 16 + lane);
+    float* o = prm.out + ((b * p.H + h) * p.nseg + seg) * D * D + int64_t(row) * D;
+#pragma unroll
+    for (int c = 0; c < D / 16; ++c) {
+      float v[16];
+      tmem_ld16(tmem + ((q4 * 32) << 16) + c * 16, v);
+      tmem_ld_wait();
+      if (valid) {
+#pragma unroll
+        for (int u = 0; u < 16; u += 4) *reinterpret_cast<float4*>(o + c * 16 + u) = make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<(D < 64 ? 64 : D)>(tmem);
+}
+
+// ================================================================================================
+// core_tc
+// ================================================================================================
+template <int D>
+struct CoreLayout {
+  static constexpr int NBOX = D / 64;
+  static constexpr uint32_t TILE = NBOX * BOX;           // one [128][D] bf16 tile
+  static constexpr int STAGES = 2;
+  static constexpr uint32_t A(int s) { return uint32_t(s) * 3 * TILE; }
+  static constexpr uint32_t B_(int s) { return uint32_t(s) * 3 * TILE + TILE; }
+  static constexpr uint32_t C_(int s) { return uint32_t(s) * 3 * TILE + 2 * TILE; }
+  static constexpr uint32_t KU = STAGES * 3 * TILE;
+  static constexpr uint32_t P = KU + TILE;               // [128][128] bf16, 2 K-atoms of 16 KB
+  static constexpr uint32_t SBF = P + 2 * BOX;           // [D][D] bf16 hi part, NBOX MN-blocks of D*128 B
+  static constexpr uint32_t SLO = SBF + D * D * 2;       // [D][D] bf16 lo part (S - hi)
+  static constexpr uint32_t OST = SLO + D * D * 2;       // 2 x [128][D] bf16 output staging
+  static constexpr uint32_t PW = OST + 2 * TILE;         // float[BT + 1]
+  static constexpr uint32_t BARS = PW + 1024;
+  static constexpr uint32_t BYTES = BARS + 256 + 1024;
+  // TMEM columns
+  static constexpr uint32_t T_S0 = 0, T_S1 = 128, T_OI = 256, T_OX = 256 + D, T_DS = 256 + 2 * D;
+};
+
+struct CoreParams {
+  CUtensorMap ma, mb, mc, mo;
+  Plan p;
+  __nv_bfloat16* out;
+  const float* state;
+  int trans;
+};
+
+struct CoreBars {
+  uint64_t full[2], empty[2], s_full[2], s_empty[2];
+  uint64_t p_full, p_empty, ku_full, ds_full, ds_empty, st_full, st_empty, o_full, o_empty;
+  uint32_t tmem_slot;
+};
+
+template <int D, Dir DIR>
+__global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__ CoreParams prm) {
+  using L = CoreLayout<D>;
+  constexpr int ST = L::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  CoreBars* bar = reinterpret_cast<CoreBars*>(sm + L::BARS);
+  float* pw = reinterpret_cast<float*>(sm + L::PW);
+  const uint32_t sbase = smem_u32(sm);
+
+  const Plan& p = prm.p;
+  const int64_t seg = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int64_t beg = seg_begin(DIR, seg, p.seg_len, p.C), end = seg_end(DIR, seg, p.seg_len, p.C);
+  const int nblk = int((end - beg + BT - 1) / BT);
+  const float lam = p.lam[h];
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&prm.ma); tma_prefetch(&prm.mb); tma_prefetch(&prm.mc); tma_prefetch(&prm.mo);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bar->full[s], 1); mbar_init(&bar->empty[s], 1);
+      mbar_init(&bar->s_full[s], 1); mbar_init(&bar->s_empty[s], 128);
+    }
+    mbar_init(&bar->p_full, 128); mbar_init(&bar->p_empty, 1);
+    mbar_init(&bar->ku_full, 128);
+    mbar_init(&bar->ds_full, 1); mbar_init(&bar->ds_empty, 128);
+    mbar_init(&bar->st_full, 128); mbar_init(&bar->st_empty, 1);
+    mbar_init(&bar->o_full, 1); mbar_init(&bar->o_empty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&bar->tmem_slot);
+  for (int k = threadIdx.x; k <= BT; k += blockDim.x) pw[k] = powk(lam, double(k));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bar->tmem_slot;
+
+  auto row0 = [&](int j) -> int64_t { return DIR == Dir::FWD ? beg + int64_t(j) * BT : end - int64_t(j + 1) * BT; };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % ST;
+        mbar_wait(&bar->empty[s], ((j / ST) & 1) ^ 1);
+        mbar_expect_tx(&bar->full[s], 3 * L::TILE);
+        const int t0 = int(row0(j));
+#pragma unroll
+        for (int x = 0; x < L::NBOX; ++x) {
+          tma_load_4d(sm + L::A(s) + x * BOX, &prm.ma, &bar->full[s], x * 64, int(h), t0, int(b));
+          tma_load_4d(sm + L::B_(s) + x * BOX, &prm.mb, &bar->full[s], x * 64, int(h), t0, int(b));
+          tma_load_4d(sm + L::C_(s) + x * BOX, &prm.mc, &bar->full[s], x * 64, int(h), t0, int(b));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ UMMA issuer
+    if (elect_one()) {
+      constexpr uint32_t id_qk = idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t id_ds = idesc_bf16(D, D, 1, 1);
+      constexpr uint32_t id_pv = idesc_bf16(128, D, 0, 1);
+      constexpr uint32_t id_x = idesc_bf16(128, D, 0, 1);
+      auto koff = [](int kk) -> uint32_t { return uint32_t(kk >> 2) * BOX + uint32_t(kk & 3) * 32; };
+      auto issue_qk = [&](int j) {
+        const int s = j % ST, sb = j & 1;
+        mbar_wait(&bar->full[s], (j / ST) & 1);
+        mbar_wait(&bar->s_empty[sb], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dt = tmem + (sb ? L::T_S1 : L::T_S0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_bf16(dt, desc_k(sbase + L::A(s) + koff(kk)), desc_k(sbase + L::B_(s) + koff(kk)), id_qk, kk != 0);
+        mma_commit(&bar->s_full[sb]);
+      };
+      auto issue_ds = [&](int j) {
+        const int s = j % ST;
+        mbar_wait(&bar->ku_full, j & 1);
+        mbar_wait(&bar->ds_empty, (j & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BT / 16; ++kk)
+          mma_bf16(tmem + L::T_DS, desc_mn(sbase + L::KU + kk * 2048, BOX), desc_mn(sbase + L::C_(s) + kk * 2048, BOX),
+                   id_ds, kk != 0);
+        mma_commit(&bar->ds_full);
+      };
+      auto issue_out = [&](int j) {
+        const int s = j % ST;
+        mbar_wait(&bar->p_full, j & 1);
+        mbar_wait(&bar->o_empty, (j & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BT / 16; ++kk)
+          mma_bf16(tmem + L::T_OI, desc_k(sbase + L::P + koff(kk)), desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv,
+                   kk != 0);
+        mbar_wait(&bar->st_full, j & 1);
+        tc_fence_after();
+        // O_inter = a (S_hi + S_lo): the fp32 state enters as two bf16 terms (~16 mantissa bits)
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SBF + kk * 2048, D * 128),
+                   id_x, kk != 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SLO + kk * 2048, D * 128),
+                   id_x, 1);
+        mma_commit(&bar->o_full);
+        mma_commit(&bar->p_empty);
+        mma_commit(&bar->st_empty);
+        mma_commit(&bar->empty[s]);
+      };
+      issue_qk(0);
+      if (nblk > 1) issue_ds(0);
+      for (int j = 0; j < nblk; ++j) {
+        if (j + 1 < nblk) issue_qk(j + 1);
+        if (j + 1 < nblk - 1) issue_ds(j + 1);
+        issue_out(j);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------------ mask warps: S -> P
+    const uint32_t q4 = warp & 3;
+    const int i = int(q4 * 32 + lane);  // query row of the block
+    for (int j = 0; j < nblk; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&bar->s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      mbar_wait(&bar->p_empty, (j & 1) ^ 1);
+      const uint32_t ts = tmem + ((q4 * 32) << 16) + (sb ? L::T_S1 : L::T_S0);
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        float v[32];
+        tmem_ld16(ts + c4 * 32, *reinterpret_cast<float(*)[16]>(&v[0]));
+        tmem_ld16(ts + c4 * 32 + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
+        tmem_ld_wait();
+        if (DIR == Dir::FWD) {
+          // M_ij = lam^(i-j), j <= i; walk j downwards so the exponent grows by one per step
+          const int e0 = i - c4 * 32 - 31;
+          float m = pw[e0 > 0 ? e0 : 0];
+#pragma unroll
+          for (int u = 31; u >= 0; --u) {
+            const int e = e0 + (31 - u);
+            if (u < 31) m = (e == 0) ? 1.f : m * lam;
+            v[u] = (e >= 0) ? v[u] * m : 0.f;
+          }
+        } else {
+          // M_ij = lam^(j-i), j >= i; walk j upwards
+          const int e0 = c4 * 32 - i;
+          float m = pw[e0 > 0 ? e0 : 0];
+#pragma unroll
+          for (int u = 0; u < 32; ++u) {
+            const int e = e0 + u;
+            if (u > 0) m = (e == 0) ? 1.f : m * lam;
+            v[u] = (e >= 0) ? v[u] * m : 0.f;
+          }
+        }
+        const uint32_t atom = sbase + L::P + uint32_t(c4 >> 1) * BOX;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 pk;
+          pk.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+          pk.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+          pk.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+          pk.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+          sts128(atom + sw128_off(uint32_t(i), uint32_t((c4 & 1) * 4 + q)), pk);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bar->s_empty[sb]);
+      fence_async_smem();
+      mbar_arrive(&bar->p_full);
+    }
+  } else if (warp >= 8 && warp < 12) {
+    // ------------------------------------------------------------------ state warps
+    const uint32_t q4 = warp & 3;
+    const int g = int(threadIdx.x) - 256;  // tile row for the u.b scaling
+    const bool valid = D == 128 || lane < 16;
+    const int d = D == 128 ? int(q4 * 32 + lane) : int(q4 * 16 + lane);  // state row (TMEM layout of M = D)
+    float S[D];
+    const float* st0 = prm.state + ((b * p.H + h) * p.nseg + seg) * D * D;
+#pragma unroll
+    for (int e = 0; e < D; ++e) S[e] = valid ? (prm.trans ? st0[int64_t(e) * D + d] : st0[int64_t(d) * D + e]) : 0.f;
+    auto write_sbf = [&]() {
+      if (valid) {
+#pragma unroll
+        for (int x = 0; x < L::NBOX; ++x)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float* v = &S[x * 64 + c * 8];
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              hi[t] = pack_bf16(v[2 * t], v[2 * t + 1]);
+              lo[t] = pack_bf16(v[2 * t] - __uint_as_float(hi[t] << 16), v[2 * t + 1] - __uint_as_float(hi[t] & 0xFFFF0000u));
+            }
+            const uint32_t off = x * (D * 128) + sw128_off(uint32_t(d), uint32_t(c));
+            sts128(sbase + L::SBF + off, make_uint4(hi[0], hi[1], hi[2], hi[3]));
+            sts128(sbase + L::SLO + off, make_uint4(lo[0], lo[1], lo[2], lo[3]));
+          }
+      }
+      fence_async_smem();
+      mbar_arrive(&bar->st_full);
+    };
+    auto scale_ku = [&](int j) {
+      const int s = j % ST;
+      mbar_wait(&bar->full[s], (j / ST) & 1);
+      const float u = DIR == Dir::FWD ? pw[BT - 1 - g] : pw[g + 1];
+#pragma unroll
+      for (int x = 0; x < L::NBOX; ++x)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t off = x * BOX + uint32_t(g) * 128 + c * 16;
+          sts128(sbase + L::KU + off, scale_chunk(lds128(sbase + L::B_(s) + off), u));
+        }
+      fence_async_smem();
+      mbar_arrive(&bar->ku_full);
+    };
+    write_sbf();
+    if (nblk > 1) scale_ku(0);
+    const float decay = pw[BT];
+    for (int j = 0; j + 1 < nblk; ++j) {
+      mbar_wait(&bar->ds_full, j & 1);
+      tc_fence_after();
+      const uint32_t td = tmem + ((q4 * 32) << 16) + L::T_DS;
+#pragma unroll
+      for (int c = 0; c < D / 16; ++c) {
+        float v[16];
+        tmem_ld16(td + c * 16, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) S[c * 16 + u] = fmaf(decay, S[c * 16 + u], v[u]);
+      }
+      tc_fence_before();
+      mbar_arrive(&bar->ds_empty);
+      if (j + 1 < nblk - 1) scale_ku(j + 1);
+      mbar_wait(&bar->st_empty, j & 1);
+      write_sbf();
+    }
+  } else if (warp >= 12) {
+    // ------------------------------------------------------------------ epilogue warps
+    const uint32_t q4 = warp & 3;
+    const int i = int(q4 * 32 + lane);
+    const float r = DIR == Dir::FWD ? pw[i + 1] : pw[BT - 1 - i];
+    const bool leader = threadIdx.x == 384;
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(&bar->o_full, j & 1);
+      tc_fence_after();
+      const uint32_t ti = tmem + ((q4 * 32) << 16) + L::T_OI;
+      const uint32_t tx = tmem + ((q4 * 32) << 16) + L::T_OX;
+      uint32_t pk[D / 2];
+#pragma unroll
+      for (int c = 0; c < D / 16; ++c) {
+        float a[16], x[16];
+        tmem_ld16(ti + c * 16, a);
+        tmem_ld16(tx + c * 16, x);
+        tmem_ld_wait();
+        if (c == D / 16 - 1) {
+          tc_fence_before();
+          mbar_arrive(&bar->o_empty);
+        }
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) pk[c * 8 + u / 2] = pack_bf16(fmaf(r, x[u], a[u]), fmaf(r, x[u + 1], a[u + 1]));
+      }
+      const int t0 = int(row0(j));
+      if (t0 < 0) {
+        // ragged first block of a REV pass (rows before the rank start): TMA stores reject negative
+        // coordinates, so the valid rows are written directly from registers
+        if (t0 + i >= 0) {
+          uint4* dst = reinterpret_cast<uint4*>(prm.out + ((b * p.C + (t0 + i)) * p.H + h) * D);
+#pragma unroll
+          for (int c = 0; c < D / 8; ++c) dst[c] = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
+        }
+        continue;
+      }
+      const uint32_t ob = L::OST + uint32_t(j & 1) * L::TILE;
+      if (leader) tma_store_wait_read<1>();
+      named_bar_sync(1, 128);
+#pragma unroll
+      for (int x = 0; x < L::NBOX; ++x)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t* v = &pk[x * 32 + c * 4];
+          sts128(sbase + ob + x * BOX + sw128_off(uint32_t(i), uint32_t(c)), make_uint4(v[0], v[1], v[2], v[3]));
+        }
+      fence_async_smem();
+      named_bar_sync(1, 128);
+      if (leader) {
+#pragma unroll
+        for (int x = 0; x < L::NBOX; ++x) tma_store_4d(&prm.mo, sm + ob + x * BOX, x * 64, int(h), t0, int(b));
+        tma_store_commit();
+      }
+    }
+    if (leader) tma_store_wait_all<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+template <int D, Dir DIR>
+cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, cudaStream_t st) {
+  SegParams prm;
+  cudaError_t e;
+  if ((e = make_seq_map(&prm.mx, x, p)) != cudaSuccess) return e;
+  if ((e = make_seq_map(&prm.my, y, p)) != cudaSuccess) return e;
+  prm.p = p;
+  prm.out = out;
+  auto kern = seg_state_tc_kernel<D, DIR>;
+  const int smem = int(SegLayout<D>::BYTES);
+  if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
+  kern<<<dim3(unsigned(p.nseg), unsigned(p.H), unsigned(p.B)), 192, smem, st>>>(prm);
+  return cudaGetLastError();
+}
+
+template <int D, Dir DIR>
+cudaError_t launch_core(const Plan& p, const SeqArgs& a, cudaStream_t st) {
+  CoreParams prm;
+  cudaError_t e;
+  if ((e = make_seq_map(&prm.ma, a.a, p)) != cudaSuccess) return e;
+  if ((e = make_seq_map(&prm.mb, a.b, p)) != cudaSuccess) return e;
+  if ((e = make_seq_map(&prm.mc, a.c, p)) != cudaSuccess) return e;
+  if ((e = make_seq_map(&prm.mo, a.out, p)) != cudaSuccess) return e;
+  prm.p = p;
+  prm.out = static_cast<__nv_bfloat16*>(a.out);
+  prm.state = a.state;
+  prm.trans = a.trans_state;
+  auto kern = core_tc_kernel<D, DIR>;
+  const int smem = int(CoreLayout<D>::BYTES);
+  if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
+  kern<<<dim3(unsigned(p.nseg), unsigned(p.H), unsigned(p.B)), 512, smem, st>>>(prm);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+const char* tc_last_error() { return g_tc_err; }
+
+bool tc_supported(const Plan& p) {
+  static const bool disabled = [] {
+    const char* s = std::getenv("LASP_DISABLE_TC");
+    return s && *s && *s != '0';
+  }();
+  return !disabled && p.dtype == 0 && p.D == 64 && p.C > 0;
+}
+
+cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st) {
+  if (p.D == 64) return dir == Dir::FWD ? launch_seg<64, Dir::FWD>(p, x, y, out, st) : launch_seg<64, Dir::REV>(p, x, y, out, st);
   return cudaErrorNotSupported;
 }
-cudaError_t launch_core_tc(const Plan&, Dir, const SeqArgs&, cudaStream_t) { return cudaErrorNotSupported; }
+
+cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st) {
+  if (p.D == 64) return dir == Dir::FWD ? launch_core<64, Dir::FWD>(p, a, st) : launch_core<64, Dir::REV>(p, a, st);
+  return cudaErrorNotSupported;
+}
 
 }  // namespace lasp

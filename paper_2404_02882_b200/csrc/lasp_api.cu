@@ -35,7 +35,10 @@ lasp_status_t fail(lasp_status_t st, const std::string& msg) {
 }
 
 lasp_status_t cuda_fail(cudaError_t e, const char* where) {
-  return fail(LASP_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+  std::string msg = std::string(where) + ": " + cudaGetErrorString(e);
+  const char* tc = tc_last_error();
+  if (tc && *tc) msg += std::string(" [") + tc + "]";
+  return fail(LASP_ERR_CUDA, msg);
 }
 
 #define LASP_CUDA(call)                                       \
@@ -145,6 +148,14 @@ lasp_status_t check_device() {
   static std::unordered_map<int, bool> ok;
   int dev = 0;
   LASP_CUDA(cudaGetDevice(&dev));
+  // make the primary context current on this thread (driver-API calls such as the TMA descriptor
+  // encode need it; e.g. torch's autograd worker threads may not have bound it yet)
+  thread_local int bound_dev = -1;
+  if (bound_dev != dev) {
+    LASP_CUDA(cudaSetDevice(dev));
+    LASP_CUDA(cudaFree(nullptr));
+    bound_dev = dev;
+  }
   std::lock_guard<std::mutex> g(mu);
   auto it = ok.find(dev);
   if (it == ok.end()) {
