@@ -97,13 +97,25 @@ __global__ void prefix_kernel(Plan p, Dir dir, const float* __restrict__ init, c
   if (idx >= p.B * p.H * DD) return;
   const int64_t bh = idx / DD, e = idx % DD, h = bh % p.H;
   const float lam = p.lam[h];
+  const float dec_full = powk(lam, double(p.seg_len));
   float cur = init ? init[idx] : 0.f;
-  for (int64_t s = 0; s < p.nseg; ++s) {
-    const int64_t len = seg_end(dir, s, p.seg_len, p.C) - seg_begin(dir, s, p.seg_len, p.C);
-    const int64_t off = (bh * p.nseg + s) * DD + e;
-    const float v = seg_states ? seg_states[off] : 0.f;
-    if (prefix) prefix[off] = cur;
-    cur = fmaf(powk(lam, double(len)), cur, v);
+  // loads are batched ahead of the dependent fold so the chain is not latency-bound
+  constexpr int U = 32;
+  for (int64_t s0 = 0; s0 < p.nseg; s0 += U) {
+    float v[U];
+#pragma unroll
+    for (int t = 0; t < U; ++t) {
+      const int64_t s = s0 + t;
+      v[t] = (s < p.nseg && seg_states) ? seg_states[(bh * p.nseg + s) * DD + e] : 0.f;
+    }
+#pragma unroll
+    for (int t = 0; t < U; ++t) {
+      const int64_t s = s0 + t;
+      if (s >= p.nseg) break;
+      const int64_t len = seg_end(dir, s, p.seg_len, p.C) - seg_begin(dir, s, p.seg_len, p.C);
+      if (prefix) prefix[(bh * p.nseg + s) * DD + e] = cur;
+      cur = fmaf(len == p.seg_len ? dec_full : powk(lam, double(len)), cur, v[t]);
+    }
   }
   if (final_out) final_out[idx] = cur;
 }

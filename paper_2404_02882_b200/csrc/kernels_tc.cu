@@ -101,17 +101,68 @@ __device__ __forceinline__ uint64_t desc_k(uint32_t addr) { return smem_desc(add
 __device__ __forceinline__ uint64_t desc_mn(uint32_t addr, uint32_t lbo) { return smem_desc(addr, lbo, 1024); }
 
 // ================================================================================================
-// seg_state_tc
+// work items: (batch, head, segment), round-robin over a persistent grid (one CTA per SM)
+// ================================================================================================
+struct Item {
+  int64_t b, h, seg, beg, end;
+  int nblk;
+};
+
+__device__ __forceinline__ Item get_item(const Plan& p, Dir dir, int64_t w) {
+  Item it;
+  it.seg = w % p.nseg;
+  const int64_t bh = w / p.nseg;
+  it.h = bh % p.H;
+  it.b = bh / p.H;
+  it.beg = seg_begin(dir, it.seg, p.seg_len, p.C);
+  it.end = seg_end(dir, it.seg, p.seg_len, p.C);
+  it.nblk = int((it.end - it.beg + BT - 1) / BT);
+  return it;
+}
+
+// first row of block j of an item: FWD blocks ascend from the segment begin, REV blocks descend
+// from the segment end (so a ragged block only occurs where no state leaves it)
+__device__ __forceinline__ int64_t block_row(Dir dir, const Item& it, int j) {
+  return dir == Dir::FWD ? it.beg + int64_t(j) * BT : it.end - int64_t(j + 1) * BT;
+}
+
+// cursor over the flattened (item, block) sequence of this CTA
+struct Cur {
+  int64_t w;
+  int j, nblk;
+  uint32_t J;
+  bool done;
+};
+__device__ __forceinline__ void cur_init(Cur& c, const Plan& p, Dir dir, int64_t W) {
+  c.w = blockIdx.x; c.j = 0; c.J = 0; c.done = c.w >= W;
+  c.nblk = c.done ? 0 : get_item(p, dir, c.w).nblk;
+}
+__device__ __forceinline__ void cur_next(Cur& c, const Plan& p, Dir dir, int64_t W) {
+  ++c.J;
+  if (++c.j >= c.nblk) {
+    c.w += gridDim.x; c.j = 0; c.done = c.w >= W;
+    c.nblk = c.done ? 0 : get_item(p, dir, c.w).nblk;
+  }
+}
+
+__device__ __forceinline__ void watchdog(long long t0) {
+  if (clock64() - t0 > (1ll << 36)) __trap();
+}
+
+// ================================================================================================
+// seg_state_tc (persistent): warp 0 TMA, warp 1 UMMA, warps 4-7 scale X rows, warps 8-11 drain
+// the (double-buffered) TMEM accumulator of finished items to global memory.
 // ================================================================================================
 template <int D>
 struct SegLayout {
   static constexpr int NBOX = D / 64;
   static constexpr uint32_t TILE = NBOX * BOX;
-  static constexpr int STAGES = D == 64 ? 3 : 2;
+  static constexpr int STAGES = D == 64 ? 4 : 2;
   static constexpr uint32_t X(int s) { return uint32_t(s) * 2 * TILE; }
   static constexpr uint32_t Y(int s) { return uint32_t(s) * 2 * TILE + TILE; }
   static constexpr uint32_t BARS = STAGES * 2 * TILE;
-  static constexpr uint32_t BYTES = BARS + 256 + 1024;  // barriers + tmem slot + alignment slack
+  static constexpr uint32_t BYTES = BARS + 512 + 1024;  // barriers + tmem slot + alignment slack
+  static constexpr uint32_t TCOLS = 2 * D;             // two accumulators
 };
 
 struct SegParams {
@@ -121,7 +172,7 @@ struct SegParams {
 };
 
 template <int D, Dir DIR>
-__global__ void __launch_bounds__(192, 1) seg_state_tc_kernel(const __grid_constant__ SegParams prm) {
+__global__ void __launch_bounds__(384, 1) seg_state_tc_kernel(const __grid_constant__ SegParams prm) {
   using L = SegLayout<D>;
   constexpr int ST = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -129,120 +180,144 @@ __global__ void __launch_bounds__(192, 1) seg_state_tc_kernel(const __grid_const
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::BARS);
   uint64_t* scaled = full + ST;
   uint64_t* empty = scaled + ST;
-  uint64_t* done = empty + ST;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* acc_full = empty + ST;     // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const uint32_t sbase = smem_u32(sm);
 
   const Plan& p = prm.p;
-  const int64_t seg = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int64_t beg = seg_begin(DIR, seg, p.seg_len, p.C), end = seg_end(DIR, seg, p.seg_len, p.C);
-  const int nblk = int((end - beg + BT - 1) / BT);
-  const float lam = p.lam[h];
+  const int64_t W = p.B * p.H * p.nseg;
   const uint32_t warp = warp_id(), lane = lane_id();
 
   if (threadIdx.x == 0) {
     tma_prefetch(&prm.mx);
     tma_prefetch(&prm.my);
     for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&scaled[s], 128); mbar_init(&empty[s], 1); }
-    mbar_init(done, 1);
+    for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], 128); }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<(D < 64 ? 64 : D)>(tmem_slot);
+  if (warp == 1) tmem_alloc<L::TCOLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  auto row0 = [&](int j) -> int64_t { return DIR == Dir::FWD ? beg + int64_t(j) * BT : end - int64_t(j + 1) * BT; };
-
   if (warp == 0) {
     if (elect_one()) {
-      for (int j = 0; j < nblk; ++j) {
-        const int s = j % ST;
-        mbar_wait(&empty[s], ((j / ST) & 1) ^ 1);
-        mbar_expect_tx(&full[s], 2 * L::TILE);
-        const int t0 = int(row0(j));
+      uint32_t J = 0;
+      for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+        const Item it = get_item(p, DIR, w);
+        for (int j = 0; j < it.nblk; ++j, ++J) {
+          const int s = J % ST;
+          mbar_wait(&empty[s], ((J / ST) & 1) ^ 1);
+          mbar_expect_tx(&full[s], 2 * L::TILE);
+          const int t0 = int(block_row(DIR, it, j));
 #pragma unroll
-        for (int x = 0; x < L::NBOX; ++x) {
-          tma_load_4d(sm + L::X(s) + x * BOX, &prm.mx, &full[s], x * 64, int(h), t0, int(b));
-          tma_load_4d(sm + L::Y(s) + x * BOX, &prm.my, &full[s], x * 64, int(h), t0, int(b));
+          for (int x = 0; x < L::NBOX; ++x) {
+            tma_load_4d(sm + L::X(s) + x * BOX, &prm.mx, &full[s], x * 64, int(it.h), t0, int(it.b));
+            tma_load_4d(sm + L::Y(s) + x * BOX, &prm.my, &full[s], x * 64, int(it.h), t0, int(it.b));
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_bf16(D, D, 1, 1);
-      for (int j = 0; j < nblk; ++j) {
-        const int s = j % ST;
-        mbar_wait(&scaled[s], (j / ST) & 1);
+      uint32_t J = 0, k = 0;
+      for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
+        const Item it = get_item(p, DIR, w);
+        const uint32_t acc = tmem + (k & 1) * D;
+        mbar_wait(&acc_empty[k & 1], ((k >> 1) & 1) ^ 1);
         tc_fence_after();
+        for (int j = 0; j < it.nblk; ++j, ++J) {
+          const int s = J % ST;
+          mbar_wait(&scaled[s], (J / ST) & 1);
+          tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < BT / 16; ++kk)
-          mma_bf16(tmem, desc_mn(sbase + L::X(s) + kk * 2048, BOX), desc_mn(sbase + L::Y(s) + kk * 2048, BOX), idesc,
-                   (j | kk) != 0);
-        mma_commit(&empty[s]);
-      }
-      mma_commit(done);
-    }
-  } else {
-    // warps 2..5: scale X rows by the decay weight, then drain the accumulator
-    const int g = int(threadIdx.x) - 64;  // row of the tile
-    for (int j = 0; j < nblk; ++j) {
-      const int s = j % ST;
-      mbar_wait(&full[s], (j / ST) & 1);
-      const int64_t pos = row0(j) + g;
-      float w = 0.f;
-      if (pos >= beg && pos < end) w = powk(lam, DIR == Dir::FWD ? double(end - 1 - pos) : double(pos - beg + 1));
-#pragma unroll
-      for (int x = 0; x < L::NBOX; ++x)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t a = sbase + L::X(s) + x * BOX + uint32_t(g) * 128 + c * 16;
-          sts128(a, scale_chunk(lds128(a), w));
+          for (int kk = 0; kk < BT / 16; ++kk)
+            mma_bf16(acc, desc_mn(sbase + L::X(s) + kk * 2048, BOX), desc_mn(sbase + L::Y(s) + kk * 2048, BOX), idesc,
+                     (j | kk) != 0);
+          mma_commit(&empty[s]);
         }
-      fence_async_smem();
-      mbar_arrive(&scaled[s]);
+        mma_commit(&acc_full[k & 1]);
+      }
     }
-    mbar_wait(done, 0);
-    tc_fence_after();
+  } else if (warp >= 4 && warp < 8) {
+    // scale X rows by the decay weight (Eq. 12 / Eq. 21 weights, relative to the segment end / begin)
+    const int g = int(threadIdx.x) - 128;  // tile row
+    uint32_t J = 0;
+    for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+      const Item it = get_item(p, DIR, w);
+      const float l2 = p.l2lam[it.h];
+      for (int j = 0; j < it.nblk; ++j, ++J) {
+        const int s = J % ST;
+        mbar_wait(&full[s], (J / ST) & 1);
+        const int64_t pos = block_row(DIR, it, j) + g;
+        float wgt = 0.f;
+        if (pos >= it.beg && pos < it.end)
+          wgt = exp2f(float(DIR == Dir::FWD ? (it.end - 1 - pos) : (pos - it.beg + 1)) * l2);
+#pragma unroll
+        for (int x = 0; x < L::NBOX; ++x)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {  // swizzled chunk order: conflict-free across 8 rows
+            const uint32_t a = sbase + L::X(s) + x * BOX + uint32_t(g) * 128 + ((uint32_t(c) ^ (uint32_t(g) & 7)) << 4);
+            sts128(a, scale_chunk(lds128(a), wgt));
+          }
+        fence_async_smem();
+        mbar_arrive(&scaled[s]);
+      }
+    }
+  } else if (warp >= 8) {
+    // drain finished accumulators: rows of L (TMEM layout of M = D), fp32 to [B][H][nseg][D][D]
     const uint32_t q4 = warp & 3;
     const bool valid = D == 128 || lane < 16;
     const int row = D == 128 ? int(q4 * 32 + lane) : int(q4 * 16 + lane);
-    float* o = prm.out + ((b * p.H + h) * p.nseg + seg) * D * D + int64_t(row) * D;
+    uint32_t k = 0;
+    for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
+      const Item it = get_item(p, DIR, w);
+      mbar_wait(&acc_full[k & 1], (k >> 1) & 1);
+      tc_fence_after();
+      float* o = prm.out + ((it.b * p.H + it.h) * p.nseg + it.seg) * D * D + int64_t(row) * D;
+      const uint32_t ta = tmem + ((q4 * 32) << 16) + (k & 1) * D;
 #pragma unroll
-    for (int c = 0; c < D / 16; ++c) {
-      float v[16];
-      tmem_ld16(tmem + ((q4 * 32) << 16) + c * 16, v);
-      tmem_ld_wait();
-      if (valid) {
+      for (int c = 0; c < D / 16; ++c) {
+        float v[16];
+        tmem_ld16(ta + c * 16, v);
+        tmem_ld_wait();
+        if (c == D / 16 - 1) {
+          tc_fence_before();
+          mbar_arrive(&acc_empty[k & 1]);
+        }
+        if (valid) {
 #pragma unroll
-        for (int u = 0; u < 16; u += 4) *reinterpret_cast<float4*>(o + c * 16 + u) = make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]);
+          for (int u = 0; u < 16; u += 4)
+            *reinterpret_cast<float4*>(o + c * 16 + u) = make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]);
+        }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<(D < 64 ? 64 : D)>(tmem);
+  if (warp == 1) tmem_dealloc<L::TCOLS>(tmem);
 }
 
 // ================================================================================================
-// core_tc
+// core_tc (persistent)
 // ================================================================================================
 template <int D>
 struct CoreLayout {
   static constexpr int NBOX = D / 64;
   static constexpr uint32_t TILE = NBOX * BOX;           // one [128][D] bf16 tile
-  static constexpr int STAGES = 2;
+  static constexpr int STAGES = 3;
   static constexpr uint32_t A(int s) { return uint32_t(s) * 3 * TILE; }
   static constexpr uint32_t B_(int s) { return uint32_t(s) * 3 * TILE + TILE; }
   static constexpr uint32_t C_(int s) { return uint32_t(s) * 3 * TILE + 2 * TILE; }
-  static constexpr uint32_t KU = STAGES * 3 * TILE;
+  static constexpr uint32_t KU = STAGES * 3 * TILE;      // u (.) b, [128][D]
   static constexpr uint32_t P = KU + TILE;               // [128][128] bf16, 2 K-atoms of 16 KB
-  static constexpr uint32_t SBF = P + 2 * BOX;           // [D][D] bf16 hi part, NBOX MN-blocks of D*128 B
+  static constexpr uint32_t SBF = P + 2 * BOX;           // [D][D] bf16 hi part of the state
   static constexpr uint32_t SLO = SBF + D * D * 2;       // [D][D] bf16 lo part (S - hi)
-  static constexpr uint32_t OST = SLO + D * D * 2;       // 2 x [128][D] bf16 output staging
-  static constexpr uint32_t PW = OST + 2 * TILE;         // float[BT + 1]
-  static constexpr uint32_t BARS = PW + 1024;
+  static constexpr uint32_t OST = SLO + D * D * 2;       // [128][D] bf16 output staging
+  static constexpr uint32_t BARS = OST + TILE;
   static constexpr uint32_t BYTES = BARS + 256 + 1024;
   // TMEM columns
   static constexpr uint32_t T_S0 = 0, T_S1 = 128, T_OI = 256, T_OX = 256 + D, T_DS = 256 + 2 * D;
@@ -257,7 +332,7 @@ struct CoreParams {
 };
 
 struct CoreBars {
-  uint64_t full[2], empty[2], s_full[2], s_empty[2];
+  uint64_t full[3], empty[3], s_full[2], s_empty[2];
   uint64_t p_full, p_empty, ku_full, ds_full, ds_empty, st_full, st_empty, o_full, o_empty;
   uint32_t tmem_slot;
 };
@@ -269,22 +344,16 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   CoreBars* bar = reinterpret_cast<CoreBars*>(sm + L::BARS);
-  float* pw = reinterpret_cast<float*>(sm + L::PW);
   const uint32_t sbase = smem_u32(sm);
 
   const Plan& p = prm.p;
-  const int64_t seg = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int64_t beg = seg_begin(DIR, seg, p.seg_len, p.C), end = seg_end(DIR, seg, p.seg_len, p.C);
-  const int nblk = int((end - beg + BT - 1) / BT);
-  const float lam = p.lam[h];
+  const int64_t W = p.B * p.H * p.nseg;
   const uint32_t warp = warp_id(), lane = lane_id();
 
   if (threadIdx.x == 0) {
     tma_prefetch(&prm.ma); tma_prefetch(&prm.mb); tma_prefetch(&prm.mc); tma_prefetch(&prm.mo);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&bar->full[s], 1); mbar_init(&bar->empty[s], 1);
-      mbar_init(&bar->s_full[s], 1); mbar_init(&bar->s_empty[s], 128);
-    }
+    for (int s = 0; s < ST; ++s) { mbar_init(&bar->full[s], 1); mbar_init(&bar->empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&bar->s_full[s], 1); mbar_init(&bar->s_empty[s], 128); }
     mbar_init(&bar->p_full, 128); mbar_init(&bar->p_empty, 1);
     mbar_init(&bar->ku_full, 128);
     mbar_init(&bar->ds_full, 1); mbar_init(&bar->ds_empty, 128);
@@ -293,145 +362,167 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(&bar->tmem_slot);
-  for (int k = threadIdx.x; k <= BT; k += blockDim.x) pw[k] = powk(lam, double(k));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bar->tmem_slot;
 
-  auto row0 = [&](int j) -> int64_t { return DIR == Dir::FWD ? beg + int64_t(j) * BT : end - int64_t(j + 1) * BT; };
-
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
     if (elect_one()) {
-      for (int j = 0; j < nblk; ++j) {
-        const int s = j % ST;
-        mbar_wait(&bar->empty[s], ((j / ST) & 1) ^ 1);
-        mbar_expect_tx(&bar->full[s], 3 * L::TILE);
-        const int t0 = int(row0(j));
+      uint32_t J = 0;
+      for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+        const Item it = get_item(p, DIR, w);
+        for (int j = 0; j < it.nblk; ++j, ++J) {
+          const int s = J % ST;
+          mbar_wait(&bar->empty[s], ((J / ST) & 1) ^ 1);
+          mbar_expect_tx(&bar->full[s], 3 * L::TILE);
+          const int t0 = int(block_row(DIR, it, j));
 #pragma unroll
-        for (int x = 0; x < L::NBOX; ++x) {
-          tma_load_4d(sm + L::A(s) + x * BOX, &prm.ma, &bar->full[s], x * 64, int(h), t0, int(b));
-          tma_load_4d(sm + L::B_(s) + x * BOX, &prm.mb, &bar->full[s], x * 64, int(h), t0, int(b));
-          tma_load_4d(sm + L::C_(s) + x * BOX, &prm.mc, &bar->full[s], x * 64, int(h), t0, int(b));
+          for (int x = 0; x < L::NBOX; ++x) {
+            tma_load_4d(sm + L::A(s) + x * BOX, &prm.ma, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
+            tma_load_4d(sm + L::B_(s) + x * BOX, &prm.mb, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
+            tma_load_4d(sm + L::C_(s) + x * BOX, &prm.mc, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
+          }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------------ UMMA issuer
+    // ------------------------------------------------------------------ UMMA issuer (dynamic order)
     if (elect_one()) {
       constexpr uint32_t id_qk = idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t id_ds = idesc_bf16(D, D, 1, 1);
       constexpr uint32_t id_pv = idesc_bf16(128, D, 0, 1);
       constexpr uint32_t id_x = idesc_bf16(128, D, 0, 1);
       auto koff = [](int kk) -> uint32_t { return uint32_t(kk >> 2) * BOX + uint32_t(kk & 3) * 32; };
-      auto issue_qk = [&](int j) {
-        const int s = j % ST, sb = j & 1;
-        mbar_wait(&bar->full[s], (j / ST) & 1);
-        mbar_wait(&bar->s_empty[sb], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t dt = tmem + (sb ? L::T_S1 : L::T_S0);
+      Cur cq, cd, co;
+      cur_init(cq, p, DIR, W);
+      cur_init(cd, p, DIR, W);
+      cur_init(co, p, DIR, W);
+      while (!cd.done && cd.j == cd.nblk - 1) cur_next(cd, p, DIR, W);  // ds only for non-last blocks
+      uint32_t kd = 0;
+      const long long t_start = clock64();
+      uint32_t spins = 0;
+      while (!co.done) {
+        // S = a b^T for the next block (double-buffered in TMEM)
+        if (!cq.done && cq.J < co.J + 2 && mbar_test(&bar->full[cq.J % ST], (cq.J / ST) & 1) &&
+            mbar_test(&bar->s_empty[cq.J & 1], ((cq.J >> 1) & 1) ^ 1)) {
+          tc_fence_after();
+          const int s = cq.J % ST;
+          const uint32_t dt = tmem + ((cq.J & 1) ? L::T_S1 : L::T_S0);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_bf16(dt, desc_k(sbase + L::A(s) + koff(kk)), desc_k(sbase + L::B_(s) + koff(kk)), id_qk, kk != 0);
-        mma_commit(&bar->s_full[sb]);
-      };
-      auto issue_ds = [&](int j) {
-        const int s = j % ST;
-        mbar_wait(&bar->ku_full, j & 1);
-        mbar_wait(&bar->ds_empty, (j & 1) ^ 1);
-        tc_fence_after();
+          for (int kk = 0; kk < D / 16; ++kk)
+            mma_bf16(dt, desc_k(sbase + L::A(s) + koff(kk)), desc_k(sbase + L::B_(s) + koff(kk)), id_qk, kk != 0);
+          mma_commit(&bar->s_full[cq.J & 1]);
+          cur_next(cq, p, DIR, W);
+        }
+        // dS = (u . b)^T c (state chain; only for blocks that are not the last of their segment)
+        if (!cd.done && mbar_test(&bar->ku_full, kd & 1) && mbar_test(&bar->ds_empty, (kd & 1) ^ 1)) {
+          tc_fence_after();
+          const int s = cd.J % ST;
 #pragma unroll
-        for (int kk = 0; kk < BT / 16; ++kk)
-          mma_bf16(tmem + L::T_DS, desc_mn(sbase + L::KU + kk * 2048, BOX), desc_mn(sbase + L::C_(s) + kk * 2048, BOX),
-                   id_ds, kk != 0);
-        mma_commit(&bar->ds_full);
-      };
-      auto issue_out = [&](int j) {
-        const int s = j % ST;
-        mbar_wait(&bar->p_full, j & 1);
-        mbar_wait(&bar->o_empty, (j & 1) ^ 1);
-        tc_fence_after();
+          for (int kk = 0; kk < BT / 16; ++kk)
+            mma_bf16(tmem + L::T_DS, desc_mn(sbase + L::KU + kk * 2048, BOX),
+                     desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_ds, kk != 0);
+          mma_commit(&bar->ds_full);
+          ++kd;
+          cur_next(cd, p, DIR, W);
+          while (!cd.done && cd.j == cd.nblk - 1) cur_next(cd, p, DIR, W);
+        }
+        // O_intra = P c, O_inter = a (S_hi + S_lo)
+        // (out(J) releases the stage, so ds(J) of a non-last block must already be issued)
+        if (co.J < cq.J && (co.j == co.nblk - 1 || cd.done || cd.J > co.J) && mbar_test(&bar->p_full, co.J & 1) && mbar_test(&bar->o_empty, (co.J & 1) ^ 1) &&
+            mbar_test(&bar->st_full, co.J & 1)) {
+          tc_fence_after();
+          const int s = co.J % ST;
 #pragma unroll
-        for (int kk = 0; kk < BT / 16; ++kk)
-          mma_bf16(tmem + L::T_OI, desc_k(sbase + L::P + koff(kk)), desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv,
-                   kk != 0);
-        mbar_wait(&bar->st_full, j & 1);
-        tc_fence_after();
-        // O_inter = a (S_hi + S_lo): the fp32 state enters as two bf16 terms (~16 mantissa bits)
+          for (int kk = 0; kk < BT / 16; ++kk)
+            mma_bf16(tmem + L::T_OI, desc_k(sbase + L::P + koff(kk)), desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv,
+                     kk != 0);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SBF + kk * 2048, D * 128),
-                   id_x, kk != 0);
+          for (int kk = 0; kk < D / 16; ++kk)
+            mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SBF + kk * 2048, D * 128),
+                     id_x, kk != 0);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SLO + kk * 2048, D * 128),
-                   id_x, 1);
-        mma_commit(&bar->o_full);
-        mma_commit(&bar->p_empty);
-        mma_commit(&bar->st_empty);
-        mma_commit(&bar->empty[s]);
-      };
-      issue_qk(0);
-      if (nblk > 1) issue_ds(0);
-      for (int j = 0; j < nblk; ++j) {
-        if (j + 1 < nblk) issue_qk(j + 1);
-        if (j + 1 < nblk - 1) issue_ds(j + 1);
-        issue_out(j);
+          for (int kk = 0; kk < D / 16; ++kk)
+            mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SLO + kk * 2048, D * 128),
+                     id_x, 1);
+          mma_commit(&bar->o_full);
+          mma_commit(&bar->p_empty);
+          mma_commit(&bar->st_empty);
+          mma_commit(&bar->empty[s]);
+          cur_next(co, p, DIR, W);
+        }
+        if ((++spins & 4095u) == 0) watchdog(t_start);
       }
     }
   } else if (warp >= 4 && warp < 8) {
-    // ------------------------------------------------------------------ mask warps: S -> P
+    // ------------------------------------------------------------------ mask warps: S -> P (bf16)
     const uint32_t q4 = warp & 3;
     const int i = int(q4 * 32 + lane);  // query row of the block
-    for (int j = 0; j < nblk; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&bar->s_full[sb], (j >> 1) & 1);
-      tc_fence_after();
-      mbar_wait(&bar->p_empty, (j & 1) ^ 1);
-      const uint32_t ts = tmem + ((q4 * 32) << 16) + (sb ? L::T_S1 : L::T_S0);
+    uint32_t J = 0;
+    for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+      const Item it = get_item(p, DIR, w);
+      const float l2 = p.l2lam[it.h];
+      const float lam = p.lam[it.h];
+      for (int j = 0; j < it.nblk; ++j, ++J) {
+        const int sb = J & 1;
+        mbar_wait(&bar->s_full[sb], (J >> 1) & 1);
+        tc_fence_after();
+        mbar_wait(&bar->p_empty, (J & 1) ^ 1);
+        const uint32_t ts = tmem + ((q4 * 32) << 16) + (sb ? L::T_S1 : L::T_S0);
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
-        float v[32];
-        tmem_ld16(ts + c4 * 32, *reinterpret_cast<float(*)[16]>(&v[0]));
-        tmem_ld16(ts + c4 * 32 + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
-        tmem_ld_wait();
-        if (DIR == Dir::FWD) {
-          // M_ij = lam^(i-j), j <= i; walk j downwards so the exponent grows by one per step
-          const int e0 = i - c4 * 32 - 31;
-          float m = pw[e0 > 0 ? e0 : 0];
+        for (int c4 = 0; c4 < 4; ++c4) {
+          // chunk columns [32 c4, 32 c4 + 32); warp rows [32 q4, 32 q4 + 32)
+          const bool dead = DIR == Dir::FWD ? (c4 > int(q4)) : (c4 < int(q4));
+          float v[32];
+          if (!dead) {
+            tmem_ld16(ts + c4 * 32, *reinterpret_cast<float(*)[16]>(&v[0]));
+            tmem_ld16(ts + c4 * 32 + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
+            tmem_ld_wait();
 #pragma unroll
-          for (int u = 31; u >= 0; --u) {
-            const int e = e0 + (31 - u);
-            if (u < 31) m = (e == 0) ? 1.f : m * lam;
-            v[u] = (e >= 0) ? v[u] * m : 0.f;
+            for (int g8 = 0; g8 < 4; ++g8) {
+              // 4 independent chains of 8: M_ij = lam^e, e = i - j (FWD) or j - i (REV)
+              if (DIR == Dir::FWD) {
+                const int e0 = i - c4 * 32 - (8 * g8 + 7);  // exponent at u = 8 g8 + 7
+                float m = exp2f(float(e0 > 0 ? e0 : 0) * l2);
+#pragma unroll
+                for (int t = 7; t >= 0; --t) {
+                  const int u = 8 * g8 + t, e = e0 + (7 - t);
+                  if (t < 7) m = (e == 0) ? 1.f : m * lam;
+                  v[u] = (e >= 0) ? v[u] * m : 0.f;
+                }
+              } else {
+                const int e0 = c4 * 32 + 8 * g8 - i;  // exponent at u = 8 g8
+                float m = exp2f(float(e0 > 0 ? e0 : 0) * l2);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                  const int u = 8 * g8 + t, e = e0 + t;
+                  if (t > 0) m = (e == 0) ? 1.f : m * lam;
+                  v[u] = (e >= 0) ? v[u] * m : 0.f;
+                }
+              }
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) v[u] = 0.f;
           }
-        } else {
-          // M_ij = lam^(j-i), j >= i; walk j upwards
-          const int e0 = c4 * 32 - i;
-          float m = pw[e0 > 0 ? e0 : 0];
+          const uint32_t atom = sbase + L::P + uint32_t(c4 >> 1) * BOX;
 #pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            const int e = e0 + u;
-            if (u > 0) m = (e == 0) ? 1.f : m * lam;
-            v[u] = (e >= 0) ? v[u] * m : 0.f;
+          for (int q = 0; q < 4; ++q) {
+            uint4 pk;
+            pk.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+            pk.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+            pk.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+            pk.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+            sts128(atom + sw128_off(uint32_t(i), uint32_t((c4 & 1) * 4 + q)), pk);
           }
         }
-        const uint32_t atom = sbase + L::P + uint32_t(c4 >> 1) * BOX;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 pk;
-          pk.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
-          pk.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
-          pk.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
-          pk.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
-          sts128(atom + sw128_off(uint32_t(i), uint32_t((c4 & 1) * 4 + q)), pk);
-        }
+        tc_fence_before();
+        mbar_arrive(&bar->s_empty[sb]);
+        fence_async_smem();
+        mbar_arrive(&bar->p_full);
       }
-      tc_fence_before();
-      mbar_arrive(&bar->s_empty[sb]);
-      fence_async_smem();
-      mbar_arrive(&bar->p_full);
     }
   } else if (warp >= 8 && warp < 12) {
     // ------------------------------------------------------------------ state warps
@@ -440,9 +531,22 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     const bool valid = D == 128 || lane < 16;
     const int d = D == 128 ? int(q4 * 32 + lane) : int(q4 * 16 + lane);  // state row (TMEM layout of M = D)
     float S[D];
-    const float* st0 = prm.state + ((b * p.H + h) * p.nseg + seg) * D * D;
+    auto load_state = [&](const Item& it) {
+      const float* st0 = prm.state + ((it.b * p.H + it.h) * p.nseg + it.seg) * D * D;
+      if (!valid) {
 #pragma unroll
-    for (int e = 0; e < D; ++e) S[e] = valid ? (prm.trans ? st0[int64_t(e) * D + d] : st0[int64_t(d) * D + e]) : 0.f;
+        for (int e = 0; e < D; ++e) S[e] = 0.f;
+      } else if (prm.trans) {
+#pragma unroll
+        for (int e = 0; e < D; ++e) S[e] = __ldg(st0 + int64_t(e) * D + d);
+      } else {
+#pragma unroll
+        for (int e = 0; e < D; e += 4) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(st0 + int64_t(d) * D + e));
+          S[e] = t.x; S[e + 1] = t.y; S[e + 2] = t.z; S[e + 3] = t.w;
+        }
+      }
+    };
     auto write_sbf = [&]() {
       if (valid) {
 #pragma unroll
@@ -454,7 +558,8 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
               hi[t] = pack_bf16(v[2 * t], v[2 * t + 1]);
-              lo[t] = pack_bf16(v[2 * t] - __uint_as_float(hi[t] << 16), v[2 * t + 1] - __uint_as_float(hi[t] & 0xFFFF0000u));
+              lo[t] = pack_bf16(v[2 * t] - __uint_as_float(hi[t] << 16),
+                                v[2 * t + 1] - __uint_as_float(hi[t] & 0xFFFF0000u));
             }
             const uint32_t off = x * (D * 128) + sw128_off(uint32_t(d), uint32_t(c));
             sts128(sbase + L::SBF + off, make_uint4(hi[0], hi[1], hi[2], hi[3]));
@@ -464,93 +569,108 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       fence_async_smem();
       mbar_arrive(&bar->st_full);
     };
-    auto scale_ku = [&](int j) {
-      const int s = j % ST;
-      mbar_wait(&bar->full[s], (j / ST) & 1);
-      const float u = DIR == Dir::FWD ? pw[BT - 1 - g] : pw[g + 1];
+    auto scale_ku = [&](uint32_t J, float u) {
+      const int s = J % ST;
+      mbar_wait(&bar->full[s], (J / ST) & 1);
 #pragma unroll
       for (int x = 0; x < L::NBOX; ++x)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const uint32_t off = x * BOX + uint32_t(g) * 128 + c * 16;
+          const uint32_t off = x * BOX + uint32_t(g) * 128 + ((uint32_t(c) ^ (uint32_t(g) & 7)) << 4);
           sts128(sbase + L::KU + off, scale_chunk(lds128(sbase + L::B_(s) + off), u));
         }
       fence_async_smem();
       mbar_arrive(&bar->ku_full);
     };
-    write_sbf();
-    if (nblk > 1) scale_ku(0);
-    const float decay = pw[BT];
-    for (int j = 0; j + 1 < nblk; ++j) {
-      mbar_wait(&bar->ds_full, j & 1);
-      tc_fence_after();
-      const uint32_t td = tmem + ((q4 * 32) << 16) + L::T_DS;
+    uint32_t J = 0, kd = 0;
+    int64_t w = blockIdx.x;
+    Item it;
+    if (w < W) { it = get_item(p, DIR, w); load_state(it); }
+    for (; w < W;) {
+      const float l2 = p.l2lam[it.h];
+      const float u = exp2f(float(DIR == Dir::FWD ? (BT - 1 - g) : (g + 1)) * l2);
+      const float decay = exp2f(float(BT) * l2);
+      if (J > 0) mbar_wait(&bar->st_empty, (J - 1) & 1);
+      write_sbf();                                   // state entering block J (segment prefix)
+      if (it.nblk > 1) scale_ku(J, u);
+      for (int j = 0; j + 1 < it.nblk; ++j, ++J) {
+        mbar_wait(&bar->ds_full, kd & 1);
+        tc_fence_after();
+        const uint32_t td = tmem + ((q4 * 32) << 16) + L::T_DS;
 #pragma unroll
-      for (int c = 0; c < D / 16; ++c) {
-        float v[16];
-        tmem_ld16(td + c * 16, v);
-        tmem_ld_wait();
+        for (int c = 0; c < D / 16; ++c) {
+          float v[16];
+          tmem_ld16(td + c * 16, v);
+          tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 16; ++u) S[c * 16 + u] = fmaf(decay, S[c * 16 + u], v[u]);
+          for (int t = 0; t < 16; ++t) S[c * 16 + t] = fmaf(decay, S[c * 16 + t], v[t]);
+        }
+        tc_fence_before();
+        mbar_arrive(&bar->ds_empty);
+        ++kd;
+        if (j + 2 < it.nblk) scale_ku(J + 1, u);
+        mbar_wait(&bar->st_empty, J & 1);
+        write_sbf();                                 // state entering block J + 1
       }
-      tc_fence_before();
-      mbar_arrive(&bar->ds_empty);
-      if (j + 1 < nblk - 1) scale_ku(j + 1);
-      mbar_wait(&bar->st_empty, j & 1);
-      write_sbf();
+      ++J;  // past the last block of this segment
+      w += gridDim.x;
+      if (w < W) { it = get_item(p, DIR, w); load_state(it); }  // overlaps the last block's MMAs
     }
   } else if (warp >= 12) {
     // ------------------------------------------------------------------ epilogue warps
     const uint32_t q4 = warp & 3;
     const int i = int(q4 * 32 + lane);
-    const float r = DIR == Dir::FWD ? pw[i + 1] : pw[BT - 1 - i];
     const bool leader = threadIdx.x == 384;
-    for (int j = 0; j < nblk; ++j) {
-      mbar_wait(&bar->o_full, j & 1);
-      tc_fence_after();
-      const uint32_t ti = tmem + ((q4 * 32) << 16) + L::T_OI;
-      const uint32_t tx = tmem + ((q4 * 32) << 16) + L::T_OX;
-      uint32_t pk[D / 2];
+    uint32_t J = 0;
+    for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+      const Item it = get_item(p, DIR, w);
+      const float r = exp2f(float(DIR == Dir::FWD ? (i + 1) : (BT - 1 - i)) * p.l2lam[it.h]);
+      for (int j = 0; j < it.nblk; ++j, ++J) {
+        mbar_wait(&bar->o_full, J & 1);
+        tc_fence_after();
+        const uint32_t ti = tmem + ((q4 * 32) << 16) + L::T_OI;
+        const uint32_t tx = tmem + ((q4 * 32) << 16) + L::T_OX;
+        uint32_t pk[D / 2];
 #pragma unroll
-      for (int c = 0; c < D / 16; ++c) {
-        float a[16], x[16];
-        tmem_ld16(ti + c * 16, a);
-        tmem_ld16(tx + c * 16, x);
-        tmem_ld_wait();
-        if (c == D / 16 - 1) {
-          tc_fence_before();
-          mbar_arrive(&bar->o_empty);
+        for (int c = 0; c < D / 16; ++c) {
+          float a[16], x[16];
+          tmem_ld16(ti + c * 16, a);
+          tmem_ld16(tx + c * 16, x);
+          tmem_ld_wait();
+          if (c == D / 16 - 1) {
+            tc_fence_before();
+            mbar_arrive(&bar->o_empty);
+          }
+#pragma unroll
+          for (int u = 0; u < 16; u += 2) pk[c * 8 + u / 2] = pack_bf16(fmaf(r, x[u], a[u]), fmaf(r, x[u + 1], a[u + 1]));
         }
+        const int t0 = int(block_row(DIR, it, j));
+        if (t0 < 0) {
+          // ragged first block of a REV pass (rows before the rank start): TMA stores reject
+          // negative coordinates, so the valid rows are written directly from registers
+          if (t0 + i >= 0) {
+            uint4* dst = reinterpret_cast<uint4*>(prm.out + ((it.b * p.C + (t0 + i)) * p.H + it.h) * D);
 #pragma unroll
-        for (int u = 0; u < 16; u += 2) pk[c * 8 + u / 2] = pack_bf16(fmaf(r, x[u], a[u]), fmaf(r, x[u + 1], a[u + 1]));
-      }
-      const int t0 = int(row0(j));
-      if (t0 < 0) {
-        // ragged first block of a REV pass (rows before the rank start): TMA stores reject negative
-        // coordinates, so the valid rows are written directly from registers
-        if (t0 + i >= 0) {
-          uint4* dst = reinterpret_cast<uint4*>(prm.out + ((b * p.C + (t0 + i)) * p.H + h) * D);
-#pragma unroll
-          for (int c = 0; c < D / 8; ++c) dst[c] = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
+            for (int c = 0; c < D / 8; ++c) dst[c] = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
+          }
+          continue;
         }
-        continue;
-      }
-      const uint32_t ob = L::OST + uint32_t(j & 1) * L::TILE;
-      if (leader) tma_store_wait_read<1>();
-      named_bar_sync(1, 128);
+        if (leader) tma_store_wait_read<0>();
+        named_bar_sync(1, 128);
 #pragma unroll
-      for (int x = 0; x < L::NBOX; ++x)
+        for (int x = 0; x < L::NBOX; ++x)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t* v = &pk[x * 32 + c * 4];
-          sts128(sbase + ob + x * BOX + sw128_off(uint32_t(i), uint32_t(c)), make_uint4(v[0], v[1], v[2], v[3]));
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t* v = &pk[x * 32 + c * 4];
+            sts128(sbase + L::OST + x * BOX + sw128_off(uint32_t(i), uint32_t(c)), make_uint4(v[0], v[1], v[2], v[3]));
+          }
+        fence_async_smem();
+        named_bar_sync(1, 128);
+        if (leader) {
+#pragma unroll
+          for (int x = 0; x < L::NBOX; ++x) tma_store_4d(&prm.mo, sm + L::OST + x * BOX, x * 64, int(it.h), t0, int(it.b));
+          tma_store_commit();
         }
-      fence_async_smem();
-      named_bar_sync(1, 128);
-      if (leader) {
-#pragma unroll
-        for (int x = 0; x < L::NBOX; ++x) tma_store_4d(&prm.mo, sm + ob + x * BOX, x * 64, int(h), t0, int(b));
-        tma_store_commit();
       }
     }
     if (leader) tma_store_wait_all<0>();
@@ -558,6 +678,22 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+unsigned persistent_grid(const Plan& p) {
+  const int64_t W = p.B * p.H * p.nseg;
+  const int64_t g = W < sm_count() ? W : sm_count();
+  return unsigned(g > 0 ? g : 1);
 }
 
 template <int D, Dir DIR>
@@ -571,7 +707,7 @@ cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, 
   auto kern = seg_state_tc_kernel<D, DIR>;
   const int smem = int(SegLayout<D>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
-  kern<<<dim3(unsigned(p.nseg), unsigned(p.H), unsigned(p.B)), 192, smem, st>>>(prm);
+  kern<<<persistent_grid(p), 384, smem, st>>>(prm);
   return cudaGetLastError();
 }
 
@@ -590,7 +726,7 @@ cudaError_t launch_core(const Plan& p, const SeqArgs& a, cudaStream_t st) {
   auto kern = core_tc_kernel<D, DIR>;
   const int smem = int(CoreLayout<D>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
-  kern<<<dim3(unsigned(p.nseg), unsigned(p.H), unsigned(p.B)), 512, smem, st>>>(prm);
+  kern<<<persistent_grid(p), 512, smem, st>>>(prm);
   return cudaGetLastError();
 }
 

@@ -98,6 +98,7 @@ lasp_status_t load_lambda(Plan& p, const float* lambda) {
       return fail(LASP_ERR_DOMAIN, buf);
     }
     p.lam[h] = l;
+    p.l2lam[h] = float(std::log2(double(l)));
   }
   return LASP_OK;
 }

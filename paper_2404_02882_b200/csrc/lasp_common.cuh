@@ -26,6 +26,7 @@ struct Plan {
   int64_t seg_len;     // multiple of kSegQuantum
   int64_t nseg;        // >= 1
   float lam[256];      // per-head decay (fp32, the boundary's precision; reading A8), by value
+  float l2lam[256];    // log2(lam) computed in fp64 on the host, rounded once (tcgen05 path: exp2 powers)
 };
 constexpr int64_t kMaxHeads = 256;
 
