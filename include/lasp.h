@@ -101,6 +101,9 @@ uint64_t lasp_launch_count(void);
  * {"stage": [launches, total_ms], ...} into buf (NUL-terminated, truncated to cap) and clears the
  * records; returns the JSON length, or -1 if an event could not be read. */
 void lasp_profile_enable(int on);
+/* Debug only: when non-NULL, tcgen05 core kernels record a clock64 timeline of CTA 0 into the
+ * device buffer (16 events x 64 blocks, unsigned 64-bit). Pass NULL to disable. */
+void lasp_debug_trace(unsigned long long* device_buf);
 int lasp_profile_read(char* buf, size_t cap);
 
 /* Bytes of the caller-owned per-layer KV cache for `shape` (fp32 segment states: the state entering

@@ -10,7 +10,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblasp.so")
+LIB_PATH = os.environ.get("LASP_LIB") or os.path.join(HERE, "liblasp.so")  # LASP_LIB: debug builds
 HEADER = os.path.join(os.path.dirname(HERE), "include", "lasp.h")
 
 LASP_BF16, LASP_FP32 = 0, 1
@@ -42,6 +42,7 @@ _SIGS = {
     "lasp_launch_count": ([], ctypes.c_uint64),
     "lasp_profile_enable": ([ctypes.c_int], None),
     "lasp_profile_read": ([ctypes.c_char_p, ctypes.c_size_t], ctypes.c_int),
+    "lasp_debug_trace": ([_vp], None),
     "lasp_workspace_bytes": ([_sp], ctypes.c_size_t),
     "lasp_segment_len": ([_sp], ctypes.c_int64),
     "lasp_fwd_local": ([_sp, _vp, _vp, _vp, _fp, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),

@@ -33,8 +33,9 @@ def _stale() -> bool:
     return any(os.path.exists(d) and os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    lib = out or LIB
+    if not force and out is None and not _stale():
         return LIB
     objs = []
     jobs = []
@@ -43,6 +44,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
                "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
                "-I", _nccl_include(), "-c", os.path.join(CSRC, src), "-o", obj]
+        if os.environ.get("LASP_TRACE_BUILD"):
+            cmd += ["-DLASP_TRACE_BUILD"]
         if os.environ.get("LASP_PTXAS_VERBOSE"):
             cmd += ["-Xptxas", "-v"]
         jobs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT))
@@ -56,14 +59,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
             failed = True
     if failed:
         raise RuntimeError("nvcc failed")
-    tmp = LIB + f".{os.getpid()}.tmp"
+    tmp = lib + f".{os.getpid()}.tmp"
     subprocess.check_call([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs +
                           ["-ldl", "-lcudart"])
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    out = None
+    if "--out" in sys.argv:
+        out = sys.argv[sys.argv.index("--out") + 1]
+    print(build(force="--force" in sys.argv or out is not None, verbose=True, out=out))

@@ -92,32 +92,37 @@ __global__ void __launch_bounds__(kThreads) seg_state_simt_kernel(Plan p, const 
 // (Alg. 2 P:171 / Alg. 3 P:648 applied between segments). `prefix` may alias `seg_states`.
 __global__ void prefix_kernel(Plan p, Dir dir, const float* __restrict__ init, const float* seg_states,
                               float* prefix, float* __restrict__ final_out) {
+  // one thread per 4 consecutive state elements (float4); segments folded in order
   const int64_t DD = p.D * p.D;
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over B*H*D*D
-  if (idx >= p.B * p.H * DD) return;
-  const int64_t bh = idx / DD, e = idx % DD, h = bh % p.H;
+  const int64_t idx4 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over B*H*D*D/4
+  if (idx4 * 4 >= p.B * p.H * DD) return;
+  const int64_t bh = (idx4 * 4) / DD, e = (idx4 * 4) % DD, h = bh % p.H;
   const float lam = p.lam[h];
+  // every segment has seg_len tokens except possibly the last one (both directions)
+  const int64_t last_len = p.C - (p.nseg - 1) * p.seg_len;
   const float dec_full = powk(lam, double(p.seg_len));
-  float cur = init ? init[idx] : 0.f;
-  // loads are batched ahead of the dependent fold so the chain is not latency-bound
-  constexpr int U = 32;
+  const float dec_last = powk(lam, double(last_len > 0 ? last_len : 0));
+  float4 cur = init ? *reinterpret_cast<const float4*>(init + idx4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* src = seg_states ? seg_states + bh * p.nseg * DD + e : nullptr;
+  float* dst = prefix ? prefix + bh * p.nseg * DD + e : nullptr;
+  constexpr int U = 8;
   for (int64_t s0 = 0; s0 < p.nseg; s0 += U) {
-    float v[U];
+    float4 v[U];
+#pragma unroll
+    for (int t = 0; t < U; ++t)
+      v[t] = (src && s0 + t < p.nseg) ? *reinterpret_cast<const float4*>(src + (s0 + t) * DD) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int t = 0; t < U; ++t) {
-      const int64_t s = s0 + t;
-      v[t] = (s < p.nseg && seg_states) ? seg_states[(bh * p.nseg + s) * DD + e] : 0.f;
-    }
-#pragma unroll
-    for (int t = 0; t < U; ++t) {
-      const int64_t s = s0 + t;
-      if (s >= p.nseg) break;
-      const int64_t len = seg_end(dir, s, p.seg_len, p.C) - seg_begin(dir, s, p.seg_len, p.C);
-      if (prefix) prefix[(bh * p.nseg + s) * DD + e] = cur;
-      cur = fmaf(len == p.seg_len ? dec_full : powk(lam, double(len)), cur, v[t]);
+      const int64_t sg = s0 + t;
+      if (sg < p.nseg) {
+        if (dst) *reinterpret_cast<float4*>(dst + sg * DD) = cur;
+        const float dcy = (sg == p.nseg - 1) ? dec_last : dec_full;
+        cur.x = fmaf(dcy, cur.x, v[t].x); cur.y = fmaf(dcy, cur.y, v[t].y);
+        cur.z = fmaf(dcy, cur.z, v[t].z); cur.w = fmaf(dcy, cur.w, v[t].w);
+      }
     }
   }
-  if (final_out) final_out[idx] = cur;
+  if (final_out) *reinterpret_cast<float4*>(final_out + idx4 * 4) = cur;
 }
 
 // kv_out = lam^C kv_in + local (the ring's combine step, Alg. 2 P:171 with the local part hoisted)
@@ -277,8 +282,8 @@ cudaError_t launch_core_simt(const Plan& p, Dir dir, const SeqArgs& a, cudaStrea
 
 cudaError_t launch_prefix(const Plan& p, Dir dir, const float* init, const float* seg_states, float* prefix_out,
                           float* final_out, cudaStream_t st) {
-  const int64_t n = p.B * p.H * p.D * p.D;
-  const int threads = 256;
+  const int64_t n = p.B * p.H * p.D * p.D / 4;  // D*D is a multiple of 4
+  const int threads = 128;
   prefix_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, st>>>(p, dir, init, seg_states,
                                                                             prefix_out, final_out);
   return cudaGetLastError();

@@ -73,19 +73,15 @@ cudaError_t make_seq_map(CUtensorMap* m, const void* base, const Plan& p) {
   return cudaSuccess;
 }
 
-__device__ __forceinline__ float powk(float lam, double k) { return (float)pow((double)lam, k); }
 
-// scale the 8 bf16 of a 16-byte chunk by w
-__device__ __forceinline__ uint4 scale_chunk(uint4 v, float w) {
+// scale the 8 bf16 of a 16-byte chunk by w (packed bf16x2 multiply; w is rounded to bf16 once)
+__device__ __forceinline__ uint4 scale_chunk(uint4 v, uint32_t w2) {
   uint32_t* u = reinterpret_cast<uint32_t*>(&v);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float lo = __uint_as_float(u[i] << 16) * w;
-    const float hi = __uint_as_float(u[i] & 0xFFFF0000u) * w;
-    u[i] = pack_bf16(lo, hi);
-  }
+  for (int i = 0; i < 4; ++i) asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(u[i]) : "r"(u[i]), "r"(w2));
   return v;
 }
+__device__ __forceinline__ uint32_t bf16x2_splat(float w) { return pack_bf16(w, w); }
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
@@ -95,6 +91,24 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
+}
+
+// segment-state array [B][H][nseg][D][D] fp32 as 2-D rows of D floats, box [32 floats][D rows]
+cudaError_t make_state_map(CUtensorMap* m, const float* base, const Plan& p) {
+  auto fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  cuuint64_t dims[2] = {cuuint64_t(p.D), cuuint64_t(p.B * p.H * p.nseg * p.D)};
+  cuuint64_t strides[1] = {cuuint64_t(p.D * 4)};
+  cuuint32_t box[2] = {32, cuuint32_t(p.D)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(g_tc_err, sizeof g_tc_err, "cuTensorMapEncodeTiled (state) failed (CUresult %d)", int(r));
+    return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
 }
 
 __device__ __forceinline__ uint64_t desc_k(uint32_t addr) { return smem_desc(addr, 16, 1024); }
@@ -108,12 +122,16 @@ struct Item {
   int nblk;
 };
 
-__device__ __forceinline__ Item get_item(const Plan& p, Dir dir, int64_t w) {
-  Item it;
-  it.seg = w % p.nseg;
-  const int64_t bh = w / p.nseg;
-  it.h = bh % p.H;
-  it.b = bh / p.H;
+__device__ __noinline__ Item get_item(const Plan& p, Dir dir, int64_t w) {  // out of line: code size
+  // Segment-major order: the CTAs in flight at any time cover the same token ranges for all
+  // (batch, head) pairs, so the 128-byte head slices of each [H][D] token row are fetched together
+  // (DRAM page locality, L2 sector promotion shared by neighbouring heads).
+  Item it;  // 32-bit decode (the host guarantees B*H*nseg < 2^31): keeps the hot loops small
+  const uint32_t wu = uint32_t(w), nbh = uint32_t(p.B * p.H), nh = uint32_t(p.H);
+  const uint32_t bh = wu % nbh;
+  it.seg = wu / nbh;
+  it.b = bh / nh;
+  it.h = bh - uint32_t(it.b) * nh;
   it.beg = seg_begin(dir, it.seg, p.seg_len, p.C);
   it.end = seg_end(dir, it.seg, p.seg_len, p.C);
   it.nblk = int((it.end - it.beg + BT - 1) / BT);
@@ -261,7 +279,7 @@ __global__ void __launch_bounds__(384, 1) seg_state_tc_kernel(const __grid_const
 #pragma unroll
           for (int c = 0; c < 8; ++c) {  // swizzled chunk order: conflict-free across 8 rows
             const uint32_t a = sbase + L::X(s) + x * BOX + uint32_t(g) * 128 + ((uint32_t(c) ^ (uint32_t(g) & 7)) << 4);
-            sts128(a, scale_chunk(lds128(a), wgt));
+            sts128(a, scale_chunk(lds128(a), bf16x2_splat(wgt)));
           }
         fence_async_smem();
         mbar_arrive(&scaled[s]);
@@ -313,31 +331,45 @@ struct CoreLayout {
   static constexpr uint32_t B_(int s) { return uint32_t(s) * 3 * TILE + TILE; }
   static constexpr uint32_t C_(int s) { return uint32_t(s) * 3 * TILE + 2 * TILE; }
   static constexpr uint32_t KU = STAGES * 3 * TILE;      // u (.) b, [128][D]
-  static constexpr uint32_t P = KU + TILE;               // [128][128] bf16, 2 K-atoms of 16 KB
-  static constexpr uint32_t SBF = P + 2 * BOX;           // [D][D] bf16 hi part of the state
-  static constexpr uint32_t SLO = SBF + D * D * 2;       // [D][D] bf16 lo part (S - hi)
-  static constexpr uint32_t OST = SLO + D * D * 2;       // [128][D] bf16 output staging
-  static constexpr uint32_t BARS = OST + TILE;
-  static constexpr uint32_t BYTES = BARS + 256 + 1024;
-  // TMEM columns
+  // state copies, double-buffered by block parity: [D][D] bf16 hi part and lo part (S - hi)
+  static constexpr uint32_t SBF(int b) { return KU + TILE + uint32_t(b) * 4 * D * D; }
+  static constexpr uint32_t SLO(int b) { return SBF(b) + 2 * D * D; }
+  static constexpr uint32_t OST = KU + TILE + 8 * D * D;  // [128][D] bf16 output staging
+  static constexpr uint32_t STG = OST + TILE;              // [D][D] fp32 segment prefix state (TMA, SW128)
+  static constexpr uint32_t BARS = STG + 4 * D * D;        // barriers (256 B) + mask column factors (512 B)
+  static constexpr uint32_t BYTES = BARS + 256 + 512 + 1024;
+  // TMEM columns (P, bf16, overwrites the first 64 columns of its S buffer: FA4-style TS MMA)
   static constexpr uint32_t T_S0 = 0, T_S1 = 128, T_OI = 256, T_OX = 256 + D, T_DS = 256 + 2 * D;
 };
 
 struct CoreParams {
   CUtensorMap ma, mb, mc, mo;
+  CUtensorMap ms;  // segment prefix states, fp32 2-D [rows = B*H*nseg*D][D], box [32][D], 128B swizzle
   Plan p;
   __nv_bfloat16* out;
   const float* state;
+  unsigned long long* trace;  // debug timeline (lasp_debug_trace), nullptr in production
   int trans;
 };
 
 struct CoreBars {
   uint64_t full[3], empty[3], s_full[2], s_empty[2];
-  uint64_t p_full, p_empty, ku_full, ds_full, ds_empty, st_full, st_empty, o_full, o_empty;
+  uint64_t p_full[2], ku_full, ds_full, ds_empty, st_full[2], st_empty[2], o_full, o_empty;
+  uint64_t stg_full, stg_empty;
   uint32_t tmem_slot;
 };
 
-template <int D, Dir DIR>
+// debug timeline: event ev (0..15) of block J (< 64) of CTA 0 -> trace[ev * 64 + J] = clock64()
+#ifdef LASP_TRACE_BUILD
+#define LASP_TRACE(ev, J)                                                                    \
+  do {                                                                                       \
+    if (prm.trace != nullptr && blockIdx.x == 0 && (J) < 64) prm.trace[(ev) * 64 + (J)] = clock64(); \
+  } while (0)
+#else
+#define LASP_TRACE(ev, J) do { } while (0)
+#endif
+
+template <int D, Dir DIR, bool TRANS>
 __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__ CoreParams prm) {
   using L = CoreLayout<D>;
   constexpr int ST = L::STAGES;
@@ -352,12 +384,14 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
 
   if (threadIdx.x == 0) {
     tma_prefetch(&prm.ma); tma_prefetch(&prm.mb); tma_prefetch(&prm.mc); tma_prefetch(&prm.mo);
+    tma_prefetch(&prm.ms);
+    mbar_init(&bar->stg_full, 1); mbar_init(&bar->stg_empty, 128);
     for (int s = 0; s < ST; ++s) { mbar_init(&bar->full[s], 1); mbar_init(&bar->empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&bar->s_full[s], 1); mbar_init(&bar->s_empty[s], 128); }
-    mbar_init(&bar->p_full, 128); mbar_init(&bar->p_empty, 1);
+    for (int s = 0; s < 2; ++s) { mbar_init(&bar->s_full[s], 1); mbar_init(&bar->s_empty[s], 1); }
+    mbar_init(&bar->p_full[0], 128); mbar_init(&bar->p_full[1], 128);
     mbar_init(&bar->ku_full, 128);
     mbar_init(&bar->ds_full, 1); mbar_init(&bar->ds_empty, 128);
-    mbar_init(&bar->st_full, 128); mbar_init(&bar->st_empty, 1);
+    for (int b2 = 0; b2 < 2; ++b2) { mbar_init(&bar->st_full[b2], 128); mbar_init(&bar->st_empty[b2], 1); }
     mbar_init(&bar->o_full, 1); mbar_init(&bar->o_empty, 128);
     fence_mbar_init();
   }
@@ -370,12 +404,19 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
     if (elect_one()) {
-      uint32_t J = 0;
-      for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+      uint32_t J = 0, k = 0;
+      for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
         const Item it = get_item(p, DIR, w);
+        // the segment's prefix state -> STG (single buffer, released by the state warps)
+        mbar_wait(&bar->stg_empty, (k & 1) ^ 1);
+        mbar_expect_tx(&bar->stg_full, 4 * D * D);
+        const int srow = int(((it.b * p.H + it.h) * p.nseg + it.seg) * D);
+#pragma unroll
+        for (int x = 0; x < D / 32; ++x) tma_load_2d(sm + L::STG + x * (D * 128), &prm.ms, &bar->stg_full, x * 32, srow);
         for (int j = 0; j < it.nblk; ++j, ++J) {
           const int s = J % ST;
           mbar_wait(&bar->empty[s], ((J / ST) & 1) ^ 1);
+          LASP_TRACE(0, J);
           mbar_expect_tx(&bar->full[s], 3 * L::TILE);
           const int t0 = int(block_row(DIR, it, j));
 #pragma unroll
@@ -404,6 +445,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       const long long t_start = clock64();
       uint32_t spins = 0;
       while (!co.done) {
+        bool progress = false;
         // S = a b^T for the next block (double-buffered in TMEM)
         if (!cq.done && cq.J < co.J + 2 && mbar_test(&bar->full[cq.J % ST], (cq.J / ST) & 1) &&
             mbar_test(&bar->s_empty[cq.J & 1], ((cq.J >> 1) & 1) ^ 1)) {
@@ -414,6 +456,8 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           for (int kk = 0; kk < D / 16; ++kk)
             mma_bf16(dt, desc_k(sbase + L::A(s) + koff(kk)), desc_k(sbase + L::B_(s) + koff(kk)), id_qk, kk != 0);
           mma_commit(&bar->s_full[cq.J & 1]);
+          LASP_TRACE(1, cq.J);
+          progress = true;
           cur_next(cq, p, DIR, W);
         }
         // dS = (u . b)^T c (state chain; only for blocks that are not the last of their segment)
@@ -425,34 +469,39 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             mma_bf16(tmem + L::T_DS, desc_mn(sbase + L::KU + kk * 2048, BOX),
                      desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_ds, kk != 0);
           mma_commit(&bar->ds_full);
+          LASP_TRACE(2, cd.J);
+          progress = true;
           ++kd;
           cur_next(cd, p, DIR, W);
           while (!cd.done && cd.j == cd.nblk - 1) cur_next(cd, p, DIR, W);
         }
         // O_intra = P c, O_inter = a (S_hi + S_lo)
         // (out(J) releases the stage, so ds(J) of a non-last block must already be issued)
-        if (co.J < cq.J && (co.j == co.nblk - 1 || cd.done || cd.J > co.J) && mbar_test(&bar->p_full, co.J & 1) && mbar_test(&bar->o_empty, (co.J & 1) ^ 1) &&
-            mbar_test(&bar->st_full, co.J & 1)) {
+        if (co.J < cq.J && (co.j == co.nblk - 1 || cd.done || cd.J > co.J) && mbar_test(&bar->p_full[co.J & 1], (co.J >> 1) & 1) && mbar_test(&bar->o_empty, (co.J & 1) ^ 1) &&
+            mbar_test(&bar->st_full[co.J & 1], (co.J >> 1) & 1)) {
           tc_fence_after();
           const int s = co.J % ST;
+          const uint32_t pt = tmem + ((co.J & 1) ? L::T_S1 : L::T_S0);  // P in TMEM (2 bf16 / column)
 #pragma unroll
           for (int kk = 0; kk < BT / 16; ++kk)
-            mma_bf16(tmem + L::T_OI, desc_k(sbase + L::P + koff(kk)), desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv,
-                     kk != 0);
+            mma_bf16_ts(tmem + L::T_OI, pt + kk * 8, desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv, kk != 0);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
-            mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SBF + kk * 2048, D * 128),
+            mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SBF(co.J & 1) + kk * 2048, D * 128),
                      id_x, kk != 0);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
-            mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SLO + kk * 2048, D * 128),
+            mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SLO(co.J & 1) + kk * 2048, D * 128),
                      id_x, 1);
           mma_commit(&bar->o_full);
-          mma_commit(&bar->p_empty);
-          mma_commit(&bar->st_empty);
+          LASP_TRACE(3, co.J);
+          progress = true;
+          mma_commit(&bar->s_empty[co.J & 1]);  // S/P buffer reusable once P c has been read
+          mma_commit(&bar->st_empty[co.J & 1]);
           mma_commit(&bar->empty[s]);
           cur_next(co, p, DIR, W);
         }
+        if (!progress) __nanosleep(40);  // yield the SMSP to the mask / state / epilogue warps
         if ((++spins & 4095u) == 0) watchdog(t_start);
       }
     }
@@ -460,68 +509,65 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     // ------------------------------------------------------------------ mask warps: S -> P (bf16)
     const uint32_t q4 = warp & 3;
     const int i = int(q4 * 32 + lane);  // query row of the block
+    float* colf = reinterpret_cast<float*>(sm + L::BARS + 256) + q4 * 32;  // per-warp column factors
     uint32_t J = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
       const Item it = get_item(p, DIR, w);
       const float l2 = p.l2lam[it.h];
-      const float lam = p.lam[it.h];
+      // off-diagonal chunks: M_ij = lam^(i-j) = rowf(i, chunk) * colf[u]; colf[u] = lam^(31-u) (FWD)
+      // or lam^u (REV), both in [lam^31, 1] (no overflow); the row factor's exponent is >= 1 there.
+      __syncwarp();
+      colf[lane] = exp2f(float(DIR == Dir::FWD ? 31 - int(lane) : int(lane)) * l2);
+      __syncwarp();
       for (int j = 0; j < it.nblk; ++j, ++J) {
         const int sb = J & 1;
         mbar_wait(&bar->s_full[sb], (J >> 1) & 1);
+        if (lane == 0 && q4 == 3) LASP_TRACE(4, J);
         tc_fence_after();
-        mbar_wait(&bar->p_empty, (J & 1) ^ 1);
         const uint32_t ts = tmem + ((q4 * 32) << 16) + (sb ? L::T_S1 : L::T_S0);
-#pragma unroll
+#pragma unroll 1
         for (int c4 = 0; c4 < 4; ++c4) {
-          // chunk columns [32 c4, 32 c4 + 32); warp rows [32 q4, 32 q4 + 32)
+          // chunk columns [32 c4, 32 c4 + 32) against warp rows [32 q4, 32 q4 + 32):
+          //   FWD e = i - j = R + (31 - u), R = i - 32 c4 - 31;  REV e = j - i = R + u, R = 32 c4 - i
+          //   off-diagonal chunk (R >= 1): M = lam^R * colf[u]; diagonal chunk: M = colf[k], k = u - R (FWD)
+          //   or R + u (REV) when 0 <= k <= 31 (else 0, the causal cut); dead chunk: 0.
           const bool dead = DIR == Dir::FWD ? (c4 > int(q4)) : (c4 < int(q4));
-          float v[32];
-          if (!dead) {
+          uint32_t pk[16];
+          if (dead) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) pk[q] = 0u;
+          } else {
+            float v[32];
             tmem_ld16(ts + c4 * 32, *reinterpret_cast<float(*)[16]>(&v[0]));
             tmem_ld16(ts + c4 * 32 + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
             tmem_ld_wait();
+            const int R = DIR == Dir::FWD ? i - 32 * c4 - 31 : 32 * c4 - i;
+            if (c4 != int(q4)) {
+              const float rowf = exp2f(float(R) * l2);
 #pragma unroll
-            for (int g8 = 0; g8 < 4; ++g8) {
-              // 4 independent chains of 8: M_ij = lam^e, e = i - j (FWD) or j - i (REV)
-              if (DIR == Dir::FWD) {
-                const int e0 = i - c4 * 32 - (8 * g8 + 7);  // exponent at u = 8 g8 + 7
-                float m = exp2f(float(e0 > 0 ? e0 : 0) * l2);
+              for (int u = 0; u < 32; u += 4) {
+                const float4 cf = *reinterpret_cast<const float4*>(&colf[u]);
+                v[u] *= rowf * cf.x; v[u + 1] *= rowf * cf.y; v[u + 2] *= rowf * cf.z; v[u + 3] *= rowf * cf.w;
+              }
+            } else {
 #pragma unroll
-                for (int t = 7; t >= 0; --t) {
-                  const int u = 8 * g8 + t, e = e0 + (7 - t);
-                  if (t < 7) m = (e == 0) ? 1.f : m * lam;
-                  v[u] = (e >= 0) ? v[u] * m : 0.f;
-                }
-              } else {
-                const int e0 = c4 * 32 + 8 * g8 - i;  // exponent at u = 8 g8
-                float m = exp2f(float(e0 > 0 ? e0 : 0) * l2);
-#pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                  const int u = 8 * g8 + t, e = e0 + t;
-                  if (t > 0) m = (e == 0) ? 1.f : m * lam;
-                  v[u] = (e >= 0) ? v[u] * m : 0.f;
-                }
+              for (int u = 0; u < 32; ++u) {
+                const int k = DIR == Dir::FWD ? u - R : R + u;
+                v[u] = (k >= 0 && k <= 31) ? v[u] * colf[k & 31] : 0.f;
               }
             }
-          } else {
 #pragma unroll
-            for (int u = 0; u < 32; ++u) v[u] = 0.f;
+            for (int q = 0; q < 16; ++q) pk[q] = pack_bf16(v[2 * q], v[2 * q + 1]);
           }
-          const uint32_t atom = sbase + L::P + uint32_t(c4 >> 1) * BOX;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 pk;
-            pk.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
-            pk.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
-            pk.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
-            pk.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
-            sts128(atom + sw128_off(uint32_t(i), uint32_t((c4 & 1) * 4 + q)), pk);
-          }
+          // P chunk -> TMEM columns [16 c4, 16 c4 + 16) of the same buffer (already consumed S columns)
+          tmem_st16(ts + c4 * 16, pk);
         }
+        if (lane == 0 && q4 == 3) LASP_TRACE(14, J);
+        tmem_st_wait();
+        if (lane == 0 && q4 == 3) LASP_TRACE(15, J);
         tc_fence_before();
-        mbar_arrive(&bar->s_empty[sb]);
-        fence_async_smem();
-        mbar_arrive(&bar->p_full);
+        mbar_arrive(&bar->p_full[sb]);  // per-buffer: mask(J+1) may finish before out(J) is issued
+        if (lane == 0 && q4 == 3) LASP_TRACE(5, J);
       }
     }
   } else if (warp >= 8 && warp < 12) {
@@ -531,70 +577,79 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     const bool valid = D == 128 || lane < 16;
     const int d = D == 128 ? int(q4 * 32 + lane) : int(q4 * 16 + lane);  // state row (TMEM layout of M = D)
     float S[D];
-    auto load_state = [&](const Item& it) {
-      const float* st0 = prm.state + ((it.b * p.H + it.h) * p.nseg + it.seg) * D * D;
-      if (!valid) {
+    // segment prefix state from STG (TMA, 128B-swizzled fp32 rows of 32 floats): row d of S, or
+    // column d for S^T; both access patterns are (nearly) bank-conflict free
+    auto load_state = [&](uint32_t k) {
+      mbar_wait(&bar->stg_full, k & 1);
+      if (valid) {
+        if (TRANS) {
+          const uint32_t x = uint32_t(d) >> 5, c = (uint32_t(d) & 31) >> 2, wd = uint32_t(d) & 3;
 #pragma unroll
-        for (int e = 0; e < D; ++e) S[e] = 0.f;
-      } else if (prm.trans) {
+          for (int e = 0; e < D; ++e)
+            S[e] = *reinterpret_cast<const float*>(sm + L::STG + x * (D * 128) + e * 128 + ((c ^ (e & 7)) << 4) + wd * 4);
+        } else {
 #pragma unroll
-        for (int e = 0; e < D; ++e) S[e] = __ldg(st0 + int64_t(e) * D + d);
-      } else {
-#pragma unroll
-        for (int e = 0; e < D; e += 4) {
-          const float4 t = __ldg(reinterpret_cast<const float4*>(st0 + int64_t(d) * D + e));
-          S[e] = t.x; S[e + 1] = t.y; S[e + 2] = t.z; S[e + 3] = t.w;
+          for (int e = 0; e < D; e += 4) {
+            const uint32_t x = uint32_t(e) >> 5, c = (uint32_t(e) & 31) >> 2;
+            const float4 t = *reinterpret_cast<const float4*>(sm + L::STG + x * (D * 128) + d * 128 +
+                                                              ((c ^ (uint32_t(d) & 7)) << 4));
+            S[e] = t.x; S[e + 1] = t.y; S[e + 2] = t.z; S[e + 3] = t.w;
+          }
         }
       }
+      mbar_arrive(&bar->stg_empty);
     };
-    auto write_sbf = [&]() {
-      if (valid) {
+    uint32_t J = 0, kd = 0, k = 0;
+    for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
+      const Item it = get_item(p, DIR, w);
+      load_state(k);
+      const float l2 = p.l2lam[it.h];
+      const uint32_t u2 = bf16x2_splat(exp2f(float(DIR == Dir::FWD ? (BT - 1 - g) : (g + 1)) * l2));
+      const float decay = exp2f(float(BT) * l2);
+      // u (.) b for dS = (u . b)^T c of block JJ (the Ku buffer is free once dS of the previous block
+      // has been loaded), done early so the dS MMA is never waiting on it
+      auto scale_ku = [&](uint32_t JJ) {
+        const int s = JJ % ST;
+        mbar_wait(&bar->full[s], (JJ / ST) & 1);
 #pragma unroll
         for (int x = 0; x < L::NBOX; ++x)
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            const float* v = &S[x * 64 + c * 8];
-            uint32_t hi[4], lo[4];
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              hi[t] = pack_bf16(v[2 * t], v[2 * t + 1]);
-              lo[t] = pack_bf16(v[2 * t] - __uint_as_float(hi[t] << 16),
-                                v[2 * t + 1] - __uint_as_float(hi[t] & 0xFFFF0000u));
-            }
-            const uint32_t off = x * (D * 128) + sw128_off(uint32_t(d), uint32_t(c));
-            sts128(sbase + L::SBF + off, make_uint4(hi[0], hi[1], hi[2], hi[3]));
-            sts128(sbase + L::SLO + off, make_uint4(lo[0], lo[1], lo[2], lo[3]));
+            const uint32_t off = x * BOX + uint32_t(g) * 128 + ((uint32_t(c) ^ (uint32_t(g) & 7)) << 4);
+            sts128(sbase + L::KU + off, scale_chunk(lds128(sbase + L::B_(s) + off), u2));
           }
-      }
-      fence_async_smem();
-      mbar_arrive(&bar->st_full);
-    };
-    auto scale_ku = [&](uint32_t J, float u) {
-      const int s = J % ST;
-      mbar_wait(&bar->full[s], (J / ST) & 1);
+        fence_async_smem();
+        mbar_arrive(&bar->ku_full);
+      };
+      if (it.nblk > 1) scale_ku(J);
+      for (int j = 0;; ++j, ++J) {
+        // bf16 hi/lo copy of the state entering block J into buffer J & 1 (free once out(J-2) is done)
+        mbar_wait(&bar->st_empty[J & 1], ((J >> 1) & 1) ^ 1);
+        if (valid) {
 #pragma unroll
-      for (int x = 0; x < L::NBOX; ++x)
+          for (int x = 0; x < L::NBOX; ++x)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t off = x * BOX + uint32_t(g) * 128 + ((uint32_t(c) ^ (uint32_t(g) & 7)) << 4);
-          sts128(sbase + L::KU + off, scale_chunk(lds128(sbase + L::B_(s) + off), u));
+            for (int c = 0; c < 8; ++c) {
+              const float* v = &S[x * 64 + c * 8];
+              uint32_t hi[4], lo[4];
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                hi[t] = pack_bf16(v[2 * t], v[2 * t + 1]);
+                lo[t] = pack_bf16(v[2 * t] - __uint_as_float(hi[t] << 16),
+                                  v[2 * t + 1] - __uint_as_float(hi[t] & 0xFFFF0000u));
+              }
+              const uint32_t off = x * (D * 128) + sw128_off(uint32_t(d), uint32_t(c));
+              sts128(sbase + L::SBF(J & 1) + off, make_uint4(hi[0], hi[1], hi[2], hi[3]));
+              sts128(sbase + L::SLO(J & 1) + off, make_uint4(lo[0], lo[1], lo[2], lo[3]));
+            }
         }
-      fence_async_smem();
-      mbar_arrive(&bar->ku_full);
-    };
-    uint32_t J = 0, kd = 0;
-    int64_t w = blockIdx.x;
-    Item it;
-    if (w < W) { it = get_item(p, DIR, w); load_state(it); }
-    for (; w < W;) {
-      const float l2 = p.l2lam[it.h];
-      const float u = exp2f(float(DIR == Dir::FWD ? (BT - 1 - g) : (g + 1)) * l2);
-      const float decay = exp2f(float(BT) * l2);
-      if (J > 0) mbar_wait(&bar->st_empty, (J - 1) & 1);
-      write_sbf();                                   // state entering block J (segment prefix)
-      if (it.nblk > 1) scale_ku(J, u);
-      for (int j = 0; j + 1 < it.nblk; ++j, ++J) {
+        fence_async_smem();
+        mbar_arrive(&bar->st_full[J & 1]);
+        if (g == 0) LASP_TRACE(7, J);
+        if (j + 1 == it.nblk) break;  // no state leaves the last block of a segment
+        // S_{J+1} = lam^128 S_J + dS_J
         mbar_wait(&bar->ds_full, kd & 1);
+        if (g == 0) LASP_TRACE(6, J);
         tc_fence_after();
         const uint32_t td = tmem + ((q4 * 32) << 16) + L::T_DS;
 #pragma unroll
@@ -608,13 +663,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         tc_fence_before();
         mbar_arrive(&bar->ds_empty);
         ++kd;
-        if (j + 2 < it.nblk) scale_ku(J + 1, u);
-        mbar_wait(&bar->st_empty, J & 1);
-        write_sbf();                                 // state entering block J + 1
+        if (j + 2 < it.nblk) scale_ku(J + 1);
       }
-      ++J;  // past the last block of this segment
-      w += gridDim.x;
-      if (w < W) { it = get_item(p, DIR, w); load_state(it); }  // overlaps the last block's MMAs
+      ++J;  // the break skipped the increment of the last block
     }
   } else if (warp >= 12) {
     // ------------------------------------------------------------------ epilogue warps
@@ -627,6 +678,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       const float r = exp2f(float(DIR == Dir::FWD ? (i + 1) : (BT - 1 - i)) * p.l2lam[it.h]);
       for (int j = 0; j < it.nblk; ++j, ++J) {
         mbar_wait(&bar->o_full, J & 1);
+        if (i == 0) LASP_TRACE(8, J);
         tc_fence_after();
         const uint32_t ti = tmem + ((q4 * 32) << 16) + L::T_OI;
         const uint32_t tx = tmem + ((q4 * 32) << 16) + L::T_OX;
@@ -655,6 +707,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           }
           continue;
         }
+        const uint32_t ob = L::OST;
         if (leader) tma_store_wait_read<0>();
         named_bar_sync(1, 128);
 #pragma unroll
@@ -662,14 +715,15 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const uint32_t* v = &pk[x * 32 + c * 4];
-            sts128(sbase + L::OST + x * BOX + sw128_off(uint32_t(i), uint32_t(c)), make_uint4(v[0], v[1], v[2], v[3]));
+            sts128(sbase + ob + x * BOX + sw128_off(uint32_t(i), uint32_t(c)), make_uint4(v[0], v[1], v[2], v[3]));
           }
         fence_async_smem();
         named_bar_sync(1, 128);
         if (leader) {
 #pragma unroll
-          for (int x = 0; x < L::NBOX; ++x) tma_store_4d(&prm.mo, sm + L::OST + x * BOX, x * 64, int(it.h), t0, int(it.b));
+          for (int x = 0; x < L::NBOX; ++x) tma_store_4d(&prm.mo, sm + ob + x * BOX, x * 64, int(it.h), t0, int(it.b));
           tma_store_commit();
+          LASP_TRACE(9, J);
         }
       }
     }
@@ -679,6 +733,8 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
+
+unsigned long long* g_trace = nullptr;
 
 int sm_count() {
   static int n = 0;
@@ -719,11 +775,13 @@ cudaError_t launch_core(const Plan& p, const SeqArgs& a, cudaStream_t st) {
   if ((e = make_seq_map(&prm.mb, a.b, p)) != cudaSuccess) return e;
   if ((e = make_seq_map(&prm.mc, a.c, p)) != cudaSuccess) return e;
   if ((e = make_seq_map(&prm.mo, a.out, p)) != cudaSuccess) return e;
+  if ((e = make_state_map(&prm.ms, a.state, p)) != cudaSuccess) return e;
   prm.p = p;
   prm.out = static_cast<__nv_bfloat16*>(a.out);
   prm.state = a.state;
   prm.trans = a.trans_state;
-  auto kern = core_tc_kernel<D, DIR>;
+  prm.trace = g_trace;
+  auto kern = a.trans_state ? core_tc_kernel<D, DIR, true> : core_tc_kernel<D, DIR, false>;
   const int smem = int(CoreLayout<D>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
   kern<<<persistent_grid(p), 512, smem, st>>>(prm);
@@ -733,6 +791,8 @@ cudaError_t launch_core(const Plan& p, const SeqArgs& a, cudaStream_t st) {
 }  // namespace
 
 const char* tc_last_error() { return g_tc_err; }
+
+void tc_set_trace(unsigned long long* buf) { g_trace = buf; }
 
 bool tc_supported(const Plan& p) {
   static const bool disabled = [] {

@@ -347,6 +347,8 @@ const char* lasp_last_error(void) { return g_err.c_str(); }
 
 uint64_t lasp_launch_count(void) { return g_launches.load(); }
 
+void lasp_debug_trace(unsigned long long* device_buf) { tc_set_trace(device_buf); }
+
 void lasp_profile_enable(int on) { g_profile.store(on ? 1 : 0); }
 
 int lasp_profile_read(char* buf, size_t cap) {

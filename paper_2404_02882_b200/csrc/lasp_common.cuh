@@ -62,7 +62,8 @@ cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local
 
 // tcgen05 path (bf16 only); returns cudaErrorNotSupported when the shape is not covered.
 bool tc_supported(const Plan& p);
-const char* tc_last_error();  // detail of the last tcgen05-path host failure on this thread
+const char* tc_last_error();
+void tc_set_trace(unsigned long long* buf);  // debug: per-block clock64 timeline of CTA 0  // detail of the last tcgen05-path host failure on this thread
 cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out,
                                 cudaStream_t st);
 cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st);

@@ -1,0 +1,19 @@
+"""Timeline of CTA 0 of the tcgen05 core kernel (cycles relative to the first event)."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch, synth
+import paper_2404_02882_b200 as L
+from paper_2404_02882_b200 import _native as N
+p = synth.problem(0, 1, 32768, 16, 64, dtype="bf16", with_do=False)
+q, k, v = (torch.from_numpy(p[x]).cuda().to(torch.bfloat16) for x in ("q", "k", "v"))
+L.fwd_local(q, k, v, p["lam"]); torch.cuda.synchronize()
+buf = torch.zeros(16 * 64, dtype=torch.int64, device="cuda")
+N.lib().lasp_debug_trace(ctypes.c_void_p(buf.data_ptr()))
+L.fwd_local(q, k, v, p["lam"]); torch.cuda.synchronize()
+N.lib().lasp_debug_trace(None)
+t = buf.cpu().numpy().reshape(16, 64).astype(np.int64)
+base = t[t > 0].min()
+names = ["tma_issue", "qk_iss", "ds_iss", "out_iss", "mask_beg", "mask_end", "ds_ready", "sbf_next", "o_full", "store", "ld0", "ld1", "ld2", "ld3", "st_iss", "st_done"]
+print("J   " + " ".join(f"{n:>9s}" for n in names))
+for J in range(int(sys.argv[1]) if len(sys.argv) > 1 else 30):
+    print(f"{J:3d} " + " ".join(f"{(t[e, J] - base) if t[e, J] else -1:9d}" for e in range(len(names))))
