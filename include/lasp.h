@@ -143,6 +143,11 @@ lasp_status_t lasp_unique_id(uint8_t id[128]);
 lasp_status_t lasp_ctx_create(int rank, int world, const uint8_t id[128], int device, lasp_ctx_t* out);
 lasp_status_t lasp_ctx_destroy(lasp_ctx_t ctx);
 
+/* Ring schedule (host-only, no GPU): the peer this rank receives its state from and sends its state to
+ * (-1 = none). Forward (backward = 0): from r-1, to r+1 (Alg. 2); backward: from r+1, to r-1
+ * (Alg. 3, reading A2 of P:649). Used by lasp_fwd/lasp_bwd; exposed for protocol tests. */
+lasp_status_t lasp_ring_peers(int rank, int world, int backward, int* recv_from, int* send_to);
+
 /* Messages and fp32 elements per message this ctx will send per direction per call (protocol
  * introspection for tests: world-1 hops in total, this rank sends 0 or 1). */
 lasp_status_t lasp_ctx_protocol(lasp_ctx_t ctx, const lasp_shape_t* shape, int64_t* sends_fwd,

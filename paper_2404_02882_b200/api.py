@@ -106,6 +106,13 @@ def bwd_local(q, k, v, lam, do, cache, dkv_in=None, *, dq=None, dk=None, dv=None
     return dq, dk, dv, dkv_out_t
 
 
+def ring_peers(rank: int, world: int, backward: bool) -> tuple[int, int]:
+    """(recv_from, send_to) of the library's ring schedule (-1 = none); host-only."""
+    a, b = ctypes.c_int(), ctypes.c_int()
+    N.check(N.lib().lasp_ring_peers(rank, world, int(backward), ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
 class Ring:
     """The LASP ring over the default torch.distributed group: rank r owns tokens [rC, (r+1)C)
     (Alg. 1 with T = W). Rank 0 creates the NCCL id; torch broadcasts it."""

@@ -480,13 +480,29 @@ lasp_status_t lasp_ctx_destroy(lasp_ctx_t c) {
   return LASP_OK;
 }
 
+lasp_status_t lasp_ring_peers(int rank, int world, int backward, int* recv_from, int* send_to) {
+  if (!recv_from || !send_to) return fail(LASP_ERR_SHAPE, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(LASP_ERR_PARTITION, "rank outside [0, world)");
+  if (!backward) {  // Alg. 2: Recv KV_{t-1} from i-1, Send KV_t to i+1
+    *recv_from = rank > 0 ? rank - 1 : -1;
+    *send_to = rank < world - 1 ? rank + 1 : -1;
+  } else {          // Alg. 3: Recv dKV_{t+1} from i+1, Send dKV_t to i-1 (reading A2)
+    *recv_from = rank < world - 1 ? rank + 1 : -1;
+    *send_to = rank > 0 ? rank - 1 : -1;
+  }
+  return LASP_OK;
+}
+
 lasp_status_t lasp_ctx_protocol(lasp_ctx_t c, const lasp_shape_t* shape, int64_t* sends_fwd, int64_t* sends_bwd,
                                 int64_t* elems_per_msg) {
   if (!c) return fail(LASP_ERR_SHAPE, "ctx is NULL");
   lasp_status_t s = validate_shape(shape);
   if (s != LASP_OK) return s;
-  if (sends_fwd) *sends_fwd = c->rank < c->world - 1 ? 1 : 0;  // Alg. 2: send to i+1
-  if (sends_bwd) *sends_bwd = c->rank > 0 ? 1 : 0;             // Alg. 3 P:649 (reading A2): to i-1
+  int f = -1, t = -1;
+  lasp_ring_peers(c->rank, c->world, 0, &f, &t);
+  if (sends_fwd) *sends_fwd = t >= 0 ? 1 : 0;  // Alg. 2: send to i+1
+  lasp_ring_peers(c->rank, c->world, 1, &f, &t);
+  if (sends_bwd) *sends_bwd = t >= 0 ? 1 : 0;  // Alg. 3 P:649 (reading A2): to i-1
   if (elems_per_msg) *elems_per_msg = shape->batch * shape->heads * shape->head_dim * shape->head_dim;
   return LASP_OK;
 }
@@ -503,19 +519,21 @@ lasp_status_t lasp_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   Workspace w = carve(p, workspace);
   const size_t n = state_elems(p);
   NcclApi& nc = nccl();
+  int from = -1, to = -1;
+  lasp_ring_peers(c->rank, c->world, 0, &from, &to);
   if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st));                     // F1
   LASP_CUDA(prefix(p, Dir::FWD, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
   // F2 ring hop: Recv KV_in from r-1 (Alg. 2), combine, Send to r+1
-  if (c->rank > 0) {
-    ncclResult_t r = nc.Recv(w.in, n, ncclFloat32, c->rank - 1, c->comm, st);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclRecv(KV)", c->rank, c->rank - 1);
+  if (from >= 0) {
+    ncclResult_t r = nc.Recv(w.in, n, ncclFloat32, from, c->comm, st);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclRecv(KV)", c->rank, from);
   } else {
     LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), st));
   }
-  if (c->rank < c->world - 1) {
+  if (to >= 0) {
     LASP_CUDA(combine(p, w.in, w.local, w.out, st));
-    ncclResult_t r = nc.Send(w.out, n, ncclFloat32, c->rank + 1, c->comm, st);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclSend(KV)", c->rank, c->rank + 1);
+    ncclResult_t r = nc.Send(w.out, n, ncclFloat32, to, c->comm, st);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclSend(KV)", c->rank, to);
   }
   if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, st)) != LASP_OK) return s;  // F2 + F3
   register_cache(p, cache, c->rank, c->world);
@@ -542,16 +560,18 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   // B2 ring hop on the comm stream: Recv dKV_in from r+1 (Alg. 3), combine, Send to r-1
   LASP_CUDA(cudaEventRecord(c->ev_ready, st));
   LASP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
-  if (c->rank < c->world - 1) {
-    ncclResult_t r = nc.Recv(w.in, n, ncclFloat32, c->rank + 1, c->comm, c->comm_stream);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclRecv(dKV)", c->rank, c->rank + 1);
+  int from = -1, to = -1;
+  lasp_ring_peers(c->rank, c->world, 1, &from, &to);
+  if (from >= 0) {
+    ncclResult_t r = nc.Recv(w.in, n, ncclFloat32, from, c->comm, c->comm_stream);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclRecv(dKV)", c->rank, from);
   } else {
     LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), c->comm_stream));
   }
-  if (c->rank > 0) {
+  if (to >= 0) {
     LASP_CUDA(combine(p, w.in, w.local, w.out, c->comm_stream));
-    ncclResult_t r = nc.Send(w.out, n, ncclFloat32, c->rank - 1, c->comm, c->comm_stream);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclSend(dKV)", c->rank, c->rank - 1);
+    ncclResult_t r = nc.Send(w.out, n, ncclFloat32, to, c->comm, c->comm_stream);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclSend(dKV)", c->rank, to);
   }
   LASP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
   // dQ needs only the cache: it runs while the dKV hop is in flight
