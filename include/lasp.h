@@ -102,7 +102,8 @@ uint64_t lasp_launch_count(void);
  * records; returns the JSON length, or -1 if an event could not be read. */
 void lasp_profile_enable(int on);
 /* Debug only: when non-NULL, tcgen05 core kernels record a clock64 timeline of CTA 0 into the
- * device buffer (16 events x 64 blocks, unsigned 64-bit). Pass NULL to disable. */
+ * device buffer (2 regions of 16 events x 64 blocks, unsigned 64-bit: core kernel, then segment-state
+ * kernel). Pass NULL to disable. */
 void lasp_debug_trace(unsigned long long* device_buf);
 int lasp_profile_read(char* buf, size_t cap);
 

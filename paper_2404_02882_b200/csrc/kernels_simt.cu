@@ -37,6 +37,8 @@ template <typename T, int D, Dir DIR>
 __global__ void __launch_bounds__(kThreads) seg_state_simt_kernel(Plan p, const T* __restrict__ x,
                                                                   const T* __restrict__ y,
                                                                   float* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int TT = 32;        // tokens per smem tile
   constexpr int R = D / 16;     // per-thread register tile R x R
   __shared__ float xs[TT][D + 1];
@@ -92,6 +94,8 @@ __global__ void __launch_bounds__(kThreads) seg_state_simt_kernel(Plan p, const 
 // (Alg. 2 P:171 / Alg. 3 P:648 applied between segments). `prefix` may alias `seg_states`.
 __global__ void prefix_kernel(Plan p, Dir dir, const float* __restrict__ init, const float* seg_states,
                               float* prefix, float* __restrict__ final_out) {
+  pdl_trigger();
+  pdl_wait();
   // one thread per 4 consecutive state elements (float4); segments folded in order
   const int64_t DD = p.D * p.D;
   const int64_t idx4 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over B*H*D*D/4
@@ -105,7 +109,7 @@ __global__ void prefix_kernel(Plan p, Dir dir, const float* __restrict__ init, c
   float4 cur = init ? *reinterpret_cast<const float4*>(init + idx4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
   const float* src = seg_states ? seg_states + bh * p.nseg * DD + e : nullptr;
   float* dst = prefix ? prefix + bh * p.nseg * DD + e : nullptr;
-  constexpr int U = 8;
+  constexpr int U = 16;
   for (int64_t s0 = 0; s0 < p.nseg; s0 += U) {
     float4 v[U];
 #pragma unroll
@@ -128,6 +132,8 @@ __global__ void prefix_kernel(Plan p, Dir dir, const float* __restrict__ init, c
 // kv_out = lam^C kv_in + local (the ring's combine step, Alg. 2 P:171 with the local part hoisted)
 __global__ void combine_kernel(Plan p, const float* __restrict__ kv_in,
                                const float* __restrict__ local, float* __restrict__ kv_out) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t DD = p.D * p.D;
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= p.B * p.H * DD) return;
@@ -141,6 +147,8 @@ __global__ void combine_kernel(Plan p, const float* __restrict__ kv_in,
 // state S in shared memory (fp32).
 template <typename T, int D, Dir DIR>
 __global__ void __launch_bounds__(kThreads) core_simt_kernel(Plan p, SeqArgs a) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int BT = 32;
   extern __shared__ float smem[];
   float* sa = smem;                  // [BT][D+1]
@@ -228,9 +236,9 @@ cudaError_t seg_state_dispatch_dir(const Plan& p, Dir dir, const void* x, const 
                                    cudaStream_t st) {
   dim3 grid((unsigned)p.nseg, (unsigned)p.H, (unsigned)p.B);
   if (dir == Dir::FWD)
-    seg_state_simt_kernel<T, D, Dir::FWD><<<grid, kThreads, 0, st>>>(p, (const T*)x, (const T*)y, out);
+    return launch_k(seg_state_simt_kernel<T, D, Dir::FWD>, grid, dim3(kThreads), 0, st, p, (const T*)x, (const T*)y, out);
   else
-    seg_state_simt_kernel<T, D, Dir::REV><<<grid, kThreads, 0, st>>>(p, (const T*)x, (const T*)y, out);
+    return launch_k(seg_state_simt_kernel<T, D, Dir::REV>, grid, dim3(kThreads), 0, st, p, (const T*)x, (const T*)y, out);
   return cudaGetLastError();
 }
 
@@ -242,8 +250,7 @@ cudaError_t core_launch(const Plan& p, const SeqArgs& a, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)p.nseg, (unsigned)p.H, (unsigned)p.B);
-  kern<<<grid, kThreads, smem, st>>>(p, a);
-  return cudaGetLastError();
+  return launch_k(kern, grid, dim3(kThreads), smem, st, p, a);
 }
 
 template <typename T>
@@ -283,17 +290,16 @@ cudaError_t launch_core_simt(const Plan& p, Dir dir, const SeqArgs& a, cudaStrea
 cudaError_t launch_prefix(const Plan& p, Dir dir, const float* init, const float* seg_states, float* prefix_out,
                           float* final_out, cudaStream_t st) {
   const int64_t n = p.B * p.H * p.D * p.D / 4;  // D*D is a multiple of 4
-  const int threads = 128;
-  prefix_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, st>>>(p, dir, init, seg_states,
-                                                                            prefix_out, final_out);
-  return cudaGetLastError();
+  const int threads = 64;
+  return launch_k(prefix_kernel, dim3((unsigned)((n + threads - 1) / threads)), dim3(threads), 0, st, p, dir, init,
+                  seg_states, prefix_out, final_out);
 }
 
 cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local, float* kv_out, cudaStream_t st) {
   const int64_t n = p.B * p.H * p.D * p.D;
   const int threads = 256;
-  combine_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, st>>>(p, kv_in, local, kv_out);
-  return cudaGetLastError();
+  return launch_k(combine_kernel, dim3((unsigned)((n + threads - 1) / threads)), dim3(threads), 0, st, p, kv_in, local,
+                  kv_out);
 }
 
 }  // namespace lasp

@@ -51,6 +51,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 thread_local char g_tc_err[256];
+unsigned long long* g_trace = nullptr;  // debug timeline buffer (lasp_debug_trace)
 
 cudaError_t make_seq_map(CUtensorMap* m, const void* base, const Plan& p) {
   auto fn = encode_fn();
@@ -175,7 +176,8 @@ template <int D>
 struct SegLayout {
   static constexpr int NBOX = D / 64;
   static constexpr uint32_t TILE = NBOX * BOX;
-  static constexpr int STAGES = D == 64 ? 4 : 2;
+  static constexpr int STAGES = D == 64 ? 3 : 2;
+  static constexpr int CTAS_PER_SM = D == 64 ? 2 : 1;  // 2 x (96 KB smem, 128 TMEM columns) per SM
   static constexpr uint32_t X(int s) { return uint32_t(s) * 2 * TILE; }
   static constexpr uint32_t Y(int s) { return uint32_t(s) * 2 * TILE + TILE; }
   static constexpr uint32_t BARS = STAGES * 2 * TILE;
@@ -187,10 +189,21 @@ struct SegParams {
   CUtensorMap mx, my;
   Plan p;
   float* out;
+  unsigned long long* trace;
 };
 
+// debug timeline: event ev (0..15) of block J (< 64) of CTA 0 -> trace[ev * 64 + J] = clock64()
+#ifdef LASP_TRACE_BUILD
+#define LASP_TRACE(ev, J)                                                                    \
+  do {                                                                                       \
+    if (prm.trace != nullptr && blockIdx.x == 0 && (J) < 64) prm.trace[(ev) * 64 + (J)] = clock64(); \
+  } while (0)
+#else
+#define LASP_TRACE(ev, J) do { } while (0)
+#endif
+
 template <int D, Dir DIR>
-__global__ void __launch_bounds__(384, 1) seg_state_tc_kernel(const __grid_constant__ SegParams prm) {
+__global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_constant__ SegParams prm) {
   using L = SegLayout<D>;
   constexpr int ST = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -214,11 +227,13 @@ __global__ void __launch_bounds__(384, 1) seg_state_tc_kernel(const __grid_const
     for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], 128); }
     fence_mbar_init();
   }
+  pdl_trigger();
   if (warp == 1) tmem_alloc<L::TCOLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the previous kernel of the stream has completed and its writes are visible
 
   if (warp == 0) {
     if (elect_one()) {
@@ -228,6 +243,7 @@ __global__ void __launch_bounds__(384, 1) seg_state_tc_kernel(const __grid_const
         for (int j = 0; j < it.nblk; ++j, ++J) {
           const int s = J % ST;
           mbar_wait(&empty[s], ((J / ST) & 1) ^ 1);
+          LASP_TRACE(0, J);
           mbar_expect_tx(&full[s], 2 * L::TILE);
           const int t0 = int(block_row(DIR, it, j));
 #pragma unroll
@@ -250,6 +266,7 @@ __global__ void __launch_bounds__(384, 1) seg_state_tc_kernel(const __grid_const
         for (int j = 0; j < it.nblk; ++j, ++J) {
           const int s = J % ST;
           mbar_wait(&scaled[s], (J / ST) & 1);
+          LASP_TRACE(3, J);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < BT / 16; ++kk)
@@ -270,6 +287,7 @@ __global__ void __launch_bounds__(384, 1) seg_state_tc_kernel(const __grid_const
       for (int j = 0; j < it.nblk; ++j, ++J) {
         const int s = J % ST;
         mbar_wait(&full[s], (J / ST) & 1);
+        if (g == 0) LASP_TRACE(1, J);
         const int64_t pos = block_row(DIR, it, j) + g;
         float wgt = 0.f;
         if (pos >= it.beg && pos < it.end)
@@ -283,6 +301,7 @@ __global__ void __launch_bounds__(384, 1) seg_state_tc_kernel(const __grid_const
           }
         fence_async_smem();
         mbar_arrive(&scaled[s]);
+        if (g == 0) LASP_TRACE(2, J);
       }
     }
   } else if (warp >= 8) {
@@ -359,15 +378,7 @@ struct CoreBars {
   uint32_t tmem_slot;
 };
 
-// debug timeline: event ev (0..15) of block J (< 64) of CTA 0 -> trace[ev * 64 + J] = clock64()
-#ifdef LASP_TRACE_BUILD
-#define LASP_TRACE(ev, J)                                                                    \
-  do {                                                                                       \
-    if (prm.trace != nullptr && blockIdx.x == 0 && (J) < 64) prm.trace[(ev) * 64 + (J)] = clock64(); \
-  } while (0)
-#else
-#define LASP_TRACE(ev, J) do { } while (0)
-#endif
+
 
 template <int D, Dir DIR, bool TRANS>
 __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__ CoreParams prm) {
@@ -395,11 +406,13 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     mbar_init(&bar->o_full, 1); mbar_init(&bar->o_empty, 128);
     fence_mbar_init();
   }
+  pdl_trigger();
   if (warp == 1) tmem_alloc<512>(&bar->tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bar->tmem_slot;
+  pdl_wait();  // the previous kernel of the stream has completed and its writes are visible
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
@@ -734,8 +747,6 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
-unsigned long long* g_trace = nullptr;
-
 int sm_count() {
   static int n = 0;
   if (n == 0) {
@@ -746,9 +757,9 @@ int sm_count() {
   return n;
 }
 
-unsigned persistent_grid(const Plan& p) {
+unsigned persistent_grid(const Plan& p, int per_sm = 1) {
   const int64_t W = p.B * p.H * p.nseg;
-  const int64_t g = W < sm_count() ? W : sm_count();
+  const int64_t g = W < int64_t(sm_count()) * per_sm ? W : int64_t(sm_count()) * per_sm;
   return unsigned(g > 0 ? g : 1);
 }
 
@@ -760,11 +771,11 @@ cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, 
   if ((e = make_seq_map(&prm.my, y, p)) != cudaSuccess) return e;
   prm.p = p;
   prm.out = out;
+  prm.trace = g_trace ? g_trace + 16 * 64 : nullptr;  // second trace region: segment-state kernel
   auto kern = seg_state_tc_kernel<D, DIR>;
   const int smem = int(SegLayout<D>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
-  kern<<<persistent_grid(p), 384, smem, st>>>(prm);
-  return cudaGetLastError();
+  return launch_k(kern, dim3(persistent_grid(p, SegLayout<D>::CTAS_PER_SM)), dim3(384), smem, st, prm);
 }
 
 template <int D, Dir DIR>
@@ -784,8 +795,7 @@ cudaError_t launch_core(const Plan& p, const SeqArgs& a, cudaStream_t st) {
   auto kern = a.trans_state ? core_tc_kernel<D, DIR, true> : core_tc_kernel<D, DIR, false>;
   const int smem = int(CoreLayout<D>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
-  kern<<<persistent_grid(p), 512, smem, st>>>(prm);
-  return cudaGetLastError();
+  return launch_k(kern, dim3(persistent_grid(p)), dim3(512), smem, st, prm);
 }
 
 }  // namespace

@@ -13,10 +13,42 @@
 //   ragged block only ever sits where no state leaves it.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
 namespace lasp {
+
+// Programmatic dependent launch: every kernel of the path is launched with programmatic stream
+// serialization; a kernel signals its dependents at entry and waits for its prerequisite grid before
+// touching global memory, so a kernel's prologue (TMEM alloc, barrier init, descriptor prefetch) and
+// its CTAs' start overlap the previous kernel's tail. LASP_NO_PDL=1 disables it (debugging).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* s = std::getenv("LASP_NO_PDL");
+    return !(s && *s && *s != '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 enum class Dir : int { FWD = 0, REV = 1 };
 

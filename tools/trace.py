@@ -7,11 +7,11 @@ from paper_2404_02882_b200 import _native as N
 p = synth.problem(0, 1, 32768, 16, 64, dtype="bf16", with_do=False)
 q, k, v = (torch.from_numpy(p[x]).cuda().to(torch.bfloat16) for x in ("q", "k", "v"))
 L.fwd_local(q, k, v, p["lam"]); torch.cuda.synchronize()
-buf = torch.zeros(16 * 64, dtype=torch.int64, device="cuda")
+buf = torch.zeros(2 * 16 * 64, dtype=torch.int64, device="cuda")
 N.lib().lasp_debug_trace(ctypes.c_void_p(buf.data_ptr()))
 L.fwd_local(q, k, v, p["lam"]); torch.cuda.synchronize()
 N.lib().lasp_debug_trace(None)
-t = buf.cpu().numpy().reshape(16, 64).astype(np.int64)
+t = buf.cpu().numpy().reshape(2, 16, 64)[0].astype(np.int64)
 base = t[t > 0].min()
 names = ["tma_issue", "qk_iss", "ds_iss", "out_iss", "mask_beg", "mask_end", "ds_ready", "sbf_next", "o_full", "store", "ld0", "ld1", "ld2", "ld3", "st_iss", "st_done"]
 print("J   " + " ".join(f"{n:>9s}" for n in names))
