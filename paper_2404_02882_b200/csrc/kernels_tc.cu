@@ -392,6 +392,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   const Plan& p = prm.p;
   const int64_t W = p.B * p.H * p.nseg;
   const uint32_t warp = warp_id(), lane = lane_id();
+#ifdef LASP_TRACE_BUILD
+  if (prm.trace != nullptr && threadIdx.x == 0) prm.trace[2 * 1024 + blockIdx.x * 2] = globaltimer();
+#endif
 
   if (threadIdx.x == 0) {
     tma_prefetch(&prm.ma); tma_prefetch(&prm.mb); tma_prefetch(&prm.mc); tma_prefetch(&prm.mo);
@@ -744,6 +747,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   }
   tc_fence_before();
   __syncthreads();
+#ifdef LASP_TRACE_BUILD
+  if (prm.trace != nullptr && threadIdx.x == 0) prm.trace[2 * 1024 + blockIdx.x * 2 + 1] = globaltimer();
+#endif
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
