@@ -114,12 +114,14 @@ __global__ void prefix_kernel(Plan p, Dir dir, const float* __restrict__ init, c
   for (int64_t s0 = 0; s0 < p.nseg; s0 += U) {
     float4 v[U];
 #pragma unroll
-    for (int t = 0; t < U; ++t)
-      v[t] = (src && s0 + t < p.nseg) ? *reinterpret_cast<const float4*>(src + (s0 + t) * DD) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int t = 0; t < U; ++t) {
+      const int64_t sg = dir == Dir::FWD ? s0 + t : p.nseg - 1 - (s0 + t);  // REV folds from the rank end
+      v[t] = (src && s0 + t < p.nseg) ? *reinterpret_cast<const float4*>(src + sg * DD) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
 #pragma unroll
     for (int t = 0; t < U; ++t) {
-      const int64_t sg = s0 + t;
-      if (sg < p.nseg) {
+      const int64_t sg = dir == Dir::FWD ? s0 + t : p.nseg - 1 - (s0 + t);
+      if (s0 + t < p.nseg) {
         if (dst) *reinterpret_cast<float4*>(dst + sg * DD) = cur;
         const float dcy = (sg == p.nseg - 1) ? dec_last : dec_full;
         cur.x = fmaf(dcy, cur.x, v[t].x); cur.y = fmaf(dcy, cur.y, v[t].y);

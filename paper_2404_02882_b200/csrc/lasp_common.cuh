@@ -9,7 +9,7 @@
 //                              S'    = lam^BT S + sum_s lam^(s+1) b_s c_s^T
 //   with (a,b,c,S) = (Q,K,V,KV) for O, (dO,V,K,KV^T) for dQ, (K,Q,dO,dKV) for dV and
 //   (V,dO,Q,dKV^T) for dK (Eq. 4 and Eq. 13 rewritten; the REV state has exponent starting at 1,
-//   reading A3). FWD segments are aligned to the rank start, REV segments to the rank end, so a
+//   reading A3). Segments are aligned to the rank start in both directions (see seg_begin), so a
 //   ragged block only ever sits where no state leaves it.
 #pragma once
 #include <cstdint>
@@ -64,15 +64,14 @@ constexpr int64_t kMaxHeads = 256;
 
 constexpr int64_t kSegQuantum = 128;  // every kernel's block size divides this
 
-// Segment p geometry. FWD: [p*L, min((p+1)*L, C)). REV (end-aligned): [max(0, C-(p+1)L), C-p*L).
-__host__ __device__ inline int64_t seg_begin(Dir dir, int64_t p, int64_t L, int64_t C) {
-  if (dir == Dir::FWD) return p * L;
-  int64_t b = C - (p + 1) * L;
-  return b < 0 ? 0 : b;
-}
-__host__ __device__ inline int64_t seg_end(Dir dir, int64_t p, int64_t L, int64_t C) {
-  if (dir == Dir::FWD) { int64_t e = (p + 1) * L; return e > C ? C : e; }
-  return C - p * L;
+// Segment p geometry (both directions): [p*L, min((p+1)*L, C)). FWD blocks ascend from the segment
+// begin, REV blocks descend from the segment end, so a ragged block is the last one processed in its
+// segment (no state leaves it); REV folds segments from p = nseg-1 down to 0. Using the same token
+// ranges in both directions lets the backward passes of one segment run side by side (L2 reuse).
+__host__ __device__ inline int64_t seg_begin(Dir, int64_t p, int64_t L, int64_t) { return p * L; }
+__host__ __device__ inline int64_t seg_end(Dir, int64_t p, int64_t L, int64_t C) {
+  const int64_t e = (p + 1) * L;
+  return e > C ? C : e;
 }
 
 // Kernel launch interfaces (kernels_simt.cu, kernels_tc.cu). All return cudaGetLastError().
