@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 namespace lasp {
@@ -146,24 +147,6 @@ __device__ __forceinline__ int64_t block_row(Dir dir, const Item& it, int j) {
 }
 
 // cursor over the flattened (item, block) sequence of this CTA
-struct Cur {
-  int64_t w;
-  int j, nblk;
-  uint32_t J;
-  bool done;
-};
-__device__ __forceinline__ void cur_init(Cur& c, const Plan& p, Dir dir, int64_t W) {
-  c.w = blockIdx.x; c.j = 0; c.J = 0; c.done = c.w >= W;
-  c.nblk = c.done ? 0 : get_item(p, dir, c.w).nblk;
-}
-__device__ __forceinline__ void cur_next(Cur& c, const Plan& p, Dir dir, int64_t W) {
-  ++c.J;
-  if (++c.j >= c.nblk) {
-    c.w += gridDim.x; c.j = 0; c.done = c.w >= W;
-    c.nblk = c.done ? 0 : get_item(p, dir, c.w).nblk;
-  }
-}
-
 __device__ __forceinline__ void watchdog(long long t0) {
   if (clock64() - t0 > (1ll << 36)) __trap();
 }
@@ -361,15 +344,71 @@ struct CoreLayout {
   static constexpr uint32_t T_S0 = 0, T_S1 = 128, T_OI = 256, T_OX = 256 + D, T_DS = 256 + 2 * D;
 };
 
-struct CoreParams {
-  CUtensorMap ma, mb, mc, mo;
-  CUtensorMap ms;  // segment prefix states, fp32 2-D [rows = B*H*nseg*D][D], box [32][D], 128B swizzle
-  Plan p;
-  __nv_bfloat16* out;
-  const float* state;
-  unsigned long long* trace;  // debug timeline (lasp_debug_trace), nullptr in production
-  int trans;
+// One launch runs up to 3 passes of the core identity (e.g. dQ, dV and dK of the backward), with the
+// passes of one segment interleaved so that their shared input tiles are re-read from L2.
+struct CorePass {
+  int dir;        // Dir::FWD / Dir::REV
+  int trans;      // use S^T of the stored segment state
+  int a, b, c;    // indices into CoreParams::min
+  int out;        // index into CoreParams::mout / outp
+  int state;      // index into CoreParams::mst
 };
+
+struct CoreParams {
+  CUtensorMap min[4];  // distinct input sequence tensors
+  CUtensorMap mout[3]; // outputs
+  CUtensorMap mst[2];  // segment prefix states, fp32 2-D [rows = B*H*nseg*D][D], box [32][D], 128B swizzle
+  Plan p;
+  CorePass pass[3];
+  __nv_bfloat16* outp[3];
+  unsigned long long* trace;  // debug timeline (lasp_debug_trace), nullptr in production
+  int npass;
+};
+
+struct CItem {
+  int64_t b, h, seg, beg, end;
+  int nblk, pass;
+  Dir dir;
+};
+
+// item w -> (segment, pass, batch*head): segment-major, then pass, then (b, h)
+__device__ __noinline__ CItem get_citem(const CoreParams& prm, int64_t w) {
+  const Plan& p = prm.p;
+  CItem it;
+  const uint32_t nbh = uint32_t(p.B * p.H), per = nbh * uint32_t(prm.npass), nh = uint32_t(p.H);
+  const uint32_t wu = uint32_t(w);
+  it.seg = wu / per;
+  const uint32_t rem = wu - uint32_t(it.seg) * per;
+  it.pass = int(rem / nbh);
+  const uint32_t bh = rem - uint32_t(it.pass) * nbh;
+  it.b = bh / nh;
+  it.h = bh - uint32_t(it.b) * nh;
+  it.dir = Dir(prm.pass[it.pass].dir);
+  it.beg = seg_begin(it.dir, it.seg, p.seg_len, p.C);
+  it.end = seg_end(it.dir, it.seg, p.seg_len, p.C);
+  it.nblk = int((it.end - it.beg + BT - 1) / BT);
+  return it;
+}
+__device__ __forceinline__ int64_t cblock_row(const CItem& it, int j) {
+  return it.dir == Dir::FWD ? it.beg + int64_t(j) * BT : it.end - int64_t(j + 1) * BT;
+}
+struct CCur {
+  int64_t w;
+  int j, nblk;
+  uint32_t J;
+  bool done;
+};
+__device__ __forceinline__ void ccur_init(CCur& c, const CoreParams& prm, int64_t W) {
+  c.w = blockIdx.x; c.j = 0; c.J = 0; c.done = c.w >= W;
+  c.nblk = c.done ? 0 : get_citem(prm, c.w).nblk;
+}
+__device__ __forceinline__ void ccur_next(CCur& c, const CoreParams& prm, int64_t W) {
+  ++c.J;
+  if (++c.j >= c.nblk) {
+    c.w += gridDim.x; c.j = 0; c.done = c.w >= W;
+    c.nblk = c.done ? 0 : get_citem(prm, c.w).nblk;
+  }
+}
 
 struct CoreBars {
   uint64_t full[3], empty[3], s_full[2], s_empty[2];
@@ -380,7 +419,7 @@ struct CoreBars {
 
 
 
-template <int D, Dir DIR, bool TRANS>
+template <int D>
 __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__ CoreParams prm) {
   using L = CoreLayout<D>;
   constexpr int ST = L::STAGES;
@@ -390,15 +429,16 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   const uint32_t sbase = smem_u32(sm);
 
   const Plan& p = prm.p;
-  const int64_t W = p.B * p.H * p.nseg;
+  const int64_t W = p.B * p.H * p.nseg * prm.npass;
   const uint32_t warp = warp_id(), lane = lane_id();
 #ifdef LASP_TRACE_BUILD
   if (prm.trace != nullptr && threadIdx.x == 0) prm.trace[2 * 1024 + blockIdx.x * 2] = globaltimer();
 #endif
 
   if (threadIdx.x == 0) {
-    tma_prefetch(&prm.ma); tma_prefetch(&prm.mb); tma_prefetch(&prm.mc); tma_prefetch(&prm.mo);
-    tma_prefetch(&prm.ms);
+    for (int x = 0; x < 4; ++x) tma_prefetch(&prm.min[x]);
+    for (int x = 0; x < prm.npass; ++x) tma_prefetch(&prm.mout[x]);
+    tma_prefetch(&prm.mst[0]); tma_prefetch(&prm.mst[1]);
     mbar_init(&bar->stg_full, 1); mbar_init(&bar->stg_empty, 128);
     for (int s = 0; s < ST; ++s) { mbar_init(&bar->full[s], 1); mbar_init(&bar->empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&bar->s_full[s], 1); mbar_init(&bar->s_empty[s], 1); }
@@ -422,24 +462,29 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     if (elect_one()) {
       uint32_t J = 0, k = 0;
       for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
-        const Item it = get_item(p, DIR, w);
+        const CItem it = get_citem(prm, w);
+        const CorePass& ps = prm.pass[it.pass];
         // the segment's prefix state -> STG (single buffer, released by the state warps)
         mbar_wait(&bar->stg_empty, (k & 1) ^ 1);
         mbar_expect_tx(&bar->stg_full, 4 * D * D);
         const int srow = int(((it.b * p.H + it.h) * p.nseg + it.seg) * D);
 #pragma unroll
-        for (int x = 0; x < D / 32; ++x) tma_load_2d(sm + L::STG + x * (D * 128), &prm.ms, &bar->stg_full, x * 32, srow);
+        for (int x = 0; x < D / 32; ++x)
+          tma_load_2d(sm + L::STG + x * (D * 128), &prm.mst[ps.state], &bar->stg_full, x * 32, srow);
+        const CUtensorMap* ma = &prm.min[ps.a];
+        const CUtensorMap* mb = &prm.min[ps.b];
+        const CUtensorMap* mc = &prm.min[ps.c];
         for (int j = 0; j < it.nblk; ++j, ++J) {
           const int s = J % ST;
           mbar_wait(&bar->empty[s], ((J / ST) & 1) ^ 1);
           LASP_TRACE(0, J);
           mbar_expect_tx(&bar->full[s], 3 * L::TILE);
-          const int t0 = int(block_row(DIR, it, j));
+          const int t0 = int(cblock_row(it, j));
 #pragma unroll
           for (int x = 0; x < L::NBOX; ++x) {
-            tma_load_4d(sm + L::A(s) + x * BOX, &prm.ma, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
-            tma_load_4d(sm + L::B_(s) + x * BOX, &prm.mb, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
-            tma_load_4d(sm + L::C_(s) + x * BOX, &prm.mc, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
+            tma_load_4d(sm + L::A(s) + x * BOX, ma, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
+            tma_load_4d(sm + L::B_(s) + x * BOX, mb, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
+            tma_load_4d(sm + L::C_(s) + x * BOX, mc, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
           }
         }
       }
@@ -452,11 +497,11 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       constexpr uint32_t id_pv = idesc_bf16(128, D, 0, 1);
       constexpr uint32_t id_x = idesc_bf16(128, D, 0, 1);
       auto koff = [](int kk) -> uint32_t { return uint32_t(kk >> 2) * BOX + uint32_t(kk & 3) * 32; };
-      Cur cq, cd, co;
-      cur_init(cq, p, DIR, W);
-      cur_init(cd, p, DIR, W);
-      cur_init(co, p, DIR, W);
-      while (!cd.done && cd.j == cd.nblk - 1) cur_next(cd, p, DIR, W);  // ds only for non-last blocks
+      CCur cq, cd, co;
+      ccur_init(cq, prm, W);
+      ccur_init(cd, prm, W);
+      ccur_init(co, prm, W);
+      while (!cd.done && cd.j == cd.nblk - 1) ccur_next(cd, prm, W);  // ds only for non-last blocks
       uint32_t kd = 0;
       const long long t_start = clock64();
       uint32_t spins = 0;
@@ -474,7 +519,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           mma_commit(&bar->s_full[cq.J & 1]);
           LASP_TRACE(1, cq.J);
           progress = true;
-          cur_next(cq, p, DIR, W);
+          ccur_next(cq, prm, W);
         }
         // dS = (u . b)^T c (state chain; only for blocks that are not the last of their segment)
         if (!cd.done && mbar_test(&bar->ku_full, kd & 1) && mbar_test(&bar->ds_empty, (kd & 1) ^ 1)) {
@@ -488,8 +533,8 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           LASP_TRACE(2, cd.J);
           progress = true;
           ++kd;
-          cur_next(cd, p, DIR, W);
-          while (!cd.done && cd.j == cd.nblk - 1) cur_next(cd, p, DIR, W);
+          ccur_next(cd, prm, W);
+          while (!cd.done && cd.j == cd.nblk - 1) ccur_next(cd, prm, W);
         }
         // O_intra = P c, O_inter = a (S_hi + S_lo)
         // (out(J) releases the stage, so ds(J) of a non-last block must already be issued)
@@ -515,7 +560,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           mma_commit(&bar->s_empty[co.J & 1]);  // S/P buffer reusable once P c has been read
           mma_commit(&bar->st_empty[co.J & 1]);
           mma_commit(&bar->empty[s]);
-          cur_next(co, p, DIR, W);
+          ccur_next(co, prm, W);
         }
         if (!progress) __nanosleep(40);  // yield the SMSP to the mask / state / epilogue warps
         if ((++spins & 4095u) == 0) watchdog(t_start);
@@ -528,12 +573,13 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     float* colf = reinterpret_cast<float*>(sm + L::BARS + 256) + q4 * 32;  // per-warp column factors
     uint32_t J = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
-      const Item it = get_item(p, DIR, w);
+      const CItem it = get_citem(prm, w);
+      const bool fwd = it.dir == Dir::FWD;
       const float l2 = p.l2lam[it.h];
       // off-diagonal chunks: M_ij = lam^(i-j) = rowf(i, chunk) * colf[u]; colf[u] = lam^(31-u) (FWD)
       // or lam^u (REV), both in [lam^31, 1] (no overflow); the row factor's exponent is >= 1 there.
       __syncwarp();
-      colf[lane] = exp2f(float(DIR == Dir::FWD ? 31 - int(lane) : int(lane)) * l2);
+      colf[lane] = exp2f(float(fwd ? 31 - int(lane) : int(lane)) * l2);
       __syncwarp();
       for (int j = 0; j < it.nblk; ++j, ++J) {
         const int sb = J & 1;
@@ -547,7 +593,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           //   FWD e = i - j = R + (31 - u), R = i - 32 c4 - 31;  REV e = j - i = R + u, R = 32 c4 - i
           //   off-diagonal chunk (R >= 1): M = lam^R * colf[u]; diagonal chunk: M = colf[k], k = u - R (FWD)
           //   or R + u (REV) when 0 <= k <= 31 (else 0, the causal cut); dead chunk: 0.
-          const bool dead = DIR == Dir::FWD ? (c4 > int(q4)) : (c4 < int(q4));
+          const bool dead = fwd ? (c4 > int(q4)) : (c4 < int(q4));
           uint32_t pk[16];
           if (dead) {
 #pragma unroll
@@ -557,7 +603,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             tmem_ld16(ts + c4 * 32, *reinterpret_cast<float(*)[16]>(&v[0]));
             tmem_ld16(ts + c4 * 32 + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
             tmem_ld_wait();
-            const int R = DIR == Dir::FWD ? i - 32 * c4 - 31 : 32 * c4 - i;
+            const int R = fwd ? i - 32 * c4 - 31 : 32 * c4 - i;
             if (c4 != int(q4)) {
               const float rowf = exp2f(float(R) * l2);
 #pragma unroll
@@ -568,7 +614,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             } else {
 #pragma unroll
               for (int u = 0; u < 32; ++u) {
-                const int k = DIR == Dir::FWD ? u - R : R + u;
+                const int k = fwd ? u - R : R + u;
                 v[u] = (k >= 0 && k <= 31) ? v[u] * colf[k & 31] : 0.f;
               }
             }
@@ -595,10 +641,10 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     float S[D];
     // segment prefix state from STG (TMA, 128B-swizzled fp32 rows of 32 floats): row d of S, or
     // column d for S^T; both access patterns are (nearly) bank-conflict free
-    auto load_state = [&](uint32_t k) {
+    auto load_state = [&](uint32_t k, bool trans) {
       mbar_wait(&bar->stg_full, k & 1);
       if (valid) {
-        if (TRANS) {
+        if (trans) {
           const uint32_t x = uint32_t(d) >> 5, c = (uint32_t(d) & 31) >> 2, wd = uint32_t(d) & 3;
 #pragma unroll
           for (int e = 0; e < D; ++e)
@@ -617,10 +663,10 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     };
     uint32_t J = 0, kd = 0, k = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
-      const Item it = get_item(p, DIR, w);
-      load_state(k);
+      const CItem it = get_citem(prm, w);
+      load_state(k, prm.pass[it.pass].trans != 0);
       const float l2 = p.l2lam[it.h];
-      const uint32_t u2 = bf16x2_splat(exp2f(float(DIR == Dir::FWD ? (BT - 1 - g) : (g + 1)) * l2));
+      const uint32_t u2 = bf16x2_splat(exp2f(float(it.dir == Dir::FWD ? (BT - 1 - g) : (g + 1)) * l2));
       const float decay = exp2f(float(BT) * l2);
       // u (.) b for dS = (u . b)^T c of block JJ (the Ku buffer is free once dS of the previous block
       // has been loaded), done early so the dS MMA is never waiting on it
@@ -690,8 +736,10 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     const bool leader = threadIdx.x == 384;
     uint32_t J = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
-      const Item it = get_item(p, DIR, w);
-      const float r = exp2f(float(DIR == Dir::FWD ? (i + 1) : (BT - 1 - i)) * p.l2lam[it.h]);
+      const CItem it = get_citem(prm, w);
+      const CUtensorMap* mo = &prm.mout[prm.pass[it.pass].out];
+      __nv_bfloat16* outp = prm.outp[prm.pass[it.pass].out];
+      const float r = exp2f(float(it.dir == Dir::FWD ? (i + 1) : (BT - 1 - i)) * p.l2lam[it.h]);
       for (int j = 0; j < it.nblk; ++j, ++J) {
         mbar_wait(&bar->o_full, J & 1);
         if (i == 0) LASP_TRACE(8, J);
@@ -712,12 +760,12 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
 #pragma unroll
           for (int u = 0; u < 16; u += 2) pk[c * 8 + u / 2] = pack_bf16(fmaf(r, x[u], a[u]), fmaf(r, x[u + 1], a[u + 1]));
         }
-        const int t0 = int(block_row(DIR, it, j));
+        const int t0 = int(cblock_row(it, j));
         if (t0 < 0) {
           // ragged first block of a REV pass (rows before the rank start): TMA stores reject
           // negative coordinates, so the valid rows are written directly from registers
           if (t0 + i >= 0) {
-            uint4* dst = reinterpret_cast<uint4*>(prm.out + ((it.b * p.C + (t0 + i)) * p.H + it.h) * D);
+            uint4* dst = reinterpret_cast<uint4*>(outp + ((it.b * p.C + (t0 + i)) * p.H + it.h) * D);
 #pragma unroll
             for (int c = 0; c < D / 8; ++c) dst[c] = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
           }
@@ -737,7 +785,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         named_bar_sync(1, 128);
         if (leader) {
 #pragma unroll
-          for (int x = 0; x < L::NBOX; ++x) tma_store_4d(&prm.mo, sm + ob + x * BOX, x * 64, int(it.h), t0, int(it.b));
+          for (int x = 0; x < L::NBOX; ++x) tma_store_4d(mo, sm + ob + x * BOX, x * 64, int(it.h), t0, int(it.b));
           tma_store_commit();
           LASP_TRACE(9, J);
         }
@@ -784,24 +832,55 @@ cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, 
   return launch_k(kern, dim3(persistent_grid(p, SegLayout<D>::CTAS_PER_SM)), dim3(384), smem, st, prm);
 }
 
-template <int D, Dir DIR>
-cudaError_t launch_core(const Plan& p, const SeqArgs& a, cudaStream_t st) {
+template <int D>
+cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st) {
   CoreParams prm;
+  std::memset(&prm, 0, sizeof prm);
   cudaError_t e;
-  if ((e = make_seq_map(&prm.ma, a.a, p)) != cudaSuccess) return e;
-  if ((e = make_seq_map(&prm.mb, a.b, p)) != cudaSuccess) return e;
-  if ((e = make_seq_map(&prm.mc, a.c, p)) != cudaSuccess) return e;
-  if ((e = make_seq_map(&prm.mo, a.out, p)) != cudaSuccess) return e;
-  if ((e = make_state_map(&prm.ms, a.state, p)) != cudaSuccess) return e;
+  const void* ins[4];
+  int nin = 0;
+  auto in_index = [&](const void* ptr) -> int {
+    for (int x = 0; x < nin; ++x)
+      if (ins[x] == ptr) return x;
+    ins[nin] = ptr;
+    return nin++;
+  };
+  const float* sts[2];
+  int nst = 0;
+  for (int x = 0; x < npass; ++x) {
+    CorePass& ps = prm.pass[x];
+    ps.dir = int(dirs[x]);
+    ps.trans = a[x].trans_state;
+    ps.a = in_index(a[x].a);
+    ps.b = in_index(a[x].b);
+    ps.c = in_index(a[x].c);
+    if (nin > 4) return cudaErrorInvalidValue;
+    ps.out = x;
+    prm.outp[x] = static_cast<__nv_bfloat16*>(a[x].out);
+    if ((e = make_seq_map(&prm.mout[x], a[x].out, p)) != cudaSuccess) return e;
+    ps.state = -1;
+    for (int y = 0; y < nst; ++y)
+      if (sts[y] == a[x].state) ps.state = y;
+    if (ps.state < 0) {
+      if (nst == 2) return cudaErrorInvalidValue;
+      sts[nst] = a[x].state;
+      if ((e = make_state_map(&prm.mst[nst], a[x].state, p)) != cudaSuccess) return e;
+      ps.state = nst++;
+    }
+  }
+  for (int x = 0; x < nin; ++x)
+    if ((e = make_seq_map(&prm.min[x], ins[x], p)) != cudaSuccess) return e;
+  for (int x = nin; x < 4; ++x) prm.min[x] = prm.min[0];
+  if (nst < 2) prm.mst[1] = prm.mst[0];
   prm.p = p;
-  prm.out = static_cast<__nv_bfloat16*>(a.out);
-  prm.state = a.state;
-  prm.trans = a.trans_state;
+  prm.npass = npass;
   prm.trace = g_trace;
-  auto kern = a.trans_state ? core_tc_kernel<D, DIR, true> : core_tc_kernel<D, DIR, false>;
+  auto kern = core_tc_kernel<D>;
   const int smem = int(CoreLayout<D>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
-  return launch_k(kern, dim3(persistent_grid(p)), dim3(512), smem, st, prm);
+  const int64_t W = p.B * p.H * p.nseg * npass;
+  const unsigned grid = unsigned(W < sm_count() ? W : sm_count());
+  return launch_k(kern, dim3(grid), dim3(512), smem, st, prm);
 }
 
 }  // namespace
@@ -824,7 +903,12 @@ cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const voi
 }
 
 cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st) {
-  if (p.D == 64) return dir == Dir::FWD ? launch_core<64, Dir::FWD>(p, a, st) : launch_core<64, Dir::REV>(p, a, st);
+  return launch_core_tc_multi(p, 1, &a, &dir, st);
+}
+
+cudaError_t launch_core_tc_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st) {
+  if (npass < 1 || npass > 3) return cudaErrorInvalidValue;
+  if (p.D == 64) return launch_core_multi<64>(p, npass, a, dirs, st);
   return cudaErrorNotSupported;
 }
 

@@ -269,6 +269,20 @@ cudaError_t combine(const Plan& p, const float* in, const float* local, float* o
   return staged("combine", st, [&] { return launch_combine(p, in, local, out, st); });
 }
 
+// several core passes: one persistent tensor-core launch (passes of a segment interleaved, their
+// shared inputs re-read from L2), or one CUDA-core launch per pass
+cudaError_t core_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st) {
+  if (tc_supported(p))
+    return staged(npass == 3 ? "core_bwd3_tc" : "core_multi_tc", st,
+                  [&] { return launch_core_tc_multi(p, npass, a, dirs, st); });
+  for (int x = 0; x < npass; ++x) {
+    cudaError_t e = staged(dirs[x] == Dir::FWD ? "core_fwd_simt" : "core_rev_simt", st,
+                           [&] { return launch_core_simt(p, dirs[x], a[x], st); });
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 // ---- common prologue -------------------------------------------------------------------------
 lasp_status_t prologue(const lasp_shape_t* shape, const float* lambda, Plan& p) {
   lasp_status_t s = validate_shape(shape);
@@ -430,11 +444,12 @@ lasp_status_t lasp_bwd_local(const lasp_shape_t* shape, const void* q, const voi
     LASP_CUDA(prefix(p, Dir::REV, dkv_in, nullptr, nullptr, dkv_out, st));
     return LASP_OK;
   }
-  LASP_CUDA(core(p, Dir::FWD, d_o, v, k, dq, P, 1, st));                     // dQ (cache only)
   LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st));                      // B1
-  LASP_CUDA(prefix(p, Dir::REV, dkv_in, w.seg, w.seg, dkv_out, st));  // B2 (in place)
-  LASP_CUDA(core(p, Dir::REV, k, q, d_o, dv, w.seg, 0, st));                 // dV
-  LASP_CUDA(core(p, Dir::REV, v, d_o, q, dk, w.seg, 1, st));                 // dK
+  LASP_CUDA(prefix(p, Dir::REV, dkv_in, w.seg, w.seg, dkv_out, st));         // B2 (in place)
+  // B3: dQ (needs only the cache), dV and dK in one launch
+  const SeqArgs passes[3] = {{d_o, v, k, dq, P, 1}, {k, q, d_o, dv, w.seg, 0}, {v, d_o, q, dk, w.seg, 1}};
+  const Dir dirs[3] = {Dir::FWD, Dir::REV, Dir::REV};
+  LASP_CUDA(core_multi(p, 3, passes, dirs, st));
   return LASP_OK;
 }
 
@@ -579,8 +594,11 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   LASP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
   if (p.C == 0) return LASP_OK;
   LASP_CUDA(prefix(p, Dir::REV, w.in, w.seg, w.seg, nullptr, st));               // B2
-  LASP_CUDA(core(p, Dir::REV, k, q, d_o, dv, w.seg, 0, st));                            // dV
-  LASP_CUDA(core(p, Dir::REV, v, d_o, q, dk, w.seg, 1, st));                            // dK
+  {  // dV and dK in one launch
+    const SeqArgs passes[2] = {{k, q, d_o, dv, w.seg, 0}, {v, d_o, q, dk, w.seg, 1}};
+    const Dir dirs[2] = {Dir::REV, Dir::REV};
+    LASP_CUDA(core_multi(p, 2, passes, dirs, st));
+  }
   return LASP_OK;
 }
 

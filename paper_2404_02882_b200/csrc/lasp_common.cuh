@@ -98,5 +98,7 @@ void tc_set_trace(unsigned long long* buf);  // debug: per-block clock64 timelin
 cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out,
                                 cudaStream_t st);
 cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st);
+// up to 3 core passes in one persistent launch (their segments interleaved: shared inputs hit L2)
+cudaError_t launch_core_tc_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st);
 
 }  // namespace lasp
