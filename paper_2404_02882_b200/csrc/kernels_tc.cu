@@ -607,9 +607,13 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             if (c4 != int(q4)) {
               const float rowf = exp2f(float(R) * l2);
 #pragma unroll
-              for (int u = 0; u < 32; u += 4) {
+              for (int u = 0; u < 32; u += 4) {  // packed fp32x2 multiplies (FMUL2)
                 const float4 cf = *reinterpret_cast<const float4*>(&colf[u]);
-                v[u] *= rowf * cf.x; v[u + 1] *= rowf * cf.y; v[u + 2] *= rowf * cf.z; v[u + 3] *= rowf * cf.w;
+                float m0 = cf.x, m1 = cf.y, m2 = cf.z, m3 = cf.w;
+                fmul2(m0, m1, rowf, rowf);
+                fmul2(m2, m3, rowf, rowf);
+                fmul2(v[u], v[u + 1], m0, m1);
+                fmul2(v[u + 2], v[u + 3], m2, m3);
               }
             } else {
 #pragma unroll

@@ -225,6 +225,15 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, 
          | (uint32_t(M >> 4) << 24);      // m_dim
 }
 
+// (x0, x1) *= (y0, y1) with one packed fp32x2 multiply (FMUL2, sm_100)
+__device__ __forceinline__ void fmul2(float& x0, float& x1, float y0, float y1) {
+  uint64_t a, b;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(x0), "f"(x1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(y0), "f"(y1));
+  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(a) : "l"(b));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x0), "=f"(x1) : "l"(a));
+}
+
 // byte offset of (row r, 16-byte chunk c) inside a 128B-swizzled tile with 128-byte rows
 __device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t c) { return r * 128u + ((c ^ (r & 7u)) << 4); }
 
