@@ -304,7 +304,12 @@ def run_lasp(args):
         a_[1] += ms_
     dom_name, (dom_n, dom_ms) = max(fam.items(), key=lambda kv: kv[1][1]) if fam else ("none", (1, 0.0))
     per_launch_ms = dom_ms / max(dom_n, 1)
-    if dom_name.startswith("core"):
+    if dom_name.startswith("core_bwd3"):
+        # one launch runs the whole B3 row (dQ, dV, dK passes): algorithmic bytes read Q, K, V, dO and write
+        # dQ, dK, dV once (>= 14D B per token-head); the three passes stream 24D
+        bytes_per_launch = 7 * 2 * D * B * C * H
+        unit_note = "14*D bytes per token-head (Q,K,V,dO bf16 reads + dQ,dK,dV bf16 writes; B3 row)"
+    elif dom_name.startswith("core"):
         bytes_per_launch = 4 * 2 * D * B * C * H          # reads a, b, c and writes out (bf16): 8D B/token-head
         unit_note = "8*D bytes per token-head (3 bf16 reads + 1 bf16 write)"
     elif dom_name.startswith("seg_state"):

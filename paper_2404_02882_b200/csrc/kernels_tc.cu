@@ -392,24 +392,6 @@ __device__ __noinline__ CItem get_citem(const CoreParams& prm, int64_t w) {
 __device__ __forceinline__ int64_t cblock_row(const CItem& it, int j) {
   return it.dir == Dir::FWD ? it.beg + int64_t(j) * BT : it.end - int64_t(j + 1) * BT;
 }
-struct CCur {
-  int64_t w;
-  int j, nblk;
-  uint32_t J;
-  bool done;
-};
-__device__ __forceinline__ void ccur_init(CCur& c, const CoreParams& prm, int64_t W) {
-  c.w = blockIdx.x; c.j = 0; c.J = 0; c.done = c.w >= W;
-  c.nblk = c.done ? 0 : get_citem(prm, c.w).nblk;
-}
-__device__ __forceinline__ void ccur_next(CCur& c, const CoreParams& prm, int64_t W) {
-  ++c.J;
-  if (++c.j >= c.nblk) {
-    c.w += gridDim.x; c.j = 0; c.done = c.w >= W;
-    c.nblk = c.done ? 0 : get_citem(prm, c.w).nblk;
-  }
-}
-
 struct CoreBars {
   uint64_t full[3], empty[3], s_full[2], s_empty[2];
   uint64_t p_full[2], ku_full, ds_full, ds_empty, st_full[2], st_empty[2], o_full, o_empty;
@@ -440,7 +422,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     for (int x = 0; x < prm.npass; ++x) tma_prefetch(&prm.mout[x]);
     tma_prefetch(&prm.mst[0]); tma_prefetch(&prm.mst[1]);
     mbar_init(&bar->stg_full, 1); mbar_init(&bar->stg_empty, 128);
-    for (int s = 0; s < ST; ++s) { mbar_init(&bar->full[s], 1); mbar_init(&bar->empty[s], 1); }
+    for (int s = 0; s < ST; ++s) { mbar_init(&bar->full[s], 1); mbar_init(&bar->empty[s], 2); }
     for (int s = 0; s < 2; ++s) { mbar_init(&bar->s_full[s], 1); mbar_init(&bar->s_empty[s], 1); }
     mbar_init(&bar->p_full[0], 128); mbar_init(&bar->p_full[1], 128);
     mbar_init(&bar->ku_full, 128);
@@ -489,81 +471,76 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         }
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------------ UMMA issuer (dynamic order)
+  } else if (warp >= 1 && warp <= 3) {
+    // ------------------------------------------------------------------ UMMA issuers
+    // Three single-thread issuers, each in program order with blocking waits (tcgen05.commit covers the
+    // issuing thread's own MMAs): warp 2 issues S = a b^T, warp 3 the state chain dS = (u . b)^T c,
+    // warp 1 the outputs O_intra = P c (P read from TMEM) and O_inter = a (S_hi + S_lo). A stage is
+    // released when both its dS and its output MMAs are done (empty count 2; a segment's last block
+    // has no dS, so its output issuer arrives twice).
     if (elect_one()) {
       constexpr uint32_t id_qk = idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t id_ds = idesc_bf16(D, D, 1, 1);
       constexpr uint32_t id_pv = idesc_bf16(128, D, 0, 1);
       constexpr uint32_t id_x = idesc_bf16(128, D, 0, 1);
       auto koff = [](int kk) -> uint32_t { return uint32_t(kk >> 2) * BOX + uint32_t(kk & 3) * 32; };
-      CCur cq, cd, co;
-      ccur_init(cq, prm, W);
-      ccur_init(cd, prm, W);
-      ccur_init(co, prm, W);
-      while (!cd.done && cd.j == cd.nblk - 1) ccur_next(cd, prm, W);  // ds only for non-last blocks
-      uint32_t kd = 0;
-      const long long t_start = clock64();
-      uint32_t spins = 0;
-      while (!co.done) {
-        bool progress = false;
-        // S = a b^T for the next block (double-buffered in TMEM)
-        if (!cq.done && cq.J < co.J + 2 && mbar_test(&bar->full[cq.J % ST], (cq.J / ST) & 1) &&
-            mbar_test(&bar->s_empty[cq.J & 1], ((cq.J >> 1) & 1) ^ 1)) {
-          tc_fence_after();
-          const int s = cq.J % ST;
-          const uint32_t dt = tmem + ((cq.J & 1) ? L::T_S1 : L::T_S0);
+      uint32_t J = 0, kd = 0;
+      for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+        const int nblk = get_citem(prm, w).nblk;
+        for (int j = 0; j < nblk; ++j, ++J) {
+          const int s = int(J % ST);
+          if (warp == 2) {
+            // S = a b^T (double-buffered in TMEM; buffer J & 1 is free once out(J-2) has read its P)
+            mbar_wait(&bar->full[s], (J / ST) & 1);
+            mbar_wait(&bar->s_empty[J & 1], ((J >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t dt = tmem + ((J & 1) ? L::T_S1 : L::T_S0);
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            mma_bf16(dt, desc_k(sbase + L::A(s) + koff(kk)), desc_k(sbase + L::B_(s) + koff(kk)), id_qk, kk != 0);
-          mma_commit(&bar->s_full[cq.J & 1]);
-          LASP_TRACE(1, cq.J);
-          progress = true;
-          ccur_next(cq, prm, W);
+            for (int kk = 0; kk < D / 16; ++kk)
+              mma_bf16(dt, desc_k(sbase + L::A(s) + koff(kk)), desc_k(sbase + L::B_(s) + koff(kk)), id_qk, kk != 0);
+            mma_commit(&bar->s_full[J & 1]);
+            LASP_TRACE(1, J);
+          } else if (warp == 3) {
+            // dS = (u . b)^T c, only for blocks that are not the last of their segment
+            if (j + 1 < nblk) {
+              mbar_wait(&bar->ku_full, kd & 1);
+              mbar_wait(&bar->ds_empty, (kd & 1) ^ 1);
+              tc_fence_after();
+#pragma unroll
+              for (int kk = 0; kk < BT / 16; ++kk)
+                mma_bf16(tmem + L::T_DS, desc_mn(sbase + L::KU + kk * 2048, BOX),
+                         desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_ds, kk != 0);
+              mma_commit(&bar->ds_full);
+              mma_commit(&bar->empty[s]);
+              LASP_TRACE(2, J);
+              ++kd;
+            }
+          } else {
+            // O_intra = P c, O_inter = a (S_hi + S_lo)
+            mbar_wait(&bar->p_full[J & 1], (J >> 1) & 1);
+            mbar_wait(&bar->o_empty, (J & 1) ^ 1);
+            mbar_wait(&bar->st_full[J & 1], (J >> 1) & 1);
+            tc_fence_after();
+            const uint32_t pt = tmem + ((J & 1) ? L::T_S1 : L::T_S0);  // P in TMEM (2 bf16 / column)
+#pragma unroll
+            for (int kk = 0; kk < BT / 16; ++kk)
+              mma_bf16_ts(tmem + L::T_OI, pt + kk * 8, desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv, kk != 0);
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+              mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)),
+                       desc_mn(sbase + L::SBF(J & 1) + kk * 2048, D * 128), id_x, kk != 0);
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+              mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)),
+                       desc_mn(sbase + L::SLO(J & 1) + kk * 2048, D * 128), id_x, 1);
+            mma_commit(&bar->o_full);
+            mma_commit(&bar->s_empty[J & 1]);  // S/P buffer reusable once P c has been read
+            mma_commit(&bar->st_empty[J & 1]);
+            mma_commit(&bar->empty[s]);
+            if (j + 1 == nblk) mma_commit(&bar->empty[s]);  // no dS for the segment's last block
+            LASP_TRACE(3, J);
+          }
         }
-        // dS = (u . b)^T c (state chain; only for blocks that are not the last of their segment)
-        if (!cd.done && mbar_test(&bar->ku_full, kd & 1) && mbar_test(&bar->ds_empty, (kd & 1) ^ 1)) {
-          tc_fence_after();
-          const int s = cd.J % ST;
-#pragma unroll
-          for (int kk = 0; kk < BT / 16; ++kk)
-            mma_bf16(tmem + L::T_DS, desc_mn(sbase + L::KU + kk * 2048, BOX),
-                     desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_ds, kk != 0);
-          mma_commit(&bar->ds_full);
-          LASP_TRACE(2, cd.J);
-          progress = true;
-          ++kd;
-          ccur_next(cd, prm, W);
-          while (!cd.done && cd.j == cd.nblk - 1) ccur_next(cd, prm, W);
-        }
-        // O_intra = P c, O_inter = a (S_hi + S_lo)
-        // (out(J) releases the stage, so ds(J) of a non-last block must already be issued)
-        if (co.J < cq.J && (co.j == co.nblk - 1 || cd.done || cd.J > co.J) && mbar_test(&bar->p_full[co.J & 1], (co.J >> 1) & 1) && mbar_test(&bar->o_empty, (co.J & 1) ^ 1) &&
-            mbar_test(&bar->st_full[co.J & 1], (co.J >> 1) & 1)) {
-          tc_fence_after();
-          const int s = co.J % ST;
-          const uint32_t pt = tmem + ((co.J & 1) ? L::T_S1 : L::T_S0);  // P in TMEM (2 bf16 / column)
-#pragma unroll
-          for (int kk = 0; kk < BT / 16; ++kk)
-            mma_bf16_ts(tmem + L::T_OI, pt + kk * 8, desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv, kk != 0);
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SBF(co.J & 1) + kk * 2048, D * 128),
-                     id_x, kk != 0);
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SLO(co.J & 1) + kk * 2048, D * 128),
-                     id_x, 1);
-          mma_commit(&bar->o_full);
-          LASP_TRACE(3, co.J);
-          progress = true;
-          mma_commit(&bar->s_empty[co.J & 1]);  // S/P buffer reusable once P c has been read
-          mma_commit(&bar->st_empty[co.J & 1]);
-          mma_commit(&bar->empty[s]);
-          ccur_next(co, prm, W);
-        }
-        if (!progress) __nanosleep(40);  // yield the SMSP to the mask / state / epilogue warps
-        if ((++spins & 4095u) == 0) watchdog(t_start);
       }
     }
   } else if (warp >= 4 && warp < 8) {

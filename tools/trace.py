@@ -13,7 +13,7 @@ L.fwd_local(q, k, v, p["lam"]); torch.cuda.synchronize()
 N.lib().lasp_debug_trace(None)
 t = buf.cpu().numpy().reshape(2, 16, 64)[0].astype(np.int64)
 base = t[t > 0].min()
-names = ["tma_issue", "qk_iss", "ds_iss", "out_iss", "mask_beg", "mask_end", "ds_ready", "sbf_next", "o_full", "store", "ld0", "ld1", "ld2", "ld3", "st_iss", "st_done"]
+names = ["tma_issue", "qk_iss", "ds_iss", "out_iss", "mask_beg", "mask_end", "ds_ready", "sbf_next", "o_full", "store", "g_qk", "g_ds", "g_pfull", "g_oempty", "st_iss", "st_done"]
 print("J   " + " ".join(f"{n:>9s}" for n in names))
 for J in range(int(sys.argv[1]) if len(sys.argv) > 1 else 30):
     print(f"{J:3d} " + " ".join(f"{(t[e, J] - base) if t[e, J] else -1:9d}" for e in range(len(names))))
