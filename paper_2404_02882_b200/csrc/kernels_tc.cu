@@ -326,22 +326,30 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
 // ================================================================================================
 template <int D>
 struct CoreLayout {
-  static constexpr int NBOX = D / 64;
-  static constexpr uint32_t TILE = NBOX * BOX;           // one [128][D] bf16 tile
-  static constexpr int STAGES = 3;
-  static constexpr uint32_t A(int s) { return uint32_t(s) * 3 * TILE; }
-  static constexpr uint32_t B_(int s) { return uint32_t(s) * 3 * TILE + TILE; }
-  static constexpr uint32_t C_(int s) { return uint32_t(s) * 3 * TILE + 2 * TILE; }
-  static constexpr uint32_t KU = STAGES * 3 * TILE;      // u (.) b, [128][D]
-  // state copies, double-buffered by block parity: [D][D] bf16 hi part and lo part (S - hi)
-  static constexpr uint32_t SBF(int b) { return KU + TILE + uint32_t(b) * 4 * D * D; }
-  static constexpr uint32_t SLO(int b) { return SBF(b) + 2 * D * D; }
-  static constexpr uint32_t OST = KU + TILE + 8 * D * D;  // [128][D] bf16 output staging
-  static constexpr uint32_t STG = OST + TILE;              // [D][D] fp32 segment prefix state (TMA, SW128)
-  static constexpr uint32_t BARS = STG + 4 * D * D;        // barriers (256 B) + mask column factors (512 B)
+  // Items work on one 64-wide slice of the value dimension (NV = D / 64 slices per head), with the
+  // full key dimension DK = D: a, b tiles are [128][DK], c / u.c / out tiles are [128][64], the state
+  // slice is [DK][64].
+  static constexpr int DK = D, NBOX = D / 64, NV = D / 64;
+  static constexpr uint32_t TA = NBOX * BOX;             // [128][DK] bf16 (a, b)
+  static constexpr uint32_t TC = BOX;                    // [128][64] bf16 (c, u.c, out)
+  static constexpr int STAGES = D == 64 ? 3 : 2;
+  static constexpr int NSB = D == 64 ? 2 : 1;            // bf16 state copies (double-buffered if smem allows)
+  static constexpr bool HAS_STG = D == 64;               // TMA-staged prefix state (else read directly)
+  static constexpr uint32_t STAGE = 2 * TA + TC;
+  static constexpr uint32_t A(int s) { return uint32_t(s) * STAGE; }
+  static constexpr uint32_t B_(int s) { return uint32_t(s) * STAGE + TA; }
+  static constexpr uint32_t C_(int s) { return uint32_t(s) * STAGE + 2 * TA; }
+  static constexpr uint32_t KU = STAGES * STAGE;         // u (.) c, [128][64]
+  // state slice as bf16 hi part and lo part (S - hi), [DK][64] each, per buffer
+  static constexpr uint32_t SBF(int b) { return KU + TC + uint32_t(b) * DK * 256; }
+  static constexpr uint32_t SLO(int b) { return SBF(b) + DK * 128; }
+  static constexpr uint32_t OST = KU + TC + NSB * DK * 256;  // [128][64] bf16 output staging
+  static constexpr uint32_t STG = OST + TC;                  // [D][D] fp32 segment prefix state (TMA, SW128)
+  static constexpr uint32_t BARS = STG + (HAS_STG ? 4 * D * D : 0);  // barriers (256 B) + mask factors (512 B)
   static constexpr uint32_t BYTES = BARS + 256 + 512 + 1024;
   // TMEM columns (P, bf16, overwrites the first 64 columns of its S buffer: FA4-style TS MMA)
-  static constexpr uint32_t T_S0 = 0, T_S1 = 128, T_OI = 256, T_OX = 256 + D, T_DS = 256 + 2 * D;
+  static constexpr uint32_t T_S0 = 0, T_S1 = 128, T_OI = 256, T_OX = 320, T_DS = 384;
+  static_assert(BYTES <= 232448, "shared memory budget");
 };
 
 // One launch runs up to 3 passes of the core identity (e.g. dQ, dV and dK of the backward), with the
@@ -358,6 +366,7 @@ struct CoreParams {
   CUtensorMap min[4];  // distinct input sequence tensors
   CUtensorMap mout[3]; // outputs
   CUtensorMap mst[2];  // segment prefix states, fp32 2-D [rows = B*H*nseg*D][D], box [32][D], 128B swizzle
+  const float* stp[2]; // the same states as plain pointers (D = 128: read directly by the state warps)
   Plan p;
   CorePass pass[3];
   __nv_bfloat16* outp[3];
@@ -367,20 +376,22 @@ struct CoreParams {
 
 struct CItem {
   int64_t b, h, seg, beg, end;
-  int nblk, pass;
+  int nblk, pass, v;  // v: 64-wide value slice
   Dir dir;
 };
 
-// item w -> (segment, pass, batch*head): segment-major, then pass, then (b, h)
-__device__ __noinline__ CItem get_citem(const CoreParams& prm, int64_t w) {
+// item w -> (segment, pass, batch*head, value slice): segment-major, value slice innermost
+__device__ __noinline__ CItem get_citem(const CoreParams& prm, int64_t w, int nv) {
   const Plan& p = prm.p;
   CItem it;
-  const uint32_t nbh = uint32_t(p.B * p.H), per = nbh * uint32_t(prm.npass), nh = uint32_t(p.H);
+  const uint32_t nbh = uint32_t(p.B * p.H) * uint32_t(nv), per = nbh * uint32_t(prm.npass), nh = uint32_t(p.H);
   const uint32_t wu = uint32_t(w);
   it.seg = wu / per;
   const uint32_t rem = wu - uint32_t(it.seg) * per;
   it.pass = int(rem / nbh);
-  const uint32_t bh = rem - uint32_t(it.pass) * nbh;
+  const uint32_t bhv = rem - uint32_t(it.pass) * nbh;
+  const uint32_t bh = bhv / uint32_t(nv);
+  it.v = int(bhv - bh * uint32_t(nv));
   it.b = bh / nh;
   it.h = bh - uint32_t(it.b) * nh;
   it.dir = Dir(prm.pass[it.pass].dir);
@@ -411,7 +422,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   const uint32_t sbase = smem_u32(sm);
 
   const Plan& p = prm.p;
-  const int64_t W = p.B * p.H * p.nseg * prm.npass;
+  const int64_t W = p.B * p.H * p.nseg * prm.npass * L::NV;
   const uint32_t warp = warp_id(), lane = lane_id();
 #ifdef LASP_TRACE_BUILD
   if (prm.trace != nullptr && threadIdx.x == 0) prm.trace[2 * 1024 + blockIdx.x * 2] = globaltimer();
@@ -427,7 +438,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     mbar_init(&bar->p_full[0], 128); mbar_init(&bar->p_full[1], 128);
     mbar_init(&bar->ku_full, 128);
     mbar_init(&bar->ds_full, 1); mbar_init(&bar->ds_empty, 128);
-    for (int b2 = 0; b2 < 2; ++b2) { mbar_init(&bar->st_full[b2], 128); mbar_init(&bar->st_empty[b2], 1); }
+    for (int b2 = 0; b2 < L::NSB; ++b2) { mbar_init(&bar->st_full[b2], 128); mbar_init(&bar->st_empty[b2], 1); }
     mbar_init(&bar->o_full, 1); mbar_init(&bar->o_empty, 128);
     fence_mbar_init();
   }
@@ -444,15 +455,17 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     if (elect_one()) {
       uint32_t J = 0, k = 0;
       for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
-        const CItem it = get_citem(prm, w);
+        const CItem it = get_citem(prm, w, L::NV);
         const CorePass& ps = prm.pass[it.pass];
-        // the segment's prefix state -> STG (single buffer, released by the state warps)
-        mbar_wait(&bar->stg_empty, (k & 1) ^ 1);
-        mbar_expect_tx(&bar->stg_full, 4 * D * D);
-        const int srow = int(((it.b * p.H + it.h) * p.nseg + it.seg) * D);
+        if constexpr (L::HAS_STG) {
+          // the segment's prefix state -> STG (single buffer, released by the state warps)
+          mbar_wait(&bar->stg_empty, (k & 1) ^ 1);
+          mbar_expect_tx(&bar->stg_full, 4 * D * D);
+          const int srow = int(((it.b * p.H + it.h) * p.nseg + it.seg) * D);
 #pragma unroll
-        for (int x = 0; x < D / 32; ++x)
-          tma_load_2d(sm + L::STG + x * (D * 128), &prm.mst[ps.state], &bar->stg_full, x * 32, srow);
+          for (int x = 0; x < D / 32; ++x)
+            tma_load_2d(sm + L::STG + x * (D * 128), &prm.mst[ps.state], &bar->stg_full, x * 32, srow);
+        }
         const CUtensorMap* ma = &prm.min[ps.a];
         const CUtensorMap* mb = &prm.min[ps.b];
         const CUtensorMap* mc = &prm.min[ps.c];
@@ -460,33 +473,33 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           const int s = J % ST;
           mbar_wait(&bar->empty[s], ((J / ST) & 1) ^ 1);
           LASP_TRACE(0, J);
-          mbar_expect_tx(&bar->full[s], 3 * L::TILE);
+          mbar_expect_tx(&bar->full[s], L::STAGE);
           const int t0 = int(cblock_row(it, j));
 #pragma unroll
           for (int x = 0; x < L::NBOX; ++x) {
             tma_load_4d(sm + L::A(s) + x * BOX, ma, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
             tma_load_4d(sm + L::B_(s) + x * BOX, mb, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
-            tma_load_4d(sm + L::C_(s) + x * BOX, mc, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
           }
+          tma_load_4d(sm + L::C_(s), mc, &bar->full[s], it.v * 64, int(it.h), t0, int(it.b));
         }
       }
     }
   } else if (warp >= 1 && warp <= 3) {
     // ------------------------------------------------------------------ UMMA issuers
     // Three single-thread issuers, each in program order with blocking waits (tcgen05.commit covers the
-    // issuing thread's own MMAs): warp 2 issues S = a b^T, warp 3 the state chain dS = (u . b)^T c,
+    // issuing thread's own MMAs): warp 2 issues S = a b^T, warp 3 the state chain dS = b^T (u . c),
     // warp 1 the outputs O_intra = P c (P read from TMEM) and O_inter = a (S_hi + S_lo). A stage is
     // released when both its dS and its output MMAs are done (empty count 2; a segment's last block
     // has no dS, so its output issuer arrives twice).
     if (elect_one()) {
       constexpr uint32_t id_qk = idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t id_ds = idesc_bf16(D, D, 1, 1);
-      constexpr uint32_t id_pv = idesc_bf16(128, D, 0, 1);
-      constexpr uint32_t id_x = idesc_bf16(128, D, 0, 1);
+      constexpr uint32_t id_ds = idesc_bf16(L::DK, 64, 1, 1);
+      constexpr uint32_t id_pv = idesc_bf16(128, 64, 0, 1);
+      constexpr uint32_t id_x = idesc_bf16(128, 64, 0, 1);
       auto koff = [](int kk) -> uint32_t { return uint32_t(kk >> 2) * BOX + uint32_t(kk & 3) * 32; };
       uint32_t J = 0, kd = 0;
       for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
-        const int nblk = get_citem(prm, w).nblk;
+        const int nblk = get_citem(prm, w, L::NV).nblk;
         for (int j = 0; j < nblk; ++j, ++J) {
           const int s = int(J % ST);
           if (warp == 2) {
@@ -496,20 +509,20 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             tc_fence_after();
             const uint32_t dt = tmem + ((J & 1) ? L::T_S1 : L::T_S0);
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)
+            for (int kk = 0; kk < L::DK / 16; ++kk)
               mma_bf16(dt, desc_k(sbase + L::A(s) + koff(kk)), desc_k(sbase + L::B_(s) + koff(kk)), id_qk, kk != 0);
             mma_commit(&bar->s_full[J & 1]);
             LASP_TRACE(1, J);
           } else if (warp == 3) {
-            // dS = (u . b)^T c, only for blocks that are not the last of their segment
+            // dS = b^T (u . c), only for blocks that are not the last of their segment
             if (j + 1 < nblk) {
               mbar_wait(&bar->ku_full, kd & 1);
               mbar_wait(&bar->ds_empty, (kd & 1) ^ 1);
               tc_fence_after();
 #pragma unroll
               for (int kk = 0; kk < BT / 16; ++kk)
-                mma_bf16(tmem + L::T_DS, desc_mn(sbase + L::KU + kk * 2048, BOX),
-                         desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_ds, kk != 0);
+                mma_bf16(tmem + L::T_DS, desc_mn(sbase + L::B_(s) + kk * 2048, BOX),
+                         desc_mn(sbase + L::KU + kk * 2048, BOX), id_ds, kk != 0);
               mma_commit(&bar->ds_full);
               mma_commit(&bar->empty[s]);
               LASP_TRACE(2, J);
@@ -519,23 +532,24 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             // O_intra = P c, O_inter = a (S_hi + S_lo)
             mbar_wait(&bar->p_full[J & 1], (J >> 1) & 1);
             mbar_wait(&bar->o_empty, (J & 1) ^ 1);
-            mbar_wait(&bar->st_full[J & 1], (J >> 1) & 1);
+            mbar_wait(&bar->st_full[J % L::NSB], (J / L::NSB) & 1);
             tc_fence_after();
             const uint32_t pt = tmem + ((J & 1) ? L::T_S1 : L::T_S0);  // P in TMEM (2 bf16 / column)
 #pragma unroll
             for (int kk = 0; kk < BT / 16; ++kk)
               mma_bf16_ts(tmem + L::T_OI, pt + kk * 8, desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv, kk != 0);
+            const int sb = int(J % L::NSB);
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)
-              mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)),
-                       desc_mn(sbase + L::SBF(J & 1) + kk * 2048, D * 128), id_x, kk != 0);
+            for (int kk = 0; kk < L::DK / 16; ++kk)
+              mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SBF(sb) + kk * 2048, BOX),
+                       id_x, kk != 0);
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)
-              mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)),
-                       desc_mn(sbase + L::SLO(J & 1) + kk * 2048, D * 128), id_x, 1);
+            for (int kk = 0; kk < L::DK / 16; ++kk)
+              mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SLO(sb) + kk * 2048, BOX),
+                       id_x, 1);
             mma_commit(&bar->o_full);
             mma_commit(&bar->s_empty[J & 1]);  // S/P buffer reusable once P c has been read
-            mma_commit(&bar->st_empty[J & 1]);
+            mma_commit(&bar->st_empty[J % L::NSB]);
             mma_commit(&bar->empty[s]);
             if (j + 1 == nblk) mma_commit(&bar->empty[s]);  // no dS for the segment's last block
             LASP_TRACE(3, J);
@@ -550,7 +564,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     float* colf = reinterpret_cast<float*>(sm + L::BARS + 256) + q4 * 32;  // per-warp column factors
     uint32_t J = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
-      const CItem it = get_citem(prm, w);
+      const CItem it = get_citem(prm, w, L::NV);
       const bool fwd = it.dir == Dir::FWD;
       const float l2 = p.l2lam[it.h];
       // off-diagonal chunks: M_ij = lam^(i-j) = rowf(i, chunk) * colf[u]; colf[u] = lam^(31-u) (FWD)
@@ -615,79 +629,96 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     }
   } else if (warp >= 8 && warp < 12) {
     // ------------------------------------------------------------------ state warps
+    // Thread d owns row d (key index) of the [DK][64] state slice (TMEM layout of M = DK for dS).
     const uint32_t q4 = warp & 3;
-    const int g = int(threadIdx.x) - 256;  // tile row for the u.b scaling
-    const bool valid = D == 128 || lane < 16;
-    const int d = D == 128 ? int(q4 * 32 + lane) : int(q4 * 16 + lane);  // state row (TMEM layout of M = D)
-    float S[D];
-    // segment prefix state from STG (TMA, 128B-swizzled fp32 rows of 32 floats): row d of S, or
-    // column d for S^T; both access patterns are (nearly) bank-conflict free
-    auto load_state = [&](uint32_t k, bool trans) {
-      mbar_wait(&bar->stg_full, k & 1);
-      if (valid) {
+    const int g = int(threadIdx.x) - 256;  // tile row for the u.c scaling
+    const bool valid = L::DK == 128 || lane < 16;
+    const int d = L::DK == 128 ? int(q4 * 32 + lane) : int(q4 * 16 + lane);
+    float S[64];
+    auto load_state = [&](uint32_t k, const CItem& it, bool trans, int state) {
+      if constexpr (L::HAS_STG) {
+        // segment prefix state from STG (TMA, 128B-swizzled fp32 rows of 32 floats): row d of S, or
+        // column d for S^T; both access patterns are (nearly) bank-conflict free
+        mbar_wait(&bar->stg_full, k & 1);
+        if (valid) {
+          if (trans) {
+            const uint32_t x = uint32_t(d) >> 5, c = (uint32_t(d) & 31) >> 2, wd = uint32_t(d) & 3;
+#pragma unroll
+            for (int e = 0; e < D; ++e)
+              S[e] = *reinterpret_cast<const float*>(sm + L::STG + x * (D * 128) + e * 128 + ((c ^ (e & 7)) << 4) + wd * 4);
+          } else {
+#pragma unroll
+            for (int e = 0; e < D; e += 4) {
+              const uint32_t x = uint32_t(e) >> 5, c = (uint32_t(e) & 31) >> 2;
+              const float4 t = *reinterpret_cast<const float4*>(sm + L::STG + x * (D * 128) + d * 128 +
+                                                                ((c ^ (uint32_t(d) & 7)) << 4));
+              S[e] = t.x; S[e + 1] = t.y; S[e + 2] = t.z; S[e + 3] = t.w;
+            }
+          }
+        }
+        mbar_arrive(&bar->stg_empty);
+      } else {
+        // straight from the (L2-resident) prefix states: row d, columns [64 v, 64 v + 64) of S, or
+        // column d, rows [64 v, 64 v + 64) for S^T (coalesced across the warp)
+        const float* st = prm.stp[state] + ((it.b * p.H + it.h) * p.nseg + it.seg) * D * D;
         if (trans) {
-          const uint32_t x = uint32_t(d) >> 5, c = (uint32_t(d) & 31) >> 2, wd = uint32_t(d) & 3;
 #pragma unroll
-          for (int e = 0; e < D; ++e)
-            S[e] = *reinterpret_cast<const float*>(sm + L::STG + x * (D * 128) + e * 128 + ((c ^ (e & 7)) << 4) + wd * 4);
+          for (int e = 0; e < 64; ++e) S[e] = __ldg(st + (it.v * 64 + e) * D + d);
         } else {
+          const float4* row = reinterpret_cast<const float4*>(st + d * D + it.v * 64);
 #pragma unroll
-          for (int e = 0; e < D; e += 4) {
-            const uint32_t x = uint32_t(e) >> 5, c = (uint32_t(e) & 31) >> 2;
-            const float4 t = *reinterpret_cast<const float4*>(sm + L::STG + x * (D * 128) + d * 128 +
-                                                              ((c ^ (uint32_t(d) & 7)) << 4));
-            S[e] = t.x; S[e + 1] = t.y; S[e + 2] = t.z; S[e + 3] = t.w;
+          for (int e = 0; e < 16; ++e) {
+            const float4 t = __ldg(row + e);
+            S[4 * e] = t.x; S[4 * e + 1] = t.y; S[4 * e + 2] = t.z; S[4 * e + 3] = t.w;
           }
         }
       }
-      mbar_arrive(&bar->stg_empty);
     };
     uint32_t J = 0, kd = 0, k = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
-      const CItem it = get_citem(prm, w);
-      load_state(k, prm.pass[it.pass].trans != 0);
+      const CItem it = get_citem(prm, w, L::NV);
+      const CorePass& ps = prm.pass[it.pass];
+      load_state(k, it, ps.trans != 0, ps.state);
       const float l2 = p.l2lam[it.h];
       const uint32_t u2 = bf16x2_splat(exp2f(float(it.dir == Dir::FWD ? (BT - 1 - g) : (g + 1)) * l2));
       const float decay = exp2f(float(BT) * l2);
-      // u (.) b for dS = (u . b)^T c of block JJ (the Ku buffer is free once dS of the previous block
+      // u (.) c for dS = b^T (u . c) of block JJ (the Ku buffer is free once dS of the previous block
       // has been loaded), done early so the dS MMA is never waiting on it
       auto scale_ku = [&](uint32_t JJ) {
         const int s = JJ % ST;
         mbar_wait(&bar->full[s], (JJ / ST) & 1);
 #pragma unroll
-        for (int x = 0; x < L::NBOX; ++x)
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const uint32_t off = x * BOX + uint32_t(g) * 128 + ((uint32_t(c) ^ (uint32_t(g) & 7)) << 4);
-            sts128(sbase + L::KU + off, scale_chunk(lds128(sbase + L::B_(s) + off), u2));
-          }
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t off = uint32_t(g) * 128 + ((uint32_t(c) ^ (uint32_t(g) & 7)) << 4);
+          sts128(sbase + L::KU + off, scale_chunk(lds128(sbase + L::C_(s) + off), u2));
+        }
         fence_async_smem();
         mbar_arrive(&bar->ku_full);
       };
       if (it.nblk > 1) scale_ku(J);
       for (int j = 0;; ++j, ++J) {
-        // bf16 hi/lo copy of the state entering block J into buffer J & 1 (free once out(J-2) is done)
-        mbar_wait(&bar->st_empty[J & 1], ((J >> 1) & 1) ^ 1);
+        // bf16 hi/lo copy of the state entering block J into buffer J % NSB (free once the output MMAs
+        // of block J - NSB are done)
+        const int sb = int(J % L::NSB);
+        mbar_wait(&bar->st_empty[sb], ((J / L::NSB) & 1) ^ 1);
         if (valid) {
 #pragma unroll
-          for (int x = 0; x < L::NBOX; ++x)
+          for (int c = 0; c < 8; ++c) {
+            const float* v = &S[c * 8];
+            uint32_t hi[4], lo[4];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const float* v = &S[x * 64 + c * 8];
-              uint32_t hi[4], lo[4];
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                hi[t] = pack_bf16(v[2 * t], v[2 * t + 1]);
-                lo[t] = pack_bf16(v[2 * t] - __uint_as_float(hi[t] << 16),
-                                  v[2 * t + 1] - __uint_as_float(hi[t] & 0xFFFF0000u));
-              }
-              const uint32_t off = x * (D * 128) + sw128_off(uint32_t(d), uint32_t(c));
-              sts128(sbase + L::SBF(J & 1) + off, make_uint4(hi[0], hi[1], hi[2], hi[3]));
-              sts128(sbase + L::SLO(J & 1) + off, make_uint4(lo[0], lo[1], lo[2], lo[3]));
+            for (int t = 0; t < 4; ++t) {
+              hi[t] = pack_bf16(v[2 * t], v[2 * t + 1]);
+              lo[t] = pack_bf16(v[2 * t] - __uint_as_float(hi[t] << 16),
+                                v[2 * t + 1] - __uint_as_float(hi[t] & 0xFFFF0000u));
             }
+            const uint32_t off = sw128_off(uint32_t(d), uint32_t(c));
+            sts128(sbase + L::SBF(sb) + off, make_uint4(hi[0], hi[1], hi[2], hi[3]));
+            sts128(sbase + L::SLO(sb) + off, make_uint4(lo[0], lo[1], lo[2], lo[3]));
+          }
         }
         fence_async_smem();
-        mbar_arrive(&bar->st_full[J & 1]);
+        mbar_arrive(&bar->st_full[sb]);
         if (g == 0) LASP_TRACE(7, J);
         if (j + 1 == it.nblk) break;  // no state leaves the last block of a segment
         // S_{J+1} = lam^128 S_J + dS_J
@@ -696,7 +727,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         tc_fence_after();
         const uint32_t td = tmem + ((q4 * 32) << 16) + L::T_DS;
 #pragma unroll
-        for (int c = 0; c < D / 16; ++c) {
+        for (int c = 0; c < 4; ++c) {
           float v[16];
           tmem_ld16(td + c * 16, v);
           tmem_ld_wait();
@@ -717,7 +748,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     const bool leader = threadIdx.x == 384;
     uint32_t J = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
-      const CItem it = get_citem(prm, w);
+      const CItem it = get_citem(prm, w, L::NV);
       const CUtensorMap* mo = &prm.mout[prm.pass[it.pass].out];
       __nv_bfloat16* outp = prm.outp[prm.pass[it.pass].out];
       const float r = exp2f(float(it.dir == Dir::FWD ? (i + 1) : (BT - 1 - i)) * p.l2lam[it.h]);
@@ -727,14 +758,14 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         tc_fence_after();
         const uint32_t ti = tmem + ((q4 * 32) << 16) + L::T_OI;
         const uint32_t tx = tmem + ((q4 * 32) << 16) + L::T_OX;
-        uint32_t pk[D / 2];
+        uint32_t pk[32];
 #pragma unroll
-        for (int c = 0; c < D / 16; ++c) {
+        for (int c = 0; c < 4; ++c) {
           float a[16], x[16];
           tmem_ld16(ti + c * 16, a);
           tmem_ld16(tx + c * 16, x);
           tmem_ld_wait();
-          if (c == D / 16 - 1) {
+          if (c == 3) {
             tc_fence_before();
             mbar_arrive(&bar->o_empty);
           }
@@ -746,9 +777,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           // ragged first block of a REV pass (rows before the rank start): TMA stores reject
           // negative coordinates, so the valid rows are written directly from registers
           if (t0 + i >= 0) {
-            uint4* dst = reinterpret_cast<uint4*>(outp + ((it.b * p.C + (t0 + i)) * p.H + it.h) * D);
+            uint4* dst = reinterpret_cast<uint4*>(outp + ((it.b * p.C + (t0 + i)) * p.H + it.h) * D + it.v * 64);
 #pragma unroll
-            for (int c = 0; c < D / 8; ++c) dst[c] = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
+            for (int c = 0; c < 8; ++c) dst[c] = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
           }
           continue;
         }
@@ -756,17 +787,14 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         if (leader) tma_store_wait_read<0>();
         named_bar_sync(1, 128);
 #pragma unroll
-        for (int x = 0; x < L::NBOX; ++x)
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const uint32_t* v = &pk[x * 32 + c * 4];
-            sts128(sbase + ob + x * BOX + sw128_off(uint32_t(i), uint32_t(c)), make_uint4(v[0], v[1], v[2], v[3]));
-          }
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t* v = &pk[c * 4];
+          sts128(sbase + ob + sw128_off(uint32_t(i), uint32_t(c)), make_uint4(v[0], v[1], v[2], v[3]));
+        }
         fence_async_smem();
         named_bar_sync(1, 128);
         if (leader) {
-#pragma unroll
-          for (int x = 0; x < L::NBOX; ++x) tma_store_4d(mo, sm + ob + x * BOX, x * 64, int(it.h), t0, int(it.b));
+          tma_store_4d(mo, sm + ob, it.v * 64, int(it.h), t0, int(it.b));
           tma_store_commit();
           LASP_TRACE(9, J);
         }
@@ -846,20 +874,21 @@ cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const 
       if (nst == 2) return cudaErrorInvalidValue;
       sts[nst] = a[x].state;
       if ((e = make_state_map(&prm.mst[nst], a[x].state, p)) != cudaSuccess) return e;
+      prm.stp[nst] = a[x].state;
       ps.state = nst++;
     }
   }
   for (int x = 0; x < nin; ++x)
     if ((e = make_seq_map(&prm.min[x], ins[x], p)) != cudaSuccess) return e;
   for (int x = nin; x < 4; ++x) prm.min[x] = prm.min[0];
-  if (nst < 2) prm.mst[1] = prm.mst[0];
+  if (nst < 2) { prm.mst[1] = prm.mst[0]; prm.stp[1] = prm.stp[0]; }
   prm.p = p;
   prm.npass = npass;
   prm.trace = g_trace;
   auto kern = core_tc_kernel<D>;
   const int smem = int(CoreLayout<D>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
-  const int64_t W = p.B * p.H * p.nseg * npass;
+  const int64_t W = p.B * p.H * p.nseg * npass * CoreLayout<D>::NV;
   const unsigned grid = unsigned(W < sm_count() ? W : sm_count());
   return launch_k(kern, dim3(grid), dim3(512), smem, st, prm);
 }
@@ -875,11 +904,12 @@ bool tc_supported(const Plan& p) {
     const char* s = std::getenv("LASP_DISABLE_TC");
     return s && *s && *s != '0';
   }();
-  return !disabled && p.dtype == 0 && p.D == 64 && p.C > 0;
+  return !disabled && p.dtype == 0 && (p.D == 64 || p.D == 128) && p.C > 0;
 }
 
 cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st) {
   if (p.D == 64) return dir == Dir::FWD ? launch_seg<64, Dir::FWD>(p, x, y, out, st) : launch_seg<64, Dir::REV>(p, x, y, out, st);
+  if (p.D == 128) return dir == Dir::FWD ? launch_seg<128, Dir::FWD>(p, x, y, out, st) : launch_seg<128, Dir::REV>(p, x, y, out, st);
   return cudaErrorNotSupported;
 }
 
@@ -890,6 +920,7 @@ cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_
 cudaError_t launch_core_tc_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st) {
   if (npass < 1 || npass > 3) return cudaErrorInvalidValue;
   if (p.D == 64) return launch_core_multi<64>(p, npass, a, dirs, st);
+  if (p.D == 128) return launch_core_multi<128>(p, npass, a, dirs, st);
   return cudaErrorNotSupported;
 }
 

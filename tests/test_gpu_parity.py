@@ -191,9 +191,20 @@ def test_config2_full_size_parity(L, oracle_mod):
     print("config2 errors", errs)
 
 
-def test_constant_input_closed_form_long_sequence(L):
+# ---- config 3 (TNL-1B, 16 heads x 128) at the per-rank shape bench.py --config tnl1b times -------
+def test_config3_rank_shape_parity(L, oracle_mod):
+    """16 heads x 128, n_local = 32K (config 3's per-rank shard), two simulated ranks so that the second
+    one runs with a received KV_in / dKV_in; every element against the oracle."""
+    p = synth.problem(3, 1, 65536, 16, 128, dtype="bf16")
+    res = run_sim_ring(L, p, 2, torch.bfloat16, 65536)
+    errs = check_against_oracle(oracle_mod, p, res, BF16_TOL)
+    print("config3 errors", errs)
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_constant_input_closed_form_long_sequence(L, D):
     """Closed forms for constant inputs (derived from Eq. 4): no oracle needed, N = 256K."""
-    N, H, D = 262144, 2, 64
+    N, H = 262144, 2
     lam = np.array([0.999, 1.0], dtype=np.float32)
     rng = np.random.default_rng(0)
     qv, kv_, vv, dov = (synth.round_bf16(rng.standard_normal((H, D)).astype(np.float32) * 0.3) for _ in range(4))
