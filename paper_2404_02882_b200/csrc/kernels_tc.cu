@@ -181,8 +181,13 @@ struct SegParams {
   do {                                                                                       \
     if (prm.trace != nullptr && blockIdx.x == 0 && (J) < 64) prm.trace[(ev) * 64 + (J)] = clock64(); \
   } while (0)
+#define LASP_TRACE2(ev, J)                                                                   \
+  do {                                                                                       \
+    if (prm.trace != nullptr && blockIdx.x == 0 && (J) < 64) prm.trace[1024 + (ev) * 64 + (J)] = clock64(); \
+  } while (0)
 #else
 #define LASP_TRACE(ev, J) do { } while (0)
+#define LASP_TRACE2(ev, J) do { } while (0)
 #endif
 
 template <int D, Dir DIR>
@@ -505,6 +510,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           if (warp == 2) {
             // S = a b^T (double-buffered in TMEM; buffer J & 1 is free once out(J-2) has read its P)
             mbar_wait(&bar->full[s], (J / ST) & 1);
+            LASP_TRACE(10, J);
             mbar_wait(&bar->s_empty[J & 1], ((J >> 1) & 1) ^ 1);
             tc_fence_after();
             const uint32_t dt = tmem + ((J & 1) ? L::T_S1 : L::T_S0);
@@ -531,7 +537,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           } else {
             // O_intra = P c, O_inter = a (S_hi + S_lo)
             mbar_wait(&bar->p_full[J & 1], (J >> 1) & 1);
+            LASP_TRACE(11, J);
             mbar_wait(&bar->o_empty, (J & 1) ^ 1);
+            LASP_TRACE(12, J);
             mbar_wait(&bar->st_full[J % L::NSB], (J / L::NSB) & 1);
             tc_fence_after();
             const uint32_t pt = tmem + ((J & 1) ? L::T_S1 : L::T_S0);  // P in TMEM (2 bf16 / column)
@@ -561,17 +569,23 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     // ------------------------------------------------------------------ mask warps: S -> P (bf16)
     const uint32_t q4 = warp & 3;
     const int i = int(q4 * 32 + lane);  // query row of the block
-    float* colf = reinterpret_cast<float*>(sm + L::BARS + 256) + q4 * 32;  // per-warp column factors
     uint32_t J = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
       const CItem it = get_citem(prm, w, L::NV);
       const bool fwd = it.dir == Dir::FWD;
       const float l2 = p.l2lam[it.h];
-      // off-diagonal chunks: M_ij = lam^(i-j) = rowf(i, chunk) * colf[u]; colf[u] = lam^(31-u) (FWD)
-      // or lam^u (REV), both in [lam^31, 1] (no overflow); the row factor's exponent is >= 1 there.
-      __syncwarp();
-      colf[lane] = exp2f(float(fwd ? 31 - int(lane) : int(lane)) * l2);
-      __syncwarp();
+      // Per-thread decay factors of its row, kept in registers for the whole item. With e(u) = lane - u
+      // (FWD) or u - lane (REV), column u of chunk c4 has M = lam^(32 |c4 - q4| + e(u)) on the live side:
+      //   diagonal chunk (c4 = q4):  dm[u] = lam^e(u) for e(u) >= 0, else 0 (the causal cut)
+      //   off-diagonal chunks:       t[u] = lam^(32 + e(u)), times lam^(32 (|c4 - q4| - 1))
+      // All exponents are >= 0, so no factor overflows for any lam in (0, 1].
+      float dm[32], t[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int e = fwd ? int(lane) - u : u - int(lane);
+        dm[u] = e >= 0 ? exp2f(float(e) * l2) : 0.f;
+        t[u] = exp2f(float(32 + e) * l2);
+      }
       for (int j = 0; j < it.nblk; ++j, ++J) {
         const int sb = J & 1;
         mbar_wait(&bar->s_full[sb], (J >> 1) & 1);
@@ -580,13 +594,12 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         const uint32_t ts = tmem + ((q4 * 32) << 16) + (sb ? L::T_S1 : L::T_S0);
 #pragma unroll 1
         for (int c4 = 0; c4 < 4; ++c4) {
-          // chunk columns [32 c4, 32 c4 + 32) against warp rows [32 q4, 32 q4 + 32):
-          //   FWD e = i - j = R + (31 - u), R = i - 32 c4 - 31;  REV e = j - i = R + u, R = 32 c4 - i
-          //   off-diagonal chunk (R >= 1): M = lam^R * colf[u]; diagonal chunk: M = colf[k], k = u - R (FWD)
-          //   or R + u (REV) when 0 <= k <= 31 (else 0, the causal cut); dead chunk: 0.
-          const bool dead = fwd ? (c4 > int(q4)) : (c4 < int(q4));
+          // chunk columns [32 c4, 32 c4 + 32) against warp rows [32 q4, 32 q4 + 32); dead chunks
+          // (entirely on the non-causal side) are 0
+          const int dist = fwd ? int(q4) - c4 : c4 - int(q4);
           uint32_t pk[16];
-          if (dead) {
+          if (lane == 0 && q4 == 3) LASP_TRACE2(c4 * 3, J);
+          if (dist < 0) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) pk[q] = 0u;
           } else {
@@ -594,23 +607,17 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             tmem_ld16(ts + c4 * 32, *reinterpret_cast<float(*)[16]>(&v[0]));
             tmem_ld16(ts + c4 * 32 + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
             tmem_ld_wait();
-            const int R = fwd ? i - 32 * c4 - 31 : 32 * c4 - i;
-            if (c4 != int(q4)) {
-              const float rowf = exp2f(float(R) * l2);
+            if (lane == 0 && q4 == 3) LASP_TRACE2(c4 * 3 + 1, J);
+            if (dist == 0) {
 #pragma unroll
-              for (int u = 0; u < 32; u += 4) {  // packed fp32x2 multiplies (FMUL2)
-                const float4 cf = *reinterpret_cast<const float4*>(&colf[u]);
-                float m0 = cf.x, m1 = cf.y, m2 = cf.z, m3 = cf.w;
-                fmul2(m0, m1, rowf, rowf);
-                fmul2(m2, m3, rowf, rowf);
-                fmul2(v[u], v[u + 1], m0, m1);
-                fmul2(v[u + 2], v[u + 3], m2, m3);
-              }
+              for (int u = 0; u < 32; u += 2) fmul2(v[u], v[u + 1], dm[u], dm[u + 1]);  // packed fp32x2
             } else {
 #pragma unroll
-              for (int u = 0; u < 32; ++u) {
-                const int k = fwd ? u - R : R + u;
-                v[u] = (k >= 0 && k <= 31) ? v[u] * colf[k & 31] : 0.f;
+              for (int u = 0; u < 32; u += 2) fmul2(v[u], v[u + 1], t[u], t[u + 1]);
+              if (dist > 1) {
+                const float sc = exp2f(float(32 * (dist - 1)) * l2);
+#pragma unroll
+                for (int u = 0; u < 32; u += 2) fmul2(v[u], v[u + 1], sc, sc);
               }
             }
 #pragma unroll
@@ -618,6 +625,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           }
           // P chunk -> TMEM columns [16 c4, 16 c4 + 16) of the same buffer (already consumed S columns)
           tmem_st16(ts + c4 * 16, pk);
+          if (lane == 0 && q4 == 3) LASP_TRACE2(c4 * 3 + 2, J);
         }
         if (lane == 0 && q4 == 3) LASP_TRACE(14, J);
         tmem_st_wait();

@@ -78,11 +78,24 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 }
 // Bounded wait: a protocol bug traps (launch failure reported to the host) instead of hanging the GPU.
 // The slow path is out of line to keep the warp-specialized kernels' hot code small (I-cache).
+// try_wait with an explicit suspend-time hint (ns): the thread sleeps in hardware until the phase
+// completes or the hint expires, instead of re-issuing the probe
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
 __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
   const long long t0 = clock64();
   uint32_t n = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    if ((++n & 1023u) == 0 && clock64() - t0 > (1ll << 35)) __trap();  // ~17 s at 2 GHz
+  while (!mbar_try_wait_sleep(bar, parity)) {
+    if ((++n & 63u) == 0 && clock64() - t0 > (1ll << 35)) __trap();  // ~17 s at 2 GHz
   }
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {

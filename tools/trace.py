@@ -11,9 +11,16 @@ buf = torch.zeros(2 * 16 * 64, dtype=torch.int64, device="cuda")
 N.lib().lasp_debug_trace(ctypes.c_void_p(buf.data_ptr()))
 L.fwd_local(q, k, v, p["lam"]); torch.cuda.synchronize()
 N.lib().lasp_debug_trace(None)
-t = buf.cpu().numpy().reshape(2, 16, 64)[0].astype(np.int64)
+tt = buf.cpu().numpy().reshape(2, 16, 64).astype(np.int64)
+t = tt[0]
 base = t[t > 0].min()
-names = ["tma_issue", "qk_iss", "ds_iss", "out_iss", "mask_beg", "mask_end", "ds_ready", "sbf_next", "o_full", "store", "g_qk", "g_ds", "g_pfull", "g_oempty", "st_iss", "st_done"]
+names = ["tma_issue", "qk_iss", "ds_iss", "out_iss", "mask_beg", "mask_end", "ds_ready", "sbf_next", "o_full", "store", "g_full", "g_pfull", "g_oempty", "-", "st_iss", "st_done"]
 print("J   " + " ".join(f"{n:>9s}" for n in names))
 for J in range(int(sys.argv[1]) if len(sys.argv) > 1 else 30):
     print(f"{J:3d} " + " ".join(f"{(t[e, J] - base) if t[e, J] else -1:9d}" for e in range(len(names))))
+
+print("mask warp 3 chunks (c4: before ld, after ld wait, after st), relative to mask_beg")
+for J in range(int(sys.argv[1]) if len(sys.argv) > 1 else 30):
+    if t[4, J] == 0:
+        break
+    print(f"{J:3d} " + " ".join(f"{(tt[1, e, J] - t[4, J]) if tt[1, e, J] else -1:6d}" for e in range(12)))
