@@ -7,15 +7,16 @@
 //                issues UMMA (M = N = D, K = 128, both operands MN-major) accumulating in TMEM.
 //                Eq. 12 for the forward, Eq. 21 for the backward.
 //
-//  core_tc       (F3 / B3): per segment, blocks of 128 tokens in direction order, with warp roles
-//                  warp 0       TMA producer (a, b, c tiles; 2-stage ring)
-//                  warp 1       UMMA issuer:  S = a b^T            (M=128, N=128, K=D)   [Eq. 7]
-//                                             dS = (u.b)^T c        (M=D,   N=D,   K=128) [Eq. 12]
-//                                             O_intra = P c         (M=128, N=D,   K=128) [Eq. 7]
-//                                             O_inter = a S_j       (M=128, N=D,   K=D)   [Eq. 9]
-//                  warps 4-7    mask: S (TMEM) -> (.) M_lambda -> bf16 P (smem, 128B-swizzled)
-//                  warps 8-11   state: u.b (smem), S_{j+1} = lambda^128 S_j + dS in fp32 registers,
-//                               bf16 copy of S_{j+1} for the next block's inter MMA
+//  core_tc       (F3 / B3): per (segment, pass, batch x head, 64-wide value slice) item, blocks of 128
+//                tokens in direction order, with warp roles
+//                  warp 0       TMA producer (a, b, c tiles; 3-stage ring at D = 64, 2 at D = 128)
+//                  warp 2       UMMA issuer  S = a b^T             (M=128, N=128, K=D)   [Eq. 7]
+//                  warp 3       UMMA issuer  dS = b^T (u.c)        (M=D,   N=64,  K=128) [Eq. 12]
+//                  warp 1       UMMA issuer  O_intra = P c         (M=128, N=64,  K=128) [Eq. 7]
+//                                            O_inter = a S_j       (M=128, N=64,  K=D)   [Eq. 9]
+//                  warps 4-7    mask: S (TMEM) -> (.) M_lambda -> bf16 P (TMEM, over the consumed S)
+//                  warps 8-11   state: u.c (smem), S_{j+1} = lambda^128 S_j + dS in fp32 registers,
+//                               bf16 hi/lo copy of S_{j+1} for the next block's inter MMA
 //                  warps 12-15  epilogue: out = O_intra + r (.) O_inter -> bf16 -> TMA store
 //                The running state is the paper's KV (dKV) state applied between GPU blocks; the
 //                segment's initial state comes from the prefix kernel (KV_in of the ring included).

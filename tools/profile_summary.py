@@ -58,11 +58,19 @@ def full(rep, out, key=None):
         for m, (v, u) in got.items():
             f.write(f"| {m} | {v} | {u} |\n")
         f.write("\n## Section summary (ncu details page)\n\n")
-        for r in csv.reader(io.StringIO(det)):
-            if len(r) >= 4 and r[-3] in ("Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput",
-                                        "Executed Ipc Active", "Registers Per Thread", "Achieved Occupancy",
-                                        "L2 Hit Rate", "Warp Cycles Per Issued Instruction", "No Eligible"):
-                f.write(f"- {r[-3]}: {r[-1]} {r[-2]}\n")
+        want = ("Duration", "SM Frequency", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput",
+                "Executed Ipc Active", "Registers Per Thread", "Achieved Occupancy", "L2 Hit Rate",
+                "Warp Cycles Per Issued Instruction", "No Eligible")
+        rows = list(csv.reader(io.StringIO(det)))
+        if rows:
+            h = rows[0]
+            iname, iunit, ival = h.index("Metric Name"), h.index("Metric Unit"), h.index("Metric Value")
+            isec = h.index("Section Name")
+            seen = set()
+            for r in rows[1:]:
+                if len(r) > ival and r[iname] in want and (r[isec], r[iname]) not in seen:
+                    seen.add((r[isec], r[iname]))
+                    f.write(f"- {r[isec]} / {r[iname]}: {r[ival]} {r[iunit]}\n")
     print(open(out).read())
     if key and "dram__bytes_read.sum" in got:
         def to_bytes(v, u):

@@ -1,0 +1,16 @@
+# Round evidence: bench lines (both head dims), ncu launch list, ncu --set full of the top kernels.
+# usage (on the GPU box): bash tools/round_profile.sh <tag>
+tag=${1:-r}
+mkdir -p gpurun_out
+timeout 900 python bench.py --steps 50 --warmup 5 > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
+timeout 600 python bench.py --config tnl1b --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/${tag}_bench_tnl1b.json 2> gpurun_out/${tag}_bench_tnl1b.err
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/${tag}_launches.csv \
+  python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+# launches per step: seg_state(F) prefix core(F) seg_state(R) prefix core(bwd3) -> core instance 4 = fwd, 5 = bwd3
+for sk in 4 5; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:core_tc --launch-skip $sk --launch-count 1 \
+    -o gpurun_out/${tag}_core_skip$sk -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:seg_state_tc --launch-skip 4 --launch-count 1 \
+  -o gpurun_out/${tag}_seg_skip4 -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+ls -la gpurun_out | tail -12
