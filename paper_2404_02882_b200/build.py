@@ -45,7 +45,9 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
                "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
                "-I", _nccl_include(), "-c", os.path.join(CSRC, src), "-o", obj]
         if os.environ.get("LASP_TRACE_BUILD"):
-            cmd += ["-DLASP_TRACE_BUILD"] + (["-DLASP_EXPERIMENT_NOMASK"] if os.environ.get("LASP_NOMASK") else []) + (["-DLASP_EXPERIMENT_NOSTORE"] if os.environ.get("LASP_NOSTORE") else [])
+            cmd += ["-DLASP_TRACE_BUILD"]
+        if os.environ.get("LASP_EXTRA_NVCC"):  # debug / experiment builds only (always with --out)
+            cmd += os.environ["LASP_EXTRA_NVCC"].split()
         if os.environ.get("LASP_PTXAS_VERBOSE"):
             cmd += ["-Xptxas", "-v"]
         jobs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT))

@@ -593,6 +593,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         if (lane == 0 && q4 == 3) LASP_TRACE(4, J);
         tc_fence_after();
         const uint32_t ts = tmem + ((q4 * 32) << 16) + (sb ? L::T_S1 : L::T_S0);
+#ifdef LASP_EXPERIMENT_NOMASK  // timing experiment only (tools/cmp_variants.sh): P = garbage
+        if (false)
+#endif
 #pragma unroll 1
         for (int c4 = 0; c4 < 4; ++c4) {
           // chunk columns [32 c4, 32 c4 + 32) against warp rows [32 q4, 32 q4 + 32); dead chunks
@@ -696,6 +699,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       auto scale_ku = [&](uint32_t JJ) {
         const int s = JJ % ST;
         mbar_wait(&bar->full[s], (JJ / ST) & 1);
+#ifdef LASP_EXPERIMENT_NOSTATE
+        if (false)
+#endif
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const uint32_t off = uint32_t(g) * 128 + ((uint32_t(c) ^ (uint32_t(g) & 7)) << 4);
@@ -710,6 +716,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         // of block J - NSB are done)
         const int sb = int(J % L::NSB);
         mbar_wait(&bar->st_empty[sb], ((J / L::NSB) & 1) ^ 1);
+#ifdef LASP_EXPERIMENT_NOSTATE  // timing experiment only: no state math
+        if (false)
+#endif
         if (valid) {
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
@@ -735,6 +744,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         if (g == 0) LASP_TRACE(6, J);
         tc_fence_after();
         const uint32_t td = tmem + ((q4 * 32) << 16) + L::T_DS;
+#ifdef LASP_EXPERIMENT_NOSTATE
+        if (false)
+#endif
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           float v[16];
@@ -765,6 +777,11 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         mbar_wait(&bar->o_full, J & 1);
         if (i == 0) LASP_TRACE(8, J);
         tc_fence_after();
+#ifdef LASP_EXPERIMENT_NOEPI  // timing experiment only: no output
+        tc_fence_before();
+        mbar_arrive(&bar->o_empty);
+        continue;
+#endif
         const uint32_t ti = tmem + ((q4 * 32) << 16) + L::T_OI;
         const uint32_t tx = tmem + ((q4 * 32) << 16) + L::T_OX;
         uint32_t pk[32];
