@@ -37,8 +37,8 @@ template <typename T, int D, Dir DIR>
 __global__ void __launch_bounds__(kThreads) seg_state_simt_kernel(Plan p, const T* __restrict__ x,
                                                                   const T* __restrict__ y,
                                                                   float* __restrict__ out) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   constexpr int TT = 32;        // tokens per smem tile
   constexpr int R = D / 16;     // per-thread register tile R x R
   __shared__ float xs[TT][D + 1];
@@ -94,8 +94,8 @@ __global__ void __launch_bounds__(kThreads) seg_state_simt_kernel(Plan p, const 
 // (Alg. 2 P:171 / Alg. 3 P:648 applied between segments). `prefix` may alias `seg_states`.
 __global__ void prefix_kernel(Plan p, Dir dir, const float* __restrict__ init, const float* seg_states,
                               float* prefix, float* __restrict__ final_out) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   // one thread per 4 consecutive state elements (float4); segments folded in order
   const int64_t DD = p.D * p.D;
   const int64_t idx4 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over B*H*D*D/4
@@ -135,8 +135,8 @@ __global__ void prefix_kernel(Plan p, Dir dir, const float* __restrict__ init, c
 // kv_out = lam^C kv_in + local (the ring's combine step, Alg. 2 P:171 with the local part hoisted)
 __global__ void combine_kernel(Plan p, const float* __restrict__ kv_in,
                                const float* __restrict__ local, float* __restrict__ kv_out) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   const int64_t DD = p.D * p.D;
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= p.B * p.H * DD) return;
@@ -150,8 +150,8 @@ __global__ void combine_kernel(Plan p, const float* __restrict__ kv_in,
 // state S in shared memory (fp32).
 template <typename T, int D, Dir DIR>
 __global__ void __launch_bounds__(kThreads) core_simt_kernel(Plan p, SeqArgs a) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   constexpr int BT = 32;
   extern __shared__ float smem[];
   float* sa = smem;                  // [BT][D+1]

@@ -147,10 +147,6 @@ __device__ __forceinline__ int64_t block_row(Dir dir, const Item& it, int j) {
   return dir == Dir::FWD ? it.beg + int64_t(j) * BT : it.end - int64_t(j + 1) * BT;
 }
 
-// cursor over the flattened (item, block) sequence of this CTA
-__device__ __forceinline__ void watchdog(long long t0) {
-  if (clock64() - t0 > (1ll << 36)) __trap();
-}
 
 // ================================================================================================
 // seg_state_tc (persistent): warp 0 TMA, warp 1 UMMA, warps 4-7 scale X rows, warps 8-11 drain
@@ -160,8 +156,12 @@ template <int D>
 struct SegLayout {
   static constexpr int NBOX = D / 64;
   static constexpr uint32_t TILE = NBOX * BOX;
-  static constexpr int STAGES = D == 64 ? 3 : 2;
-  static constexpr int CTAS_PER_SM = D == 64 ? 2 : 1;  // 2 x (96 KB smem, 128 TMEM columns) per SM
+#ifndef LASP_SEG_STAGES64
+#define LASP_SEG_STAGES64 3
+#define LASP_SEG_CTAS64 2
+#endif
+  static constexpr int STAGES = D == 64 ? LASP_SEG_STAGES64 : 2;
+  static constexpr int CTAS_PER_SM = D == 64 ? LASP_SEG_CTAS64 : 1;  // 2 x (96 KB smem, 128 TMEM columns) per SM
   static constexpr uint32_t X(int s) { return uint32_t(s) * 2 * TILE; }
   static constexpr uint32_t Y(int s) { return uint32_t(s) * 2 * TILE + TILE; }
   static constexpr uint32_t BARS = STAGES * 2 * TILE;
@@ -182,10 +182,14 @@ struct SegParams {
   do {                                                                                       \
     if (prm.trace != nullptr && blockIdx.x == 0 && (J) < 64) prm.trace[(ev) * 64 + (J)] = clock64(); \
   } while (0)
+#ifdef LASP_NO_TRACE2
+#define LASP_TRACE2(ev, J) do { } while (0)
+#else
 #define LASP_TRACE2(ev, J)                                                                   \
   do {                                                                                       \
     if (prm.trace != nullptr && blockIdx.x == 0 && (J) < 64) prm.trace[1024 + (ev) * 64 + (J)] = clock64(); \
   } while (0)
+#endif
 #else
 #define LASP_TRACE(ev, J) do { } while (0)
 #define LASP_TRACE2(ev, J) do { } while (0)
@@ -216,13 +220,13 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
     for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], 128); }
     fence_mbar_init();
   }
-  pdl_trigger();
   if (warp == 1) tmem_alloc<L::TCOLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // the previous kernel of the stream has completed and its writes are visible
+  pdl_trigger();  // only after the wait (see core_tc_kernel)
 
   if (warp == 0) {
     if (elect_one()) {
@@ -448,34 +452,47 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     mbar_init(&bar->o_full, 1); mbar_init(&bar->o_empty, 128);
     fence_mbar_init();
   }
-  pdl_trigger();
   if (warp == 1) tmem_alloc<512>(&bar->tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bar->tmem_slot;
-  pdl_wait();  // the previous kernel of the stream has completed and its writes are visible
+  // Programmatic dependent launch: every kernel of the library triggers its dependents only after its
+  // own griddepcontrol.wait, so when this kernel starts, the kernel two launches back (and everything
+  // before it) has completed. The a, b, c tiles are inputs of that earlier work, so the producer fills
+  // the ring before waiting; only the segment prefix states (written by the immediately preceding
+  // kernel) are read after the wait (producer: STG; state warps at D = 128: direct loads).
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
     if (elect_one()) {
+      bool waited = false;
       uint32_t J = 0, k = 0;
       for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
         const CItem it = get_citem(prm, w, L::NV);
         const CorePass& ps = prm.pass[it.pass];
-        if constexpr (L::HAS_STG) {
-          // the segment's prefix state -> STG (single buffer, released by the state warps)
-          mbar_wait(&bar->stg_empty, (k & 1) ^ 1);
-          mbar_expect_tx(&bar->stg_full, 4 * D * D);
-          const int srow = int(((it.b * p.H + it.h) * p.nseg + it.seg) * D);
+        // the segment's prefix state -> STG (single buffer, released by the state warps)
+        auto load_stg = [&]() {
+          if constexpr (L::HAS_STG) {
+            mbar_wait(&bar->stg_empty, (k & 1) ^ 1);
+            mbar_expect_tx(&bar->stg_full, 4 * D * D);
+            const int srow = int(((it.b * p.H + it.h) * p.nseg + it.seg) * D);
 #pragma unroll
-          for (int x = 0; x < D / 32; ++x)
-            tma_load_2d(sm + L::STG + x * (D * 128), &prm.mst[ps.state], &bar->stg_full, x * 32, srow);
-        }
+            for (int x = 0; x < D / 32; ++x)
+              tma_load_2d(sm + L::STG + x * (D * 128), &prm.mst[ps.state], &bar->stg_full, x * 32, srow);
+          }
+        };
+        if (waited) load_stg();
         const CUtensorMap* ma = &prm.min[ps.a];
         const CUtensorMap* mb = &prm.min[ps.b];
         const CUtensorMap* mc = &prm.min[ps.c];
         for (int j = 0; j < it.nblk; ++j, ++J) {
+          if (!waited && j == (it.nblk < ST ? it.nblk : ST)) {
+            pdl_wait();
+            pdl_trigger();
+            waited = true;
+            load_stg();
+          }
           const int s = J % ST;
           mbar_wait(&bar->empty[s], ((J / ST) & 1) ^ 1);
           LASP_TRACE(0, J);
@@ -487,6 +504,12 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             tma_load_4d(sm + L::B_(s) + x * BOX, mb, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
           }
           tma_load_4d(sm + L::C_(s), mc, &bar->full[s], it.v * 64, int(it.h), t0, int(it.b));
+        }
+        if (!waited) {  // first item shorter than the ring
+          pdl_wait();
+          pdl_trigger();
+          waited = true;
+          load_stg();
         }
       }
     }
@@ -568,8 +591,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     }
   } else if (warp >= 4 && warp < 8) {
     // ------------------------------------------------------------------ mask warps: S -> P (bf16)
-    const uint32_t q4 = warp & 3;
-    const int i = int(q4 * 32 + lane);  // query row of the block
+    const uint32_t q4 = warp & 3;  // rows [32 q4, 32 q4 + 32) of the block
     uint32_t J = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
       const CItem it = get_citem(prm, w, L::NV);
@@ -672,6 +694,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       } else {
         // straight from the (L2-resident) prefix states: row d, columns [64 v, 64 v + 64) of S, or
         // column d, rows [64 v, 64 v + 64) for S^T (coalesced across the warp)
+        if (k == 0) pdl_wait();  // the prefix states come from the preceding kernel
         const float* st = prm.stp[state] + ((it.b * p.H + it.h) * p.nseg + it.seg) * D * D;
         if (trans) {
 #pragma unroll
