@@ -144,6 +144,16 @@ lasp_status_t lasp_unique_id(uint8_t id[128]);
 lasp_status_t lasp_ctx_create(int rank, int world, const uint8_t id[128], int device, lasp_ctx_t* out);
 lasp_status_t lasp_ctx_destroy(lasp_ctx_t ctx);
 
+/* Same ring context with an in-process loopback transport instead of NCCL: the `world` ranks are
+ * threads of one process sharing CUDA device `device`, joined by the group name `group` (NUL-terminated,
+ * owned by the caller). A send stages the message in a stream-ordered device allocation and records an
+ * event on the sender's stream; the matching receive makes the receiver's stream wait on that event and
+ * copies the message out, the receiving host thread blocking (up to 120 s, then LASP_ERR_COMM) until the
+ * send is posted. Exists so that lasp_fwd / lasp_bwd with world > 1 can be exercised on a single GPU
+ * (NCCL refuses two ranks on one device). LASP_ERR_PARTITION for a rank outside [0, world) or a group
+ * name already in use with another world size. Destroy with lasp_ctx_destroy. */
+lasp_status_t lasp_ctx_create_loopback(int rank, int world, const char* group, int device, lasp_ctx_t* out);
+
 /* Ring schedule (host-only, no GPU): the peer this rank receives its state from and sends its state to
  * (-1 = none). Forward (backward = 0): from r-1, to r+1 (Alg. 2); backward: from r+1, to r-1
  * (Alg. 3, reading A2 of P:649). Used by lasp_fwd/lasp_bwd; exposed for protocol tests. */

@@ -50,6 +50,8 @@ _SIGS = {
     "lasp_unique_id": ([ctypes.c_char_p], ctypes.c_int),
     "lasp_ctx_create": ([ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(_vp)],
                         ctypes.c_int),
+    "lasp_ctx_create_loopback": ([ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(_vp)],
+                                 ctypes.c_int),
     "lasp_ctx_destroy": ([_vp], ctypes.c_int),
     "lasp_ctx_protocol": ([_vp, _sp, _i64p, _i64p, _i64p], ctypes.c_int),
     "lasp_ring_peers": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int),

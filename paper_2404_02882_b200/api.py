@@ -131,6 +131,18 @@ class Ring:
         N.check(N.lib().lasp_ctx_create(self.rank, self.world, obj[0], self.device.index or 0,
                                         ctypes.byref(self._ctx)))
 
+    @classmethod
+    def loopback(cls, rank: int, world: int, group: str, device=None) -> "Ring":
+        """A ring context whose ranks are threads of this process on one GPU (in-process loopback
+        transport instead of NCCL; for exercising the multi-rank path on a single device)."""
+        self = cls.__new__(cls)
+        self.rank, self.world = rank, world
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self._ctx = ctypes.c_void_p()
+        N.check(N.lib().lasp_ctx_create_loopback(rank, world, group.encode(), self.device.index or 0,
+                                                 ctypes.byref(self._ctx)))
+        return self
+
     def close(self):
         if self._ctx:
             N.lib().lasp_ctx_destroy(self._ctx)

@@ -14,6 +14,11 @@
 #include <nccl.h>
 
 #include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <map>
+#include <memory>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -346,14 +351,92 @@ lasp_status_t nccl_fail(ncclResult_t r, const char* what, int rank, int peer) {
   return fail(LASP_ERR_COMM, buf);
 }
 
+// ---- loopback transport: the ring's ranks as threads of one process on one GPU (testing) ------
+// A message is staged in a stream-ordered allocation: the sender copies into it and records an event,
+// the receiver's stream waits on that event, copies out and frees it. Same ordering contract as
+// ncclSend/ncclRecv on the given streams; the receiving host thread blocks until the send is posted.
+struct LoopMsg {
+  void* buf = nullptr;
+  cudaEvent_t ev = nullptr;
+  size_t bytes = 0;
+};
+struct LoopGroup {
+  int world = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::map<std::pair<int, int>, std::deque<LoopMsg>> q;  // (src, dst) -> messages in send order
+};
+std::mutex g_loop_mu;
+std::unordered_map<std::string, std::weak_ptr<LoopGroup>> g_loops;
+
+std::shared_ptr<LoopGroup> loop_group(const std::string& name, int world) {
+  std::lock_guard<std::mutex> g(g_loop_mu);
+  auto it = g_loops.find(name);
+  if (it != g_loops.end())
+    if (auto sp = it->second.lock()) return sp->world == world ? sp : nullptr;
+  auto sp = std::make_shared<LoopGroup>();
+  sp->world = world;
+  g_loops[name] = sp;
+  return sp;
+}
+
 }  // namespace
 
 struct lasp_ctx {
   ncclComm_t comm = nullptr;
+  std::shared_ptr<LoopGroup> loop;  // non-null: loopback transport instead of NCCL
   int rank = 0, world = 1, device = 0;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
 };
+
+namespace {
+
+lasp_status_t ring_send(lasp_ctx* c, const float* buf, size_t n, int peer, cudaStream_t st, const char* what) {
+  if (!c->loop) {
+    ncclResult_t r = nccl().Send(buf, n, ncclFloat32, peer, c->comm, st);
+    return r == ncclSuccess ? LASP_OK : nccl_fail(r, what, c->rank, peer);
+  }
+  LoopMsg m;
+  m.bytes = n * sizeof(float);
+  LASP_CUDA(cudaMallocAsync(&m.buf, m.bytes, st));
+  LASP_CUDA(cudaMemcpyAsync(m.buf, buf, m.bytes, cudaMemcpyDeviceToDevice, st));
+  LASP_CUDA(cudaEventCreateWithFlags(&m.ev, cudaEventDisableTiming));
+  LASP_CUDA(cudaEventRecord(m.ev, st));
+  {
+    std::lock_guard<std::mutex> g(c->loop->mu);
+    c->loop->q[{c->rank, peer}].push_back(m);
+  }
+  c->loop->cv.notify_all();
+  return LASP_OK;
+}
+
+lasp_status_t ring_recv(lasp_ctx* c, float* buf, size_t n, int peer, cudaStream_t st, const char* what) {
+  if (!c->loop) {
+    ncclResult_t r = nccl().Recv(buf, n, ncclFloat32, peer, c->comm, st);
+    return r == ncclSuccess ? LASP_OK : nccl_fail(r, what, c->rank, peer);
+  }
+  LoopMsg m;
+  {
+    std::unique_lock<std::mutex> g(c->loop->mu);
+    auto& dq = c->loop->q[{peer, c->rank}];
+    if (!c->loop->cv.wait_for(g, std::chrono::seconds(120), [&] { return !dq.empty(); })) {
+      char b[160];
+      std::snprintf(b, sizeof b, "%s: loopback receive from rank %d timed out on rank %d", what, peer, c->rank);
+      return fail(LASP_ERR_COMM, b);
+    }
+    m = dq.front();
+    dq.pop_front();
+  }
+  if (m.bytes != n * sizeof(float)) return fail(LASP_ERR_COMM, "loopback message size mismatch");
+  LASP_CUDA(cudaStreamWaitEvent(st, m.ev, 0));
+  LASP_CUDA(cudaMemcpyAsync(buf, m.buf, m.bytes, cudaMemcpyDeviceToDevice, st));
+  LASP_CUDA(cudaFreeAsync(m.buf, st));
+  LASP_CUDA(cudaEventDestroy(m.ev));
+  return LASP_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -485,6 +568,23 @@ lasp_status_t lasp_ctx_create(int rank, int world, const uint8_t id[128], int de
   return LASP_OK;
 }
 
+lasp_status_t lasp_ctx_create_loopback(int rank, int world, const char* group, int device, lasp_ctx_t* out) {
+  if (!out || !group) return fail(LASP_ERR_SHAPE, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(LASP_ERR_PARTITION, "rank outside [0, world)");
+  LASP_CUDA(cudaSetDevice(device));
+  auto grp = loop_group(group, world);
+  if (!grp) return fail(LASP_ERR_PARTITION, "loopback group exists with a different world size");
+  lasp_ctx* c = new lasp_ctx;
+  c->rank = rank; c->world = world; c->device = device;
+  c->loop = grp;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming);
+  if (e != cudaSuccess) { delete c; return cuda_fail(e, "ctx stream/event"); }
+  *out = c;
+  return LASP_OK;
+}
+
 lasp_status_t lasp_ctx_destroy(lasp_ctx_t c) {
   if (!c) return LASP_OK;
   if (c->comm) nccl().CommDestroy(c->comm);
@@ -533,22 +633,19 @@ lasp_status_t lasp_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Workspace w = carve(p, workspace);
   const size_t n = state_elems(p);
-  NcclApi& nc = nccl();
   int from = -1, to = -1;
   lasp_ring_peers(c->rank, c->world, 0, &from, &to);
   if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st));                     // F1
   LASP_CUDA(prefix(p, Dir::FWD, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
   // F2 ring hop: Recv KV_in from r-1 (Alg. 2), combine, Send to r+1
   if (from >= 0) {
-    ncclResult_t r = nc.Recv(w.in, n, ncclFloat32, from, c->comm, st);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclRecv(KV)", c->rank, from);
+    if ((s = ring_recv(c, w.in, n, from, st, "ncclRecv(KV)")) != LASP_OK) return s;
   } else {
     LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), st));
   }
   if (to >= 0) {
     LASP_CUDA(combine(p, w.in, w.local, w.out, st));
-    ncclResult_t r = nc.Send(w.out, n, ncclFloat32, to, c->comm, st);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclSend(KV)", c->rank, to);
+    if ((s = ring_send(c, w.out, n, to, st, "ncclSend(KV)")) != LASP_OK) return s;
   }
   if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, st)) != LASP_OK) return s;  // F2 + F3
   register_cache(p, cache, c->rank, c->world);
@@ -568,7 +665,6 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Workspace w = carve(p, workspace);
   const size_t n = state_elems(p);
-  NcclApi& nc = nccl();
   const float* P = static_cast<const float*>(cache);
   if (p.C > 0) LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st));                    // B1
   LASP_CUDA(prefix(p, Dir::REV, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
@@ -578,15 +674,13 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   int from = -1, to = -1;
   lasp_ring_peers(c->rank, c->world, 1, &from, &to);
   if (from >= 0) {
-    ncclResult_t r = nc.Recv(w.in, n, ncclFloat32, from, c->comm, c->comm_stream);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclRecv(dKV)", c->rank, from);
+    if ((s = ring_recv(c, w.in, n, from, c->comm_stream, "ncclRecv(dKV)")) != LASP_OK) return s;
   } else {
     LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), c->comm_stream));
   }
   if (to >= 0) {
     LASP_CUDA(combine(p, w.in, w.local, w.out, c->comm_stream));
-    ncclResult_t r = nc.Send(w.out, n, ncclFloat32, to, c->comm, c->comm_stream);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclSend(dKV)", c->rank, to);
+    if ((s = ring_send(c, w.out, n, to, c->comm_stream, "ncclSend(dKV)")) != LASP_OK) return s;
   }
   LASP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
   // dQ needs only the cache: it runs while the dKV hop is in flight

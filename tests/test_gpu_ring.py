@@ -65,3 +65,83 @@ def test_ring_cache_tag_checks_rank(ring):
     with pytest.raises(LaspError) as e:
         ring.bwd(q, q, q, [0.9, 0.9], q, cache)
     assert e.value.name == "LASP_ERR_STATE"
+
+
+# ---- world > 1 on one GPU: the same lasp_fwd / lasp_bwd code with the in-process loopback transport ----
+def _run_loopback(p, world, n_global, dtype, group):
+    """Each rank is a thread with its own CUDA stream and ring context; returns the gathered outputs."""
+    import threading
+    import paper_2404_02882_b200 as lasp
+    C = n_global // world
+    out, errors = [None] * world, []
+    done = threading.Barrier(world)
+
+    def worker(r):
+        ring = None
+        try:
+            torch.cuda.set_device(0)
+            ring = lasp.Ring.loopback(r, world, group)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                sl = slice(r * C, (r + 1) * C)
+                q, k, v, do = (torch.from_numpy(np.ascontiguousarray(p[x][:, sl])).cuda().to(dtype)
+                               for x in ("q", "k", "v", "do"))
+                o, cache = ring.fwd(q, k, v, p["lam"])
+                dq, dk, dv = ring.bwd(q, k, v, p["lam"], do, cache)
+            stream.synchronize()
+            B, Cr, H, D = q.shape
+            seg = lasp.segment_len(lasp.api._shape(q))
+            nseg = (Cr + seg - 1) // seg
+            # cache [B][H][nseg][D][D]; entry 0 of each (b, h) = KV_in(r), the state entering the rank
+            kv_in = cache.view(torch.float32)[:B * H * nseg * D * D].view(B, H, nseg, D, D)[:, :, 0]
+            out[r] = [t.float().cpu().numpy() for t in (o, dq, dk, dv)] + [kv_in.cpu().numpy()]
+        except BaseException as e:  # noqa: BLE001 - re-raised by the test
+            errors.append(e)
+            done.abort()
+            return
+        finally:
+            try:
+                done.wait(timeout=300)  # keep every context alive until all ranks are finished
+            except threading.BrokenBarrierError:
+                pass
+            if ring is not None:
+                ring.close()
+
+    ts = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    assert not errors, errors
+    return [np.concatenate([out[r][i] for r in range(world)], axis=1) for i in range(4)], [o[4] for o in out]
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_loopback_ring_bf16_matches_oracle(oracle_mod, world):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    N = 768 * world
+    p = synth.problem(40 + world, 1, N, 4, 64, dtype="bf16")
+    got, _ = _run_loopback(p, world, N, torch.bfloat16, f"bf16-w{world}")
+    refs = [oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])] + \
+        list(oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"]))
+    for x, r in zip(got, refs):
+        assert oracle_mod.normwise_err(x, r) <= 2e-2
+
+
+def test_loopback_ring_config1_fp32(oracle_mod):
+    """BASELINE configs[0] on the real ring code: 1 head x 32, N=512, lambda=0.99, 4 ranks, fp32."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    p = synth.problem(0, 1, 512, 1, 32, dtype="fp32", lam=0.99)
+    got, kv_in = _run_loopback(p, 4, 512, torch.float32, "config1")
+    refs = [oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])] + \
+        list(oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"]))
+    for x, r in zip(got, refs):
+        assert oracle_mod.normwise_err(x, r) <= 1e-5
+    # each rank's cache holds the state that entered it (Alg. 2 P:168, reading A4)
+    _, cache, _, _ = oracle_mod.lasp_fwd_sim(p["q"], p["k"], p["v"], p["lam"], 4)
+    for r in range(4):
+        ref = np.asarray(cache[r]).reshape(kv_in[r].shape)
+        den = max(np.max(np.abs(ref)), 1e-30)
+        assert np.max(np.abs(kv_in[r] - ref)) / den <= 1e-5 or (r == 0 and np.max(np.abs(kv_in[r])) == 0)
