@@ -201,7 +201,7 @@ def run_lasp(args):
     q, k, v, do = d_in["q"], d_in["k"], d_in["v"], d_in["do"]
     o, dq, dk, dv = (torch.empty_like(q) for _ in range(4))
     cache, ws = lasp.alloc_cache(q), lasp.alloc_workspace(q)
-    ring = lasp.Ring(dev) if world > 1 else None
+    ring = lasp.Ring(dev).set_exchange(args.exchange) if world > 1 else None
 
     def step():
         if ring is None:
@@ -347,7 +347,8 @@ def run_lasp(args):
                        "head_dim": D, "lambda": "per-head 1-2^-(1+14h/(H-1))",
                        "segment_len": lasp.segment_len(N.shape(B, C, H, D, N.LASP_BF16)),
                        "l2": "flushed between timed steps (256 MiB read outside the step events); inputs 4x"
-                             f" {B * C * H * D * 2 >> 20} MiB", "parallelism": f"sp{world}"},
+                             f" {B * C * H * D * 2 >> 20} MiB", "parallelism": f"sp{world}",
+                       "exchange": args.exchange if world > 1 else "none"},
             "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e, "roofline": roofline,
             "path": path, "cpu_baseline": cpu}
     if rank == 0:
@@ -366,6 +367,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["lasp", "reference"], default="lasp")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="tnl04b")
+    ap.add_argument("--exchange", choices=["ring", "allgather"], default="ring",
+                    help="state exchange at N > 1: the paper's ring (default) or one all-gather (NEXT-2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

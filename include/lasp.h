@@ -154,13 +154,25 @@ lasp_status_t lasp_ctx_destroy(lasp_ctx_t ctx);
  * name already in use with another world size. Destroy with lasp_ctx_destroy. */
 lasp_status_t lasp_ctx_create_loopback(int rank, int world, const char* group, int device, lasp_ctx_t* out);
 
+/* State exchange of lasp_fwd / lasp_bwd (not in the paper, which only has the ring).
+ *   LASP_EXCHANGE_RING (default): the paper's T-1 dependent hops, Alg. 2 P:167-172 / Alg. 3 P:629-649.
+ *   LASP_EXCHANGE_ALLGATHER: one all-gather of the T local states (B*H*D*D fp32 each; ncclAllGather, or
+ *     pairwise sends on a loopback ctx) into a ctx-owned buffer, then each rank folds the states it would
+ *     have received: KV_in(r) = sum_{j<r} lam^(C(r-1-j)) L_j, dKV_in(r) = sum_{j>r} lam^(C(j-r-1)) G_j.
+ *     Same results up to fp32 summation order; assumes every rank has the same n_local (Alg. 1: C = N/T).
+ * LASP_ERR_DOMAIN for any other value. */
+#define LASP_EXCHANGE_RING 0
+#define LASP_EXCHANGE_ALLGATHER 1
+lasp_status_t lasp_ctx_set_exchange(lasp_ctx_t ctx, int exchange);
+
 /* Ring schedule (host-only, no GPU): the peer this rank receives its state from and sends its state to
  * (-1 = none). Forward (backward = 0): from r-1, to r+1 (Alg. 2); backward: from r+1, to r-1
  * (Alg. 3, reading A2 of P:649). Used by lasp_fwd/lasp_bwd; exposed for protocol tests. */
 lasp_status_t lasp_ring_peers(int rank, int world, int backward, int* recv_from, int* send_to);
 
 /* Messages and fp32 elements per message this ctx will send per direction per call (protocol
- * introspection for tests: world-1 hops in total, this rank sends 0 or 1). */
+ * introspection for tests: ring exchange: world-1 hops in total, this rank sends 0 or 1; all-gather
+ * exchange: one contribution per rank when world > 1). */
 lasp_status_t lasp_ctx_protocol(lasp_ctx_t ctx, const lasp_shape_t* shape, int64_t* sends_fwd,
                                 int64_t* sends_bwd, int64_t* elems_per_msg);
 

@@ -143,6 +143,13 @@ class Ring:
                                                  ctypes.byref(self._ctx)))
         return self
 
+    def set_exchange(self, exchange: str) -> "Ring":
+        """'ring' (the paper's T-1 hops, default) or 'allgather' (one all-gather of the local states plus a
+        local fold)."""
+        mode = {"ring": N.LASP_EXCHANGE_RING, "allgather": N.LASP_EXCHANGE_ALLGATHER}[exchange]
+        N.check(N.lib().lasp_ctx_set_exchange(self._ctx, mode))
+        return self
+
     def close(self):
         if self._ctx:
             N.lib().lasp_ctx_destroy(self._ctx)

@@ -298,6 +298,32 @@ cudaError_t launch_prefix(const Plan& p, Dir dir, const float* init, const float
                   seg_states, prefix_out, final_out);
 }
 
+// All-gather exchange: fold the gathered per-rank local states of ranks
+// j0, j0 + step, ... (count of them) in that order: cur = lam^C cur + g[j], starting from 0. Forward:
+// KV_in(r) = sum_{j<r} lam^(C (r-1-j)) L_j (j0 = 0, step +1, count r); backward: dKV_in(r) =
+// sum_{j>r} lam^(C (j-r-1)) G_j (j0 = T-1, step -1, count T-1-r). Same decay as combine_kernel.
+__global__ void fold_ranks_kernel(Plan p, const float* __restrict__ g, int j0, int step, int count,
+                                  float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t n = p.B * p.H * p.D * p.D;
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  const int64_t h = (idx / (p.D * p.D)) % p.H;
+  const float dec = powk(p.lam[h], double(p.C));
+  float cur = 0.f;
+  for (int t = 0; t < count; ++t) cur = fmaf(dec, cur, g[int64_t(j0 + t * step) * n + idx]);
+  out[idx] = cur;
+}
+
+cudaError_t launch_fold_ranks(const Plan& p, const float* gathered, int j0, int step, int count, float* out,
+                              cudaStream_t st) {
+  const int64_t n = p.B * p.H * p.D * p.D;
+  const int threads = 256;
+  return launch_k(fold_ranks_kernel, dim3((unsigned)((n + threads - 1) / threads)), dim3(threads), 0, st, p, gathered,
+                  j0, step, count, out);
+}
+
 cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local, float* kv_out, cudaStream_t st) {
   const int64_t n = p.B * p.H * p.D * p.D;
   const int threads = 256;

@@ -318,6 +318,7 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -336,6 +337,7 @@ NcclApi& nccl() {
     api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
     api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
     api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+    api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
     api.loaded = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
                  api.GetErrorString;
@@ -386,8 +388,11 @@ struct lasp_ctx {
   ncclComm_t comm = nullptr;
   std::shared_ptr<LoopGroup> loop;  // non-null: loopback transport instead of NCCL
   int rank = 0, world = 1, device = 0;
+  int exchange = LASP_EXCHANGE_RING;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+  float* gather = nullptr;  // all-gather exchange: [world][B*H*D*D] fp32 (ctx-owned, grown on demand)
+  size_t gather_elems = 0;
 };
 
 namespace {
@@ -434,6 +439,36 @@ lasp_status_t ring_recv(lasp_ctx* c, float* buf, size_t n, int peer, cudaStream_
   LASP_CUDA(cudaFreeAsync(m.buf, st));
   LASP_CUDA(cudaEventDestroy(m.ev));
   return LASP_OK;
+}
+
+// All-gather exchange (NEXT-2): every rank's local state into ctx->gather[world][n], then the state this
+// rank would have received over the ring is folded from the gathered ones (fold_ranks_kernel).
+lasp_status_t exchange_allgather(lasp_ctx* c, const Plan& p, const float* local, float* in, bool backward,
+                                 cudaStream_t st) {
+  const size_t n = size_t(p.B * p.H * p.D * p.D);
+  if (c->gather_elems < n * size_t(c->world)) {
+    if (c->gather) LASP_CUDA(cudaFree(c->gather));
+    c->gather = nullptr;
+    c->gather_elems = 0;
+    LASP_CUDA(cudaMalloc(&c->gather, n * size_t(c->world) * sizeof(float)));
+    c->gather_elems = n * size_t(c->world);
+  }
+  if (!c->loop) {
+    if (!nccl().AllGather) return fail(LASP_ERR_COMM, "libnccl.so.2 lacks ncclAllGather");
+    ncclResult_t r = nccl().AllGather(local, c->gather, n, ncclFloat32, c->comm, st);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather(state)", c->rank, -1);
+  } else {
+    lasp_status_t s;
+    for (int j = 0; j < c->world; ++j)
+      if (j != c->rank && (s = ring_send(c, local, n, j, st, "allgather send")) != LASP_OK) return s;
+    for (int j = 0; j < c->world; ++j)
+      if (j != c->rank && (s = ring_recv(c, c->gather + size_t(j) * n, n, j, st, "allgather recv")) != LASP_OK) return s;
+    LASP_CUDA(cudaMemcpyAsync(c->gather + size_t(c->rank) * n, local, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  }
+  const int j0 = backward ? c->world - 1 : 0, step = backward ? -1 : 1;
+  const int count = backward ? c->world - 1 - c->rank : c->rank;
+  return launch_fold_ranks(p, c->gather, j0, step, count, in, st) == cudaSuccess ? LASP_OK
+                                                                                 : cuda_fail(cudaGetLastError(), "fold_ranks");
 }
 
 }  // namespace
@@ -585,8 +620,17 @@ lasp_status_t lasp_ctx_create_loopback(int rank, int world, const char* group, i
   return LASP_OK;
 }
 
+lasp_status_t lasp_ctx_set_exchange(lasp_ctx_t c, int exchange) {
+  if (!c) return fail(LASP_ERR_SHAPE, "ctx is NULL");
+  if (exchange != LASP_EXCHANGE_RING && exchange != LASP_EXCHANGE_ALLGATHER)
+    return fail(LASP_ERR_DOMAIN, "exchange must be LASP_EXCHANGE_RING or LASP_EXCHANGE_ALLGATHER");
+  c->exchange = exchange;
+  return LASP_OK;
+}
+
 lasp_status_t lasp_ctx_destroy(lasp_ctx_t c) {
   if (!c) return LASP_OK;
+  if (c->gather) cudaFree(c->gather);
   if (c->comm) nccl().CommDestroy(c->comm);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
@@ -618,6 +662,10 @@ lasp_status_t lasp_ctx_protocol(lasp_ctx_t c, const lasp_shape_t* shape, int64_t
   if (sends_fwd) *sends_fwd = t >= 0 ? 1 : 0;  // Alg. 2: send to i+1
   lasp_ring_peers(c->rank, c->world, 1, &f, &t);
   if (sends_bwd) *sends_bwd = t >= 0 ? 1 : 0;  // Alg. 3 P:649 (reading A2): to i-1
+  if (c->exchange == LASP_EXCHANGE_ALLGATHER) {  // one all-gather contribution per direction
+    if (sends_fwd) *sends_fwd = c->world > 1 ? 1 : 0;
+    if (sends_bwd) *sends_bwd = c->world > 1 ? 1 : 0;
+  }
   if (elems_per_msg) *elems_per_msg = shape->batch * shape->heads * shape->head_dim * shape->head_dim;
   return LASP_OK;
 }
@@ -637,6 +685,12 @@ lasp_status_t lasp_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   lasp_ring_peers(c->rank, c->world, 0, &from, &to);
   if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st));                     // F1
   LASP_CUDA(prefix(p, Dir::FWD, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
+  if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
+    if ((s = exchange_allgather(c, p, w.local, w.in, false, st)) != LASP_OK) return s;
+    if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, st)) != LASP_OK) return s;  // F2 + F3
+    register_cache(p, cache, c->rank, c->world);
+    return LASP_OK;
+  }
   // F2 ring hop: Recv KV_in from r-1 (Alg. 2), combine, Send to r+1
   if (from >= 0) {
     if ((s = ring_recv(c, w.in, n, from, st, "ncclRecv(KV)")) != LASP_OK) return s;
@@ -673,12 +727,14 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   LASP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
   int from = -1, to = -1;
   lasp_ring_peers(c->rank, c->world, 1, &from, &to);
-  if (from >= 0) {
+  if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
+    if ((s = exchange_allgather(c, p, w.local, w.in, true, c->comm_stream)) != LASP_OK) return s;
+  } else if (from >= 0) {
     if ((s = ring_recv(c, w.in, n, from, c->comm_stream, "ncclRecv(dKV)")) != LASP_OK) return s;
   } else {
     LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), c->comm_stream));
   }
-  if (to >= 0) {
+  if (to >= 0 && c->exchange != LASP_EXCHANGE_ALLGATHER) {
     LASP_CUDA(combine(p, w.in, w.local, w.out, c->comm_stream));
     if ((s = ring_send(c, w.out, n, to, c->comm_stream, "ncclSend(dKV)")) != LASP_OK) return s;
   }

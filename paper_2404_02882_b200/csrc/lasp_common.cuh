@@ -88,6 +88,8 @@ cudaError_t launch_seg_state_simt(const Plan& p, Dir dir, const void* x, const v
 cudaError_t launch_prefix(const Plan& p, Dir dir, const float* init, const float* seg_states,
                           float* prefix_out, float* final_out, cudaStream_t st);
 cudaError_t launch_core_simt(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st);
+cudaError_t launch_fold_ranks(const Plan& p, const float* gathered, int j0, int step, int count, float* out,
+                              cudaStream_t st);
 cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local, float* kv_out,
                            cudaStream_t st);
 

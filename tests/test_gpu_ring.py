@@ -68,7 +68,7 @@ def test_ring_cache_tag_checks_rank(ring):
 
 
 # ---- world > 1 on one GPU: the same lasp_fwd / lasp_bwd code with the in-process loopback transport ----
-def _run_loopback(p, world, n_global, dtype, group):
+def _run_loopback(p, world, n_global, dtype, group, exchange="ring"):
     """Each rank is a thread with its own CUDA stream and ring context; returns the gathered outputs."""
     import threading
     import paper_2404_02882_b200 as lasp
@@ -80,7 +80,7 @@ def _run_loopback(p, world, n_global, dtype, group):
         ring = None
         try:
             torch.cuda.set_device(0)
-            ring = lasp.Ring.loopback(r, world, group)
+            ring = lasp.Ring.loopback(r, world, group).set_exchange(exchange)
             stream = torch.cuda.Stream()
             with torch.cuda.stream(stream):
                 sl = slice(r * C, (r + 1) * C)
@@ -116,25 +116,27 @@ def _run_loopback(p, world, n_global, dtype, group):
     return [np.concatenate([out[r][i] for r in range(world)], axis=1) for i in range(4)], [o[4] for o in out]
 
 
+@pytest.mark.parametrize("exchange", ["ring", "allgather"])
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_loopback_ring_bf16_matches_oracle(oracle_mod, world):
+def test_loopback_ring_bf16_matches_oracle(oracle_mod, world, exchange):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     N = 768 * world
     p = synth.problem(40 + world, 1, N, 4, 64, dtype="bf16")
-    got, _ = _run_loopback(p, world, N, torch.bfloat16, f"bf16-w{world}")
+    got, _ = _run_loopback(p, world, N, torch.bfloat16, f"bf16-w{world}-{exchange}", exchange)
     refs = [oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])] + \
         list(oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"]))
     for x, r in zip(got, refs):
         assert oracle_mod.normwise_err(x, r) <= 2e-2
 
 
-def test_loopback_ring_config1_fp32(oracle_mod):
+@pytest.mark.parametrize("exchange", ["ring", "allgather"])
+def test_loopback_ring_config1_fp32(oracle_mod, exchange):
     """BASELINE configs[0] on the real ring code: 1 head x 32, N=512, lambda=0.99, 4 ranks, fp32."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     p = synth.problem(0, 1, 512, 1, 32, dtype="fp32", lam=0.99)
-    got, kv_in = _run_loopback(p, 4, 512, torch.float32, "config1")
+    got, kv_in = _run_loopback(p, 4, 512, torch.float32, f"config1-{exchange}", exchange)
     refs = [oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])] + \
         list(oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"]))
     for x, r in zip(got, refs):
@@ -145,3 +147,17 @@ def test_loopback_ring_config1_fp32(oracle_mod):
         ref = np.asarray(cache[r]).reshape(kv_in[r].shape)
         den = max(np.max(np.abs(ref)), 1e-30)
         assert np.max(np.abs(kv_in[r] - ref)) / den <= 1e-5 or (r == 0 and np.max(np.abs(kv_in[r])) == 0)
+
+
+def test_allgather_protocol_and_domain(ring):
+    import paper_2404_02882_b200 as lasp
+    from paper_2404_02882_b200._native import LaspError
+    q = torch.zeros((1, 256, 2, 64), dtype=torch.bfloat16, device="cuda")
+    r = lasp.Ring.loopback(0, 3, "proto").set_exchange("allgather")
+    try:
+        assert r.protocol(q) == (1, 1, 2 * 64 * 64)
+        with pytest.raises(LaspError) as e:
+            lasp._native.check(lasp._native.lib().lasp_ctx_set_exchange(r._ctx, 7))
+        assert e.value.name == "LASP_ERR_DOMAIN"
+    finally:
+        r.close()

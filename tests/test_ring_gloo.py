@@ -116,3 +116,57 @@ def test_ring_peers_edges():
     assert [ring_peers(r, 3, True) for r in range(3)] == [(1, -1), (2, 0), (-1, 1)]
     with pytest.raises(LaspError):
         ring_peers(3, 3, False)
+
+
+def _allgather_worker(rank, world, port, N, H, D, out_dir):
+    """SURVEY §8(f) NEXT-2 rule on real processes: all-gather the local states, fold the received ones."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        C = N // world
+        p = synth.problem(12, 1, N, H, D, dtype="fp32", token_lo=rank * C, token_hi=(rank + 1) * C)
+        lam = p["lam"]
+        parts = [oracle.build_decay(C, lam[h]) for h in range(H)]
+        L = np.stack([oracle.kv_update(None, p["k"][0, :, h], p["v"][0, :, h], parts[h][2], parts[h][3])
+                      for h in range(H)])
+        G = np.stack([oracle.dkv_update(None, p["q"][0, :, h], p["do"][0, :, h], parts[h][1], parts[h][3])
+                      for h in range(H)])
+        gl = [torch.zeros(H * D * D, dtype=torch.float64) for _ in range(world)]
+        gg = [torch.zeros(H * D * D, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(gl, torch.from_numpy(np.ascontiguousarray(L).reshape(-1)))
+        dist.all_gather(gg, torch.from_numpy(np.ascontiguousarray(G).reshape(-1)))
+        lc = np.array([parts[h][3] for h in range(H)])[:, None, None]  # lam^C per head
+        kv_in = np.zeros((H, D, D))
+        for j in range(rank):                      # KV_in(r) = sum_{j<r} lam^(C(r-1-j)) L_j
+            kv_in = lc * kv_in + gl[j].numpy().reshape(H, D, D)
+        dkv_in = np.zeros((H, D, D))
+        for j in range(world - 1, rank, -1):       # dKV_in(r) = sum_{j>r} lam^(C(j-r-1)) G_j
+            dkv_in = lc * dkv_in + gg[j].numpy().reshape(H, D, D)
+        np.savez(os.path.join(out_dir, f"ag{rank}.npz"), kv_in=kv_in, dkv_in=dkv_in)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,N", [(2, 64), (4, 128)])
+def test_allgather_exchange_over_gloo(tmp_path, oracle_mod, world, N):
+    """The folded all-gather states equal the ring's messages: the oracle's Alg. 2 cache (state entering
+    each rank) and, for the backward, the definition of dKV_in(r) evaluated directly."""
+    H, D = 2, 4
+    mp.start_processes(_allgather_worker, args=(world, _free_port(), N, H, D, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    res = [np.load(tmp_path / f"ag{r}.npz") for r in range(world)]
+    p = synth.problem(12, 1, N, H, D, dtype="fp32")
+    _, cache, _, _ = oracle_mod.lasp_fwd_sim(p["q"], p["k"], p["v"], p["lam"], world)
+    C = N // world
+    for r in range(world):
+        assert np.max(np.abs(res[r]["kv_in"] - cache[r][0])) <= 1e-12 * max(1.0, np.max(np.abs(cache[r][0])))
+        # dKV_in(r) = sum_{g >= (r+1)C} lam^(g-(r+1)C+1) q_g do_g^T  (SURVEY Appendix A, reading A3)
+        ref = np.zeros((H, D, D))
+        for h in range(H):
+            lam = float(np.float32(p["lam"][h]))
+            for g in range((r + 1) * C, N):
+                ref[h] += lam ** (g - (r + 1) * C + 1) * np.outer(p["q"][0, g, h].astype(np.float64),
+                                                                 p["do"][0, g, h].astype(np.float64))
+        assert np.max(np.abs(res[r]["dkv_in"] - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
