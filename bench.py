@@ -193,15 +193,21 @@ def run_lasp(args):
     B = 1
     lib = N.lib()
 
-    # inputs: this rank's shard [r*C, (r+1)*C) of the global sequence
-    p = synth.problem(0, B, C * world, H, D, dtype="bf16", token_lo=rank * C, token_hi=(rank + 1) * C)
+    # data-sequence hybrid (Alg. 1, NEXT-1): G = world/T groups of T ranks, each on its own sequence
+    T = args.sp_size or world
+    grp_id, grank, _ = lasp.topology(rank, world, T)
+    G = world // T
+    # inputs: this rank's shard [t*C, (t+1)*C) of its group's sequence (seed = group id)
+    p = synth.problem(grp_id, B, C * T, H, D, dtype="bf16", token_lo=grank * C, token_hi=(grank + 1) * C)
     lam = p["lam"]
     host = {k: torch.from_numpy(p[k]) for k in ("q", "k", "v", "do")}
     d_in = {k: v.to(dev, torch.bfloat16) for k, v in host.items()}
     q, k, v, do = d_in["q"], d_in["k"], d_in["v"], d_in["do"]
     o, dq, dk, dv = (torch.empty_like(q) for _ in range(4))
     cache, ws = lasp.alloc_cache(q), lasp.alloc_workspace(q)
-    ring = lasp.Ring(dev).set_exchange(args.exchange) if world > 1 else None
+    ring = None
+    if T > 1:
+        ring = lasp.Ring(dev, group=lasp.sp_group(T) if T < world else None).set_exchange(args.exchange)
 
     def step():
         if ring is None:
@@ -343,12 +349,12 @@ def run_lasp(args):
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (synth/, seed 0; bf16 inputs)",
-            "config": {"workload": desc, "global_batch": B, "seq_len": C * world, "n_local": C, "heads": H,
+            "config": {"workload": desc, "global_batch": B * G, "seq_len": C * T, "n_local": C, "heads": H,
                        "head_dim": D, "lambda": "per-head 1-2^-(1+14h/(H-1))",
                        "segment_len": lasp.segment_len(N.shape(B, C, H, D, N.LASP_BF16)),
                        "l2": "flushed between timed steps (256 MiB read outside the step events); inputs 4x"
-                             f" {B * C * H * D * 2 >> 20} MiB", "parallelism": f"sp{world}",
-                       "exchange": args.exchange if world > 1 else "none"},
+                             f" {B * C * H * D * 2 >> 20} MiB", "parallelism": f"dp{G}xsp{T}" if G > 1 else f"sp{T}",
+                       "exchange": args.exchange if T > 1 else "none"},
             "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e, "roofline": roofline,
             "path": path, "cpu_baseline": cpu}
     if rank == 0:
@@ -367,6 +373,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["lasp", "reference"], default="lasp")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="tnl04b")
+    ap.add_argument("--sp-size", type=int, default=0,
+                    help="sequence-parallel size T (default: all ranks in one ring); G = N/T data-parallel groups "
+                         "(Alg. 1 data-sequence hybrid, NEXT-1)")
     ap.add_argument("--exchange", choices=["ring", "allgather"], default="ring",
                     help="state exchange at N > 1: the paper's ring (default) or one all-gather (NEXT-2)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -170,6 +170,15 @@ lasp_status_t lasp_ctx_set_exchange(lasp_ctx_t ctx, int exchange);
  * (Alg. 3, reading A2 of P:649). Used by lasp_fwd/lasp_bwd; exposed for protocol tests. */
 lasp_status_t lasp_ring_peers(int rank, int world, int backward, int* recv_from, int* send_to);
 
+/* Data-sequence hybrid topology (host-only, no GPU): Alg. 1
+ * with W = world ranks and sequence-parallel size T = sp_size: G = W/T groups; global rank R belongs to
+ * group floor(R/T), holds chunk R mod T of that group's sequence (tokens [(R mod T) C, (R mod T + 1) C)),
+ * and the group's source rank is floor(R/T)*T (R_src, Alg. 1 line 5). Each group runs its own ring: create
+ * one ctx per group with lasp_ctx_create(group_rank, T, <the group's id>, ...); no message crosses a group.
+ * Any output pointer may be NULL. LASP_ERR_PARTITION if sp_size < 1, world % sp_size != 0 (reading A6: T
+ * divides W) or rank outside [0, world). */
+lasp_status_t lasp_topology(int rank, int world, int sp_size, int* group, int* group_rank, int* src_rank);
+
 /* Messages and fp32 elements per message this ctx will send per direction per call (protocol
  * introspection for tests: ring exchange: world-1 hops in total, this rank sends 0 or 1; all-gather
  * exchange: one contribution per rank when world > 1). */

@@ -58,6 +58,8 @@ _SIGS = {
     "lasp_ctx_protocol": ([_vp, _sp, _i64p, _i64p, _i64p], ctypes.c_int),
     "lasp_ring_peers": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                          ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "lasp_topology": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "lasp_fwd": ([_vp, _sp, _vp, _vp, _vp, _fp, _vp, _vp, _vp, _vp], ctypes.c_int),
     "lasp_bwd": ([_vp, _sp, _vp, _vp, _vp, _fp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
 }

@@ -6,6 +6,8 @@ PyTorch is used for device memory, streams and process groups. Tensors use the b
 * ``fwd_local`` / ``bwd_local`` -- one rank's Alg. 2 / Alg. 3 compute without transport.
 * ``Ring``                        -- Alg. 2 / Alg. 3 across a torch.distributed world (NCCL P2P).
 * ``LaspAttention``               -- torch.autograd.Function over ``Ring`` or the local path.
+* ``topology`` / ``sp_group`` / ``scatter_sequence`` -- data-sequence hybrid parallelism (Alg. 1): G = W/T
+  sequence-parallel groups, one ring per group.
 """
 from __future__ import annotations
 
@@ -111,6 +113,48 @@ def ring_peers(rank: int, world: int, backward: bool) -> tuple[int, int]:
     a, b = ctypes.c_int(), ctypes.c_int()
     N.check(N.lib().lasp_ring_peers(rank, world, int(backward), ctypes.byref(a), ctypes.byref(b)))
     return a.value, b.value
+
+
+def topology(rank: int, world: int, sp_size: int) -> tuple[int, int, int]:
+    """(group, group_rank, src_rank) of global ``rank`` with sequence-parallel size T = ``sp_size``
+    (Alg. 1: G = W/T groups of T consecutive ranks, R_src = floor(R/T)*T); host-only."""
+    g, r, s = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    N.check(N.lib().lasp_topology(rank, world, sp_size, ctypes.byref(g), ctypes.byref(r), ctypes.byref(s)))
+    return g.value, r.value, s.value
+
+
+def sp_group(sp_size: int):
+    """This rank's sequence-parallel process group (a torch.distributed subgroup of T consecutive ranks).
+    Every rank of the default group must call it (torch creates all G subgroups collectively)."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(), dist.get_rank()
+    mine = topology(rank, world, sp_size)[0]
+    groups = [dist.new_group(list(range(g * sp_size, (g + 1) * sp_size))) for g in range(world // sp_size)]
+    return groups[mine]
+
+
+def scatter_sequence(x, group, sp_size: int):
+    """Alg. 1 lines 6-8: the group's source rank holds the whole [batch][N][heads][D] sequence ``x``
+    (other ranks pass None), splits it into T chunks of C = N/T tokens and scatters chunk t to the rank
+    with group_rank t. Returns this rank's chunk. LASP_ERR_PARTITION-style ValueError if T does not
+    divide N."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    src = dist.get_global_rank(group, 0)
+    meta = [None]
+    if rank == 0:
+        if x.shape[1] % sp_size != 0:
+            raise ValueError(f"sequence length {x.shape[1]} is not divisible by sp_size {sp_size} (C = N/T)")
+        meta = [(tuple(x.shape), x.dtype)]
+    dist.broadcast_object_list(meta, src=src, group=group)
+    shape, dtype = meta[0]
+    C = shape[1] // sp_size
+    dev = x.device if x is not None else (torch.device("cuda", torch.cuda.current_device())
+                                          if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+    out = torch.empty((shape[0], C) + tuple(shape[2:]), dtype=dtype, device=dev)
+    chunks = [c.contiguous() for c in x.split(C, dim=1)] if rank == 0 else None
+    dist.scatter(out, chunks, src=src, group=group)
+    return out
 
 
 class Ring:

@@ -652,6 +652,19 @@ lasp_status_t lasp_ring_peers(int rank, int world, int backward, int* recv_from,
   return LASP_OK;
 }
 
+lasp_status_t lasp_topology(int rank, int world, int sp_size, int* group, int* group_rank, int* src_rank) {
+  if (sp_size < 1 || world < 1 || world % sp_size != 0) {
+    char b[128];
+    std::snprintf(b, sizeof b, "sequence parallel size %d does not divide world size %d", sp_size, world);
+    return fail(LASP_ERR_PARTITION, b);
+  }
+  if (rank < 0 || rank >= world) return fail(LASP_ERR_PARTITION, "rank outside [0, world)");
+  if (group) *group = rank / sp_size;                 // Alg. 1: groups of T consecutive ranks
+  if (group_rank) *group_rank = rank % sp_size;       // chunk index inside the group
+  if (src_rank) *src_rank = (rank / sp_size) * sp_size;  // R_src = floor(R/T) * T (Alg. 1 line 5)
+  return LASP_OK;
+}
+
 lasp_status_t lasp_ctx_protocol(lasp_ctx_t c, const lasp_shape_t* shape, int64_t* sends_fwd, int64_t* sends_bwd,
                                 int64_t* elems_per_msg) {
   if (!c) return fail(LASP_ERR_SHAPE, "ctx is NULL");
