@@ -92,45 +92,48 @@ __global__ void __launch_bounds__(kThreads) seg_state_simt_kernel(Plan p, const 
 // ---------------------------------------------------------------------------------------------
 // prefix: per element, cur = init; for p: prefix[p] = cur; cur = lam^len_p cur + seg[p]; final = cur
 // (Alg. 2 P:171 / Alg. 3 P:648 applied between segments). `prefix` may alias `seg_states`.
-__global__ void __launch_bounds__(256) prefix_kernel(Plan p, Dir dir, const float* __restrict__ init,
-                                                     const float* seg_states, float* prefix,
-                                                     float* __restrict__ final_out) {
+__global__ void __launch_bounds__(64) prefix_kernel(Plan p, Dir dir, const float* __restrict__ init,
+                                                    const float* seg_states, float* prefix,
+                                                    float* __restrict__ final_out) {
   pdl_wait();
   pdl_trigger();
-  // One thread per state element; all (up to U) segment loads of a batch are issued before the serial
-  // fold, so the kernel costs about one L2 round trip per batch (nseg <= U: one batch). A warp reads
-  // 128 contiguous bytes of each segment state (coalesced).
+  // One thread per 4 consecutive state elements (float4); all (up to U) segment loads of a batch are
+  // issued before the serial fold (nseg <= U: one L2 round trip). `prefix` may alias `seg_states`: a
+  // thread loads every segment of a batch before it stores any of them.
   const int64_t DD = p.D * p.D;
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over B*H*D*D
-  if (idx >= p.B * p.H * DD) return;
-  const int64_t bh = idx / DD, e = idx % DD, h = bh % p.H;
+  const int64_t idx4 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over B*H*D*D/4
+  if (idx4 * 4 >= p.B * p.H * DD) return;
+  const int64_t bh = (idx4 * 4) / DD, e = (idx4 * 4) % DD, h = bh % p.H;
   // every segment has seg_len tokens except possibly the last one (both directions)
   const int64_t last_len = p.C - (p.nseg - 1) * p.seg_len;
   // lam^len = exp2(len * log2(lam)) with log2(lam) from the host in fp64 (relative error ~1e-6 at len ~ 1e3)
   const float l2 = p.l2lam[h];
   const float dec_full = exp2f(float(p.seg_len) * l2);
   const float dec_last = exp2f(float(last_len > 0 ? last_len : 0) * l2);
-  float cur = init ? init[idx] : 0.f;
+  float4 cur = init ? *reinterpret_cast<const float4*>(init + idx4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
   const float* src = seg_states ? seg_states + bh * p.nseg * DD + e : nullptr;
   float* dst = prefix ? prefix + bh * p.nseg * DD + e : nullptr;
-  constexpr int U = 48;
+  constexpr int U = 40;
   for (int64_t s0 = 0; s0 < p.nseg; s0 += U) {
-    float v[U];
+    float4 v[U];
 #pragma unroll
     for (int t = 0; t < U; ++t) {
       const int64_t sg = dir == Dir::FWD ? s0 + t : p.nseg - 1 - (s0 + t);  // REV folds from the rank end
-      v[t] = (src && s0 + t < p.nseg) ? __ldcg(src + sg * DD) : 0.f;
+      v[t] = (src && s0 + t < p.nseg) ? __ldcg(reinterpret_cast<const float4*>(src + sg * DD))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int t = 0; t < U; ++t) {
       const int64_t sg = dir == Dir::FWD ? s0 + t : p.nseg - 1 - (s0 + t);
       if (s0 + t < p.nseg) {
-        if (dst) dst[sg * DD] = cur;
-        cur = fmaf((sg == p.nseg - 1) ? dec_last : dec_full, cur, v[t]);
+        if (dst) *reinterpret_cast<float4*>(dst + sg * DD) = cur;
+        const float dcy = (sg == p.nseg - 1) ? dec_last : dec_full;
+        cur.x = fmaf(dcy, cur.x, v[t].x); cur.y = fmaf(dcy, cur.y, v[t].y);
+        cur.z = fmaf(dcy, cur.z, v[t].z); cur.w = fmaf(dcy, cur.w, v[t].w);
       }
     }
   }
-  if (final_out) final_out[idx] = cur;
+  if (final_out) *reinterpret_cast<float4*>(final_out + idx4 * 4) = cur;
 }
 
 // kv_out = lam^C kv_in + local (the ring's combine step, Alg. 2 P:171 with the local part hoisted)
@@ -293,8 +296,8 @@ cudaError_t launch_core_simt(const Plan& p, Dir dir, const SeqArgs& a, cudaStrea
 
 cudaError_t launch_prefix(const Plan& p, Dir dir, const float* init, const float* seg_states, float* prefix_out,
                           float* final_out, cudaStream_t st) {
-  const int64_t n = p.B * p.H * p.D * p.D;
-  const int threads = 256;
+  const int64_t n = p.B * p.H * p.D * p.D / 4;  // D*D is a multiple of 4
+  const int threads = 64;
   return launch_k(prefix_kernel, dim3((unsigned)((n + threads - 1) / threads)), dim3(threads), 0, st, p, dir, init,
                   seg_states, prefix_out, final_out);
 }

@@ -4,13 +4,20 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, synth
 import paper_2404_02882_b200 as L
 from paper_2404_02882_b200 import _native as N
-p = synth.problem(0, 1, 32768, 16, 64, dtype="bf16", with_do=False)
-q, k, v = (torch.from_numpy(p[x]).cuda().to(torch.bfloat16) for x in ("q", "k", "v"))
-L.fwd_local(q, k, v, p["lam"]); torch.cuda.synchronize()
-buf = torch.zeros(2 * 16 * 64, dtype=torch.int64, device="cuda")
+# usage: python tools/trace.py [n_blocks] [fwd|bwd]   (bwd: the fused dQ/dV/dK launch)
+mode = sys.argv[2] if len(sys.argv) > 2 else "fwd"
+p = synth.problem(0, 1, 32768, 16, 64, dtype="bf16")
+q, k, v, do = (torch.from_numpy(p[x]).cuda().to(torch.bfloat16) for x in ("q", "k", "v", "do"))
+o, _, cache = L.fwd_local(q, k, v, p["lam"]); torch.cuda.synchronize()
+buf = torch.zeros(3 * 1024 + 2 * 148, dtype=torch.int64, device="cuda")
 N.lib().lasp_debug_trace(ctypes.c_void_p(buf.data_ptr()))
-L.fwd_local(q, k, v, p["lam"]); torch.cuda.synchronize()
+if mode == "bwd":
+    L.bwd_local(q, k, v, p["lam"], do, cache)
+else:
+    L.fwd_local(q, k, v, p["lam"])
+torch.cuda.synchronize()
 N.lib().lasp_debug_trace(None)
+buf = buf[:2 * 16 * 64]
 tt = buf.cpu().numpy().reshape(2, 16, 64).astype(np.int64)
 t = tt[0]
 base = t[t > 0].min()
