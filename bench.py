@@ -10,6 +10,7 @@ bf16, per-head lambda_h = 1 - 2^-(1 + 14h/15). N>1 keeps 32K tokens per GPU (wea
 NCCL KV/dKV ring (one process per GPU, launched by torchrun). Synthetic inputs from synth/ (seeded).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lasp|reference] [--config tnl04b|tnl1b|tnl7b]
+       [--exchange ring|allgather] [--sp-size T] [--no-graph] [--no-e2e] [--no-cpu-baseline]
 """
 from __future__ import annotations
 
@@ -234,6 +235,17 @@ def run_lasp(args):
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream(dev)
+    # --graph: the step's launches captured once into a CUDA graph (programmatic-dependent-launch edges are
+    # kept), replayed in the timed region: same kernels, no per-launch host work
+    graph, graph_launches = None, 0
+    if args.graph and ring is None:  # (the NCCL ring path launches eagerly)
+        graph = torch.cuda.CUDAGraph()
+        l0 = lib.lasp_launch_count()
+        with torch.cuda.graph(graph):
+            step()
+        graph_launches = lib.lasp_launch_count() - l0
+        graph.replay()
+        torch.cuda.synchronize()
 
     def timed_loop(n, profile):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
@@ -243,7 +255,10 @@ def run_lasp(args):
         for i in range(n):
             l2_flush()                       # outside the step events
             ev[i][0].record(stream)
-            step()
+            if graph is not None and not profile:
+                graph.replay()
+            else:
+                step()
             ev[i][1].record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -255,7 +270,7 @@ def run_lasp(args):
     launches0 = lib.lasp_launch_count()
     with ClockSampler(local) as clk:
         total_ms = timed_loop(args.steps, False)
-    launches = lib.lasp_launch_count() - launches0
+    launches = lib.lasp_launch_count() - launches0 + graph_launches * args.steps
     # (2) the same K steps again with CUDA events recorded by the library around every kernel launch
     # (on the launching stream): per-kernel durations for the roofline of the dominant kernel
     prof_ms = timed_loop(args.steps, True)
@@ -388,6 +403,7 @@ def run_lasp(args):
                        "segment_len": lasp.segment_len(N.shape(B, C, H, D, N.LASP_BF16)),
                        "l2": "flushed between timed steps (256 MiB read outside the step events); inputs 4x"
                              f" {B * C * H * D * 2 >> 20} MiB", "parallelism": f"dp{G}xsp{T}" if G > 1 else f"sp{T}",
+                       "launch": "cuda-graph replay" if graph is not None else "eager (PDL)",
                        "exchange": args.exchange if T > 1 else "none"},
             "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e, "roofline": roofline,
             "path": path, "cpu_baseline": cpu}
@@ -407,6 +423,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["lasp", "reference"], default="lasp")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="tnl04b")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch every step eagerly instead of replaying it from a CUDA graph captured once "
+                         "(same kernels and order; the graph keeps the programmatic-dependent-launch edges)")
     ap.add_argument("--sp-size", type=int, default=0,
                     help="sequence-parallel size T (default: all ranks in one ring); G = N/T data-parallel groups "
                          "(Alg. 1 data-sequence hybrid, NEXT-1)")

@@ -162,10 +162,13 @@ struct SegLayout {
   static constexpr int NBOX = D / 64;
   static constexpr uint32_t TILE = NBOX * BOX;
 #ifndef LASP_SEG_STAGES64
-#define LASP_SEG_STAGES64 3
+#define LASP_SEG_STAGES64 2  // 2 x 2 beat 3 x 2, 4 x 1 and 6 x 1 (stages x CTAs/SM) by ~1 % (round 1 sweep)
 #define LASP_SEG_CTAS64 2
 #endif
-  static constexpr int STAGES = D == 64 ? LASP_SEG_STAGES64 : 2;
+#ifndef LASP_SEG_STAGES128
+#define LASP_SEG_STAGES128 2
+#endif
+  static constexpr int STAGES = D == 64 ? LASP_SEG_STAGES64 : LASP_SEG_STAGES128;
   static constexpr int CTAS_PER_SM = D == 64 ? LASP_SEG_CTAS64 : 1;  // 2 x (96 KB smem, 128 TMEM columns) per SM
   static constexpr uint32_t X(int s) { return uint32_t(s) * 2 * TILE; }
   static constexpr uint32_t Y(int s) { return uint32_t(s) * 2 * TILE + TILE; }

@@ -223,3 +223,66 @@ def test_constant_input_closed_form_long_sequence(L, D):
                          (dv, qk * np.outer(geo(N - s[idx] + 1), dov[h]))):
             g = got[0, idx, h].float().cpu().numpy()
             assert np.max(np.abs(g - ref)) <= BF16_TOL * np.max(np.abs(ref)) + 1e-6
+
+
+def test_cuda_graph_replay_matches_eager(L):
+    """bench.py replays the step from a CUDA graph: the captured fwd_local + bwd_local launches (with their
+    programmatic-dependent-launch edges) must reproduce the eager results bit for bit."""
+    p = synth.problem(10, 1, 4096, 4, 64, dtype="bf16")
+    q, k, v, do = (to_dev(p[x], torch.bfloat16) for x in ("q", "k", "v", "do"))
+    o, dq, dk, dv = (torch.empty_like(q) for _ in range(4))
+    cache, ws = L.alloc_cache(q), L.alloc_workspace(q)
+
+    def step():
+        L.fwd_local(q, k, v, p["lam"], o=o, kv_out=False, cache=cache, workspace=ws)
+        L.bwd_local(q, k, v, p["lam"], do, cache, dq=dq, dk=dk, dv=dv, dkv_out=False, workspace=ws)
+
+    step()
+    torch.cuda.synchronize()
+    eager = [t.clone() for t in (o, dq, dk, dv)]
+    for t in (o, dq, dk, dv):
+        t.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager, (o, dq, dk, dv)):
+        assert torch.equal(a, b)
+
+
+# ---- config 4 (TNL-7B, 32 heads x 128, per-head decay, 128K tokens per rank) ---------------------------
+def test_config4_heads_parity(L, oracle_mod):
+    """32 heads x 128 with per-head lambda (config 4's head layout and segment plan family), 32K tokens:
+    every element of every head against the oracle."""
+    p = synth.problem(4, 1, 32768, 32, 128, dtype="bf16")
+    res = run_sim_ring(L, p, 1, torch.bfloat16, 32768)
+    errs = check_against_oracle(oracle_mod, p, res, BF16_TOL)
+    print("config4 heads errors", errs)
+
+
+def test_config4_rank_shape_closed_form(L):
+    """Config 4's per-rank shard at full size (32 heads x 128, n_local = 131072, per-head lambda from the
+    TNL recipe, the plan bench.py --config tnl7b times): constant inputs per head have closed forms
+    (derived from Eq. 4), checked at sampled positions of every head."""
+    N, H, D = 131072, 32, 128
+    lam = synth.head_lambdas(H, None)
+    rng = np.random.default_rng(4)
+    qv, kv_, vv, dov = (synth.round_bf16(rng.standard_normal((H, D)).astype(np.float32) * 0.3) for _ in range(4))
+    mk = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(torch.bfloat16).cuda() \
+        .view(1, 1, H, D).expand(1, N, H, D).contiguous()
+    o, _, cache = L.fwd_local(mk(qv), mk(kv_), mk(vv), lam)
+    dq, dk, dv, _ = L.bwd_local(mk(qv), mk(kv_), mk(vv), lam, mk(dov), cache)
+    torch.cuda.synchronize()
+    idx = np.array([0, 1, 127, 128, 4095, 65535, 100000, N - 1])
+    s = idx.astype(np.float64) + 1
+    got = {n: t[0, idx].float().cpu().numpy() for n, t in (("o", o), ("dq", dq), ("dk", dk), ("dv", dv))}
+    for h in range(H):
+        l = float(lam[h])
+        geo = (lambda n: n) if l == 1.0 else (lambda n: (1 - l ** n) / (1 - l))
+        qk = float(qv[h].astype(np.float64) @ kv_[h]); vd = float(vv[h].astype(np.float64) @ dov[h])
+        for name, ref in (("o", qk * np.outer(geo(s), vv[h])), ("dq", vd * np.outer(geo(s), kv_[h])),
+                          ("dk", vd * np.outer(geo(N - s + 1), qv[h])), ("dv", qk * np.outer(geo(N - s + 1), dov[h]))):
+            g = got[name][:, h]
+            assert np.max(np.abs(g - ref)) <= BF16_TOL * np.max(np.abs(ref)) + 1e-6, (name, h)
