@@ -136,9 +136,9 @@ __device__ __noinline__ Item get_item(const Plan& p, Dir dir, int64_t w) {  // o
   // (DRAM page locality, L2 sector promotion shared by neighbouring heads).
   Item it;  // 32-bit decode (the host guarantees B*H*nseg < 2^31): keeps the hot loops small
   const uint32_t wu = uint32_t(w), nbh = uint32_t(p.B * p.H), nh = uint32_t(p.H);
-  const uint32_t bh = wu % nbh;
-  it.seg = wu / nbh;
-  it.b = bh / nh;
+  it.seg = p.div_bh.div(wu);
+  const uint32_t bh = wu - uint32_t(it.seg) * nbh;
+  it.b = p.div_h.div(bh);
   it.h = bh - uint32_t(it.b) * nh;
   it.beg = seg_begin(dir, it.seg, p.seg_len, p.C);
   it.end = seg_end(dir, it.seg, p.seg_len, p.C);
@@ -166,7 +166,7 @@ struct SegLayout {
 #define LASP_SEG_CTAS64 2
 #endif
 #ifndef LASP_SEG_STAGES128
-#define LASP_SEG_STAGES128 2
+#define LASP_SEG_STAGES128 3  // 3 x 64 KB stages, 1 CTA/SM: seg F 61.4 -> 58.0 us at TNL-1B
 #endif
   static constexpr int STAGES = D == 64 ? LASP_SEG_STAGES64 : LASP_SEG_STAGES128;
   static constexpr int CTAS_PER_SM = D == 64 ? LASP_SEG_CTAS64 : 1;  // 2 x (96 KB smem, 128 TMEM columns) per SM
@@ -390,6 +390,7 @@ struct CoreParams {
   __nv_bfloat16* outp[3];
   unsigned long long* trace;  // debug timeline (lasp_debug_trace), nullptr in production
   int npass;
+  FastDiv div_per, div_nbh;   // / (B*H*NV*npass), / (B*H*NV) (work-item decode)
 };
 
 struct CItem {
@@ -399,18 +400,19 @@ struct CItem {
 };
 
 // item w -> (segment, pass, batch*head, value slice): segment-major, value slice innermost
-__device__ __noinline__ CItem get_citem(const CoreParams& prm, int64_t w, int nv) {
+template <int NV>
+__device__ __noinline__ CItem get_citem(const CoreParams& prm, int64_t w) {
   const Plan& p = prm.p;
   CItem it;
-  const uint32_t nbh = uint32_t(p.B * p.H) * uint32_t(nv), per = nbh * uint32_t(prm.npass), nh = uint32_t(p.H);
+  const uint32_t nbh = uint32_t(p.B * p.H) * uint32_t(NV), per = nbh * uint32_t(prm.npass), nh = uint32_t(p.H);
   const uint32_t wu = uint32_t(w);
-  it.seg = wu / per;
+  it.seg = prm.div_per.div(wu);
   const uint32_t rem = wu - uint32_t(it.seg) * per;
-  it.pass = int(rem / nbh);
+  it.pass = int(prm.div_nbh.div(rem));
   const uint32_t bhv = rem - uint32_t(it.pass) * nbh;
-  const uint32_t bh = bhv / uint32_t(nv);
-  it.v = int(bhv - bh * uint32_t(nv));
-  it.b = bh / nh;
+  const uint32_t bh = bhv / uint32_t(NV);
+  it.v = int(bhv - bh * uint32_t(NV));
+  it.b = p.div_h.div(bh);
   it.h = bh - uint32_t(it.b) * nh;
   it.dir = Dir(prm.pass[it.pass].dir);
   it.beg = seg_begin(it.dir, it.seg, p.seg_len, p.C);
@@ -477,7 +479,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       bool waited = false;
       uint32_t J = 0, k = 0;
       for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
-        const CItem it = get_citem(prm, w, L::NV);
+        const CItem it = get_citem<L::NV>(prm, w);
         const CorePass& ps = prm.pass[it.pass];
         // the segment's prefix state -> STG (single buffer, released by the state warps)
         auto load_stg = [&]() {
@@ -536,7 +538,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       auto koff = [](int kk) -> uint32_t { return uint32_t(kk >> 2) * BOX + uint32_t(kk & 3) * 32; };
       uint32_t J = 0, kd = 0;
       for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
-        const int nblk = get_citem(prm, w, L::NV).nblk;
+        const int nblk = get_citem<L::NV>(prm, w).nblk;
         for (int j = 0; j < nblk; ++j, ++J) {
           const int s = int(J % ST);
           if (warp == 2) {
@@ -602,7 +604,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     const uint32_t q4 = warp & 3;  // rows [32 q4, 32 q4 + 32) of the block
     uint32_t J = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
-      const CItem it = get_citem(prm, w, L::NV);
+      const CItem it = get_citem<L::NV>(prm, w);
       const bool fwd = it.dir == Dir::FWD;
       const float l2 = p.l2lam[it.h];
       // Per-thread decay factors of its row, kept in registers for the whole item. With e(u) = lane - u
@@ -725,7 +727,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     };
     uint32_t J = 0, kd = 0, k = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
-      const CItem it = get_citem(prm, w, L::NV);
+      const CItem it = get_citem<L::NV>(prm, w);
       const CorePass& ps = prm.pass[it.pass];
       load_state(k, it, ps.trans != 0, ps.state);
       const float l2 = p.l2lam[it.h];
@@ -806,7 +808,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     const bool leader = threadIdx.x == 384;
     uint32_t J = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
-      const CItem it = get_citem(prm, w, L::NV);
+      const CItem it = get_citem<L::NV>(prm, w);
       const CUtensorMap* mo = &prm.mout[prm.pass[it.pass].out];
       __nv_bfloat16* outp = prm.outp[prm.pass[it.pass].out];
       const float r = exp2f(float(it.dir == Dir::FWD ? (i + 1) : (BT - 1 - i)) * p.l2lam[it.h]);
@@ -948,6 +950,8 @@ cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const 
   prm.p = p;
   prm.npass = npass;
   prm.trace = g_trace;
+  prm.div_nbh = FastDiv(uint32_t(p.B * p.H * CoreLayout<D>::NV));
+  prm.div_per = FastDiv(uint32_t(p.B * p.H * CoreLayout<D>::NV * npass));
   auto kern = core_tc_kernel<D>;
   const int smem = int(CoreLayout<D>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;

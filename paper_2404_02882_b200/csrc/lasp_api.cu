@@ -90,6 +90,8 @@ Plan make_plan(const lasp_shape_t* s) {
   p.dtype = s->dtype == LASP_BF16 ? 0 : 1;
   p.seg_len = choose_seg_len(p.B, p.C, p.H);
   p.nseg = p.C > 0 ? (p.C + p.seg_len - 1) / p.seg_len : 1;
+  p.div_bh = FastDiv(uint32_t(p.B * p.H));
+  p.div_h = FastDiv(uint32_t(p.H));
   return p;
 }
 

@@ -52,11 +52,35 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 
 enum class Dir : int { FWD = 0, REV = 1 };
 
+// x / d for 0 <= x < 2^31 as one multiply-high and a shift (work-item decode in the persistent kernels:
+// a runtime 32-bit division is a ~20-instruction dependent chain per call). Round-up multiplier
+// m = ceil(2^p / d), p = 31 + ceil(log2 d) (the construction CUTLASS's FastDivmod uses).
+struct FastDiv {
+  uint32_t d = 1, m = 0, sh = 0;
+  FastDiv() = default;
+  explicit FastDiv(uint32_t div) : d(div) {
+    if (d <= 1) return;
+    uint32_t l = 0;
+    while ((1u << l) < d) ++l;
+    const uint32_t p = 31 + l;
+    m = uint32_t(((uint64_t(1) << p) + d - 1) / d);
+    sh = p - 32;
+  }
+  __host__ __device__ __forceinline__ uint32_t div(uint32_t x) const {
+#ifdef __CUDA_ARCH__
+    return d == 1 ? x : (__umulhi(x, m) >> sh);
+#else
+    return d == 1 ? x : uint32_t((uint64_t(x) * m) >> (32 + sh));
+#endif
+  }
+};
+
 struct Plan {
   int64_t B, C, H, D;  // batch, n_local, heads, head_dim
   int dtype;           // 0 = bf16, 1 = fp32
   int64_t seg_len;     // multiple of kSegQuantum
   int64_t nseg;        // >= 1
+  FastDiv div_bh, div_h;  // / (B*H), / H (work-item decode)
   float lam[256];      // per-head decay (fp32, the boundary's precision; reading A8), by value
   float l2lam[256];    // log2(lam) computed in fp64 on the host, rounded once (tcgen05 path: exp2 powers)
 };
