@@ -233,8 +233,10 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();  // the previous kernel of the stream has completed and its writes are visible
-  pdl_trigger();  // only after the wait (see core_tc_kernel)
+  // Programmatic dependent launch: the producer, MMA and scaler roles only read this call's inputs, which
+  // were complete before the preceding kernel started (every kernel of the library triggers its dependents
+  // only after its own griddepcontrol.wait), so they start at once; the drain warps write the workspace,
+  // which the preceding kernel may still read: they wait (and then trigger) before their first store.
 
   if (warp == 0) {
     if (elect_one()) {
@@ -310,6 +312,8 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
     const uint32_t q4 = warp & 3;
     const bool valid = D == 128 || lane < 16;
     const int row = D == 128 ? int(q4 * 32 + lane) : int(q4 * 16 + lane);
+    pdl_wait();
+    pdl_trigger();
     uint32_t k = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
       const Item it = get_item(p, DIR, w);
