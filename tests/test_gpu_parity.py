@@ -286,3 +286,26 @@ def test_config4_rank_shape_closed_form(L):
                           ("dk", vd * np.outer(geo(N - s + 1), qv[h])), ("dv", qk * np.outer(geo(N - s + 1), dov[h]))):
             g = got[name][:, h]
             assert np.max(np.abs(g - ref)) <= BF16_TOL * np.max(np.abs(ref)) + 1e-6, (name, h)
+
+
+def test_layer_trains_through_autograd(L):
+    """A linear-attention layer (torch projections + lasp_attention) fits a fixed target: the library's
+    forward / backward inside torch.autograd drive the loss down over a few optimiser steps."""
+    torch.manual_seed(0)
+    B, N, d, H, D = 1, 2048, 256, 4, 64
+    qkv = torch.nn.Linear(d, 3 * H * D, bias=False).cuda()
+    out = torch.nn.Linear(H * D, d, bias=False).cuda()
+    opt = torch.optim.Adam(list(qkv.parameters()) + list(out.parameters()), lr=3e-3)
+    lam = [0.5, 0.9, 0.99, 0.999]
+    x = torch.randn(B, N, d, device="cuda")
+    target = torch.randn(B, N, d, device="cuda") * 0.1
+    losses = []
+    for _ in range(30):
+        q, k, v = qkv(x).view(B, N, 3, H, D).to(torch.bfloat16).unbind(2)
+        o = L.lasp_attention(q.contiguous(), k.contiguous(), v.contiguous(), lam)
+        loss = (out(o.float().reshape(B, N, H * D)) - target).square().mean()
+        opt.zero_grad()
+        loss.backward()
+        opt.step()
+        losses.append(loss.item())
+    assert all(np.isfinite(losses)) and losses[-1] < 0.5 * losses[0], losses
