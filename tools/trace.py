@@ -4,9 +4,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, synth
 import paper_2404_02882_b200 as L
 from paper_2404_02882_b200 import _native as N
-# usage: python tools/trace.py [n_blocks] [fwd|bwd]   (bwd: the fused dQ/dV/dK launch)
+# usage: python tools/trace.py [n_blocks] [fwd|bwd] [head_dim]   (bwd: the fused dQ/dV/dK launch)
 mode = sys.argv[2] if len(sys.argv) > 2 else "fwd"
-p = synth.problem(0, 1, 32768, 16, 64, dtype="bf16")
+HD = int(sys.argv[3]) if len(sys.argv) > 3 else 64
+p = synth.problem(0, 1, 32768, 16, HD, dtype="bf16")
 q, k, v, do = (torch.from_numpy(p[x]).cuda().to(torch.bfloat16) for x in ("q", "k", "v", "do"))
 o, _, cache = L.fwd_local(q, k, v, p["lam"]); torch.cuda.synchronize()
 buf = torch.zeros(3 * 1024 + 2 * 148, dtype=torch.int64, device="cuda")
