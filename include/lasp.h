@@ -41,6 +41,16 @@
  *              lambda, heads are independent, P:18 -- reading A7). lambda = 1 is plain linear
  *              attention.
  *   Streams  : all device work is enqueued on the caller's stream; calls return after enqueue.
+ *              Kernels use programmatic dependent launch: a kernel may start while the preceding
+ *              kernel on the stream is still running; it reads the call's input tensors right away
+ *              (they must be complete when the previous kernel STARTED) and writes nothing before
+ *              the preceding kernel has completed. Kernels that do not trigger early (any non-PDL
+ *              kernel, cudaMemcpy, events) are complete when the next kernel starts, so the only
+ *              restriction is: the input tensors of a call must not be outputs of the immediately
+ *              preceding LASP call on the same stream (put any other operation in between).
+ *   Graphs   : lasp_fwd_local / lasp_bwd_local and the NCCL entry points can be captured into CUDA
+ *              graphs (the programmatic launch edges are kept; bench.py replays its step from a
+ *              graph). Contexts made by lasp_ctx_create_loopback use host threads and cannot.
  *   Errors   : argument validation is synchronous and enqueues nothing. On a non-OK status
  *              lasp_last_error() returns a thread-local message. LASP_ERR_CUDA / LASP_ERR_COMM
  *              report launch / NCCL failures (with rank and peer for COMM).
