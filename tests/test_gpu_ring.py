@@ -57,6 +57,33 @@ def test_ring_world1_fp32(ring, oracle_mod):
         assert oracle_mod.normwise_err(x.cpu().numpy(), r) <= 1e-5
 
 
+def test_ring_graph_capture_matches_eager(ring):
+    """The NCCL-ctx entry points (comm stream fork/join, events, memsets) captured into a CUDA graph
+    reproduce the eager results bit for bit (include/lasp.h "Graphs")."""
+    p = synth.problem(21, 1, 2048, 4, 64, dtype="bf16")
+    q, k, v, do = (torch.from_numpy(p[x]).cuda().to(torch.bfloat16) for x in ("q", "k", "v", "do"))
+    o, dq, dk, dv = (torch.empty_like(q) for _ in range(4))
+    import paper_2404_02882_b200 as lasp
+    cache, ws = lasp.alloc_cache(q), lasp.alloc_workspace(q)
+
+    def step():
+        ring.fwd(q, k, v, p["lam"], o=o, cache=cache, workspace=ws)
+        ring.bwd(q, k, v, p["lam"], do, cache, dq=dq, dk=dk, dv=dv, workspace=ws)
+
+    step()
+    torch.cuda.synchronize()
+    eager = [t.clone() for t in (o, dq, dk, dv)]
+    for t in (o, dq, dk, dv):
+        t.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager, (o, dq, dk, dv)):
+        assert torch.equal(a, b)
+
+
 def test_ring_cache_tag_checks_rank(ring):
     import paper_2404_02882_b200 as lasp
     from paper_2404_02882_b200._native import LaspError
