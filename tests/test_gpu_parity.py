@@ -343,3 +343,21 @@ def test_config5_longest_sequence_closed_form(L):
                           ("dk", vd * np.outer(geo(N - s + 1), qv[h])), ("dv", qk * np.outer(geo(N - s + 1), dov[h]))):
             g = got[name][:, h]
             assert np.max(np.abs(g - ref)) <= BF16_TOL * np.max(np.abs(ref)) + 1e-6, (name, h)
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_random_shapes_sim_ring(L, oracle_mod, case):
+    """Seeded random shapes: batch 1-3, heads 1-5, head_dim 32/64/128, 1-4 simulated ranks of ragged or
+    block-aligned length, bf16 or fp32, random per-head lambda in (0.3, 1] (incl. exactly 1)."""
+    rng = np.random.default_rng(1000 + case)
+    B, H = int(rng.integers(1, 4)), int(rng.integers(1, 6))
+    D = int(rng.choice([32, 64, 128]))
+    T = int(rng.integers(1, 5))
+    C = int(rng.choice([int(rng.integers(1, 400)), 128 * int(rng.integers(1, 4))]))
+    dtype = "fp32" if case % 4 == 3 else "bf16"
+    lam = rng.uniform(0.3, 1.0, H).astype(np.float32)
+    lam[rng.integers(0, H)] = 1.0
+    p = synth.problem(2000 + case, B, C * T, H, D, dtype=dtype)
+    p["lam"] = lam
+    res = run_sim_ring(L, p, T, torch.float32 if dtype == "fp32" else torch.bfloat16, C * T)
+    check_against_oracle(oracle_mod, p, res, FP32_TOL if dtype == "fp32" else BF16_TOL)
