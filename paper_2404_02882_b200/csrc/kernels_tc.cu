@@ -573,17 +573,14 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
               ++kd;
             }
           } else {
-            // O_intra = P c, O_inter = a (S_hi + S_lo)
-            mbar_wait(&bar->p_full[J & 1], (J >> 1) & 1);
-            LASP_TRACE(11, J);
+            // O_inter = a (S_hi + S_lo) first: it does not depend on the mask, so the tensor pipe runs it
+            // while the mask warps build P; then O_intra = P c. (This issuer waits on the ring slot itself for
+            // the a tile; it also releases the slot, so the parity wait stays within one phase.)
+            mbar_wait(&bar->full[s], (J / ST) & 1);
             mbar_wait(&bar->o_empty, (J & 1) ^ 1);
             LASP_TRACE(12, J);
             mbar_wait(&bar->st_full[J % L::NSB], (J / L::NSB) & 1);
             tc_fence_after();
-            const uint32_t pt = tmem + ((J & 1) ? L::T_S1 : L::T_S0);  // P in TMEM (2 bf16 / column)
-#pragma unroll
-            for (int kk = 0; kk < BT / 16; ++kk)
-              mma_bf16_ts(tmem + L::T_OI, pt + kk * 8, desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv, kk != 0);
             const int sb = int(J % L::NSB);
 #pragma unroll
             for (int kk = 0; kk < L::DK / 16; ++kk)
@@ -593,6 +590,13 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             for (int kk = 0; kk < L::DK / 16; ++kk)
               mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SLO(sb) + kk * 2048, BOX),
                        id_x, 1);
+            mbar_wait(&bar->p_full[J & 1], (J >> 1) & 1);
+            LASP_TRACE(11, J);
+            tc_fence_after();
+            const uint32_t pt = tmem + ((J & 1) ? L::T_S1 : L::T_S0);  // P in TMEM (2 bf16 / column)
+#pragma unroll
+            for (int kk = 0; kk < BT / 16; ++kk)
+              mma_bf16_ts(tmem + L::T_OI, pt + kk * 8, desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv, kk != 0);
             mma_commit(&bar->o_full);
             mma_commit(&bar->s_empty[J & 1]);  // S/P buffer reusable once P c has been read
             mma_commit(&bar->st_empty[J % L::NSB]);
