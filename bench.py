@@ -364,6 +364,12 @@ def run_lasp(args):
         # dQ, dK, dV once (>= 14D B per token-head); the three passes stream 24D
         bytes_per_launch = 7 * 2 * D * B * C * H
         unit_note = "14*D bytes per token-head (Q,K,V,dO bf16 reads + dQ,dK,dV bf16 writes; B3 row)"
+        if "prefix_rev" not in stages:
+            # B2 folded into the same launch: it reads and writes the nseg fp32 D x D segment states of
+            # every (batch, head) once
+            nseg = -(-C // lasp.api.segment_len(lasp.api._shape(q)))
+            bytes_per_launch += 2 * 4 * B * H * nseg * D * D
+            unit_note += " + 8*nseg*D^2 bytes per (batch, head) (B2 fold: fp32 segment states read + written)"
     elif dom_name.startswith("core"):
         bytes_per_launch = 4 * 2 * D * B * C * H          # reads a, b, c and writes out (bf16): 8D B/token-head
         unit_note = "8*D bytes per token-head (3 bf16 reads + 1 bf16 write)"

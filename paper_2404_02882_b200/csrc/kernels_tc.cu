@@ -19,7 +19,9 @@
 //                               bf16 hi/lo copy of S_{j+1} for the next block's inter MMA
 //                  warps 12-15  epilogue: out = O_intra + r (.) O_inter -> bf16 -> TMA store
 //                The running state is the paper's KV (dKV) state applied between GPU blocks; the
-//                segment's initial state comes from the prefix kernel (KV_in of the ring included).
+//                segment's initial state comes from the prefix fold (KV_in of the ring included): the
+//                prefix kernel (ring path), or -- local path -- the same fold run by warps 8-15 of this
+//                launch before their roles start, followed by a grid barrier (cooperative launch).
 #include "lasp_common.cuh"
 #include "sm100.cuh"
 
@@ -182,6 +184,7 @@ struct SegParams {
   Plan p;
   float* out;
   unsigned long long* trace;
+  unsigned* gbar_reset;  // zeroed after the wait on the preceding kernel (fused fold of the next launch)
 };
 
 // debug timeline: event ev (0..15) of block J (< 64) of CTA 0 -> trace[ev * 64 + J] = clock64()
@@ -314,6 +317,8 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
     const int row = D == 128 ? int(q4 * 32 + lane) : int(q4 * 16 + lane);
     pdl_wait();
     pdl_trigger();
+    // the previous user of the counter (a core launch of an earlier call) has completed
+    if (prm.gbar_reset != nullptr && blockIdx.x == 0 && threadIdx.x == 256) *prm.gbar_reset = 0u;
     uint32_t k = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
       const Item it = get_item(p, DIR, w);
@@ -395,7 +400,67 @@ struct CoreParams {
   unsigned long long* trace;  // debug timeline (lasp_debug_trace), nullptr in production
   int npass;
   FastDiv div_per, div_nbh;   // / (B*H*NV*npass), / (B*H*NV) (work-item decode)
+  PrefixFold fold;            // fold.gbar != nullptr: compute the prefix states first (fused F2 / B2)
 };
+
+// Fused F2 / B2 (Alg. 2, Alg. 3 P:648 between segments; the arithmetic of prefix_kernel): per
+// element, cur = init; for each segment in fold order: prefix[p] = cur; cur = lam^len_p cur + seg[p];
+// fin = cur. Thread t of nt handles float2 elements t, t + nt, ...; all (up to U) segment loads of a
+// batch are in flight before the serial fold, and a batch is loaded before any of it is stored (in
+// place). D and the direction are compile-time so that the segment stride is an immediate offset.
+template <int D, bool FWD>
+__device__ __forceinline__ void fold_prefix_dir(const Plan& p, const PrefixFold& f, int64_t t, int64_t nt) {
+  constexpr int64_t DD = int64_t(D) * D;
+  constexpr int64_t STEP = FWD ? DD / 2 : -DD / 2;  // float2 elements between consecutive folded segments
+  constexpr int U = 40;
+  const int64_t n2 = p.B * p.H * DD / 2;
+  const int64_t last_len = p.C - (p.nseg - 1) * p.seg_len;
+  for (int64_t i2 = t; i2 < n2; i2 += nt) {
+    const int64_t bh = i2 / (DD / 2), e2 = i2 - bh * (DD / 2);
+    const float l2 = p.l2lam[bh % p.H];
+    const float dec_full = exp2f(float(p.seg_len) * l2), dec_last = exp2f(float(last_len) * l2);
+    float2 cur = f.init ? __ldcg(reinterpret_cast<const float2*>(f.init) + i2) : make_float2(0.f, 0.f);
+    // segment 0 (FWD) or nseg - 1 (REV) of this element
+    const int64_t first = (bh * p.nseg + (FWD ? 0 : p.nseg - 1)) * (DD / 2) + e2;
+    const float2* src = reinterpret_cast<const float2*>(f.seg) + first;
+    float2* dst = reinterpret_cast<float2*>(f.out) + first;
+    for (int64_t s0 = 0; s0 < p.nseg; s0 += U, src += U * STEP, dst += U * STEP) {
+      const int64_t nb = p.nseg - s0;  // segments left
+      float2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = u < nb ? __ldcg(src + u * STEP) : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (u < nb) {
+          dst[u * STEP] = cur;
+          const float dcy = (FWD ? u + 1 == nb : s0 + u == 0) ? dec_last : dec_full;  // segment nseg - 1
+          cur.x = fmaf(dcy, cur.x, v[u].x);
+          cur.y = fmaf(dcy, cur.y, v[u].y);
+        }
+      }
+    }
+    if (f.fin) reinterpret_cast<float2*>(f.fin)[i2] = cur;
+  }
+}
+template <int D>
+__device__ __forceinline__ void fold_prefix(const Plan& p, const PrefixFold& f, int64_t t, int64_t nt) {
+  if (Dir(f.dir) == Dir::FWD) fold_prefix_dir<D, true>(p, f, t, nt);
+  else fold_prefix_dir<D, false>(p, f, t, nt);
+}
+
+// grid barrier wait (acquire), then make the other CTAs' generic-proxy writes visible to this thread's
+// TMA loads; traps instead of hanging if the count is never reached
+__device__ __forceinline__ void grid_wait(const unsigned* ctr, unsigned target) {
+  uint32_t n = 0;
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= target) break;
+    __nanosleep(64);
+    if (++n == (1u << 26)) __trap();
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 struct CItem {
   int64_t b, h, seg, beg, end;
@@ -476,6 +541,19 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   // before it) has completed. The a, b, c tiles are inputs of that earlier work, so the producer fills
   // the ring before waiting; only the segment prefix states (written by the immediately preceding
   // kernel) are read after the wait (producer: STG; state warps at D = 128: direct loads).
+  // Fused fold: the state and epilogue warps (idle until the first state is needed) wait for the
+  // segment states, fold their slice, and arrive at the grid barrier; every CTA is resident (grid <=
+  // SM count, 1 CTA/SM), and the readers of prefix states (producer STG / D = 128 state warps) wait on it.
+  if (prm.fold.gbar != nullptr && warp >= 8) {
+    pdl_wait();
+    fold_prefix<D>(p, prm.fold, int64_t(blockIdx.x) * 256 + (threadIdx.x - 256), int64_t(gridDim.x) * 256);
+    named_bar_sync(2, 256);
+    if (threadIdx.x == 256) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence();
+      atomicAdd(prm.fold.gbar, 1u);
+    }
+  }
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
@@ -488,6 +566,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         // the segment's prefix state -> STG (single buffer, released by the state warps)
         auto load_stg = [&]() {
           if constexpr (L::HAS_STG) {
+            if (k == 0 && prm.fold.gbar != nullptr) grid_wait(prm.fold.gbar, gridDim.x);
             mbar_wait(&bar->stg_empty, (k & 1) ^ 1);
             mbar_expect_tx(&bar->stg_full, 4 * D * D);
             const int srow = int(((it.b * p.H + it.h) * p.nseg + it.seg) * D);
@@ -718,16 +797,23 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       } else {
         // straight from the (L2-resident) prefix states: row d, columns [64 v, 64 v + 64) of S, or
         // column d, rows [64 v, 64 v + 64) for S^T (coalesced across the warp)
-        if (k == 0) pdl_wait();  // the prefix states come from the preceding kernel
+        if (k == 0) {  // the prefix states come from the preceding kernel, or from the fused fold
+          if (prm.fold.gbar == nullptr) {
+            pdl_wait();
+          } else {
+            if (lane == 0) grid_wait(prm.fold.gbar, gridDim.x);
+            __syncwarp();
+          }
+        }
         const float* st = prm.stp[state] + ((it.b * p.H + it.h) * p.nseg + it.seg) * D * D;
         if (trans) {
 #pragma unroll
-          for (int e = 0; e < 64; ++e) S[e] = __ldg(st + (it.v * 64 + e) * D + d);
+          for (int e = 0; e < 64; ++e) S[e] = __ldcg(st + (it.v * 64 + e) * D + d);
         } else {
           const float4* row = reinterpret_cast<const float4*>(st + d * D + it.v * 64);
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            const float4 t = __ldg(row + e);
+            const float4 t = __ldcg(row + e);
             S[4 * e] = t.x; S[4 * e + 1] = t.y; S[4 * e + 2] = t.z; S[4 * e + 3] = t.w;
           }
         }
@@ -900,8 +986,10 @@ unsigned persistent_grid(const Plan& p, int per_sm = 1) {
 }
 
 template <int D, Dir DIR>
-cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, cudaStream_t st) {
+cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, cudaStream_t st,
+                       unsigned* gbar_reset) {
   SegParams prm;
+  prm.gbar_reset = gbar_reset;
   cudaError_t e;
   if ((e = make_seq_map(&prm.mx, x, p)) != cudaSuccess) return e;
   if ((e = make_seq_map(&prm.my, y, p)) != cudaSuccess) return e;
@@ -915,7 +1003,8 @@ cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, 
 }
 
 template <int D>
-cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st) {
+cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st,
+                              const PrefixFold* fold) {
   CoreParams prm;
   std::memset(&prm, 0, sizeof prm);
   cudaError_t e;
@@ -958,6 +1047,7 @@ cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const 
   prm.p = p;
   prm.npass = npass;
   prm.trace = g_trace;
+  if (fold) prm.fold = *fold;
   prm.div_nbh = FastDiv(uint32_t(p.B * p.H * CoreLayout<D>::NV));
   prm.div_per = FastDiv(uint32_t(p.B * p.H * CoreLayout<D>::NV * npass));
   auto kern = core_tc_kernel<D>;
@@ -965,7 +1055,7 @@ cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const 
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
   const int64_t W = p.B * p.H * p.nseg * npass * CoreLayout<D>::NV;
   const unsigned grid = unsigned(W < sm_count() ? W : sm_count());
-  return launch_k(kern, dim3(grid), dim3(512), smem, st, prm);
+  return launch_kx(fold != nullptr, kern, dim3(grid), dim3(512), smem, st, prm);
 }
 
 }  // namespace
@@ -982,9 +1072,10 @@ bool tc_supported(const Plan& p) {
   return !disabled && p.dtype == 0 && (p.D == 64 || p.D == 128) && p.C > 0;
 }
 
-cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st) {
-  if (p.D == 64) return dir == Dir::FWD ? launch_seg<64, Dir::FWD>(p, x, y, out, st) : launch_seg<64, Dir::REV>(p, x, y, out, st);
-  if (p.D == 128) return dir == Dir::FWD ? launch_seg<128, Dir::FWD>(p, x, y, out, st) : launch_seg<128, Dir::REV>(p, x, y, out, st);
+cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st,
+                                unsigned* r) {
+  if (p.D == 64) return dir == Dir::FWD ? launch_seg<64, Dir::FWD>(p, x, y, out, st, r) : launch_seg<64, Dir::REV>(p, x, y, out, st, r);
+  if (p.D == 128) return dir == Dir::FWD ? launch_seg<128, Dir::FWD>(p, x, y, out, st, r) : launch_seg<128, Dir::REV>(p, x, y, out, st, r);
   return cudaErrorNotSupported;
 }
 
@@ -992,10 +1083,11 @@ cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_
   return launch_core_tc_multi(p, 1, &a, &dir, st);
 }
 
-cudaError_t launch_core_tc_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st) {
+cudaError_t launch_core_tc_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st,
+                                 const PrefixFold* fold) {
   if (npass < 1 || npass > 3) return cudaErrorInvalidValue;
-  if (p.D == 64) return launch_core_multi<64>(p, npass, a, dirs, st);
-  if (p.D == 128) return launch_core_multi<128>(p, npass, a, dirs, st);
+  if (p.D == 64) return launch_core_multi<64>(p, npass, a, dirs, st, fold);
+  if (p.D == 128) return launch_core_multi<128>(p, npass, a, dirs, st, fold);
   return cudaErrorNotSupported;
 }
 

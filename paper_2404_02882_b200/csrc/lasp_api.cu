@@ -119,6 +119,7 @@ struct Workspace {
   float* local;   // [B][H][D][D] local total (ring)
   float* in;      // received state
   float* out;     // state to send
+  unsigned* gbar; // grid-barrier counter of the fused prefix fold
 };
 
 Workspace carve(const Plan& p, void* ws) {
@@ -131,11 +132,13 @@ Workspace carve(const Plan& p, void* ws) {
   w.in = reinterpret_cast<float*>(c);
   c += align256(state_elems(p) * 4);
   w.out = reinterpret_cast<float*>(c);
+  c += align256(state_elems(p) * 4);
+  w.gbar = reinterpret_cast<unsigned*>(c);
   return w;
 }
 
 size_t workspace_bytes(const Plan& p) {
-  return align256(seg_state_elems(p) * 4) + 3 * align256(state_elems(p) * 4);
+  return align256(seg_state_elems(p) * 4) + 3 * align256(state_elems(p) * 4) + 256;
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
@@ -250,12 +253,23 @@ cudaError_t staged(const char* name, cudaStream_t st, F&& launch) {
 }
 
 // ---- stage dispatch: tcgen05 for covered bf16 shapes, CUDA cores otherwise ---------------------
-cudaError_t seg_state(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st) {
+cudaError_t seg_state(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st,
+                      unsigned* gbar_reset = nullptr) {
   const bool tc = tc_supported(p);
   return staged(dir == Dir::FWD ? (tc ? "seg_state_fwd_tc" : "seg_state_fwd_simt")
                                 : (tc ? "seg_state_rev_tc" : "seg_state_rev_simt"), st, [&] {
-    return tc ? launch_seg_state_tc(p, dir, x, y, out, st) : launch_seg_state_simt(p, dir, x, y, out, st);
+    return tc ? launch_seg_state_tc(p, dir, x, y, out, st, gbar_reset) : launch_seg_state_simt(p, dir, x, y, out, st);
   });
+}
+
+// Local path on the tensor cores: the F2 / B2 prefix fold runs inside the following core launch (one
+// launch less per direction; PrefixFold). LASP_NO_FUSED_FOLD=1 keeps the separate prefix kernel.
+bool fused_fold(const Plan& p) {
+  static const bool off = [] {
+    const char* s = std::getenv("LASP_NO_FUSED_FOLD");
+    return s && *s && *s != '0';
+  }();
+  return !off && tc_supported(p);
 }
 
 cudaError_t core(const Plan& p, Dir dir, const void* a, const void* b, const void* c, void* out,
@@ -278,10 +292,11 @@ cudaError_t combine(const Plan& p, const float* in, const float* local, float* o
 
 // several core passes: one persistent tensor-core launch (passes of a segment interleaved, their
 // shared inputs re-read from L2), or one CUDA-core launch per pass
-cudaError_t core_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st) {
+cudaError_t core_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st,
+                       const PrefixFold* fold = nullptr) {
   if (tc_supported(p))
-    return staged(npass == 3 ? "core_bwd3_tc" : "core_multi_tc", st,
-                  [&] { return launch_core_tc_multi(p, npass, a, dirs, st); });
+    return staged(npass == 3 ? "core_bwd3_tc" : npass == 1 && dirs[0] == Dir::FWD ? "core_fwd_tc" : "core_multi_tc", st,
+                  [&] { return launch_core_tc_multi(p, npass, a, dirs, st, fold); });
   for (int x = 0; x < npass; ++x) {
     cudaError_t e = staged(dirs[x] == Dir::FWD ? "core_fwd_simt" : "core_rev_simt", st,
                            [&] { return launch_core_simt(p, dirs[x], a[x], st); });
@@ -542,8 +557,16 @@ lasp_status_t lasp_fwd_local(const lasp_shape_t* shape, const void* q, const voi
   if ((s = check_device()) != LASP_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Workspace w = carve(p, workspace);
-  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st));
-  if ((s = fwd_tail(p, q, k, v, kv_in, o, kv_out, cache, w.seg, st)) != LASP_OK) return s;
+  if (p.C > 0 && fused_fold(p)) {
+    LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, w.gbar));                           // F1
+    const PrefixFold fold{kv_in, w.seg, static_cast<float*>(cache), kv_out, w.gbar, int(Dir::FWD)};
+    const SeqArgs a{q, k, v, o, static_cast<const float*>(cache), 0};
+    const Dir dir = Dir::FWD;
+    LASP_CUDA(core_multi(p, 1, &a, &dir, st, &fold));                                      // F2 + F3
+  } else {
+    if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st));
+    if ((s = fwd_tail(p, q, k, v, kv_in, o, kv_out, cache, w.seg, st)) != LASP_OK) return s;
+  }
   register_cache(p, cache, -1, -1);
   return LASP_OK;
 }
@@ -564,12 +587,14 @@ lasp_status_t lasp_bwd_local(const lasp_shape_t* shape, const void* q, const voi
     LASP_CUDA(prefix(p, Dir::REV, dkv_in, nullptr, nullptr, dkv_out, st));
     return LASP_OK;
   }
-  LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st));                      // B1
-  LASP_CUDA(prefix(p, Dir::REV, dkv_in, w.seg, w.seg, dkv_out, st));         // B2 (in place)
-  // B3: dQ (needs only the cache), dV and dK in one launch
+  const bool fuse = fused_fold(p);
+  LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, fuse ? w.gbar : nullptr));         // B1
+  const PrefixFold fold{dkv_in, w.seg, w.seg, dkv_out, w.gbar, int(Dir::REV)};
+  if (!fuse) LASP_CUDA(prefix(p, Dir::REV, dkv_in, w.seg, w.seg, dkv_out, st));         // B2 (in place)
+  // B3: dQ (needs only the cache), dV and dK in one launch (with B2 folded in when fused)
   const SeqArgs passes[3] = {{d_o, v, k, dq, P, 1}, {k, q, d_o, dv, w.seg, 0}, {v, d_o, q, dk, w.seg, 1}};
   const Dir dirs[3] = {Dir::FWD, Dir::REV, Dir::REV};
-  LASP_CUDA(core_multi(p, 3, passes, dirs, st));
+  LASP_CUDA(core_multi(p, 3, passes, dirs, st, fuse ? &fold : nullptr));
   return LASP_OK;
 }
 

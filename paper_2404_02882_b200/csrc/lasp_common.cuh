@@ -35,19 +35,33 @@ inline bool pdl_enabled() {
   return on;
 }
 
+// launch with programmatic dependent launch (unless LASP_NO_PDL); coop: cooperative launch (all CTAs
+// co-resident, required by a kernel with a grid barrier)
 template <typename... KArgs, typename... Args>
-cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+cudaError_t launch_kx(bool coop, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (coop) {
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n++].val.cooperative = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  return launch_kx(false, kern, grid, block, smem, st, std::forward<Args>(args)...);
 }
 
 enum class Dir : int { FWD = 0, REV = 1 };
@@ -117,14 +131,29 @@ cudaError_t launch_fold_ranks(const Plan& p, const float* gathered, int j0, int 
 cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local, float* kv_out,
                            cudaStream_t st);
 
+// Segment-prefix fold (F2 / B2, same arithmetic as prefix_kernel) run by a core launch before its main
+// loop: the 256 state + epilogue threads of every CTA fold a slice, then meet at a grid barrier on
+// `gbar` (zeroed by the preceding segment-state launch) before any prefix state is read.
+struct PrefixFold {
+  const float* init;  // state entering the rank, or nullptr (zero)
+  const float* seg;   // segment states [B][H][nseg][D][D]
+  float* out;         // prefix states (may alias seg)
+  float* fin;         // state leaving the rank, or nullptr
+  unsigned* gbar;     // grid-barrier arrival counter, 0 at kernel start
+  int dir;            // Dir
+};
+
 // tcgen05 path (bf16 only); returns cudaErrorNotSupported when the shape is not covered.
 bool tc_supported(const Plan& p);
 const char* tc_last_error();
 void tc_set_trace(unsigned long long* buf);  // debug: per-block clock64 timeline of CTA 0  // detail of the last tcgen05-path host failure on this thread
+// gbar_reset: if non-null, set to 0 once the preceding kernel has completed (for a following fused fold)
 cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out,
-                                cudaStream_t st);
+                                cudaStream_t st, unsigned* gbar_reset = nullptr);
 cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st);
-// up to 3 core passes in one persistent launch (their segments interleaved: shared inputs hit L2)
-cudaError_t launch_core_tc_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st);
+// up to 3 core passes in one persistent launch (their segments interleaved: shared inputs hit L2);
+// fold != nullptr: the launch first computes the prefix states its passes read (PrefixFold)
+cudaError_t launch_core_tc_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st,
+                                 const PrefixFold* fold = nullptr);
 
 }  // namespace lasp

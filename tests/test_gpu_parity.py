@@ -361,3 +361,47 @@ def test_random_shapes_sim_ring(L, oracle_mod, case):
     p["lam"] = lam
     res = run_sim_ring(L, p, T, torch.float32 if dtype == "fp32" else torch.bfloat16, C * T)
     check_against_oracle(oracle_mod, p, res, FP32_TOL if dtype == "fp32" else BF16_TOL)
+
+
+_FOLD_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import synth, paper_2404_02882_b200 as L
+out = {{}}
+for D, C in ((64, 3 * 1024 + 384), (128, 2 * 1024 + 256)):
+    p = synth.problem(77 + D, 2, C, 3, D, dtype="bf16")
+    q, k, v, do = (torch.from_numpy(np.ascontiguousarray(p[x])).cuda().to(torch.bfloat16) for x in ("q", "k", "v", "do"))
+    g = torch.Generator().manual_seed(D)
+    kv_in = torch.randn(2, 3, D, D, generator=g).cuda()
+    dkv_in = torch.randn(2, 3, D, D, generator=g).cuda()
+    o, kv_out, cache = L.fwd_local(q, k, v, p["lam"], kv_in)
+    dq, dk, dv, dkv_out = L.bwd_local(q, k, v, p["lam"], do, cache, dkv_in)
+    for n, t in zip(("o", "kv_out", "dq", "dk", "dv", "dkv_out"), (o, kv_out, dq, dk, dv, dkv_out)):
+        out[f"{{n}}{{D}}"] = t.float().cpu().numpy()
+np.savez({dst!r}, **out)
+"""
+
+
+@pytest.mark.parametrize("pdl", ["on", "off"])
+def test_fused_prefix_fold_matches_separate_kernel(tmp_path, pdl):
+    """The local path folds F2 / B2 into the following core launch (grid barrier, PrefixFold); with
+    LASP_NO_FUSED_FOLD=1 it runs the separate prefix kernel. Same arithmetic in the same order, so every
+    output (including kv_out / dkv_out with a nonzero kv_in / dkv_in, D = 64 and 128, ragged segments,
+    batch 2) must agree bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for off in ("0", "1"):
+        dst = str(tmp_path / f"fold{off}.npz")
+        env = dict(os.environ, LASP_NO_FUSED_FOLD=off)
+        if pdl == "off":  # cooperative launch without the programmatic-serialization attribute
+            env["LASP_NO_PDL"] = "1"
+        script = _FOLD_SCRIPT.format(root=root, tests=os.path.join(root, "tests"), dst=dst)
+        subprocess.run([sys.executable, "-c", script], env=env, check=True, timeout=300)
+        res[off] = np.load(dst)
+    for key in res["0"].files:
+        assert np.array_equal(res["0"][key], res["1"][key]), key
