@@ -21,7 +21,7 @@
 //                The running state is the paper's KV (dKV) state applied between GPU blocks; the
 //                segment's initial state comes from the prefix fold (KV_in of the ring included): the
 //                prefix kernel (ring path), or -- local path -- the same fold run by warps 8-15 of this
-//                launch before their roles start, followed by a grid barrier (cooperative launch).
+//                launch before their roles start (claimed chunks, a done counter the readers wait on).
 #include "lasp_common.cuh"
 #include "sm100.cuh"
 
@@ -184,7 +184,7 @@ struct SegParams {
   Plan p;
   float* out;
   unsigned long long* trace;
-  unsigned* gbar_reset;  // zeroed after the wait on the preceding kernel (fused fold of the next launch)
+  unsigned* gbar_reset;  // [2] zeroed after the wait on the preceding kernel (fused fold of the next launch)
 };
 
 // debug timeline: event ev (0..15) of block J (< 64) of CTA 0 -> trace[ev * 64 + J] = clock64()
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
     pdl_wait();
     pdl_trigger();
     // the previous user of the counter (a core launch of an earlier call) has completed
-    if (prm.gbar_reset != nullptr && blockIdx.x == 0 && threadIdx.x == 256) *prm.gbar_reset = 0u;
+    if (prm.gbar_reset != nullptr && blockIdx.x == 0 && threadIdx.x == 256) prm.gbar_reset[0] = prm.gbar_reset[1] = 0u;
     uint32_t k = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
       const Item it = get_item(p, DIR, w);
@@ -405,17 +405,16 @@ struct CoreParams {
 
 // Fused F2 / B2 (Alg. 2, Alg. 3 P:648 between segments; the arithmetic of prefix_kernel): per
 // element, cur = init; for each segment in fold order: prefix[p] = cur; cur = lam^len_p cur + seg[p];
-// fin = cur. Thread t of nt handles float2 elements t, t + nt, ...; all (up to U) segment loads of a
-// batch are in flight before the serial fold, and a batch is loaded before any of it is stored (in
-// place). D and the direction are compile-time so that the segment stride is an immediate offset.
+// fin = cur, for float2 element i2 of the B*H*D*D / 2; all (up to U) segment loads of a batch are in
+// flight before the serial fold, and a batch is loaded before any of it is stored (in place). D and the
+// direction are compile-time so that the segment stride is an immediate offset.
 template <int D, bool FWD>
-__device__ __forceinline__ void fold_prefix_dir(const Plan& p, const PrefixFold& f, int64_t t, int64_t nt) {
+__device__ __forceinline__ void fold_prefix_dir(const Plan& p, const PrefixFold& f, int64_t i2) {
   constexpr int64_t DD = int64_t(D) * D;
   constexpr int64_t STEP = FWD ? DD / 2 : -DD / 2;  // float2 elements between consecutive folded segments
   constexpr int U = 40;
-  const int64_t n2 = p.B * p.H * DD / 2;
   const int64_t last_len = p.C - (p.nseg - 1) * p.seg_len;
-  for (int64_t i2 = t; i2 < n2; i2 += nt) {
+  {
     const int64_t bh = i2 / (DD / 2), e2 = i2 - bh * (DD / 2);
     const float l2 = p.l2lam[bh % p.H];
     const float dec_full = exp2f(float(p.seg_len) * l2), dec_last = exp2f(float(last_len) * l2);
@@ -443,13 +442,13 @@ __device__ __forceinline__ void fold_prefix_dir(const Plan& p, const PrefixFold&
   }
 }
 template <int D>
-__device__ __forceinline__ void fold_prefix(const Plan& p, const PrefixFold& f, int64_t t, int64_t nt) {
-  if (Dir(f.dir) == Dir::FWD) fold_prefix_dir<D, true>(p, f, t, nt);
-  else fold_prefix_dir<D, false>(p, f, t, nt);
+__device__ __forceinline__ void fold_prefix(const Plan& p, const PrefixFold& f, int64_t i2) {
+  if (Dir(f.dir) == Dir::FWD) fold_prefix_dir<D, true>(p, f, i2);
+  else fold_prefix_dir<D, false>(p, f, i2);
 }
 
-// grid barrier wait (acquire), then make the other CTAs' generic-proxy writes visible to this thread's
-// TMA loads; traps instead of hanging if the count is never reached
+// wait (acquire) until *ctr >= target, then make the other CTAs' generic-proxy writes visible to this
+// thread's TMA loads; traps instead of hanging if the count is never reached
 __device__ __forceinline__ void grid_wait(const unsigned* ctr, unsigned target) {
   uint32_t n = 0;
   for (;;) {
@@ -497,7 +496,12 @@ struct CoreBars {
   uint64_t p_full[2], ku_full, ds_full, ds_empty, st_full[2], st_empty[2], o_full, o_empty;
   uint64_t stg_full, stg_empty;
   uint32_t tmem_slot;
+  uint32_t fold_chunk;  // fused prefix fold: chunk claimed by this CTA's fold threads
 };
+constexpr int kFoldChunk = 256;  // float2 elements per claimed fold chunk (one per fold thread)
+__device__ __forceinline__ unsigned fold_chunks(const Plan& p) {
+  return unsigned((p.B * p.H * p.D * p.D / 2 + kFoldChunk - 1) / kFoldChunk);
+}
 
 
 
@@ -542,16 +546,27 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   // the ring before waiting; only the segment prefix states (written by the immediately preceding
   // kernel) are read after the wait (producer: STG; state warps at D = 128: direct loads).
   // Fused fold: the state and epilogue warps (idle until the first state is needed) wait for the
-  // segment states, fold their slice, and arrive at the grid barrier; every CTA is resident (grid <=
-  // SM count, 1 CTA/SM), and the readers of prefix states (producer STG / D = 128 state warps) wait on it.
+  // segment states, then claim chunks of kFoldChunk float2 elements from a global counter (fold.gbar[0])
+  // and fold them, counting finished chunks in fold.gbar[1]; the readers of prefix states (producer STG /
+  // D = 128 state warps) wait until every chunk is done. Chunks are claimed, not assigned, so the wait
+  // completes whichever CTAs are resident (no co-residency requirement, no cooperative launch).
   if (prm.fold.gbar != nullptr && warp >= 8) {
+    const unsigned n_chunks = fold_chunks(p);
     pdl_wait();
-    fold_prefix<D>(p, prm.fold, int64_t(blockIdx.x) * 256 + (threadIdx.x - 256), int64_t(gridDim.x) * 256);
-    named_bar_sync(2, 256);
-    if (threadIdx.x == 256) {
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      __threadfence();
-      atomicAdd(prm.fold.gbar, 1u);
+    const int64_t n2 = p.B * p.H * p.D * p.D / 2;
+    for (;;) {
+      if (threadIdx.x == 256) bar->fold_chunk = atomicAdd(&prm.fold.gbar[0], 1u);
+      named_bar_sync(2, 256);
+      const unsigned c = bar->fold_chunk;
+      if (c >= n_chunks) break;
+      const int64_t i2 = int64_t(c) * kFoldChunk + (threadIdx.x - 256);
+      if (i2 < n2) fold_prefix<D>(p, prm.fold, i2);
+      named_bar_sync(2, 256);  // chunk written (and fold_chunk read by every thread)
+      if (threadIdx.x == 256) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
+        atomicAdd(&prm.fold.gbar[1], 1u);
+      }
     }
   }
 
@@ -566,7 +581,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         // the segment's prefix state -> STG (single buffer, released by the state warps)
         auto load_stg = [&]() {
           if constexpr (L::HAS_STG) {
-            if (k == 0 && prm.fold.gbar != nullptr) grid_wait(prm.fold.gbar, gridDim.x);
+            if (k == 0 && prm.fold.gbar != nullptr) grid_wait(&prm.fold.gbar[1], fold_chunks(p));
             mbar_wait(&bar->stg_empty, (k & 1) ^ 1);
             mbar_expect_tx(&bar->stg_full, 4 * D * D);
             const int srow = int(((it.b * p.H + it.h) * p.nseg + it.seg) * D);
@@ -801,7 +816,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           if (prm.fold.gbar == nullptr) {
             pdl_wait();
           } else {
-            if (lane == 0) grid_wait(prm.fold.gbar, gridDim.x);
+            if (lane == 0) grid_wait(&prm.fold.gbar[1], fold_chunks(p));
             __syncwarp();
           }
         }
@@ -1055,12 +1070,19 @@ cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const 
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
   const int64_t W = p.B * p.H * p.nseg * npass * CoreLayout<D>::NV;
   const unsigned grid = unsigned(W < sm_count() ? W : sm_count());
-  return launch_kx(fold != nullptr, kern, dim3(grid), dim3(512), smem, st, prm);
+  return launch_k(kern, dim3(grid), dim3(512), smem, st, prm);
 }
 
 }  // namespace
 
 const char* tc_last_error() { return g_tc_err; }
+
+bool tc_fold_fusable(const Plan& p) {
+  // the fused fold runs on 256 threads per SM (a standalone prefix launch fills every SM): a win while
+  // each fold thread has at most 2 elements (TNL-0.4B 16 x 64: 0.9; measured +1-1.7 %), a loss at 3.5
+  // (TNL-1B 16 x 128: -0.4 %)
+  return tc_supported(p) && p.B * p.H * p.D * p.D / 2 <= int64_t(2) * sm_count() * kFoldChunk;
+}
 
 void tc_set_trace(unsigned long long* buf) { g_trace = buf; }
 

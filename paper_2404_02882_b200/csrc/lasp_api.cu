@@ -263,13 +263,14 @@ cudaError_t seg_state(const Plan& p, Dir dir, const void* x, const void* y, floa
 }
 
 // Local path on the tensor cores: the F2 / B2 prefix fold runs inside the following core launch (one
-// launch less per direction; PrefixFold). LASP_NO_FUSED_FOLD=1 keeps the separate prefix kernel.
+// launch less per direction; PrefixFold) when the states are small enough (tc_fold_fusable).
+// LASP_NO_FUSED_FOLD=1 keeps the separate prefix kernel.
 bool fused_fold(const Plan& p) {
   static const bool off = [] {
     const char* s = std::getenv("LASP_NO_FUSED_FOLD");
     return s && *s && *s != '0';
   }();
-  return !off && tc_supported(p);
+  return !off && tc_fold_fusable(p);
 }
 
 cudaError_t core(const Plan& p, Dir dir, const void* a, const void* b, const void* c, void* out,

@@ -35,33 +35,19 @@ inline bool pdl_enabled() {
   return on;
 }
 
-// launch with programmatic dependent launch (unless LASP_NO_PDL); coop: cooperative launch (all CTAs
-// co-resident, required by a kernel with a grid barrier)
 template <typename... KArgs, typename... Args>
-cudaError_t launch_kx(bool coop, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                      Args&&... args) {
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  unsigned n = 0;
-  if (pdl_enabled()) {
-    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[n++].val.programmaticStreamSerializationAllowed = 1;
-  }
-  if (coop) {
-    attr[n].id = cudaLaunchAttributeCooperative;
-    attr[n++].val.cooperative = 1;
-  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = n;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-}
-template <typename... KArgs, typename... Args>
-cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
-  return launch_kx(false, kern, grid, block, smem, st, std::forward<Args>(args)...);
 }
 
 enum class Dir : int { FWD = 0, REV = 1 };
@@ -132,19 +118,21 @@ cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local
                            cudaStream_t st);
 
 // Segment-prefix fold (F2 / B2, same arithmetic as prefix_kernel) run by a core launch before its main
-// loop: the 256 state + epilogue threads of every CTA fold a slice, then meet at a grid barrier on
-// `gbar` (zeroed by the preceding segment-state launch) before any prefix state is read.
+// loop: the 256 state + epilogue threads of each CTA claim chunks of elements (gbar[0]) and fold them;
+// prefix states are read once every chunk is done (gbar[1]). Both counters are zeroed by the preceding
+// segment-state launch.
 struct PrefixFold {
   const float* init;  // state entering the rank, or nullptr (zero)
   const float* seg;   // segment states [B][H][nseg][D][D]
   float* out;         // prefix states (may alias seg)
   float* fin;         // state leaving the rank, or nullptr
-  unsigned* gbar;     // grid-barrier arrival counter, 0 at kernel start
+  unsigned* gbar;     // [2]: chunks claimed, chunks done; 0 at kernel start
   int dir;            // Dir
 };
 
 // tcgen05 path (bf16 only); returns cudaErrorNotSupported when the shape is not covered.
 bool tc_supported(const Plan& p);
+bool tc_fold_fusable(const Plan& p);  // fuse the prefix fold into the core launch (small enough state)
 const char* tc_last_error();
 void tc_set_trace(unsigned long long* buf);  // debug: per-block clock64 timeline of CTA 0  // detail of the last tcgen05-path host failure on this thread
 // gbar_reset: if non-null, set to 0 once the preceding kernel has completed (for a following fused fold)
