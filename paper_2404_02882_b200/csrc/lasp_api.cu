@@ -314,12 +314,20 @@ lasp_status_t prologue(const lasp_shape_t* shape, const float* lambda, Plan& p) 
   return load_lambda(p, lambda);
 }
 
-// Forward compute after KV_in is known (F2 prefix + F3 core). `seg` already holds F1's states.
+// Forward compute after KV_in is known (F2 prefix + F3 core). `seg` already holds F1's states. gbar:
+// fused-fold counters (zeroed by F1's launch) or nullptr for the separate prefix kernel.
 lasp_status_t fwd_tail(const Plan& p, const void* q, const void* k, const void* v, const float* kv_in,
-                       void* o, float* kv_out, void* cache, float* seg, cudaStream_t st) {
+                       void* o, float* kv_out, void* cache, float* seg, unsigned* gbar, cudaStream_t st) {
   float* P = static_cast<float*>(cache);
   if (p.C == 0) {
     LASP_CUDA(prefix(p, Dir::FWD, kv_in, nullptr, P, kv_out, st));
+    return LASP_OK;
+  }
+  if (gbar) {
+    const PrefixFold fold{kv_in, seg, P, kv_out, gbar, int(Dir::FWD)};
+    const SeqArgs a{q, k, v, o, P, 0};
+    const Dir dir = Dir::FWD;
+    LASP_CUDA(core_multi(p, 1, &a, &dir, st, &fold));
     return LASP_OK;
   }
   LASP_CUDA(prefix(p, Dir::FWD, kv_in, seg, P, kv_out, st));
@@ -558,16 +566,9 @@ lasp_status_t lasp_fwd_local(const lasp_shape_t* shape, const void* q, const voi
   if ((s = check_device()) != LASP_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Workspace w = carve(p, workspace);
-  if (p.C > 0 && fused_fold(p)) {
-    LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, w.gbar));                           // F1
-    const PrefixFold fold{kv_in, w.seg, static_cast<float*>(cache), kv_out, w.gbar, int(Dir::FWD)};
-    const SeqArgs a{q, k, v, o, static_cast<const float*>(cache), 0};
-    const Dir dir = Dir::FWD;
-    LASP_CUDA(core_multi(p, 1, &a, &dir, st, &fold));                                      // F2 + F3
-  } else {
-    if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st));
-    if ((s = fwd_tail(p, q, k, v, kv_in, o, kv_out, cache, w.seg, st)) != LASP_OK) return s;
-  }
+  unsigned* gbar = p.C > 0 && fused_fold(p) ? w.gbar : nullptr;
+  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, gbar));                  // F1
+  if ((s = fwd_tail(p, q, k, v, kv_in, o, kv_out, cache, w.seg, gbar, st)) != LASP_OK) return s;  // F2 + F3
   register_cache(p, cache, -1, -1);
   return LASP_OK;
 }
@@ -724,11 +725,12 @@ lasp_status_t lasp_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   const size_t n = state_elems(p);
   int from = -1, to = -1;
   lasp_ring_peers(c->rank, c->world, 0, &from, &to);
-  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st));                     // F1
+  unsigned* gbar = p.C > 0 && fused_fold(p) ? w.gbar : nullptr;
+  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, gbar));               // F1
   LASP_CUDA(prefix(p, Dir::FWD, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
   if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
     if ((s = exchange_allgather(c, p, w.local, w.in, false, st)) != LASP_OK) return s;
-    if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, st)) != LASP_OK) return s;  // F2 + F3
+    if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, gbar, st)) != LASP_OK) return s;  // F2 + F3
     register_cache(p, cache, c->rank, c->world);
     return LASP_OK;
   }
@@ -742,7 +744,7 @@ lasp_status_t lasp_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
     LASP_CUDA(combine(p, w.in, w.local, w.out, st));
     if ((s = ring_send(c, w.out, n, to, st, "ncclSend(KV)")) != LASP_OK) return s;
   }
-  if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, st)) != LASP_OK) return s;  // F2 + F3
+  if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, gbar, st)) != LASP_OK) return s;  // F2 + F3
   register_cache(p, cache, c->rank, c->world);
   return LASP_OK;
 }
@@ -761,7 +763,8 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   Workspace w = carve(p, workspace);
   const size_t n = state_elems(p);
   const float* P = static_cast<const float*>(cache);
-  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st));                    // B1
+  const bool fuse = p.C > 0 && fused_fold(p);
+  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, fuse ? w.gbar : nullptr));  // B1
   LASP_CUDA(prefix(p, Dir::REV, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
   // B2 ring hop on the comm stream: Recv dKV_in from r+1 (Alg. 3), combine, Send to r-1
   LASP_CUDA(cudaEventRecord(c->ev_ready, st));
@@ -784,11 +787,12 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   if (p.C > 0) LASP_CUDA(core(p, Dir::FWD, d_o, v, k, dq, P, 1, st));
   LASP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
   if (p.C == 0) return LASP_OK;
-  LASP_CUDA(prefix(p, Dir::REV, w.in, w.seg, w.seg, nullptr, st));               // B2
-  {  // dV and dK in one launch
+  if (!fuse) LASP_CUDA(prefix(p, Dir::REV, w.in, w.seg, w.seg, nullptr, st));   // B2
+  {  // dV and dK in one launch (with B2 folded in when fused)
     const SeqArgs passes[2] = {{k, q, d_o, dv, w.seg, 0}, {v, d_o, q, dk, w.seg, 1}};
     const Dir dirs[2] = {Dir::REV, Dir::REV};
-    LASP_CUDA(core_multi(p, 2, passes, dirs, st));
+    const PrefixFold fold{w.in, w.seg, w.seg, nullptr, w.gbar, int(Dir::REV)};
+    LASP_CUDA(core_multi(p, 2, passes, dirs, st, fuse ? &fold : nullptr));
   }
   return LASP_OK;
 }
