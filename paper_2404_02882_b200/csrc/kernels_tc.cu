@@ -406,45 +406,43 @@ struct CoreParams {
 // Fused F2 / B2 (Alg. 2, Alg. 3 P:648 between segments; the arithmetic of prefix_kernel): per
 // element, cur = init; for each segment in fold order: prefix[p] = cur; cur = lam^len_p cur + seg[p];
 // fin = cur, for float2 element i2 of the B*H*D*D / 2; all (up to U) segment loads of a batch are in
-// flight before the serial fold, and a batch is loaded before any of it is stored (in place). D and the
-// direction are compile-time so that the segment stride is an immediate offset.
-template <int D, bool FWD>
-__device__ __forceinline__ void fold_prefix_dir(const Plan& p, const PrefixFold& f, int64_t i2) {
-  constexpr int64_t DD = int64_t(D) * D;
-  constexpr int64_t STEP = FWD ? DD / 2 : -DD / 2;  // float2 elements between consecutive folded segments
-  constexpr int U = 40;
-  const int64_t last_len = p.C - (p.nseg - 1) * p.seg_len;
-  {
-    const int64_t bh = i2 / (DD / 2), e2 = i2 - bh * (DD / 2);
-    const float l2 = p.l2lam[bh % p.H];
-    const float dec_full = exp2f(float(p.seg_len) * l2), dec_last = exp2f(float(last_len) * l2);
-    float2 cur = f.init ? __ldcg(reinterpret_cast<const float2*>(f.init) + i2) : make_float2(0.f, 0.f);
-    // segment 0 (FWD) or nseg - 1 (REV) of this element
-    const int64_t first = (bh * p.nseg + (FWD ? 0 : p.nseg - 1)) * (DD / 2) + e2;
-    const float2* src = reinterpret_cast<const float2*>(f.seg) + first;
-    float2* dst = reinterpret_cast<float2*>(f.out) + first;
-    for (int64_t s0 = 0; s0 < p.nseg; s0 += U, src += U * STEP, dst += U * STEP) {
-      const int64_t nb = p.nseg - s0;  // segments left
-      float2 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = u < nb ? __ldcg(src + u * STEP) : make_float2(0.f, 0.f);
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (u < nb) {
-          dst[u * STEP] = cur;
-          const float dcy = (FWD ? u + 1 == nb : s0 + u == 0) ? dec_last : dec_full;  // segment nseg - 1
-          cur.x = fmaf(dcy, cur.x, v[u].x);
-          cur.y = fmaf(dcy, cur.y, v[u].y);
-        }
-      }
-    }
-    if (f.fin) reinterpret_cast<float2*>(f.fin)[i2] = cur;
-  }
-}
+// flight before the serial fold, and a batch is loaded before any of it is stored (in place). One copy
+// of the unrolled body serves both directions (code size: it sits in the core kernel).
 template <int D>
 __device__ __forceinline__ void fold_prefix(const Plan& p, const PrefixFold& f, int64_t i2) {
-  if (Dir(f.dir) == Dir::FWD) fold_prefix_dir<D, true>(p, f, i2);
-  else fold_prefix_dir<D, false>(p, f, i2);
+  constexpr int64_t D2 = int64_t(D) * D / 2;  // float2 elements per state
+  constexpr int U = 40;
+  const bool fwd = Dir(f.dir) == Dir::FWD;
+  const int64_t step = fwd ? D2 : -D2;        // float2 elements between consecutive folded segments
+  const int64_t last_len = p.C - (p.nseg - 1) * p.seg_len;
+  const int64_t bh = i2 / D2, e2 = i2 - bh * D2;
+  const float l2 = p.l2lam[bh % p.H];
+  const float dec_full = exp2f(float(p.seg_len) * l2), dec_last = exp2f(float(last_len) * l2);
+  float2 cur = f.init ? __ldcg(reinterpret_cast<const float2*>(f.init) + i2) : make_float2(0.f, 0.f);
+  // segment 0 (FWD) or nseg - 1 (REV) of this element
+  const int64_t first = (bh * p.nseg + (fwd ? 0 : p.nseg - 1)) * D2 + e2;
+  const float2* src = reinterpret_cast<const float2*>(f.seg) + first;
+  float2* dst = reinterpret_cast<float2*>(f.out) + first;
+  for (int64_t s0 = 0; s0 < p.nseg; s0 += U, src += U * step, dst += U * step) {
+    const int nb = int(p.nseg - s0);  // segments left
+    // the segment nseg - 1 (length last_len) is folded last (FWD) or first (REV)
+    const int last_u = fwd ? int(nb - 1) : (s0 == 0 ? 0 : -1);
+    float2 v[U];
+    const float2* ps = src;
+#pragma unroll
+    for (int u = 0; u < U; ++u, ps += step) v[u] = __ldcg(u < nb ? ps : src);  // past the end: a valid dummy
+    float2* pd = dst;
+#pragma unroll
+    for (int u = 0; u < U; ++u, pd += step) {
+      if (u < nb) {
+        *pd = cur;
+        const float dcy = u == last_u ? dec_last : dec_full;
+        cur.x = fmaf(dcy, cur.x, v[u].x);
+        cur.y = fmaf(dcy, cur.y, v[u].y);
+      }
+    }
+  }
+  if (f.fin) reinterpret_cast<float2*>(f.fin)[i2] = cur;
 }
 
 // wait (acquire) until *ctr >= target, then make the other CTAs' generic-proxy writes visible to this
@@ -821,17 +819,23 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           }
         }
         const float* st = prm.stp[state] + ((it.b * p.H + it.h) * p.nseg + it.seg) * D * D;
-        if (trans) {
+        // states of the preceding kernel: read-only here (ld.global.nc); states folded by this launch: L2
+        // only (ld.global.cg), never a possibly stale L1 / texture copy
+        auto load = [&](auto ld) {
+          if (trans) {
 #pragma unroll
-          for (int e = 0; e < 64; ++e) S[e] = __ldcg(st + (it.v * 64 + e) * D + d);
-        } else {
-          const float4* row = reinterpret_cast<const float4*>(st + d * D + it.v * 64);
+            for (int e = 0; e < 64; ++e) S[e] = ld(st + (it.v * 64 + e) * D + d);
+          } else {
+            const float4* row = reinterpret_cast<const float4*>(st + d * D + it.v * 64);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float4 t = __ldcg(row + e);
-            S[4 * e] = t.x; S[4 * e + 1] = t.y; S[4 * e + 2] = t.z; S[4 * e + 3] = t.w;
+            for (int e = 0; e < 16; ++e) {
+              const float4 t = ld(row + e);
+              S[4 * e] = t.x; S[4 * e + 1] = t.y; S[4 * e + 2] = t.z; S[4 * e + 3] = t.w;
+            }
           }
-        }
+        };
+        if (prm.fold.gbar == nullptr) load([](auto* ptr) { return __ldg(ptr); });
+        else load([](auto* ptr) { return __ldcg(ptr); });
       }
     };
     uint32_t J = 0, kd = 0, k = 0;
