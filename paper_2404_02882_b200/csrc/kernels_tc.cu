@@ -819,8 +819,10 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           }
         }
         const float* st = prm.stp[state] + ((it.b * p.H + it.h) * p.nseg + it.seg) * D * D;
-        // states of the preceding kernel: read-only here (ld.global.nc); states folded by this launch: L2
-        // only (ld.global.cg), never a possibly stale L1 / texture copy
+        // states of the preceding kernel: read-only here (ld.global.nc); states folded by this launch: plain
+        // (L1-allocating) loads after the acquire in grid_wait -- the fold read them with ld.global.cg, so
+        // this SM's L1 holds no copy older than the fold's writes. (Each thread's 16 float4 row loads share
+        // two 128-byte lines: L2-only loads would cost TNL-1B 4 %.)
         auto load = [&](auto ld) {
           if (trans) {
 #pragma unroll
@@ -835,7 +837,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           }
         };
         if (prm.fold.gbar == nullptr) load([](auto* ptr) { return __ldg(ptr); });
-        else load([](auto* ptr) { return __ldcg(ptr); });
+        else load([](auto* ptr) { return *ptr; });
       }
     };
     uint32_t J = 0, kd = 0, k = 0;
@@ -1085,7 +1087,11 @@ bool tc_fold_fusable(const Plan& p) {
   // the fused fold runs on 256 threads per SM (a standalone prefix launch fills every SM): a win while
   // each fold thread has at most 2 elements (TNL-0.4B 16 x 64: 0.9; measured +1-1.7 %), a loss at 3.5
   // (TNL-1B 16 x 128: -0.4 %)
-  return tc_supported(p) && p.B * p.H * p.D * p.D / 2 <= int64_t(2) * sm_count() * kFoldChunk;
+  static const int64_t rounds = [] {
+    const char* s = std::getenv("LASP_FOLD_MAX_ROUNDS");
+    return s && *s ? std::atoll(s) : int64_t(2);
+  }();
+  return tc_supported(p) && p.B * p.H * p.D * p.D / 2 <= rounds * sm_count() * kFoldChunk;
 }
 
 void tc_set_trace(unsigned long long* buf) { g_trace = buf; }
