@@ -405,3 +405,34 @@ def test_fused_prefix_fold_matches_separate_kernel(tmp_path, pdl):
         res[off] = np.load(dst)
     for key in res["0"].files:
         assert np.array_equal(res["0"][key], res["1"][key]), key
+
+
+def test_concurrent_streams_fused_fold(L):
+    """The fused prefix fold waits on a done-counter of claimed chunks, not on a per-CTA barrier, so two
+    calls running at the same time on two streams (each with its own workspace; their core launches
+    compete for the SMs) complete and give the same results as the same calls run one after the other."""
+    shapes = [(1, 8192, 16, 64), (2, 4096, 4, 128)]
+    runs = []
+    for i, (B, C, H, D) in enumerate(shapes):
+        p = synth.problem(90 + i, B, C, H, D, dtype="bf16")
+        q, k, v, do = (to_dev(p[x], torch.bfloat16) for x in ("q", "k", "v", "do"))
+        runs.append((p["lam"], q, k, v, do, L.alloc_workspace(q)))
+
+    def call(r):
+        lam, q, k, v, do, ws = r
+        o, _, cache = L.fwd_local(q, k, v, lam, workspace=ws)
+        dq, dk, dv, _ = L.bwd_local(q, k, v, lam, do, cache, workspace=ws)
+        return [o, dq, dk, dv]
+
+    ref = [[t.clone() for t in call(r)] for r in runs]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in runs]
+    for _ in range(5):
+        outs = []
+        for s, r in zip(streams, runs):
+            with torch.cuda.stream(s):
+                outs.append(call(r))
+        torch.cuda.synchronize()
+        for got, want in zip(outs, ref):
+            for a, b in zip(got, want):
+                assert torch.equal(a, b)
