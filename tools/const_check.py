@@ -1,3 +1,5 @@
+"""Closed-form spot check at long lengths: constant inputs per head (lambda = 0.999 and 1) through fwd_local,
+compared with the geometric-series closed form (debug companion of the config-5 closed-form tests)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, synth

@@ -1,3 +1,4 @@
+"""Per-block role timeline of the segment-state kernel (lasp_debug_trace; build with LASP_TRACE_BUILD)."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, synth
