@@ -274,6 +274,9 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
           mbar_wait(&scaled[s], (J / ST) & 1);
           LASP_TRACE(3, J);
           tc_fence_after();
+#ifdef LASP_EXPERIMENT_SEG_NOMMA  // timing experiment only: no accumulation
+          if (false)
+#endif
 #pragma unroll
           for (int kk = 0; kk < BT / 16; ++kk)
             mma_bf16(acc, desc_mn(sbase + L::X(s) + kk * 2048, BOX), desc_mn(sbase + L::Y(s) + kk * 2048, BOX), idesc,
@@ -298,6 +301,9 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
         float wgt = 0.f;
         if (pos >= it.beg && pos < it.end)
           wgt = exp2f(float(DIR == Dir::FWD ? (it.end - 1 - pos) : (pos - it.beg + 1)) * l2);
+#ifdef LASP_EXPERIMENT_SEG_NOSCALE  // timing experiment only (tools/cmp_variants.sh): unweighted X
+        if (false)
+#endif
 #pragma unroll
         for (int x = 0; x < L::NBOX; ++x)
 #pragma unroll
