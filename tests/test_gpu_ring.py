@@ -188,3 +188,39 @@ def test_allgather_protocol_and_domain(ring):
         assert e.value.name == "LASP_ERR_DOMAIN"
     finally:
         r.close()
+
+
+_RING_FOLD_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import synth, test_gpu_ring as T
+out = {{}}
+for exchange in ("ring", "allgather"):
+    p = synth.problem(61, 1, 3 * 1152, 4, 64, dtype="bf16")
+    got, kv = T._run_loopback(p, 3, 3 * 1152, torch.bfloat16, "fold-" + exchange, exchange)
+    for n, x in zip(("o", "dq", "dk", "dv"), got):
+        out[n + exchange] = x
+    out["kv" + exchange] = np.stack(kv)
+np.savez({dst!r}, **out)
+"""
+
+
+def test_ring_fused_fold_matches_separate_kernel(tmp_path):
+    """The ring entry points fold F2 (after the hop) into the F3 launch and B2 into the dV / dK launch; with
+    LASP_NO_FUSED_FOLD=1 they run the prefix kernel. 3 loopback ranks, ring and all-gather exchange: every
+    output and every rank's received state must agree bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for off in ("0", "1"):
+        dst = str(tmp_path / f"ringfold{off}.npz")
+        script = _RING_FOLD_SCRIPT.format(root=root, tests=os.path.join(root, "tests"), dst=dst)
+        subprocess.run([sys.executable, "-c", script], env=dict(os.environ, LASP_NO_FUSED_FOLD=off), check=True,
+                       timeout=600)
+        res[off] = np.load(dst)
+    for key in res["0"].files:
+        assert np.array_equal(res["0"][key], res["1"][key]), key
