@@ -368,16 +368,17 @@ import sys, numpy as np, torch
 sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
 import synth, paper_2404_02882_b200 as L
 out = {{}}
-for D, C in ((64, 3 * 1024 + 384), (128, 2 * 1024 + 256)):
-    p = synth.problem(77 + D, 2, C, 3, D, dtype="bf16")
+# (B, H, D, C): small states; and B*H*D*D/2 = 65536 float2 = 256 fold chunks for at most 148 CTAs (2 rounds)
+for B, H, D, C in ((2, 3, 64, 3 * 1024 + 384), (2, 3, 128, 2 * 1024 + 256), (2, 16, 64, 4096 + 640)):
+    p = synth.problem(77 + D + H, B, C, H, D, dtype="bf16")
     q, k, v, do = (torch.from_numpy(np.ascontiguousarray(p[x])).cuda().to(torch.bfloat16) for x in ("q", "k", "v", "do"))
     g = torch.Generator().manual_seed(D)
-    kv_in = torch.randn(2, 3, D, D, generator=g).cuda()
-    dkv_in = torch.randn(2, 3, D, D, generator=g).cuda()
+    kv_in = torch.randn(B, H, D, D, generator=g).cuda()
+    dkv_in = torch.randn(B, H, D, D, generator=g).cuda()
     o, kv_out, cache = L.fwd_local(q, k, v, p["lam"], kv_in)
     dq, dk, dv, dkv_out = L.bwd_local(q, k, v, p["lam"], do, cache, dkv_in)
     for n, t in zip(("o", "kv_out", "dq", "dk", "dv", "dkv_out"), (o, kv_out, dq, dk, dv, dkv_out)):
-        out[f"{{n}}{{D}}"] = t.float().cpu().numpy()
+        out[f"{{n}}{{D}}_{{H}}"] = t.float().cpu().numpy()
 np.savez({dst!r}, **out)
 """
 
@@ -387,7 +388,7 @@ def test_fused_prefix_fold_matches_separate_kernel(tmp_path, pdl):
     """The local path folds F2 / B2 into the following core launch (grid barrier, PrefixFold); with
     LASP_NO_FUSED_FOLD=1 it runs the separate prefix kernel. Same arithmetic in the same order, so every
     output (including kv_out / dkv_out with a nonzero kv_in / dkv_in, D = 64 and 128, ragged segments,
-    batch 2) must agree bit for bit."""
+    batch 2, a state large enough for two rounds of fold chunks per CTA) must agree bit for bit."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import os
