@@ -10,7 +10,7 @@ bf16, per-head lambda_h = 1 - 2^-(1 + 14h/15). N>1 keeps 32K tokens per GPU (wea
 NCCL KV/dKV ring (one process per GPU, launched by torchrun). Synthetic inputs from synth/ (seeded).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lasp|reference] [--config tnl04b|tnl1b|tnl7b]
-       [--exchange ring|allgather] [--sp-size T] [--no-graph] [--no-e2e] [--no-cpu-baseline]
+       [--exchange auto|ring|allgather] [--sp-size T] [--no-graph] [--no-e2e] [--no-cpu-baseline]
 """
 from __future__ import annotations
 
@@ -207,8 +207,11 @@ def run_lasp(args):
     o, dq, dk, dv = (torch.empty_like(q) for _ in range(4))
     cache, ws = lasp.alloc_cache(q), lasp.alloc_workspace(q)
     ring = None
+    # auto: the paper's ring for T <= 2 (one hop either way); for T >= 3 one all-gather of the local states
+    # (NEXT-2): the ring's T-1 dependent hops sit on the critical path of the last rank
+    exchange = args.exchange if args.exchange != "auto" else ("ring" if T <= 2 else "allgather")
     if T > 1:
-        ring = lasp.Ring(dev, group=lasp.sp_group(T) if T < world else None).set_exchange(args.exchange)
+        ring = lasp.Ring(dev, group=lasp.sp_group(T) if T < world else None).set_exchange(exchange)
 
     def step():
         if ring is None:
@@ -410,7 +413,7 @@ def run_lasp(args):
                        "l2": "flushed between timed steps (256 MiB read outside the step events); inputs 4x"
                              f" {B * C * H * D * 2 >> 20} MiB", "parallelism": f"dp{G}xsp{T}" if G > 1 else f"sp{T}",
                        "launch": "cuda-graph replay" if graph is not None else "eager (PDL)",
-                       "exchange": args.exchange if T > 1 else "none"},
+                       "exchange": exchange if T > 1 else "none"},
             "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e, "roofline": roofline,
             "path": path, "cpu_baseline": cpu}
     if rank == 0:
@@ -435,8 +438,9 @@ def main():
     ap.add_argument("--sp-size", type=int, default=0,
                     help="sequence-parallel size T (default: all ranks in one ring); G = N/T data-parallel groups "
                          "(Alg. 1 data-sequence hybrid, NEXT-1)")
-    ap.add_argument("--exchange", choices=["ring", "allgather"], default="ring",
-                    help="state exchange at N > 1: the paper's ring (default) or one all-gather (NEXT-2)")
+    ap.add_argument("--exchange", choices=["auto", "ring", "allgather"], default="auto",
+                    help="state exchange at N > 1: the paper's ring, one all-gather (NEXT-2), or auto (ring for "
+                         "T <= 2, all-gather for T >= 3; default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
