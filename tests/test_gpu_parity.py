@@ -363,6 +363,27 @@ def test_random_shapes_sim_ring(L, oracle_mod, case):
     check_against_oracle(oracle_mod, p, res, FP32_TOL if dtype == "fp32" else BF16_TOL)
 
 
+_LONG = int(__import__("os").environ.get("LASP_LONG_SWEEP", "0"))
+
+
+@pytest.mark.parametrize("case", range(100, 100 + _LONG))
+def test_random_shapes_long_sweep(L, oracle_mod, case):
+    """Opt-in (LASP_LONG_SWEEP=<count>): the same seeded random-shape generator as above over many more
+    cases, with per-rank lengths up to 3000 tokens (several segments, ragged tails)."""
+    rng = np.random.default_rng(7000 + case)
+    B, H = int(rng.integers(1, 4)), int(rng.integers(1, 9))
+    D = int(rng.choice([32, 64, 128]))
+    T = int(rng.integers(1, 5))
+    C = int(rng.choice([int(rng.integers(1, 3000)), 128 * int(rng.integers(1, 24))]))
+    dtype = "fp32" if case % 5 == 4 else "bf16"
+    lam = rng.uniform(0.3, 1.0, H).astype(np.float32)
+    lam[rng.integers(0, H)] = 1.0
+    p = synth.problem(9000 + case, B, C * T, H, D, dtype=dtype)
+    p["lam"] = lam
+    res = run_sim_ring(L, p, T, torch.float32 if dtype == "fp32" else torch.bfloat16, C * T)
+    check_against_oracle(oracle_mod, p, res, FP32_TOL if dtype == "fp32" else BF16_TOL)
+
+
 _FOLD_SCRIPT = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
@@ -385,7 +406,7 @@ np.savez({dst!r}, **out)
 
 @pytest.mark.parametrize("pdl", ["on", "off"])
 def test_fused_prefix_fold_matches_separate_kernel(tmp_path, pdl):
-    """The local path folds F2 / B2 into the following core launch (grid barrier, PrefixFold); with
+    """The local path folds F2 / B2 into the following core launch (claimed chunks, PrefixFold); with
     LASP_NO_FUSED_FOLD=1 it runs the separate prefix kernel. Same arithmetic in the same order, so every
     output (including kv_out / dkv_out with a nonzero kv_in / dkv_in, D = 64 and 128, ragged segments,
     batch 2, a state large enough for two rounds of fold chunks per CTA) must agree bit for bit."""
