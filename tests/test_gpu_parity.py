@@ -420,7 +420,7 @@ def test_fused_prefix_fold_matches_separate_kernel(tmp_path, pdl):
     for off in ("0", "1"):
         dst = str(tmp_path / f"fold{off}.npz")
         env = dict(os.environ, LASP_NO_FUSED_FOLD=off)
-        if pdl == "off":  # cooperative launch without the programmatic-serialization attribute
+        if pdl == "off":  # launches without the programmatic-serialization attribute
             env["LASP_NO_PDL"] = "1"
         script = _FOLD_SCRIPT.format(root=root, tests=os.path.join(root, "tests"), dst=dst)
         subprocess.run([sys.executable, "-c", script], env=env, check=True, timeout=300)
