@@ -120,6 +120,18 @@ def test_bf16_ragged_lengths(L, oracle_mod, N):
     check_against_oracle(oracle_mod, p, res, BF16_TOL)
 
 
+@pytest.mark.parametrize("B,N,H,D,T", [(1, 130, 256, 64, 1),   # the maximum head count (kMaxHeads)
+                                       (1, 256, 256, 128, 2),  # max heads at head_dim 128, 2 ranks
+                                       (8, 2, 2, 128, 2),      # one token per rank, batch 8
+                                       (5, 387, 3, 64, 3)])    # batch 5, ragged 129-token ranks
+def test_extreme_shapes(L, oracle_mod, B, N, H, D, T):
+    """Edge sizes: 256 heads (per-head lambda of the TNL recipe, every head checked), batch 8 with a single
+    token per rank, batch 5 with ragged ranks -- against the oracle, through the simulated ring."""
+    p = synth.problem(5, B, N, H, D, dtype="bf16")
+    res = run_sim_ring(L, p, T, torch.bfloat16, N)
+    check_against_oracle(oracle_mod, p, res, BF16_TOL)
+
+
 @pytest.mark.parametrize("D", [32, 128])
 def test_fp32_path_other_dims(L, oracle_mod, D):
     p = synth.problem(4, 1, 700, 2, D, dtype="fp32")
