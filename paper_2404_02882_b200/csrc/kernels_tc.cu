@@ -471,7 +471,8 @@ struct CItem {
   Dir dir;
 };
 
-// item w -> (segment, pass, batch*head, value slice): segment-major, value slice innermost
+// item w -> (segment, pass, batch*head, value slice) at head_dim 64, (segment, batch*head, pass, value slice)
+// at head_dim 128: segment-major, value slice innermost
 template <int NV>
 __device__ __noinline__ CItem get_citem(const CoreParams& prm, int64_t w) {
   const Plan& p = prm.p;
@@ -480,8 +481,18 @@ __device__ __noinline__ CItem get_citem(const CoreParams& prm, int64_t w) {
   const uint32_t wu = uint32_t(w);
   it.seg = prm.div_per.div(wu);
   const uint32_t rem = wu - uint32_t(it.seg) * per;
-  it.pass = int(prm.div_nbh.div(rem));
-  const uint32_t bhv = rem - uint32_t(it.pass) * nbh;
+  uint32_t bhv;
+  if constexpr (NV > 1) {
+    // head_dim 128: (batch x head, pass, value slice) inside a segment row, so that the items re-reading one
+    // (segment, batch x head)'s a / b tiles run on adjacent CTAs (fused backward 342 -> 336.5 us at TNL-1B;
+    // at head_dim 64 the pass-major order is faster, 124.5 vs 125.8 us)
+    const uint32_t pv = uint32_t(prm.npass) * uint32_t(NV), bh0 = rem / pv, r2 = rem - bh0 * pv;
+    it.pass = int(r2 / uint32_t(NV));
+    bhv = bh0 * uint32_t(NV) + (r2 - uint32_t(it.pass) * uint32_t(NV));
+  } else {
+    it.pass = int(prm.div_nbh.div(rem));
+    bhv = rem - uint32_t(it.pass) * nbh;
+  }
   const uint32_t bh = bhv / uint32_t(NV);
   it.v = int(bhv - bh * uint32_t(NV));
   it.b = p.div_h.div(bh);
