@@ -62,14 +62,16 @@ int64_t env_i64(const char* name, int64_t dflt) {
 // Segments per (batch, head) such that the core launch has ~4 work items per SM: an item is one
 // (segment, batch x head, 64-wide value slice), so head_dim 128 (2 value slices) takes half as many
 // segments as head_dim 64 (measured: TNL-1B 56.9 -> 57.3 M tokens/s; TNL-0.4B is optimal at 4 x 148).
+// Head_dim 128 takes ~5 items per SM (same-box sweep 296..888 with the (batch x head, pass, value slice)
+// item order: TNL-1B 56.7 -> 57.0 M tokens/s, TNL-7B 27.42 -> 27.62 M; profiles/r1j_target_*.txt).
 int64_t choose_seg_len(int64_t B, int64_t C, int64_t H, int64_t D) {
   const int64_t q = kSegQuantum;
   const int64_t forced = env_i64("LASP_SEG_LEN", 0);
   if (forced > 0) return ((forced + q - 1) / q) * q;
   if (C <= 0) return q;
   const int64_t nb = (C + q - 1) / q;
-  const int64_t target = env_i64("LASP_TARGET_CTAS", 4 * 148);
   const int64_t nv = D >= 128 ? D / 64 : 1;  // value slices per item (tensor-core core kernel)
+  const int64_t target = env_i64("LASP_TARGET_CTAS", (nv > 1 ? 5 : 4) * 148);
   int64_t nseg_t = (target + B * H * nv - 1) / (B * H * nv);
   if (nseg_t < 1) nseg_t = 1;
   if (nseg_t > nb) nseg_t = nb;
