@@ -10,7 +10,12 @@ bf16, per-head lambda_h = 1 - 2^-(1 + 14h/15). N>1 keeps 32K tokens per GPU (wea
 NCCL KV/dKV ring (one process per GPU, launched by torchrun). Synthetic inputs from synth/ (seeded).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lasp|reference] [--config tnl04b|tnl1b|tnl7b]
-       [--exchange auto|ring|allgather] [--sp-size T] [--no-graph] [--no-e2e] [--no-cpu-baseline]
+       [--exchange both|ring|allgather] [--sp-size T] [--loopback N] [--tokens C] [--no-graph] [--no-e2e]
+       [--no-cpu-baseline]
+
+Before timing, every rank runs one fwd+bwd of constant per-head inputs through the same code path (ring /
+all-gather / local) and checks the closed forms of SURVEY §8(c) pin 5 at sampled global positions; the worst
+error (max over ranks) is printed as parity_max_err / parity_ok.
 """
 from __future__ import annotations
 
@@ -61,6 +66,8 @@ class ClockSampler:
         self._t = None
 
     def __enter__(self):
+        if self.index is None or self.index < 0:
+            return self
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -148,7 +155,8 @@ def run_reference(args):
             "data": "synthetic (synth/, seed 0)",
             "config": {"workload": desc, "global_batch": 1, "seq_len": C * world, "n_local": C, "heads": H,
                        "head_dim": D, "parallelism": f"sp{world}"},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "nproc": cpu_info()[0],
+                             "cpu_model": cpu_info()[1], "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -167,37 +175,120 @@ def cpu_baseline(H, D, C, desc):
         oracle.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"], nthreads=threads)
         reps += 1
         el = time.perf_counter() - t0
-    return {"value": C * reps / el, "unit": "tokens/s", "cores": min(threads, H), "kind": "oracle",
-            "sample": f"full {desc} layer, fwd+bwd in fp64, {reps} rep(s), {el:.1f} s on {min(threads, H)} threads"}
+    nproc, model = cpu_info()
+    return {"value": C * reps / el, "unit": "tokens/s", "cores": min(threads, H), "nproc": nproc, "cpu_model": model,
+            "kind": "oracle",
+            "sample": f"full {desc} layer, fwd+bwd in fp64, {reps} rep(s), {el:.1f} s on {min(threads, H)} threads "
+                      f"(one per (batch, head) work item; host has {nproc})"}
 
 
 # ----------------------------------------------------------------------------------------------------
-def run_lasp(args):
-    import ctypes
+class TorchComm:
+    """Barrier / max-over-ranks for one process per GPU (torch.distributed over NCCL)."""
 
+    def __init__(self, world, dev):
+        self.world, self.dev = world, dev
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier(device_ids=[self.dev.index])
+
+    def max(self, x):
+        if self.world == 1:
+            return float(x)
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([float(x)], dtype=torch.float64, device=self.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+
+class ThreadComm:
+    """The same for --loopback: ranks are threads of this process on one GPU."""
+
+    def __init__(self, world):
+        self.world = world
+        self._bar = threading.Barrier(world)
+        self._vals = [0.0] * world
+        self._lock = threading.Lock()
+
+    def barrier(self):
+        self._bar.wait(timeout=600)
+
+    def max(self, x, rank=None):
+        self.barrier()
+        with self._lock:
+            self._vals[rank] = float(x)
+        self.barrier()
+        m = max(self._vals)
+        self.barrier()
+        return m
+
+
+def closed_form_check(lasp, dev, B, C, H, D, lam, rank, T, run):
+    """Self-check of the timed configuration before timing (every rank, every exchange): constant inputs
+    q_s = q, k_s = k, v_s = v, do_s = do per head have closed forms derived from Eq. 4 (SURVEY §8(c) pin 5,
+    the same forms tests/test_gpu_parity.py checks): with s the GLOBAL 1-based position and N = T*C,
+      o_s = (q.k) v g(s),  dq_s = (v.do) k g(s),  dk_s = (v.do) q g(N-s+1),  dv_s = (q.k) do g(N-s+1),
+    g(n) = (1 - lam^n) / (1 - lam) (n for lam = 1). Returns the worst normwise error at sampled positions."""
     import numpy as np
     import torch
-    import torch.distributed as dist
+    rng = np.random.default_rng(123)
+    vecs = [rng.standard_normal((H, D)).astype(np.float32) * 0.3 for _ in range(4)]
+    vecs = [torch.from_numpy(v).to(torch.bfloat16).float().numpy().astype(np.float64) for v in vecs]
+    qv, kv_, vv, dov = vecs
+    mk = lambda a: torch.from_numpy(np.broadcast_to(a.astype(np.float32), (B, C, H, D)).copy()).to(
+        device=dev, dtype=torch.bfloat16)
+    o, dq, dk, dv = run(mk(qv), mk(kv_), mk(vv), mk(dov))
+    torch.cuda.synchronize(dev)
+    N = T * C
+    idx = np.unique(np.clip(np.array([0, 1, 2, 127, 128, 1000, C // 2, C - 2, C - 1]), 0, C - 1))
+    s = (rank * C + idx + 1).astype(np.float64)
+    worst = 0.0
+    for h in range(H):
+        l = float(np.float64(np.float32(lam[h])))
+        g = (lambda n: n) if l == 1.0 else (lambda n: (1 - l ** n) / (1 - l))
+        qk, vd = float(qv[h] @ kv_[h]), float(vv[h] @ dov[h])
+        for got, ref in ((o, qk * np.outer(g(s), vv[h])), (dq, vd * np.outer(g(s), kv_[h])),
+                         (dk, vd * np.outer(g(N - s + 1), qv[h])), (dv, qk * np.outer(g(N - s + 1), dov[h]))):
+            x = got[0, idx, h].float().cpu().numpy().astype(np.float64)
+            den = max(np.max(np.abs(ref)), 1e-30)
+            worst = max(worst, float(np.max(np.abs(x - ref)) / den))
+    return worst
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
+def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
+    """One rank's measurement (returns the JSON line on rank 0, None elsewhere)."""
+    import ctypes
+
+    import torch
 
     import synth
     import paper_2404_02882_b200 as lasp
     from paper_2404_02882_b200 import _native as N
 
-    world, rank, local = dist_env()
-    if world != args.gpus:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
     H, D, C, desc = CONFIGS[args.config]
+    if args.tokens:
+        C = args.tokens
     B = 1
     lib = N.lib()
-
-    # data-sequence hybrid (Alg. 1, NEXT-1): G = world/T groups of T ranks, each on its own sequence
     T = args.sp_size or world
     grp_id, grank, _ = lasp.topology(rank, world, T)
     G = world // T
+    stream = torch.cuda.current_stream(dev)
     # inputs: this rank's shard [t*C, (t+1)*C) of its group's sequence (seed = group id)
     p = synth.problem(grp_id, B, C * T, H, D, dtype="bf16", token_lo=grank * C, token_hi=(grank + 1) * C)
     lam = p["lam"]
@@ -206,24 +297,22 @@ def run_lasp(args):
     q, k, v, do = d_in["q"], d_in["k"], d_in["v"], d_in["do"]
     o, dq, dk, dv = (torch.empty_like(q) for _ in range(4))
     cache, ws = lasp.alloc_cache(q), lasp.alloc_workspace(q)
-    ring = None
-    # auto: the paper's ring for T <= 2 (one hop either way); for T >= 3 one all-gather of the local states
-    # (NEXT-2): the ring's T-1 dependent hops sit on the critical path of the last rank
-    exchange = args.exchange if args.exchange != "auto" else ("ring" if T <= 2 else "allgather")
+    # N > 1: time the paper's ring and the all-gather exchange (NEXT-2) in the same run; `value` is the ring
     if T > 1:
-        ring = lasp.Ring(dev, group=lasp.sp_group(T) if T < world else None).set_exchange(exchange)
+        exchanges = ["ring", "allgather"] if args.exchange == "both" else [args.exchange]
+        ring = make_ring()
+    else:
+        exchanges, ring = ["none"], None
 
-    def step():
-        if ring is None:
-            lasp.fwd_local(q, k, v, lam, o=o, kv_out=False, cache=cache, workspace=ws)
-            lasp.bwd_local(q, k, v, lam, do, cache, dq=dq, dk=dk, dv=dv, dkv_out=False, workspace=ws)
-        else:
-            ring.fwd(q, k, v, lam, o=o, cache=cache, workspace=ws)
-            ring.bwd(q, k, v, lam, do, cache, dq=dq, dk=dk, dv=dv, workspace=ws)
-
-    def barrier():
-        if world > 1:
-            dist.barrier(device_ids=[local])
+    def step_fn(ex):
+        def step():
+            if ring is None:
+                lasp.fwd_local(q, k, v, lam, o=o, kv_out=False, cache=cache, workspace=ws)
+                lasp.bwd_local(q, k, v, lam, do, cache, dq=dq, dk=dk, dv=dv, dkv_out=False, workspace=ws)
+            else:
+                ring.fwd(q, k, v, lam, o=o, cache=cache, workspace=ws)
+                ring.bwd(q, k, v, lam, do, cache, dq=dq, dk=dk, dv=dv, workspace=ws)
+        return step
 
     # L2 flush between timed steps: READ a 256 MiB buffer (> 126 MB L2), so L2 holds clean lines and no
     # write-back of the flush lands inside the next step (a write-based flush would)
@@ -233,66 +322,108 @@ def run_lasp(args):
     def l2_flush():
         torch.sum(flush, dim=0, dtype=torch.int64, out=flush_sink)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
+    results = {}
+    clk_summary = None
+    for ex in exchanges:
+        if ring is not None:
+            ring.set_exchange(ex)
+        # (0) parity gate through this exact code path (closed forms, every rank), before any timing
+        cws, ccache = lasp.alloc_workspace(q), lasp.alloc_cache(q)
 
-    stream = torch.cuda.current_stream(dev)
-    # --graph: the step's launches captured once into a CUDA graph (programmatic-dependent-launch edges are
-    # kept), replayed in the timed region: same kernels, no per-launch host work
-    graph, graph_launches = None, 0
-    if args.graph and ring is None:  # (the NCCL ring path launches eagerly)
-        graph = torch.cuda.CUDAGraph()
-        l0 = lib.lasp_launch_count()
-        with torch.cuda.graph(graph):
-            step()
-        graph_launches = lib.lasp_launch_count() - l0
-        graph.replay()
-        torch.cuda.synchronize()
-
-    def timed_loop(n, profile):
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
-        lib.lasp_profile_enable(1 if profile else 0)
-        barrier()
-        torch.cuda.synchronize()
-        for i in range(n):
-            l2_flush()                       # outside the step events
-            ev[i][0].record(stream)
-            if graph is not None and not profile:
-                graph.replay()
+        def run_const(a, b, c, d):
+            oo, dd = torch.empty_like(a), [torch.empty_like(a) for _ in range(3)]
+            if ring is None:
+                lasp.fwd_local(a, b, c, lam, o=oo, kv_out=False, cache=ccache, workspace=cws)
+                lasp.bwd_local(a, b, c, lam, d, ccache, dq=dd[0], dk=dd[1], dv=dd[2], dkv_out=False, workspace=cws)
             else:
-                step()
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        lib.lasp_profile_enable(0)
-        return sum(a.elapsed_time(b) for a, b in ev)
+                ring.fwd(a, b, c, lam, o=oo, cache=ccache, workspace=cws)
+                ring.bwd(a, b, c, lam, d, ccache, dq=dd[0], dk=dd[1], dv=dd[2], workspace=cws)
+            return [oo] + dd
+        err = closed_form_check(lasp, dev, B, C, H, D, lam, grank, T, run_const)
+        err = comm.max(err, rank) if loopback else comm.max(err)
+        del cws, ccache
+        step = step_fn(ex)
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize(dev)
+        # the step's launches captured once into a CUDA graph (programmatic-dependent-launch edges and the
+        # NCCL ring kept), replayed in the timed region: same kernels, no per-launch host work
+        graph, graph_launches, graph_note = None, 0, None
+        if args.graph and not loopback:
+            try:
+                comm.barrier()
+                g = torch.cuda.CUDAGraph()
+                l0 = lib.lasp_launch_count()
+                with torch.cuda.graph(g):
+                    step()
+                graph_launches = lib.lasp_launch_count() - l0
+                g.replay()
+                torch.cuda.synchronize(dev)
+                graph = g
+            except Exception as e:  # noqa: BLE001 - reported in the line
+                graph_note = f"capture failed ({type(e).__name__}: {e}); eager"
+                torch.cuda.synchronize(dev)
 
-    # (1) the measured region: K steps, no per-stage events (they would break programmatic dependent
-    # launch between the library's kernels)
-    launches0 = lib.lasp_launch_count()
-    with ClockSampler(local) as clk:
-        total_ms = timed_loop(args.steps, False)
-    launches = lib.lasp_launch_count() - launches0 + graph_launches * args.steps
-    # (2) the same K steps again with CUDA events recorded by the library around every kernel launch
-    # (on the launching stream): per-kernel durations for the roofline of the dominant kernel
-    prof_ms = timed_loop(args.steps, True)
-    buf = ctypes.create_string_buffer(1 << 16)
-    lib.lasp_profile_read(buf, len(buf))
-    stages = json.loads(buf.value.decode() or "{}")
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
-    ms_step = total_ms / args.steps
-    value = world * B * C * args.steps / (total_ms / 1e3)
+        def timed_loop(n, profile):
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+            if not loopback or rank == 0:
+                lib.lasp_profile_enable(1 if profile else 0)
+            comm.barrier()
+            torch.cuda.synchronize(dev)
+            comm.barrier()
+            for i in range(n):
+                l2_flush()                       # outside the step events
+                ev[i][0].record(stream)
+                if graph is not None and not profile:
+                    graph.replay()
+                else:
+                    step()
+                ev[i][1].record(stream)
+            torch.cuda.synchronize(dev)
+            comm.barrier()
+            if not loopback or rank == 0:
+                lib.lasp_profile_enable(0)
+            return sum(a.elapsed_time(b) for a, b in ev)
+
+        # (1) the measured region: K steps, no per-stage events (they would break programmatic dependent
+        # launch between the library's kernels)
+        launches0 = lib.lasp_launch_count()
+        with ClockSampler(dev.index if rank == 0 else -1) as clk:
+            total_ms = timed_loop(args.steps, False)
+        launches = (lib.lasp_launch_count() - launches0) // (world if loopback else 1) + graph_launches * args.steps
+        if rank == 0:
+            clk_summary = clk.summary()
+        # (2) the same K steps again with CUDA events recorded by the library around every kernel launch and
+        # around the ring hop (on the launching stream): per-kernel durations for the roofline of the dominant
+        # kernel, and the exchange time per step (in --loopback only rank 0's launches are recorded)
+        prof_ms = timed_loop(args.steps, True)
+        stages = {}
+        if not loopback or rank == 0:
+            buf = ctypes.create_string_buffer(1 << 16)
+            lib.lasp_profile_read(buf, len(buf))
+            stages = json.loads(buf.value.decode() or "{}")
+        hop = {kk: vv[1] / args.steps * 1e3 for kk, vv in stages.items() if kk.startswith("exchange")}
+        hop = {kk: (comm.max(vv, rank) if loopback else comm.max(vv)) for kk, vv in sorted(hop.items())} \
+            if (T > 1 and not loopback) else hop
+        total_ms = comm.max(total_ms, rank) if loopback else comm.max(total_ms)
+        results[ex] = {"total_ms": total_ms, "prof_ms": prof_ms, "stages": stages, "launches": launches,
+                       "graph": graph is not None, "graph_note": graph_note, "parity_err": err,
+                       "hop_us_per_step": hop}
+        del graph
+
+    main_ex = "ring" if "ring" in results else exchanges[0]
+    R = results[main_ex]
+    ms_step = R["total_ms"] / args.steps
+    value = world * B * C * args.steps / (R["total_ms"] / 1e3)
 
     # e2e through the public API with pinned host buffers: every step copies its inputs H2D, runs fwd + bwd
     # and copies its outputs D2H. Streamed the way a training loop feeds a layer: two device buffer sets and
     # three streams (H2D copy engine, compute, D2H copy engine), so step i+1's upload and step i-1's
     # download overlap step i's compute (PCIe is full duplex; the copies dominate at these sizes).
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not loopback:
+        if ring is not None:
+            ring.set_exchange(main_ex)
         pin = {kk: vv.to(torch.bfloat16).pin_memory() for kk, vv in host.items()}
         outs_h = [torch.empty(q.shape, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
         n_e2e = max(3, min(args.steps, 20))
@@ -337,89 +468,160 @@ def run_lasp(args):
             stream.wait_stream(s_dn)
 
         e2e_run(2)
-        torch.cuda.synchronize()
-        barrier()
+        torch.cuda.synchronize(dev)
+        comm.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         s_up.wait_event(e0)
         e2e_run(n_e2e)
         e1.record(stream)
-        torch.cuda.synchronize()
-        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * B * C * n_e2e / (float(et.item()) / 1e3), "unit": "tokens/s",
+        torch.cuda.synchronize(dev)
+        et = comm.max(e0.elapsed_time(e1))
+        e2e = {"value": world * B * C * n_e2e / (et / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e,
                "pipelining": "double-buffered: H2D(i+1) and D2H(i-1) overlap compute(i) on separate streams"}
 
-    # roofline of the dominant kernel, from the live per-stage CUDA events
+    if ring is not None:
+        ring.close()
+    if rank != 0:
+        return None
+
+    # roofline of the dominant kernel, from the live per-stage CUDA events of the measured exchange
+    stages = R["stages"]
     hbm, tflops, tflops_sus, peak_src = peaks()
     fam = {}
     for kk, (n_, ms_) in stages.items():  # one kernel family per template (fwd / rev directions pooled)
+        if kk.startswith("exchange") or kk.startswith("tag_"):
+            continue
         f_ = kk.replace("_fwd", "").replace("_rev", "")
         a_ = fam.setdefault(f_, [0, 0.0])
         a_[0] += n_
         a_[1] += ms_
     dom_name, (dom_n, dom_ms) = max(fam.items(), key=lambda kv: kv[1][1]) if fam else ("none", (1, 0.0))
     per_launch_ms = dom_ms / max(dom_n, 1)
+    seg_len = lasp.segment_len(N.shape(B, C, H, D, N.LASP_BF16))
+    nseg = -(-C // seg_len)
+    st_bytes = 4 * B * H * D * D                        # one fp32 D x D state per (batch, head)
     if dom_name.startswith("core_bwd3"):
-        # one launch runs the whole B3 row (dQ, dV, dK passes): algorithmic bytes read Q, K, V, dO and write
-        # dQ, dK, dV once (>= 14D B per token-head); the three passes stream 24D
-        bytes_per_launch = 7 * 2 * D * B * C * H
-        unit_note = "14*D bytes per token-head (Q,K,V,dO bf16 reads + dQ,dK,dV bf16 writes; B3 row)"
-        if "prefix_rev" not in stages:
-            # B2 folded into the same launch: it reads and writes the nseg fp32 D x D segment states of
-            # every (batch, head) once
-            nseg = -(-C // lasp.api.segment_len(lasp.api._shape(q)))
-            bytes_per_launch += 2 * 4 * B * H * nseg * D * D
-            unit_note += " + 8*nseg*D^2 bytes per (batch, head) (B2 fold: fp32 segment states read + written)"
+        # the B3 row reads Q, K, V, dO and writes dQ, dK, dV once (14D B per token-head) plus
+        # 2 states per pass (the cached KV_in and the received dKV_in)
+        bytes_per_launch = 7 * 2 * D * B * C * H + 2 * st_bytes
+        unit_note = "14*D bytes per token-head (Q,K,V,dO bf16 reads + dQ,dK,dV bf16 writes; B3 row) + 2*B*H*D^2*4"
+        # this design's extra state traffic: the 3 passes read one prefix state per segment, and (fused B2)
+        # the fold reads and writes the nseg segment states
+        overhead = 3 * nseg * st_bytes - 2 * st_bytes + (2 * nseg * st_bytes if "prefix_rev" not in stages else 0)
     elif dom_name.startswith("core"):
-        bytes_per_launch = 4 * 2 * D * B * C * H          # reads a, b, c and writes out (bf16): 8D B/token-head
-        unit_note = "8*D bytes per token-head (3 bf16 reads + 1 bf16 write)"
+        bytes_per_launch = 4 * 2 * D * B * C * H + 2 * st_bytes  # a, b, c read + out written, 8D B/token-head
+        unit_note = "8*D bytes per token-head (3 bf16 reads + 1 bf16 write) + 2*B*H*D^2*4"
+        overhead = nseg * st_bytes - 2 * st_bytes + (2 * nseg * st_bytes if "prefix" not in stages else 0)
     elif dom_name.startswith("seg_state"):
         bytes_per_launch = 2 * 2 * D * B * C * H          # reads two bf16 tensors: 4D B/token-head
         unit_note = "4*D bytes per token-head (2 bf16 reads)"
+        overhead = nseg * st_bytes
     else:
-        bytes_per_launch = 0
-        unit_note = "n/a"
+        bytes_per_launch, unit_note, overhead = 0, "n/a", 0
     achieved = bytes_per_launch / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else 0.0
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"{args.config}:{dom_name}")
+            ent = json.load(open(tpath)).get(f"{args.config}:{dom_name}")
+            if isinstance(ent, dict):
+                traffic, traffic_src = ent.get("bytes"), {kk: ent.get(kk) for kk in ("report", "git", "note")}
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "kernel": dom_name, "launches_per_step": dom_n / args.steps,
-                "bytes_per_launch": bytes_per_launch, "bytes_rule": unit_note, "peak_source": peak_src}
+                "traffic": traffic, "traffic_source": traffic_src, "kernel": dom_name,
+                "launches_per_step": dom_n / args.steps, "bytes_per_launch": bytes_per_launch,
+                "overhead_bytes_per_launch": overhead, "overhead_frac": (bytes_per_launch + overhead) / max(
+                    per_launch_ms / 1e3, 1e-12) / 1e9 / hbm, "bytes_rule": unit_note, "peak_source": peak_src,
+                "duration_us": per_launch_ms * 1e3}
     path_bytes = 22 * D * B * C * H
     path = {"bytes_per_step": path_bytes, "achieved_gbs": path_bytes / (ms_step / 1e3) / 1e9,
             "frac_of_hbm": path_bytes / (ms_step / 1e3) / 1e9 / hbm,
             "tc_peak_frac": B * C * H * alg_flops_per_token_head(D) / (ms_step / 1e3) / (tflops * 1e12),
             "stages_ms_per_step": {kk: vv[1] / args.steps for kk, vv in stages.items()},
-            "profiled_ms_per_step": prof_ms / args.steps}
+            "profiled_ms_per_step": R["prof_ms"] / args.steps}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not loopback and not args.no_cpu_baseline:
         cpu = cpu_baseline(H, D, C, desc)
 
-    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (synth/, seed 0; bf16 inputs)",
-            "config": {"workload": desc, "global_batch": B * G, "seq_len": C * T, "n_local": C, "heads": H,
-                       "head_dim": D, "lambda": "per-head 1-2^-(1+14h/(H-1))",
-                       "segment_len": lasp.segment_len(N.shape(B, C, H, D, N.LASP_BF16)),
+    ex_report = {ex: {"value": world * B * C * args.steps / (r["total_ms"] / 1e3), "ms_per_step": r["total_ms"] /
+                      args.steps, "parity_max_err": r["parity_err"], "parity_ok": r["parity_err"] <= 2e-2,
+                      "exchange_us_per_step": r["hop_us_per_step"],
+                      "launch": "cuda-graph replay" if r["graph"] else (r["graph_note"] or "eager (PDL)")}
+                 for ex, r in results.items()}
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 1 if loopback else world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (synth/, seed 0; bf16 inputs)",
+            "config": {"workload": desc if not args.tokens else f"{desc} [n_local overridden: {C}]",
+                       "global_batch": B * G, "seq_len": C * T, "n_local": C, "heads": H,
+                       "head_dim": D, "lambda": "per-head 1-2^-(1+14h/(H-1))", "segment_len": seg_len,
                        "l2": "flushed between timed steps (256 MiB read outside the step events); inputs 4x"
                              f" {B * C * H * D * 2 >> 20} MiB", "parallelism": f"dp{G}xsp{T}" if G > 1 else f"sp{T}",
-                       "launch": "cuda-graph replay" if graph is not None else "eager (PDL)",
-                       "exchange": exchange if T > 1 else "none"},
-            "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e, "roofline": roofline,
+                       "launch": ex_report[main_ex]["launch"], "exchange": main_ex},
+            "parity_ok": all(r["parity_ok"] for r in ex_report.values()),
+            "gpu_launches": int(R["launches"]), "clocks": clk_summary, "e2e": e2e, "roofline": roofline,
             "path": path, "cpu_baseline": cpu}
+    if T > 1:
+        line["exchanges"] = ex_report
+    else:
+        line["parity_max_err"] = ex_report[main_ex]["parity_max_err"]
+    if loopback:
+        line["loopback"] = {"ranks": world, "note": "all ranks are threads sharing ONE GPU (in-process transport): "
+                            "checks the N>1 code path and its parity; value is not a scaling number"}
+    return line
+
+
+def run_lasp(args):
+    import torch
+    import torch.distributed as dist
+
+    if args.loopback > 1:
+        import paper_2404_02882_b200 as lasp
+        world = args.loopback
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        comm = ThreadComm(world)
+        out, errs = [None] * world, []
+
+        def worker(r):
+            try:
+                torch.cuda.set_device(0)
+                s = torch.cuda.Stream(dev)
+                with torch.cuda.stream(s):
+                    out[r] = rank_bench(args, r, world, dev, comm,
+                                        lambda: lasp.Ring.loopback(r, world, f"bench-{os.getpid()}"), loopback=True)
+            except BaseException as e:  # noqa: BLE001
+                errs.append(e)
+                comm._bar.abort()
+
+        ts = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if errs:
+            raise errs[0]
+        print(json.dumps(out[0]), flush=True)
+        return 0
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2404_02882_b200 as lasp
+    T = args.sp_size or world
+    group = None
+    if 1 < T < world:
+        group = lasp.sp_group(T)
+    line = rank_bench(args, rank, world, dev, TorchComm(world, dev), lambda: lasp.Ring(dev, group=group))
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if ring is not None:
-        ring.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -438,9 +640,13 @@ def main():
     ap.add_argument("--sp-size", type=int, default=0,
                     help="sequence-parallel size T (default: all ranks in one ring); G = N/T data-parallel groups "
                          "(Alg. 1 data-sequence hybrid, NEXT-1)")
-    ap.add_argument("--exchange", choices=["auto", "ring", "allgather"], default="auto",
-                    help="state exchange at N > 1: the paper's ring, one all-gather (NEXT-2), or auto (ring for "
-                         "T <= 2, all-gather for T >= 3; default)")
+    ap.add_argument("--exchange", choices=["both", "ring", "allgather"], default="both",
+                    help="state exchange at N > 1: the paper's ring, one all-gather (NEXT-2), or both (default: each "
+                         "timed in the same run; `value` is the ring's, both are reported under `exchanges`)")
+    ap.add_argument("--loopback", type=int, default=0,
+                    help="run N ranks as threads on ONE GPU with the in-process loopback transport (the whole N>1 "
+                         "code path incl. the closed-form parity gate; not a scaling measurement)")
+    ap.add_argument("--tokens", type=int, default=0, help="override n_local (tokens per GPU) of --config")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -41,19 +41,16 @@
  *              lambda, heads are independent, P:18 -- reading A7). lambda = 1 is plain linear
  *              attention.
  *   Streams  : all device work is enqueued on the caller's stream; calls return after enqueue.
- *              Kernels use programmatic dependent launch: a kernel may start while the preceding
- *              kernel on the stream is still running; it reads the call's input tensors right away
- *              (they must be complete when the previous kernel STARTED) and writes nothing before
- *              the preceding kernel has completed. Kernels that do not trigger early (any non-PDL
- *              kernel, cudaMemcpy, events) are complete when the next kernel starts, so the only
- *              restriction is: the input tensors of a call must not be outputs of the immediately
- *              preceding LASP call on the same stream (put any other operation in between).
+ *              The first kernel of every call is an ordinary launch (it starts once all earlier work
+ *              on the stream has completed, whatever produced the inputs); the call's later kernels
+ *              use programmatic dependent launch among themselves only.
  *   Graphs   : lasp_fwd_local / lasp_bwd_local and the NCCL entry points can be captured into CUDA
  *              graphs (the programmatic launch edges are kept; bench.py replays its step from a
  *              graph). Contexts made by lasp_ctx_create_loopback use host threads and cannot.
  *   Errors   : argument validation is synchronous and enqueues nothing. On a non-OK status
  *              lasp_last_error() returns a thread-local message. LASP_ERR_CUDA / LASP_ERR_COMM
- *              report launch / NCCL failures (with rank and peer for COMM).
+ *              report launch / NCCL failures (with rank and peer for COMM). The KV-cache check
+ *              (LASP_ERR_STATE) runs on the device, see lasp_workspace_status.
  *   Sizes    : n_local may be any value >= 0 (a ragged last GPU block is zero-padded on load and
  *              clipped on store); n_local = 0 is a no-op that forwards the state (kv_out = kv_in).
  *              head_dim must be 32, 64 or 128 (else LASP_ERR_UNSUPPORTED).
@@ -117,9 +114,21 @@ void lasp_profile_enable(int on);
 void lasp_debug_trace(unsigned long long* device_buf);
 int lasp_profile_read(char* buf, size_t cap);
 
-/* Bytes of the caller-owned per-layer KV cache for `shape` (fp32 segment states: the state entering
- * the rank, KV_in(r), and the states entering each in-rank segment). 256-byte aligned base required. */
+/* Bytes of the caller-owned per-layer KV cache for `shape`: fp32 segment states [B][H][nseg][D][D] (entry
+ * 0 = the state entering the rank, KV_in(r), reading A4; entry p = the state entering in-rank segment p),
+ * followed by a 256-byte tag (shape, segment length, dtype, lambda hash, rank, world, generation) that
+ * lasp_fwd* writes and lasp_bwd* checks on the device. 16-byte aligned base. */
 size_t lasp_cache_bytes(const lasp_shape_t* shape);
+
+/* Result of the cache-tag check of the last lasp_bwd / lasp_bwd_local call that used `workspace` on
+ * `stream` (synchronizes the stream). LASP_OK, or LASP_ERR_STATE when the cache was not written by a
+ * lasp_fwd* call with the same shape, lambda and (ring calls) rank and world -- a buffer never written by
+ * a forward, a freed-and-reused allocation now holding another forward's cache, a different lambda, ...
+ * lasp_last_error() then names the mismatching fields. A backward whose check fails still runs, but every
+ * state it loads is NaN, so dq, dk, dv (and dkv_out) are NaN: the mismatch cannot go unnoticed. (The
+ * check is on the device so that calls stay asynchronous and capturable into CUDA graphs, and no host
+ * registry keyed by pointers can be fooled by address reuse.) */
+lasp_status_t lasp_workspace_status(const void* workspace, void* stream /* cudaStream_t */);
 
 /* Bytes of the caller-owned scratch workspace used by lasp_fwd, lasp_fwd_local, lasp_bwd and lasp_bwd_local (reusable across
  * calls on the same stream; contents are not preserved). */
@@ -139,7 +148,8 @@ lasp_status_t lasp_fwd_local(const lasp_shape_t* shape, const void* q, const voi
 
 /* Alg. 3 for one rank. dkv_in: dKV_in(r) from rank r+1 (NULL = zero, last rank).
  * dkv_out (nullable): lambda^C dKV_in + (Lambda Q)^T dO. `cache` must come from lasp_fwd_local or
- * lasp_fwd with the same shape, lambda and (rank, world); otherwise LASP_ERR_STATE. */
+ * lasp_fwd with the same shape and lambda; otherwise the outputs are NaN and lasp_workspace_status()
+ * returns LASP_ERR_STATE. */
 lasp_status_t lasp_bwd_local(const lasp_shape_t* shape, const void* q, const void* k, const void* v,
                              const float* lambda, const void* d_o, const void* cache,
                              const float* dkv_in, void* dq, void* dk, void* dv, float* dkv_out,
@@ -169,7 +179,8 @@ lasp_status_t lasp_ctx_create_loopback(int rank, int world, const char* group, i
  *   LASP_EXCHANGE_ALLGATHER: one all-gather of the T local states (B*H*D*D fp32 each; ncclAllGather, or
  *     pairwise sends on a loopback ctx) into a ctx-owned buffer, then each rank folds the states it would
  *     have received: KV_in(r) = sum_{j<r} lam^(C(r-1-j)) L_j, dKV_in(r) = sum_{j>r} lam^(C(j-r-1)) G_j.
- *     Same results up to fp32 summation order; assumes every rank has the same n_local (Alg. 1: C = N/T).
+ *     Same results up to fp32 summation order. Each rank's n_local travels with its state, so ranks of
+ *     different lengths fold correctly (rank j's contribution is decayed with lam^(C_j)).
  * LASP_ERR_DOMAIN for any other value. */
 #define LASP_EXCHANGE_RING 0
 #define LASP_EXCHANGE_ALLGATHER 1
@@ -201,7 +212,8 @@ lasp_status_t lasp_fwd(lasp_ctx_t ctx, const lasp_shape_t* shape, const void* q,
                        const void* v, const float* lambda, void* o, void* cache, void* workspace,
                        void* stream);
 
-/* Alg. 3 across the ring: receives dKV_in(r) from r+1, sends dKV_out(r) to r-1, writes dQ, dK, dV. */
+/* Alg. 3 across the ring: receives dKV_in(r) from r+1, sends dKV_out(r) to r-1, writes dQ, dK, dV.
+ * The cache's tag must match (shape, lambda, rank, world), else NaN outputs + lasp_workspace_status. */
 lasp_status_t lasp_bwd(lasp_ctx_t ctx, const lasp_shape_t* shape, const void* q, const void* k,
                        const void* v, const float* lambda, const void* d_o, const void* cache,
                        void* dq, void* dk, void* dv, void* workspace, void* stream);

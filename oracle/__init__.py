@@ -238,6 +238,8 @@ def normwise_err(x, ref):
     """max|x - ref| / max|ref| per tensor (reading A14)."""
     x = np.asarray(x, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
+    if x.shape != ref.shape:
+        raise ValueError(f"normwise_err: shape {x.shape} vs reference {ref.shape}")
     den = np.max(np.abs(ref)) if ref.size else 0.0
     num = np.max(np.abs(x - ref)) if ref.size else 0.0
     return float(num / den) if den > 0 else float(num)

@@ -4,7 +4,8 @@ C ABI in include/lasp.h); this package only marshals arguments."""
 from . import _native
 from .api import (LaspAttention, Ring, alloc_cache, alloc_workspace, bwd_local, cache_bytes, fwd_local,
                   lasp_attention, scatter_sequence, segment_len, sp_group, topology,
-                  workspace_bytes)
+                  workspace_bytes, workspace_status)
 
 __all__ = ["LaspAttention", "Ring", "alloc_cache", "alloc_workspace", "bwd_local", "cache_bytes", "fwd_local",
-           "lasp_attention", "scatter_sequence", "segment_len", "sp_group", "topology", "workspace_bytes", "_native"]
+           "lasp_attention", "scatter_sequence", "segment_len", "sp_group", "topology", "workspace_bytes",
+           "workspace_status", "_native"]

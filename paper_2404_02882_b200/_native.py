@@ -45,6 +45,7 @@ _SIGS = {
     "lasp_profile_read": ([ctypes.c_char_p, ctypes.c_size_t], ctypes.c_int),
     "lasp_debug_trace": ([_vp], None),
     "lasp_workspace_bytes": ([_sp], ctypes.c_size_t),
+    "lasp_workspace_status": ([_vp, _vp], ctypes.c_int),
     "lasp_segment_len": ([_sp], ctypes.c_int64),
     "lasp_fwd_local": ([_sp, _vp, _vp, _vp, _fp, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
     "lasp_bwd_local": ([_sp, _vp, _vp, _vp, _fp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
@@ -80,6 +81,15 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                               "(the LASP path has no CPU fallback)")
+        if not os.environ.get("LASP_NCCL_LIB"):
+            # the ring loads NCCL lazily (dlopen): point it at torch's bundled copy, the one torch.distributed uses
+            try:
+                import nvidia.nccl
+                cand = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+                if os.path.exists(cand):
+                    os.environ["LASP_NCCL_LIB"] = cand
+            except ImportError:
+                pass
         L = ctypes.CDLL(LIB_PATH)
         for name, (args, res) in _SIGS.items():
             fn = getattr(L, name)

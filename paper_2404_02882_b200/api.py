@@ -53,6 +53,35 @@ def _check_seq(*ts):
             raise ValueError("sequence tensors must be contiguous CUDA tensors of equal shape and dtype")
 
 
+def _check_state(t, q, name):
+    """kv_in / kv_out / dkv_in / dkv_out: fp32 [B][H][D][D], contiguous, on q's device (include/lasp.h)."""
+    if t is None:
+        return
+    B, _, H, D = q.shape
+    if (not isinstance(t, torch.Tensor) or t.device != q.device or t.dtype != torch.float32
+            or tuple(t.shape) != (B, H, D, D) or not t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous float32 CUDA tensor of shape {(B, H, D, D)} on {q.device}")
+
+
+def _check_like(t, q, name):
+    """Output sequence tensors: same shape, dtype and device as q, contiguous."""
+    if (not isinstance(t, torch.Tensor) or t.device != q.device or t.dtype != q.dtype or t.shape != q.shape
+            or not t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous {q.dtype} tensor of shape {tuple(q.shape)} on {q.device}")
+
+
+def _check_buf(t, nbytes, name, device):
+    if (not isinstance(t, torch.Tensor) or t.device != device or not t.is_contiguous()
+            or t.numel() * t.element_size() < nbytes):
+        raise ValueError(f"{name} must be a contiguous tensor of at least {nbytes} bytes on {device}")
+
+
+def workspace_status(workspace: torch.Tensor) -> None:
+    """Raise LaspError(LASP_ERR_STATE) if the last backward on ``workspace`` found a cache whose tag does not
+    match (synchronizes the current stream; include/lasp.h lasp_workspace_status)."""
+    N.check(N.lib().lasp_workspace_status(_p(workspace), _stream(workspace.device)))
+
+
 def cache_bytes(shape: N.lasp_shape_t) -> int:
     return int(N.lib().lasp_cache_bytes(ctypes.byref(shape)))
 
@@ -87,14 +116,21 @@ def fwd_local(q, k, v, lam, kv_in=None, *, o=None, kv_out=True, cache=None, work
     kv_out_t = _state_like(q) if kv_out is True else (kv_out if isinstance(kv_out, torch.Tensor) else None)
     cache = alloc_cache(q) if cache is None else cache
     workspace = alloc_workspace(q) if workspace is None else workspace
+    _check_like(o, q, "o")
+    _check_state(kv_in, q, "kv_in")
+    _check_state(kv_out_t, q, "kv_out")
+    _check_buf(cache, cache_bytes(s), "cache", q.device)
+    _check_buf(workspace, workspace_bytes(s), "workspace", q.device)
     _, lp = _lam(lam, s.heads)
     N.check(N.lib().lasp_fwd_local(ctypes.byref(s), _p(q), _p(k), _p(v), lp, _p(kv_in), _p(o), _p(kv_out_t),
                                    _p(cache), _p(workspace), _stream(q.device)))
     return o, kv_out_t, cache
 
 
-def bwd_local(q, k, v, lam, do, cache, dkv_in=None, *, dq=None, dk=None, dv=None, dkv_out=True, workspace=None):
-    """Alg. 3 for one rank -> (dq, dk, dv, dkv_out or None)."""
+def bwd_local(q, k, v, lam, do, cache, dkv_in=None, *, dq=None, dk=None, dv=None, dkv_out=True, workspace=None,
+              check_state=False):
+    """Alg. 3 for one rank -> (dq, dk, dv, dkv_out or None). ``check_state``: synchronize and raise
+    LaspError(LASP_ERR_STATE) if the cache's tag did not match (else a mismatch shows as NaN outputs)."""
     _check_seq(q, k, v, do)
     s = _shape(q)
     dq = torch.empty_like(q) if dq is None else dq
@@ -102,9 +138,17 @@ def bwd_local(q, k, v, lam, do, cache, dkv_in=None, *, dq=None, dk=None, dv=None
     dv = torch.empty_like(q) if dv is None else dv
     dkv_out_t = _state_like(q) if dkv_out is True else (dkv_out if isinstance(dkv_out, torch.Tensor) else None)
     workspace = alloc_workspace(q) if workspace is None else workspace
+    for t, n in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
+        _check_like(t, q, n)
+    _check_state(dkv_in, q, "dkv_in")
+    _check_state(dkv_out_t, q, "dkv_out")
+    _check_buf(cache, cache_bytes(s), "cache", q.device)
+    _check_buf(workspace, workspace_bytes(s), "workspace", q.device)
     _, lp = _lam(lam, s.heads)
     N.check(N.lib().lasp_bwd_local(ctypes.byref(s), _p(q), _p(k), _p(v), lp, _p(do), _p(cache), _p(dkv_in),
                                    _p(dq), _p(dk), _p(dv), _p(dkv_out_t), _p(workspace), _stream(q.device)))
+    if check_state:
+        workspace_status(workspace)
     return dq, dk, dv, dkv_out_t
 
 
@@ -218,21 +262,30 @@ class Ring:
         o = torch.empty_like(q) if o is None else o
         cache = alloc_cache(q) if cache is None else cache
         workspace = alloc_workspace(q) if workspace is None else workspace
+        _check_like(o, q, "o")
+        _check_buf(cache, cache_bytes(s), "cache", q.device)
+        _check_buf(workspace, workspace_bytes(s), "workspace", q.device)
         _, lp = _lam(lam, s.heads)
         N.check(N.lib().lasp_fwd(self._ctx, ctypes.byref(s), _p(q), _p(k), _p(v), lp, _p(o), _p(cache),
                                  _p(workspace), _stream(q.device)))
         return o, cache
 
-    def bwd(self, q, k, v, lam, do, cache, *, dq=None, dk=None, dv=None, workspace=None):
+    def bwd(self, q, k, v, lam, do, cache, *, dq=None, dk=None, dv=None, workspace=None, check_state=False):
         _check_seq(q, k, v, do)
         s = _shape(q)
         dq = torch.empty_like(q) if dq is None else dq
         dk = torch.empty_like(q) if dk is None else dk
         dv = torch.empty_like(q) if dv is None else dv
         workspace = alloc_workspace(q) if workspace is None else workspace
+        for t, n in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
+            _check_like(t, q, n)
+        _check_buf(cache, cache_bytes(s), "cache", q.device)
+        _check_buf(workspace, workspace_bytes(s), "workspace", q.device)
         _, lp = _lam(lam, s.heads)
         N.check(N.lib().lasp_bwd(self._ctx, ctypes.byref(s), _p(q), _p(k), _p(v), lp, _p(do), _p(cache), _p(dq),
                                  _p(dk), _p(dv), _p(workspace), _stream(q.device)))
+        if check_state:
+            workspace_status(workspace)
         return dq, dk, dv
 
 

@@ -170,9 +170,10 @@ __global__ void __launch_bounds__(kThreads) core_simt_kernel(Plan p, SeqArgs a) 
   const int tid = threadIdx.x;
   for (int k = tid; k <= BT; k += kThreads) pw[k] = powk(lam, double(k));
   const float* st0 = a.state + ((b * p.H + h) * p.nseg + seg) * D * D;
+  const float poison = tag_poisoned(a.status) ? __int_as_float(0x7fc00000) : 0.f;  // cache tag mismatch: NaN
   for (int idx = tid; idx < D * D; idx += kThreads) {
     const int d = idx / D, e = idx % D;
-    S[d * (D + 1) + e] = a.trans_state ? st0[e * D + d] : st0[idx];
+    S[d * (D + 1) + e] = (a.trans_state ? st0[e * D + d] : st0[idx]) + poison;
   }
   const T* ga = static_cast<const T*>(a.a);
   const T* gb = static_cast<const T*>(a.b);
@@ -306,7 +307,9 @@ cudaError_t launch_prefix(const Plan& p, Dir dir, const float* init, const float
 // j0, j0 + step, ... (count of them) in that order: cur = lam^C cur + g[j], starting from 0. Forward:
 // KV_in(r) = sum_{j<r} lam^(C (r-1-j)) L_j (j0 = 0, step +1, count r); backward: dKV_in(r) =
 // sum_{j>r} lam^(C (j-r-1)) G_j (j0 = T-1, step -1, count T-1-r). Same decay as combine_kernel.
-__global__ void fold_ranks_kernel(Plan p, const float* __restrict__ g, int j0, int step, int count,
+// Each rank's n_local travels with its state (ranks may hold different lengths, reading R3): folding rank j
+// in is cur = lam^(C_j) cur + g_j, the combine step rank j itself would have applied (Alg. 2).
+__global__ void fold_ranks_kernel(Plan p, const float* __restrict__ g, int64_t stride, int j0, int step, int count,
                                   float* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
@@ -314,18 +317,56 @@ __global__ void fold_ranks_kernel(Plan p, const float* __restrict__ g, int j0, i
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= n) return;
   const int64_t h = (idx / (p.D * p.D)) % p.H;
-  const float dec = powk(p.lam[h], double(p.C));
   float cur = 0.f;
-  for (int t = 0; t < count; ++t) cur = fmaf(dec, cur, g[int64_t(j0 + t * step) * n + idx]);
+  for (int t = 0; t < count; ++t) {
+    const float* gj = g + int64_t(j0 + t * step) * stride;
+    const int64_t Cj = *reinterpret_cast<const int64_t*>(gj + n);
+    cur = fmaf(powk(p.lam[h], double(Cj)), cur, gj[idx]);
+  }
   out[idx] = cur;
 }
 
-cudaError_t launch_fold_ranks(const Plan& p, const float* gathered, int j0, int step, int count, float* out,
-                              cudaStream_t st) {
+cudaError_t launch_fold_ranks(const Plan& p, const float* gathered, int64_t stride, int j0, int step, int count,
+                              float* out, cudaStream_t st) {
   const int64_t n = p.B * p.H * p.D * p.D;
   const int threads = 256;
   return launch_k(fold_ranks_kernel, dim3((unsigned)((n + threads - 1) / threads)), dim3(threads), 0, st, p, gathered,
-                  j0, step, count, out);
+                  stride, j0, step, count, out);
+}
+
+// all-gather message of one rank: its state (n floats) followed by its n_local as an int64
+__global__ void pack_state_kernel(int64_t n, int64_t C, const float* __restrict__ src, float* __restrict__ dst) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx < n) dst[idx] = src[idx];
+  if (idx == 0) *reinterpret_cast<int64_t*>(dst + n) = C;
+}
+
+cudaError_t launch_pack_state(const Plan& p, const float* src, float* dst, cudaStream_t st) {
+  const int64_t n = p.B * p.H * p.D * p.D;
+  const int threads = 256;
+  return launch_k(pack_state_kernel, dim3((unsigned)((n + threads - 1) / threads)), dim3(threads), 0, st, n, p.C, src,
+                  dst);
+}
+
+// Entry kernel of every call (launched without the programmatic attribute): writes (forward) or checks
+// (backward) the cache tag, then lets the call's next kernel start.
+__global__ void tag_kernel(CacheTag t, uint64_t* __restrict__ hdr, unsigned check_mask, unsigned* __restrict__ status) {
+  pdl_trigger();
+  const int i = threadIdx.x;
+  if (check_mask == 0u) {
+    if (i < kTagWords) hdr[i] = t.w[i];
+    if (i == 0 && status) *status = 0u;
+    return;
+  }
+  const bool bad = i < kTagWords && ((check_mask >> i) & 1u) && hdr[i] != t.w[i];
+  const unsigned bits = __ballot_sync(0xffffffffu, bad);
+  if (i == 0) *status = bits;
+}
+
+cudaError_t launch_tag(const CacheTag& t, uint64_t* hdr, unsigned check_mask, unsigned* status, cudaStream_t st) {
+  return launch_k(tag_kernel, dim3(1), dim3(32), 0, st, t, hdr, check_mask, status);
 }
 
 cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local, float* kv_out, cudaStream_t st) {

@@ -405,6 +405,7 @@ struct CoreParams {
   __nv_bfloat16* outp[3];
   unsigned long long* trace;  // debug timeline (lasp_debug_trace), nullptr in production
   int npass;
+  const unsigned* status;     // cache-tag status of a backward call (nonzero: NaN states), or nullptr
   FastDiv div_per, div_nbh;   // / (B*H*NV*npass), / (B*H*NV) (work-item decode)
   PrefixFold fold;            // fold.gbar != nullptr: compute the prefix states first (fused F2 / B2)
 };
@@ -856,6 +857,10 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         if (prm.fold.gbar == nullptr) load([](auto* ptr) { return __ldg(ptr); });
         else load([](auto* ptr) { return *ptr; });
       }
+      if (tag_poisoned(prm.status)) {  // the call's cache tag did not match: every output becomes NaN
+#pragma unroll
+        for (int e = 0; e < 64; ++e) S[e] = __int_as_float(0x7fc00000);
+      }
     };
     uint32_t J = 0, kd = 0, k = 0;
     for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
@@ -970,10 +975,12 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           for (int u = 0; u < 16; u += 2) pk[c * 8 + u / 2] = pack_bf16(fmaf(r, x[u], a[u]), fmaf(r, x[u + 1], a[u + 1]));
         }
         const int t0 = int(cblock_row(it, j));
-        if (t0 < 0) {
-          // ragged first block of a REV pass (rows before the rank start): TMA stores reject
-          // negative coordinates, so the valid rows are written directly from registers
-          if (t0 + i >= 0) {
+        if (t0 < it.beg) {
+          // ragged block of a REV pass, which starts before its segment: rows before the segment belong
+          // to the previous segment's item (or precede the rank start, where TMA stores reject negative
+          // coordinates), so only this segment's rows are written, directly from registers (ADVICE r1:
+          // a full-tile store raced with the previous segment's store of the same rows)
+          if (t0 + i >= it.beg) {
             uint4* dst = reinterpret_cast<uint4*>(outp + ((it.b * p.C + (t0 + i)) * p.H + it.h) * D + it.v * 64);
 #pragma unroll
             for (int c = 0; c < 8; ++c) dst[c] = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
@@ -1084,6 +1091,7 @@ cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const 
   if (nst < 2) { prm.mst[1] = prm.mst[0]; prm.stp[1] = prm.stp[0]; }
   prm.p = p;
   prm.npass = npass;
+  prm.status = a[0].status;
   prm.trace = g_trace;
   if (fold) prm.fold = *fold;
   prm.div_nbh = FastDiv(uint32_t(p.B * p.H * CoreLayout<D>::NV));

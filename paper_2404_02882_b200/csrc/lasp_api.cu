@@ -121,16 +121,20 @@ size_t seg_state_elems(const Plan& p) { return size_t(p.B * p.H * p.nseg * p.D *
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Workspace {
-  float* seg;     // [B][H][nseg][D][D]
-  float* local;   // [B][H][D][D] local total (ring)
-  float* in;      // received state
-  float* out;     // state to send
-  unsigned* gbar; // grid-barrier counter of the fused prefix fold
+  unsigned* gbar;   // [0..1]: counters of the fused prefix fold; [2]: cache-tag status of the call
+  float* seg;       // [B][H][nseg][D][D]
+  float* local;     // [B][H][D][D] local total (ring)
+  float* in;        // received state
+  float* out;       // state to send
+  unsigned* status() const { return gbar + 2; }
 };
 
+// the 256-byte control block sits at the start, so lasp_workspace_status needs no shape
 Workspace carve(const Plan& p, void* ws) {
   char* c = static_cast<char*>(ws);
   Workspace w;
+  w.gbar = reinterpret_cast<unsigned*>(c);
+  c += 256;
   w.seg = reinterpret_cast<float*>(c);
   c += align256(seg_state_elems(p) * 4);
   w.local = reinterpret_cast<float*>(c);
@@ -138,13 +142,16 @@ Workspace carve(const Plan& p, void* ws) {
   w.in = reinterpret_cast<float*>(c);
   c += align256(state_elems(p) * 4);
   w.out = reinterpret_cast<float*>(c);
-  c += align256(state_elems(p) * 4);
-  w.gbar = reinterpret_cast<unsigned*>(c);
   return w;
 }
 
 size_t workspace_bytes(const Plan& p) {
-  return align256(seg_state_elems(p) * 4) + 3 * align256(state_elems(p) * 4) + 256;
+  return 256 + align256(seg_state_elems(p) * 4) + 3 * align256(state_elems(p) * 4);
+}
+
+size_t cache_bytes(const Plan& p) { return align256(seg_state_elems(p) * 4) + kCacheTagBytes; }
+uint64_t* cache_tag_ptr(const Plan& p, const void* cache) {
+  return reinterpret_cast<uint64_t*>(static_cast<char*>(const_cast<void*>(cache)) + align256(seg_state_elems(p) * 4));
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
@@ -185,13 +192,10 @@ lasp_status_t check_device() {
   return LASP_OK;
 }
 
-// ---- KV-cache tag registry (backward before/without a matching forward -> STATE) -------
-struct CacheTag {
-  int64_t B, C, H, D, seg_len;
-  int dtype, rank, world;
-  uint64_t lam_hash;
-};
-
+// ---- KV-cache tag (backward before/without a matching forward -> STATE) ---------------------
+// The tag lives in the cache (after the segment states): the forward's entry kernel writes it, the
+// backward's entry kernel compares it on the device (no host-side registry: a reused or foreign buffer is
+// judged by its contents) and records mismatching words in the call's status word.
 uint64_t hash_lam(const Plan& p) {
   uint64_t h = 1469598103934665603ull;
   for (int64_t i = 0; i < p.H; ++i) {
@@ -202,25 +206,26 @@ uint64_t hash_lam(const Plan& p) {
   return h;
 }
 
-std::mutex g_tag_mu;
-std::unordered_map<const void*, CacheTag> g_tags;
+std::atomic<uint64_t> g_generation{0};
 
-void register_cache(const Plan& p, const void* cache, int rank, int world) {
-  std::lock_guard<std::mutex> g(g_tag_mu);
-  g_tags[cache] = CacheTag{p.B, p.C, p.H, p.D, p.seg_len, p.dtype, rank, world, hash_lam(p)};
+CacheTag make_tag(const Plan& p, int rank, int world) {
+  CacheTag t{};
+  t.w[kTagMagic] = kTagMagicValue;
+  t.w[kTagB] = uint64_t(p.B); t.w[kTagC] = uint64_t(p.C); t.w[kTagH] = uint64_t(p.H); t.w[kTagD] = uint64_t(p.D);
+  t.w[kTagSeg] = uint64_t(p.seg_len);
+  t.w[kTagDtype] = uint64_t(p.dtype);
+  t.w[kTagLam] = hash_lam(p);
+  t.w[kTagRank] = uint64_t(int64_t(rank));
+  t.w[kTagWorld] = uint64_t(int64_t(world));
+  t.w[kTagGen] = ++g_generation;  // diagnostics only (not compared)
+  return t;
 }
 
-lasp_status_t check_cache(const Plan& p, const void* cache, int rank, int world, bool check_rank) {
-  std::lock_guard<std::mutex> g(g_tag_mu);
-  auto it = g_tags.find(cache);
-  if (it == g_tags.end()) return fail(LASP_ERR_STATE, "cache was not written by lasp_fwd/lasp_fwd_local");
-  const CacheTag& t = it->second;
-  if (t.B != p.B || t.C != p.C || t.H != p.H || t.D != p.D || t.seg_len != p.seg_len || t.dtype != p.dtype)
-    return fail(LASP_ERR_STATE, "cache shape does not match the backward call");
-  if (t.lam_hash != hash_lam(p)) return fail(LASP_ERR_STATE, "cache lambda does not match the backward call");
-  if (check_rank && (t.rank != rank || t.world != world))
-    return fail(LASP_ERR_STATE, "cache (rank, world) does not match the ring context");
-  return LASP_OK;
+unsigned tag_mask(bool check_rank) {
+  unsigned m = 0;
+  for (int i = kTagMagic; i <= kTagLam; ++i) m |= 1u << i;
+  if (check_rank) m |= (1u << kTagRank) | (1u << kTagWorld);
+  return m;
 }
 
 // ---- launch accounting and optional per-stage CUDA-event profiling -----------------------------
@@ -258,6 +263,36 @@ cudaError_t staged(const char* name, cudaStream_t st, F&& launch) {
   return e;
 }
 
+// entry kernel of a call: write (forward) or check (backward) the cache tag; launched without the
+// programmatic attribute, so the call's later kernels (PDL) only ever overlap kernels of the same call
+cudaError_t entry_tag(const Plan& p, const void* cache, const Workspace& w, int rank, int world, bool check,
+                      bool check_rank, cudaStream_t st) {
+  const CacheTag t = make_tag(p, rank, world);
+  return staged(check ? "tag_check" : "tag_write", st, [&] {
+    g_entry_launch = true;
+    return launch_tag(t, cache_tag_ptr(p, cache), check ? tag_mask(check_rank) : 0u, w.status(), st);
+  });
+}
+
+// a profiled span that is not one launch (the ring hop / state exchange: receive ... send on one stream,
+// including the wait for the upstream rank): events recorded only while profiling is enabled
+struct ProfSpan {
+  ProfRec rec{nullptr, nullptr, nullptr};
+  ProfSpan(const char* name, cudaStream_t st) {
+    if (g_profile.load(std::memory_order_relaxed) == 0) return;
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    rec = ProfRec{name, prof_event(), prof_event()};
+    cudaEventRecord(rec.a, st);
+  }
+  void stop(cudaStream_t st) {
+    if (!rec.a) return;
+    cudaEventRecord(rec.b, st);
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_prof_recs.push_back(rec);
+    rec.a = nullptr;
+  }
+};
+
 // ---- stage dispatch: tcgen05 for covered bf16 shapes, CUDA cores otherwise ---------------------
 cudaError_t seg_state(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st,
                       unsigned* gbar_reset = nullptr) {
@@ -280,8 +315,8 @@ bool fused_fold(const Plan& p) {
 }
 
 cudaError_t core(const Plan& p, Dir dir, const void* a, const void* b, const void* c, void* out,
-                 const float* state, int trans, cudaStream_t st) {
-  SeqArgs args{a, b, c, out, state, trans};
+                 const float* state, int trans, cudaStream_t st, const unsigned* status = nullptr) {
+  SeqArgs args{a, b, c, out, state, trans, status};
   const bool tc = tc_supported(p);
   return staged(dir == Dir::FWD ? (tc ? "core_fwd_tc" : "core_fwd_simt") : (tc ? "core_rev_tc" : "core_rev_simt"),
                 st, [&] { return tc ? launch_core_tc(p, dir, args, st) : launch_core_simt(p, dir, args, st); });
@@ -358,8 +393,8 @@ NcclApi& nccl() {
   static NcclApi api;
   static std::once_flag once;
   std::call_once(once, [] {
-    const char* cands[] = {std::getenv("LASP_NCCL_LIB"), "libnccl.so.2",
-                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+    // LASP_NCCL_LIB (the Python binding points it at torch's bundled NCCL), else the loader's search path
+    const char* cands[] = {std::getenv("LASP_NCCL_LIB"), "libnccl.so.2"};
     void* h = nullptr;
     for (const char* c : cands)
       if (c && (h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
@@ -423,7 +458,7 @@ struct lasp_ctx {
   int exchange = LASP_EXCHANGE_RING;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
-  float* gather = nullptr;  // all-gather exchange: [world][B*H*D*D] fp32 (ctx-owned, grown on demand)
+  float* gather = nullptr;  // all-gather exchange: [world + 1][B*H*D*D + 64] fp32 (ctx-owned, grown on demand)
   size_t gather_elems = 0;
 };
 
@@ -477,30 +512,37 @@ lasp_status_t ring_recv(lasp_ctx* c, float* buf, size_t n, int peer, cudaStream_
 // rank would have received over the ring is folded from the gathered ones (fold_ranks_kernel).
 lasp_status_t exchange_allgather(lasp_ctx* c, const Plan& p, const float* local, float* in, bool backward,
                                  cudaStream_t st) {
+  // each rank contributes [state (n floats) | its n_local (int64) | pad] so that ranks of different lengths
+  // fold correctly (fold_ranks_kernel decays rank j's contribution with its own lam^(C_j))
   const size_t n = size_t(p.B * p.H * p.D * p.D);
-  if (c->gather_elems < n * size_t(c->world)) {
+  const size_t stride = n + 64;  // 256-byte trailer
+  if (c->gather_elems < stride * size_t(c->world + 1)) {
     if (c->gather) LASP_CUDA(cudaFree(c->gather));
     c->gather = nullptr;
     c->gather_elems = 0;
-    LASP_CUDA(cudaMalloc(&c->gather, n * size_t(c->world) * sizeof(float)));
-    c->gather_elems = n * size_t(c->world);
+    LASP_CUDA(cudaMalloc(&c->gather, stride * size_t(c->world + 1) * sizeof(float)));
+    c->gather_elems = stride * size_t(c->world + 1);
   }
+  float* mine = c->gather + size_t(c->world) * stride;  // send buffer: this rank's state + trailer
+  LASP_CUDA(launch_pack_state(p, local, mine, st));  // state + this rank's n_local
   if (!c->loop) {
     if (!nccl().AllGather) return fail(LASP_ERR_COMM, "libnccl.so.2 lacks ncclAllGather");
-    ncclResult_t r = nccl().AllGather(local, c->gather, n, ncclFloat32, c->comm, st);
+    ncclResult_t r = nccl().AllGather(mine, c->gather, stride, ncclFloat32, c->comm, st);
     if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather(state)", c->rank, -1);
   } else {
     lasp_status_t s;
     for (int j = 0; j < c->world; ++j)
-      if (j != c->rank && (s = ring_send(c, local, n, j, st, "allgather send")) != LASP_OK) return s;
+      if (j != c->rank && (s = ring_send(c, mine, stride, j, st, "allgather send")) != LASP_OK) return s;
     for (int j = 0; j < c->world; ++j)
-      if (j != c->rank && (s = ring_recv(c, c->gather + size_t(j) * n, n, j, st, "allgather recv")) != LASP_OK) return s;
-    LASP_CUDA(cudaMemcpyAsync(c->gather + size_t(c->rank) * n, local, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+      if (j != c->rank && (s = ring_recv(c, c->gather + size_t(j) * stride, stride, j, st, "allgather recv")) != LASP_OK)
+        return s;
+    LASP_CUDA(cudaMemcpyAsync(c->gather + size_t(c->rank) * stride, mine, stride * sizeof(float),
+                              cudaMemcpyDeviceToDevice, st));
   }
   const int j0 = backward ? c->world - 1 : 0, step = backward ? -1 : 1;
   const int count = backward ? c->world - 1 - c->rank : c->rank;
-  return launch_fold_ranks(p, c->gather, j0, step, count, in, st) == cudaSuccess ? LASP_OK
-                                                                                 : cuda_fail(cudaGetLastError(), "fold_ranks");
+  return launch_fold_ranks(p, c->gather, int64_t(stride), j0, step, count, in, st) == cudaSuccess
+             ? LASP_OK : cuda_fail(cudaGetLastError(), "fold_ranks");
 }
 
 }  // namespace
@@ -548,8 +590,21 @@ const char* lasp_version(void) { return "lasp-b200 0.1 (sm_100a; tcgen05 + CUDA-
 
 size_t lasp_cache_bytes(const lasp_shape_t* shape) {
   if (validate_shape(shape) != LASP_OK) return 0;
-  const Plan p = make_plan(shape);
-  return seg_state_elems(p) * sizeof(float);
+  return cache_bytes(make_plan(shape));
+}
+
+lasp_status_t lasp_workspace_status(const void* workspace, void* stream) {
+  if (!workspace || !aligned16(workspace)) return fail(LASP_ERR_SHAPE, "workspace NULL or not 16-byte aligned");
+  unsigned bits = 0;
+  LASP_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  LASP_CUDA(cudaMemcpy(&bits, static_cast<const unsigned*>(workspace) + 2, sizeof bits, cudaMemcpyDeviceToHost));
+  if (bits == 0) return LASP_OK;
+  static const char* names[kTagWords] = {"magic (not a cache written by lasp_fwd*)", "batch", "n_local", "heads",
+                                         "head_dim", "segment length", "dtype", "lambda", "rank", "world"};
+  std::string msg = "cache tag mismatch (backward without a matching forward, S:411):";
+  for (int i = 0; i < kTagWords; ++i)
+    if ((bits >> i) & 1u) msg += std::string(" ") + (names[i] ? names[i] : "?");
+  return fail(LASP_ERR_STATE, msg);
 }
 
 size_t lasp_workspace_bytes(const lasp_shape_t* shape) {
@@ -573,9 +628,9 @@ lasp_status_t lasp_fwd_local(const lasp_shape_t* shape, const void* q, const voi
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Workspace w = carve(p, workspace);
   unsigned* gbar = p.C > 0 && fused_fold(p) ? w.gbar : nullptr;
+  LASP_CUDA(entry_tag(p, cache, w, -1, -1, false, false, st));                            // cache tag
   if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, gbar));                  // F1
   if ((s = fwd_tail(p, q, k, v, kv_in, o, kv_out, cache, w.seg, gbar, st)) != LASP_OK) return s;  // F2 + F3
-  register_cache(p, cache, -1, -1);
   return LASP_OK;
 }
 
@@ -586,11 +641,11 @@ lasp_status_t lasp_bwd_local(const lasp_shape_t* shape, const void* q, const voi
   lasp_status_t s = prologue(shape, lambda, p);
   if (s != LASP_OK) return s;
   if ((s = check_ptrs(p, {q, k, v, d_o, dq, dk, dv}, cache, workspace)) != LASP_OK) return s;
-  if ((s = check_cache(p, cache, -1, -1, false)) != LASP_OK) return s;
   if ((s = check_device()) != LASP_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Workspace w = carve(p, workspace);
   const float* P = static_cast<const float*>(cache);
+  LASP_CUDA(entry_tag(p, cache, w, -1, -1, true, false, st));                             // cache tag check
   if (p.C == 0) {
     LASP_CUDA(prefix(p, Dir::REV, dkv_in, nullptr, nullptr, dkv_out, st));
     return LASP_OK;
@@ -600,7 +655,8 @@ lasp_status_t lasp_bwd_local(const lasp_shape_t* shape, const void* q, const voi
   const PrefixFold fold{dkv_in, w.seg, w.seg, dkv_out, w.gbar, int(Dir::REV)};
   if (!fuse) LASP_CUDA(prefix(p, Dir::REV, dkv_in, w.seg, w.seg, dkv_out, st));         // B2 (in place)
   // B3: dQ (needs only the cache), dV and dK in one launch (with B2 folded in when fused)
-  const SeqArgs passes[3] = {{d_o, v, k, dq, P, 1}, {k, q, d_o, dv, w.seg, 0}, {v, d_o, q, dk, w.seg, 1}};
+  const SeqArgs passes[3] = {{d_o, v, k, dq, P, 1, w.status()}, {k, q, d_o, dv, w.seg, 0, w.status()},
+                             {v, d_o, q, dk, w.seg, 1, w.status()}};
   const Dir dirs[3] = {Dir::FWD, Dir::REV, Dir::REV};
   LASP_CUDA(core_multi(p, 3, passes, dirs, st, fuse ? &fold : nullptr));
   return LASP_OK;
@@ -732,15 +788,18 @@ lasp_status_t lasp_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   int from = -1, to = -1;
   lasp_ring_peers(c->rank, c->world, 0, &from, &to);
   unsigned* gbar = p.C > 0 && fused_fold(p) ? w.gbar : nullptr;
+  LASP_CUDA(entry_tag(p, cache, w, c->rank, c->world, false, false, st));              // cache tag
   if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, gbar));               // F1
   LASP_CUDA(prefix(p, Dir::FWD, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
   if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
+    ProfSpan hop("exchange_fwd", st);
     if ((s = exchange_allgather(c, p, w.local, w.in, false, st)) != LASP_OK) return s;
+    hop.stop(st);
     if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, gbar, st)) != LASP_OK) return s;  // F2 + F3
-    register_cache(p, cache, c->rank, c->world);
     return LASP_OK;
   }
   // F2 ring hop: Recv KV_in from r-1 (Alg. 2), combine, Send to r+1
+  ProfSpan hop("exchange_fwd", st);
   if (from >= 0) {
     if ((s = ring_recv(c, w.in, n, from, st, "ncclRecv(KV)")) != LASP_OK) return s;
   } else {
@@ -750,8 +809,8 @@ lasp_status_t lasp_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
     LASP_CUDA(combine(p, w.in, w.local, w.out, st));
     if ((s = ring_send(c, w.out, n, to, st, "ncclSend(KV)")) != LASP_OK) return s;
   }
+  hop.stop(st);
   if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, gbar, st)) != LASP_OK) return s;  // F2 + F3
-  register_cache(p, cache, c->rank, c->world);
   return LASP_OK;
 }
 
@@ -763,18 +822,19 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   lasp_status_t s = prologue(shape, lambda, p);
   if (s != LASP_OK) return s;
   if ((s = check_ptrs(p, {q, k, v, d_o, dq, dk, dv}, cache, workspace)) != LASP_OK) return s;
-  if ((s = check_cache(p, cache, c->rank, c->world, true)) != LASP_OK) return s;
   if ((s = check_device()) != LASP_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Workspace w = carve(p, workspace);
   const size_t n = state_elems(p);
   const float* P = static_cast<const float*>(cache);
   const bool fuse = p.C > 0 && fused_fold(p);
+  LASP_CUDA(entry_tag(p, cache, w, c->rank, c->world, true, true, st));                 // cache tag check
   if (p.C > 0) LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, fuse ? w.gbar : nullptr));  // B1
   LASP_CUDA(prefix(p, Dir::REV, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
   // B2 ring hop on the comm stream: Recv dKV_in from r+1 (Alg. 3), combine, Send to r-1
   LASP_CUDA(cudaEventRecord(c->ev_ready, st));
   LASP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+  ProfSpan hop("exchange_bwd", c->comm_stream);
   int from = -1, to = -1;
   lasp_ring_peers(c->rank, c->world, 1, &from, &to);
   if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
@@ -788,14 +848,15 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
     LASP_CUDA(combine(p, w.in, w.local, w.out, c->comm_stream));
     if ((s = ring_send(c, w.out, n, to, c->comm_stream, "ncclSend(dKV)")) != LASP_OK) return s;
   }
+  hop.stop(c->comm_stream);
   LASP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
   // dQ needs only the cache: it runs while the dKV hop is in flight
-  if (p.C > 0) LASP_CUDA(core(p, Dir::FWD, d_o, v, k, dq, P, 1, st));
+  if (p.C > 0) LASP_CUDA(core(p, Dir::FWD, d_o, v, k, dq, P, 1, st, w.status()));
   LASP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
   if (p.C == 0) return LASP_OK;
   if (!fuse) LASP_CUDA(prefix(p, Dir::REV, w.in, w.seg, w.seg, nullptr, st));   // B2
   {  // dV and dK in one launch (with B2 folded in when fused)
-    const SeqArgs passes[2] = {{k, q, d_o, dv, w.seg, 0}, {v, d_o, q, dk, w.seg, 1}};
+    const SeqArgs passes[2] = {{k, q, d_o, dv, w.seg, 0, w.status()}, {v, d_o, q, dk, w.seg, 1, w.status()}};
     const Dir dirs[2] = {Dir::REV, Dir::REV};
     const PrefixFold fold{w.in, w.seg, w.seg, nullptr, w.gbar, int(Dir::REV)};
     LASP_CUDA(core_multi(p, 2, passes, dirs, st, fuse ? &fold : nullptr));

@@ -35,8 +35,16 @@ inline bool pdl_enabled() {
   return on;
 }
 
+// The first kernel of every entry point is launched WITHOUT the programmatic attribute (it starts once
+// everything before it on the stream has completed, whoever produced the call's inputs), so the PDL edges
+// are only ever between kernels of one call, where the library controls both sides. Set by
+// the entry points, consumed by the next launch on this thread.
+inline thread_local bool g_entry_launch = false;
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  const bool entry = g_entry_launch;
+  g_entry_launch = false;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -46,7 +54,7 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = pdl_enabled() && !entry ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -98,6 +106,21 @@ __host__ __device__ inline int64_t seg_end(Dir, int64_t p, int64_t L, int64_t C)
   return e > C ? C : e;
 }
 
+// KV-cache tag (SURVEY §8(b) "cache header"; S:411 backward without a matching forward -> STATE): 16
+// words stored in the cache itself, after the segment states. The forward's entry kernel writes it; the
+// backward's entry kernel compares the words selected by a mask and writes the mismatch bits into the
+// call's status word (workspace). A backward whose status is nonzero poisons every state it loads with
+// NaN, so all its outputs are NaN (loud), and lasp_workspace_status() reports LASP_ERR_STATE.
+enum TagWord { kTagMagic = 0, kTagB, kTagC, kTagH, kTagD, kTagSeg, kTagDtype, kTagLam, kTagRank, kTagWorld,
+               kTagGen, kTagWords = 16 };
+struct CacheTag { uint64_t w[kTagWords]; };
+constexpr size_t kCacheTagBytes = 256;
+constexpr uint64_t kTagMagicValue = 0x4c41535043414348ull;  // "LASPCACH"
+// check_mask == 0: write the tag (and clear *status); else compare the masked words into *status
+cudaError_t launch_tag(const CacheTag& t, uint64_t* hdr, unsigned check_mask, unsigned* status, cudaStream_t st);
+// true (on the device) when the call's entry kernel found a mismatching cache tag
+__device__ __forceinline__ bool tag_poisoned(const unsigned* status) { return status != nullptr && __ldcg(status) != 0u; }
+
 // Kernel launch interfaces (kernels_simt.cu, kernels_tc.cu). All return cudaGetLastError().
 // Sequence tensors are [B][C][H][D]; state arrays are [B][H][nseg][D][D] fp32.
 struct SeqArgs {
@@ -105,6 +128,7 @@ struct SeqArgs {
   void* out;
   const float* state;     // device [B][H][nseg][D][D] (state entering each segment)
   int trans_state;        // use S^T of the stored state
+  const unsigned* status = nullptr;  // cache-tag status of the call (backward), nullptr = unchecked
 };
 
 cudaError_t launch_seg_state_simt(const Plan& p, Dir dir, const void* x, const void* y,
@@ -112,8 +136,11 @@ cudaError_t launch_seg_state_simt(const Plan& p, Dir dir, const void* x, const v
 cudaError_t launch_prefix(const Plan& p, Dir dir, const float* init, const float* seg_states,
                           float* prefix_out, float* final_out, cudaStream_t st);
 cudaError_t launch_core_simt(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st);
-cudaError_t launch_fold_ranks(const Plan& p, const float* gathered, int j0, int step, int count, float* out,
-                              cudaStream_t st);
+// dst[0..n) = src (n = B*H*D*D), then p.C as an int64 at dst + n (all-gather message)
+cudaError_t launch_pack_state(const Plan& p, const float* src, float* dst, cudaStream_t st);
+// gathered: [world][stride] fp32, rank j's state at j*stride, its n_local (int64) at j*stride + n
+cudaError_t launch_fold_ranks(const Plan& p, const float* gathered, int64_t stride, int j0, int step, int count,
+                              float* out, cudaStream_t st);
 cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local, float* kv_out,
                            cudaStream_t st);
 

@@ -39,11 +39,11 @@ def test_sizes_and_plan():
     L = lib.lasp_segment_len(ctypes.byref(s))
     assert L % 128 == 0 and L > 0
     nseg = -(-32768 // L)
-    assert lib.lasp_cache_bytes(ctypes.byref(s)) == 1 * 16 * nseg * 64 * 64 * 4
+    assert lib.lasp_cache_bytes(ctypes.byref(s)) == 1 * 16 * nseg * 64 * 64 * 4 + 256  # + the tag
     assert lib.lasp_workspace_bytes(ctypes.byref(s)) >= 16 * nseg * 64 * 64 * 4 + 3 * 16 * 64 * 64 * 4
     # empty rank: one segment slot holds KV_in
     s0 = _shape(2, 0, 3, 32)
-    assert lib.lasp_cache_bytes(ctypes.byref(s0)) == 2 * 3 * 32 * 32 * 4
+    assert lib.lasp_cache_bytes(ctypes.byref(s0)) == 2 * 3 * 32 * 32 * 4 + 256
     # unsupported head_dim -> 0 bytes
     assert lib.lasp_cache_bytes(ctypes.byref(_shape(D=96))) == 0
 
@@ -71,14 +71,21 @@ def test_shape_errors():
     assert lib.lasp_fwd_local(None, None, None, None, None, None, None, None, None, None, None) == 1
 
 
-def test_backward_without_forward_is_state_error():
+def test_cache_holds_tag_after_states():
+    """The cache is the fp32 segment states [B][H][nseg][D][D] (256-byte aligned) plus a 256-byte tag that the
+    forward writes and the backward checks on the device (include/lasp.h)."""
     lib = N.lib()
-    s = _shape()
-    lam = np.full(4, 0.9, dtype=np.float32)
-    p = ctypes.c_void_p(4096)
-    st = lib.lasp_bwd_local(ctypes.byref(s), p, p, p, lam.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), p,
-                            ctypes.c_void_p(8192), None, p, p, p, None, p, None)
-    assert st == 4 and "cache" in lib.lasp_last_error().decode()
+    for B, C, H, D in ((1, 1000, 4, 64), (2, 32768, 16, 128), (1, 0, 3, 32)):
+        s = N.shape(B, C, H, D, N.LASP_BF16)
+        nseg = max(1, -(-C // lib.lasp_segment_len(ctypes.byref(s))))
+        states = B * H * nseg * D * D * 4
+        assert lib.lasp_cache_bytes(ctypes.byref(s)) == -(-states // 256) * 256 + 256
+
+
+def test_workspace_status_rejects_null():
+    lib = N.lib()
+    assert lib.lasp_workspace_status(None, None) == 1
+    assert lib.lasp_workspace_status(ctypes.c_void_p(18), None) == 1
 
 
 def test_ctx_rejects_bad_rank():

@@ -106,7 +106,7 @@ def test_bf16_sim_ring_head_dims(L, oracle_mod, D, T):
     check_against_oracle(oracle_mod, p, res, BF16_TOL)
 
 
-@pytest.mark.parametrize("lam", [1.0, 0.99, 0.9, 0.5])
+@pytest.mark.parametrize("lam", [1.0, 0.99, 0.9, 0.5, 0.1, 1e-3])
 def test_bf16_scalar_lambdas(L, oracle_mod, lam):
     p = synth.problem(2, 2, 1536, 2, 64, dtype="bf16", lam=lam)
     res = run_sim_ring(L, p, 2, torch.bfloat16, 1536)
@@ -169,14 +169,60 @@ def test_deterministic_bitwise(L):
 
 
 def test_state_error_on_mismatched_cache(L):
+    """The cache tag is checked on the device: a mismatch makes every output NaN and
+    lasp_workspace_status report LASP_ERR_STATE; a matching pair reports OK with finite outputs."""
     from paper_2404_02882_b200._native import LaspError
-    q = torch.zeros((1, 256, 2, 64), dtype=torch.bfloat16, device="cuda")
+    q = torch.full((1, 256, 2, 64), 0.25, dtype=torch.bfloat16, device="cuda")
+    ws = L.alloc_workspace(q)
     _, _, cache = L.fwd_local(q, q, q, [0.9, 0.9])
+    dq, dk, dv, dkv = L.bwd_local(q, q, q, [0.9, 0.9], q, cache, workspace=ws, check_state=True)
+    assert all(torch.isfinite(t.float()).all() for t in (dq, dk, dv, dkv))
     with pytest.raises(LaspError) as e:
-        L.bwd_local(q, q, q, [0.9, 0.8], q, cache)   # different lambda
+        L.bwd_local(q, q, q, [0.9, 0.8], q, cache, workspace=ws, check_state=True)   # different lambda
+    assert e.value.name == "LASP_ERR_STATE" and "lambda" in str(e.value)
+    dq, dk, dv, dkv = L.bwd_local(q, q, q, [0.9, 0.8], q, cache, workspace=ws)
+    assert all(torch.isnan(t.float()).all() for t in (dq, dk, dv, dkv))      # loud without the check too
+    with pytest.raises(LaspError) as e:
+        L.bwd_local(q, q, q, [0.9, 0.9], q, torch.zeros_like(cache), workspace=ws, check_state=True)  # never written
+    assert e.value.name == "LASP_ERR_STATE" and "magic" in str(e.value)
+    q2 = torch.full((1, 128, 2, 64), 0.25, dtype=torch.bfloat16, device="cuda")
+    _, _, cache2 = L.fwd_local(q2, q2, q2, [0.9, 0.9], cache=torch.empty_like(cache))
+    with pytest.raises(LaspError) as e:   # a cache of another length in a buffer large enough for this one
+        L.bwd_local(q, q, q, [0.9, 0.9], q, cache2, workspace=ws, check_state=True)
+    assert e.value.name == "LASP_ERR_STATE" and "n_local" in str(e.value)
+
+
+def test_state_error_on_reused_cache_address(L):
+    """A freed cache whose address the caching allocator hands out again is judged by its contents: after a
+    forward with another lambda has written the reused block, a backward expecting the first forward's
+    lambda fails with LASP_ERR_STATE (the r1 host-side pointer registry accepted it)."""
+    from paper_2404_02882_b200._native import LaspError
+    q = torch.full((1, 512, 4, 64), 0.5, dtype=torch.bfloat16, device="cuda")
+    ws = L.alloc_workspace(q)
+    cache = L.alloc_cache(q)
+    addr = cache.data_ptr()
+    L.fwd_local(q, q, q, [0.9] * 4, cache=cache)
+    torch.cuda.synchronize()
+    del cache
+    reused = L.alloc_cache(q)
+    assert reused.data_ptr() == addr              # the allocator reused the block
+    L.fwd_local(q, q, q, [0.7] * 4, cache=reused)  # another layer's forward writes it
+    with pytest.raises(LaspError) as e:
+        L.bwd_local(q, q, q, [0.9] * 4, q, reused, workspace=ws, check_state=True)
     assert e.value.name == "LASP_ERR_STATE"
-    with pytest.raises(LaspError):
-        L.bwd_local(q, q, q, [0.9, 0.9], q, torch.empty_like(cache))  # never written
+
+
+def test_ragged_multi_segment_rev_store_deterministic(L, oracle_mod):
+    """with several segments and a ragged rank length, the REV passes' ragged block starts inside
+    the previous segment; only the segment's own rows may be stored (else two CTAs race on those rows with
+    differently rounded values). B=1, H=4, D=64, C=1000: 8 segments of 128 tokens with a 104-token tail."""
+    assert L.segment_len(L.api._shape(torch.empty((1, 1000, 4, 64), dtype=torch.bfloat16, device="meta"))) == 128
+    p = synth.problem(11, 1, 1000, 4, 64, dtype="bf16")
+    runs = [run_sim_ring(L, p, 1, torch.bfloat16, 1000) for _ in range(6)]
+    for r in runs[1:]:
+        for x, y in zip(runs[0][:4], r[:4]):
+            assert np.array_equal(x, y)
+    check_against_oracle(oracle_mod, p, runs[0], BF16_TOL)
 
 
 def test_autograd_function(L, oracle_mod):

@@ -90,16 +90,18 @@ def test_ring_cache_tag_checks_rank(ring):
     q = torch.zeros((1, 256, 2, 64), dtype=torch.bfloat16, device="cuda")
     _, _, cache = lasp.fwd_local(q, q, q, [0.9, 0.9])   # local cache: (rank, world) = (-1, -1)
     with pytest.raises(LaspError) as e:
-        ring.bwd(q, q, q, [0.9, 0.9], q, cache)
-    assert e.value.name == "LASP_ERR_STATE"
+        ring.bwd(q, q, q, [0.9, 0.9], q, cache, check_state=True)
+    assert e.value.name == "LASP_ERR_STATE" and "rank" in str(e.value)
 
 
 # ---- world > 1 on one GPU: the same lasp_fwd / lasp_bwd code with the in-process loopback transport ----
-def _run_loopback(p, world, n_global, dtype, group, exchange="ring"):
-    """Each rank is a thread with its own CUDA stream and ring context; returns the gathered outputs."""
+def _run_loopback(p, world, n_global, dtype, group, exchange="ring", bounds=None):
+    """Each rank is a thread with its own CUDA stream and ring context; returns the gathered outputs.
+    ``bounds``: per-rank token ranges (default: equal shares C = N/T)."""
     import threading
     import paper_2404_02882_b200 as lasp
     C = n_global // world
+    bounds = bounds or [(r * C, (r + 1) * C) for r in range(world)]
     out, errors = [None] * world, []
     done = threading.Barrier(world)
 
@@ -110,7 +112,7 @@ def _run_loopback(p, world, n_global, dtype, group, exchange="ring"):
             ring = lasp.Ring.loopback(r, world, group).set_exchange(exchange)
             stream = torch.cuda.Stream()
             with torch.cuda.stream(stream):
-                sl = slice(r * C, (r + 1) * C)
+                sl = slice(*bounds[r])
                 q, k, v, do = (torch.from_numpy(np.ascontiguousarray(p[x][:, sl])).cuda().to(dtype)
                                for x in ("q", "k", "v", "do"))
                 o, cache = ring.fwd(q, k, v, p["lam"])
@@ -151,6 +153,22 @@ def test_loopback_ring_bf16_matches_oracle(oracle_mod, world, exchange):
     N = 768 * world
     p = synth.problem(40 + world, 1, N, 4, 64, dtype="bf16")
     got, _ = _run_loopback(p, world, N, torch.bfloat16, f"bf16-w{world}-{exchange}", exchange)
+    refs = [oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])] + \
+        list(oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"]))
+    for x, r in zip(got, refs):
+        assert oracle_mod.normwise_err(x, r) <= 2e-2
+
+
+@pytest.mark.parametrize("exchange", ["ring", "allgather"])
+def test_loopback_unequal_rank_lengths(oracle_mod, exchange):
+    """Ranks holding different token counts (reading R3): the ring combines with each rank's own lam^C, and
+    the all-gather exchange carries every rank's n_local with its state, so both match the
+    oracle on the whole sequence."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    bounds = [(0, 300), (300, 1324), (1324, 1500), (1500, 2200)]
+    p = synth.problem(47, 1, 2200, 4, 64, dtype="bf16")
+    got, _ = _run_loopback(p, 4, 2200, torch.bfloat16, f"unequal-{exchange}", exchange, bounds=bounds)
     refs = [oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])] + \
         list(oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"]))
     for x, r in zip(got, refs):

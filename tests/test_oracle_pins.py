@@ -162,16 +162,47 @@ def test_golden_dkv_update_c1(oracle_mod):
 
 
 def test_golden_table1_volume(oracle_mod):
+    """Table 1 LASP row: one hop carries B*d^2/h elements; at B=1, d=2048, h=16 that is
+    262144. The oracle's rank-simulated Alg. 2/3 report their own message size, compared with the
+    printed number (d = H*D, so D = d/h = 128)."""
     g = GOLD["table1_lasp_volume"]
-    # one hop of the ring carries B*H*D*D elements with D = d/h
     H, D = g["h"], g["d"] // g["h"]
-    N, T = 1024, 4
-    p = rand_problem(0, g["B"], N, 1, 2)
-    q = np.zeros((g["B"], N, H, D))
-    _, _, hops, elems = oracle_mod.lasp_fwd_sim(q[:, :, :1, :2], q[:, :, :1, :2], q[:, :, :1, :2], [0.9], T)
-    assert hops == T - 1
-    assert g["B"] * H * D * D == g["elements"]
-    del p
+    T, N = 4, 8
+    z = np.zeros((g["B"], N, H, D))
+    o, cache, hops, elems = oracle_mod.lasp_fwd_sim(z, z, z, [0.9] * H, T)
+    _, _, _, bhops, belems = oracle_mod.lasp_bwd_sim(z, z, z, [0.9] * H, z, cache, T)
+    assert (hops, bhops) == (T - 1, T - 1)
+    assert elems == g["elements"] and belems == g["elements"]
+
+
+# normwise_err (reading A14) grades every GPU parity check: pinned on hand-computed values so that a
+# mean instead of a max, a sum in the denominator or a missing abs fails
+def test_normwise_err_known_values(oracle_mod):
+    ref = np.array([[1.0, -4.0], [2.0, 0.5]])
+    x = ref.copy()
+    assert oracle_mod.normwise_err(x, ref) == 0.0
+    x[1, 1] += 0.2                       # one element off by 0.2; max|ref| = 4 (a negative entry)
+    assert oracle_mod.normwise_err(x, ref) == pytest.approx(0.05, abs=1e-15)
+    x[0, 0] -= 0.4                       # the max error, with a negative sign
+    assert oracle_mod.normwise_err(x, ref) == pytest.approx(0.1, abs=1e-15)
+    # mean-based or sum-based variants give different values on the same input
+    assert oracle_mod.normwise_err(x, ref) != pytest.approx(np.mean(np.abs(x - ref)) / np.max(np.abs(ref)))
+    assert oracle_mod.normwise_err(x, ref) != pytest.approx(np.max(np.abs(x - ref)) / np.sum(np.abs(ref)))
+    # all-zero reference: the absolute error is reported (no division by zero)
+    assert oracle_mod.normwise_err(np.array([0.0, 3.0]), np.zeros(2)) == 3.0
+    assert oracle_mod.normwise_err(np.zeros(3), np.zeros(3)) == 0.0
+    # scale invariance: the metric is relative to the tensor's own magnitude
+    assert oracle_mod.normwise_err(1e6 * x, 1e6 * ref) == pytest.approx(0.1, rel=1e-12)
+    # bf16-rounded copy of a random tensor: error within 2^-9 of the max (RNE, reading A13)
+    r = np.random.default_rng(0).standard_normal(1000)
+    xb = torch.tensor(r, dtype=torch.float32).to(torch.bfloat16).double().numpy()
+    e = oracle_mod.normwise_err(xb, r)
+    assert 0 < e <= 2.0 ** -9
+    # shape mismatch is an error, not a silent broadcast
+    with pytest.raises(ValueError):
+        oracle_mod.normwise_err(np.zeros((2, 3)), np.zeros((3, 2)))
+    with pytest.raises(ValueError):
+        oracle_mod.normwise_err(np.zeros(3), np.zeros((1, 3)))
 
 
 # pin 5: closed forms for constant inputs (derived from Eq. 4, P:187), any N
