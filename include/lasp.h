@@ -41,9 +41,10 @@
  *              lambda, heads are independent, P:18 -- reading A7). lambda = 1 is plain linear
  *              attention.
  *   Streams  : all device work is enqueued on the caller's stream; calls return after enqueue.
- *              The first kernel of every call is an ordinary launch (it starts once all earlier work
- *              on the stream has completed, whatever produced the inputs); the call's later kernels
- *              use programmatic dependent launch among themselves only.
+ *              The kernels of a call use programmatic dependent launch among themselves; the first
+ *              one waits until all earlier work on the stream has completed before any other kernel of
+ *              the call may start, so inputs produced by any earlier kernel (early-triggering or not)
+ *              are complete when they are read.
  *   Graphs   : lasp_fwd_local / lasp_bwd_local and the NCCL entry points can be captured into CUDA
  *              graphs (the programmatic launch edges are kept; bench.py replays its step from a
  *              graph). Contexts made by lasp_ctx_create_loopback use host threads and cannot.
@@ -113,6 +114,10 @@ void lasp_profile_enable(int on);
  * kernel). Pass NULL to disable. */
 void lasp_debug_trace(unsigned long long* device_buf);
 int lasp_profile_read(char* buf, size_t cap);
+/* Experiments only: launches `ctas` CTAs on `stream`, each holding `smem_bytes` of shared memory (with
+ * >= 120 KB, one per SM and no co-resident 224 KB core CTA) and spinning for `microseconds` -- a stand-in
+ * for another stream's kernels (e.g. NCCL's) occupying SMs while a persistent LASP kernel runs. */
+lasp_status_t lasp_debug_occupy(int ctas, int smem_bytes, double microseconds, void* stream);
 
 /* Bytes of the caller-owned per-layer KV cache for `shape`: fp32 segment states [B][H][nseg][D][D] (entry
  * 0 = the state entering the rank, KV_in(r), reading A4; entry p = the state entering in-rank segment p),
@@ -125,9 +130,10 @@ size_t lasp_cache_bytes(const lasp_shape_t* shape);
  * lasp_fwd* call with the same shape, lambda and (ring calls) rank and world -- a buffer never written by
  * a forward, a freed-and-reused allocation now holding another forward's cache, a different lambda, ...
  * lasp_last_error() then names the mismatching fields. A backward whose check fails still runs, but every
- * state it loads is NaN, so dq, dk, dv (and dkv_out) are NaN: the mismatch cannot go unnoticed. (The
+ * state it loads is NaN, so dq, dk and dv are NaN: the mismatch cannot go unnoticed. (The
  * check is on the device so that calls stay asynchronous and capturable into CUDA graphs, and no host
- * registry keyed by pointers can be fooled by address reuse.) */
+ * registry keyed by pointers can be fooled by address reuse.) dkv_out is computed from q and d_o only
+ * (not from the cache) and is not poisoned. */
 lasp_status_t lasp_workspace_status(const void* workspace, void* stream /* cudaStream_t */);
 
 /* Bytes of the caller-owned scratch workspace used by lasp_fwd, lasp_fwd_local, lasp_bwd and lasp_bwd_local (reusable across

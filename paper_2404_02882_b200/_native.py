@@ -44,6 +44,7 @@ _SIGS = {
     "lasp_profile_enable": ([ctypes.c_int], None),
     "lasp_profile_read": ([ctypes.c_char_p, ctypes.c_size_t], ctypes.c_int),
     "lasp_debug_trace": ([_vp], None),
+    "lasp_debug_occupy": ([ctypes.c_int, ctypes.c_int, ctypes.c_double, _vp], ctypes.c_int),
     "lasp_workspace_bytes": ([_sp], ctypes.c_size_t),
     "lasp_workspace_status": ([_vp, _vp], ctypes.c_int),
     "lasp_segment_len": ([_sp], ctypes.c_int64),

@@ -350,23 +350,26 @@ cudaError_t launch_pack_state(const Plan& p, const float* src, float* dst, cudaS
                   dst);
 }
 
-// Entry kernel of every call (launched without the programmatic attribute): writes (forward) or checks
-// (backward) the cache tag, then lets the call's next kernel start.
-__global__ void tag_kernel(CacheTag t, uint64_t* __restrict__ hdr, unsigned check_mask, unsigned* __restrict__ status) {
+// Entry kernel of every call: waits until everything before the call has completed (griddepcontrol.wait),
+// only then lets the call's next kernel start (lasp_common.cuh, PDL), writes (forward) or checks (backward)
+// the cache tag into the call's status word ctrl[2], and zeroes the call's counters (ctrl[0..1]: fused
+// prefix fold; ctrl[3..15]: work-claim counters of the persistent kernels).
+__global__ void tag_kernel(CacheTag t, uint64_t* __restrict__ hdr, unsigned check_mask, unsigned* __restrict__ ctrl) {
+  pdl_wait();
   pdl_trigger();
   const int i = threadIdx.x;
+  bool bad = false;
   if (check_mask == 0u) {
     if (i < kTagWords) hdr[i] = t.w[i];
-    if (i == 0 && status) *status = 0u;
-    return;
+  } else {
+    bad = i < kTagWords && ((check_mask >> i) & 1u) && hdr[i] != t.w[i];
   }
-  const bool bad = i < kTagWords && ((check_mask >> i) & 1u) && hdr[i] != t.w[i];
   const unsigned bits = __ballot_sync(0xffffffffu, bad);
-  if (i == 0) *status = bits;
+  if (i < 16) ctrl[i] = i == 2 ? bits : 0u;
 }
 
-cudaError_t launch_tag(const CacheTag& t, uint64_t* hdr, unsigned check_mask, unsigned* status, cudaStream_t st) {
-  return launch_k(tag_kernel, dim3(1), dim3(32), 0, st, t, hdr, check_mask, status);
+cudaError_t launch_tag(const CacheTag& t, uint64_t* hdr, unsigned check_mask, unsigned* ctrl, cudaStream_t st) {
+  return launch_k(tag_kernel, dim3(1), dim3(32), 0, st, t, hdr, check_mask, ctrl);
 }
 
 cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local, float* kv_out, cudaStream_t st) {

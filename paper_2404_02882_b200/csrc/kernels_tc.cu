@@ -125,7 +125,45 @@ __device__ __forceinline__ uint64_t desc_k(uint32_t addr) { return smem_desc(add
 __device__ __forceinline__ uint64_t desc_mn(uint32_t addr, uint32_t lbo) { return smem_desc(addr, lbo, 1024); }
 
 // ================================================================================================
-// work items: (batch, head, segment), round-robin over a persistent grid (one CTA per SM)
+// Dynamic work claiming (persistent kernels): the producer thread claims item indices in increasing
+// order from a global counter (zeroed by the call's entry kernel) and hands them to the CTA's other roles
+// through a 2-slot shared-memory queue. A CTA that starts late (its SM still busy with the previous kernel
+// or a communication kernel on another stream) simply claims fewer items, instead of owning a fixed
+// 1/grid share that stretches the launch. Items are independent (no cross-item reduction), so which CTA
+// runs an item does not change any bit of the result.
+struct ItemQueue {
+  uint64_t full[2], empty[2];
+  int64_t item[2];
+};
+__device__ __forceinline__ void q_init(ItemQueue& q, uint32_t consumers) {
+  for (int s = 0; s < 2; ++s) { mbar_init(&q.full[s], 1); mbar_init(&q.empty[s], consumers); }
+}
+// producer: claim the k-th item of this CTA (>= W: no more work; still published, as the end marker).
+// ctr == nullptr: the static round-robin assignment of round 1 (LASP_STATIC_ITEMS=1, A/B experiments)
+__device__ __forceinline__ int64_t q_claim(ItemQueue& q, uint32_t k, unsigned* ctr) {
+  const uint32_t s = k & 1u;
+  mbar_wait(&q.empty[s], ((k >> 1) & 1u) ^ 1u);
+  const int64_t w = ctr ? int64_t(atomicAdd(ctr, 1u)) : int64_t(blockIdx.x) + int64_t(k) * gridDim.x;
+  q.item[s] = w;
+  mbar_arrive(&q.full[s]);  // release: the item index is visible to the waiters
+  return w;
+}
+// consumer: the k-th item of this CTA; then q_release once per consumer warp (or single-thread role)
+__device__ __forceinline__ int64_t q_fetch(ItemQueue& q, uint32_t k) {
+  mbar_wait(&q.full[k & 1u], (k >> 1) & 1u);
+  return *reinterpret_cast<volatile int64_t*>(&q.item[k & 1u]);
+}
+__device__ __forceinline__ void q_release(ItemQueue& q, uint32_t k) { mbar_arrive(&q.empty[k & 1u]); }
+// whole-warp consumer: fetch, then lane 0 releases the slot once every lane has read it
+__device__ __forceinline__ int64_t q_fetch_warp(ItemQueue& q, uint32_t k) {
+  const int64_t w = q_fetch(q, k);
+  __syncwarp();
+  if (lane_id() == 0) q_release(q, k);
+  return w;
+}
+
+// ================================================================================================
+// work items: (batch, head, segment), claimed dynamically by a persistent grid
 // ================================================================================================
 struct Item {
   int64_t b, h, seg, beg, end;
@@ -175,7 +213,7 @@ struct SegLayout {
   static constexpr uint32_t X(int s) { return uint32_t(s) * 2 * TILE; }
   static constexpr uint32_t Y(int s) { return uint32_t(s) * 2 * TILE + TILE; }
   static constexpr uint32_t BARS = STAGES * 2 * TILE;
-  static constexpr uint32_t BYTES = BARS + 512 + 1024;  // barriers + tmem slot + alignment slack
+  static constexpr uint32_t BYTES = BARS + 512 + 1024;  // barriers + item queue + tmem slot + alignment slack
   static constexpr uint32_t TCOLS = 2 * D;             // two accumulators
 };
 
@@ -184,7 +222,7 @@ struct SegParams {
   Plan p;
   float* out;
   unsigned long long* trace;
-  unsigned* gbar_reset;  // [2] zeroed after the wait on the preceding kernel (fused fold of the next launch)
+  unsigned* claim;       // work-claim counter (ItemQueue), 0 at launch
 };
 
 // debug timeline: event ev (0..15) of block J (< 64) of CTA 0 -> trace[ev * 64 + J] = clock64()
@@ -217,7 +255,8 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
   uint64_t* empty = scaled + ST;
   uint64_t* acc_full = empty + ST;     // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  ItemQueue* iq = reinterpret_cast<ItemQueue*>(acc_empty + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(iq + 1);
   const uint32_t sbase = smem_u32(sm);
 
   const Plan& p = prm.p;
@@ -229,6 +268,7 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
     tma_prefetch(&prm.my);
     for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&scaled[s], 128); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], 128); }
+    q_init(*iq, 1 + 4 + 4);  // consumers: the UMMA thread, 4 scaler warps, 4 drain warps
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<L::TCOLS>(tmem_slot);
@@ -244,7 +284,9 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
   if (warp == 0) {
     if (elect_one()) {
       uint32_t J = 0;
-      for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+      for (uint32_t k = 0;; ++k) {
+        const int64_t w = q_claim(*iq, k, prm.claim);
+        if (w >= W) break;
         const Item it = get_item(p, DIR, w);
         for (int j = 0; j < it.nblk; ++j, ++J) {
           const int s = J % ST;
@@ -263,8 +305,11 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
   } else if (warp == 1) {
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_bf16(D, D, 1, 1);
-      uint32_t J = 0, k = 0;
-      for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
+      uint32_t J = 0;
+      for (uint32_t k = 0;; ++k) {
+        const int64_t w = q_fetch(*iq, k);
+        q_release(*iq, k);
+        if (w >= W) break;
         const Item it = get_item(p, DIR, w);
         const uint32_t acc = tmem + (k & 1) * D;
         mbar_wait(&acc_empty[k & 1], ((k >> 1) & 1) ^ 1);
@@ -290,7 +335,9 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
     // scale X rows by the decay weight (Eq. 12 / Eq. 21 weights, relative to the segment end / begin)
     const int g = int(threadIdx.x) - 128;  // tile row
     uint32_t J = 0;
-    for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+    for (uint32_t k = 0;; ++k) {
+      const int64_t w = q_fetch_warp(*iq, k);
+      if (w >= W) break;
       const Item it = get_item(p, DIR, w);
       const float l2 = p.l2lam[it.h];
       for (int j = 0; j < it.nblk; ++j, ++J) {
@@ -323,10 +370,9 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
     const int row = D == 128 ? int(q4 * 32 + lane) : int(q4 * 16 + lane);
     pdl_wait();
     pdl_trigger();
-    // the previous user of the counter (a core launch of an earlier call) has completed
-    if (prm.gbar_reset != nullptr && blockIdx.x == 0 && threadIdx.x == 256) prm.gbar_reset[0] = prm.gbar_reset[1] = 0u;
-    uint32_t k = 0;
-    for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
+    for (uint32_t k = 0;; ++k) {
+      const int64_t w = q_fetch_warp(*iq, k);
+      if (w >= W) break;
       const Item it = get_item(p, DIR, w);
       mbar_wait(&acc_full[k & 1], (k >> 1) & 1);
       tc_fence_after();
@@ -406,6 +452,7 @@ struct CoreParams {
   unsigned long long* trace;  // debug timeline (lasp_debug_trace), nullptr in production
   int npass;
   const unsigned* status;     // cache-tag status of a backward call (nonzero: NaN states), or nullptr
+  unsigned* claim;            // work-claim counter (ItemQueue), 0 at launch
   FastDiv div_per, div_nbh;   // / (B*H*NV*npass), / (B*H*NV) (work-item decode)
   PrefixFold fold;            // fold.gbar != nullptr: compute the prefix states first (fused F2 / B2)
 };
@@ -511,9 +558,11 @@ struct CoreBars {
   uint64_t full[3], empty[3], s_full[2], s_empty[2];
   uint64_t p_full[2], ku_full, ds_full, ds_empty, st_full[2], st_empty[2], o_full, o_empty;
   uint64_t stg_full, stg_empty;
+  ItemQueue iq;
   uint32_t tmem_slot;
   uint32_t fold_chunk;  // fused prefix fold: chunk claimed by this CTA's fold threads
 };
+static_assert(sizeof(CoreBars) <= 256, "CoreBars must fit its 256-byte slot");
 constexpr int kFoldChunk = 256;  // float2 elements per claimed fold chunk (one per fold thread)
 __device__ __forceinline__ unsigned fold_chunks(const Plan& p) {
   return unsigned((p.B * p.H * p.D * p.D / 2 + kFoldChunk - 1) / kFoldChunk);
@@ -549,6 +598,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     mbar_init(&bar->ds_full, 1); mbar_init(&bar->ds_empty, 128);
     for (int b2 = 0; b2 < L::NSB; ++b2) { mbar_init(&bar->st_full[b2], 128); mbar_init(&bar->st_empty[b2], 1); }
     mbar_init(&bar->o_full, 1); mbar_init(&bar->o_empty, 128);
+    q_init(bar->iq, 3 + 12);  // consumers: 3 UMMA threads, 12 SIMT warps
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(&bar->tmem_slot);
@@ -591,7 +641,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     if (elect_one()) {
       bool waited = false;
       uint32_t J = 0, k = 0;
-      for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
+      for (;; ++k) {
+        const int64_t w = q_claim(bar->iq, k, prm.claim);
+        if (w >= W) break;
         const CItem it = get_citem<L::NV>(prm, w);
         const CorePass& ps = prm.pass[it.pass];
         // the segment's prefix state -> STG (single buffer, released by the state warps)
@@ -651,7 +703,10 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       constexpr uint32_t id_x = idesc_bf16(128, 64, 0, 1);
       auto koff = [](int kk) -> uint32_t { return uint32_t(kk >> 2) * BOX + uint32_t(kk & 3) * 32; };
       uint32_t J = 0, kd = 0;
-      for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+      for (uint32_t k = 0;; ++k) {
+        const int64_t w = q_fetch(bar->iq, k);
+        q_release(bar->iq, k);
+        if (w >= W) break;
         const int nblk = get_citem<L::NV>(prm, w).nblk;
         for (int j = 0; j < nblk; ++j, ++J) {
           const int s = int(J % ST);
@@ -721,7 +776,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     // ------------------------------------------------------------------ mask warps: S -> P (bf16)
     const uint32_t q4 = warp & 3;  // rows [32 q4, 32 q4 + 32) of the block
     uint32_t J = 0;
-    for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+    for (uint32_t k = 0;; ++k) {
+      const int64_t w = q_fetch_warp(bar->iq, k);
+      if (w >= W) break;
       const CItem it = get_citem<L::NV>(prm, w);
       const bool fwd = it.dir == Dir::FWD;
       const float l2 = p.l2lam[it.h];
@@ -862,8 +919,10 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         for (int e = 0; e < 64; ++e) S[e] = __int_as_float(0x7fc00000);
       }
     };
-    uint32_t J = 0, kd = 0, k = 0;
-    for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++k) {
+    uint32_t J = 0, kd = 0;
+    for (uint32_t k = 0;; ++k) {
+      const int64_t w = q_fetch_warp(bar->iq, k);
+      if (w >= W) break;
       const CItem it = get_citem<L::NV>(prm, w);
       const CorePass& ps = prm.pass[it.pass];
       load_state(k, it, ps.trans != 0, ps.state);
@@ -944,7 +1003,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     const int i = int(q4 * 32 + lane);
     const bool leader = threadIdx.x == 384;
     uint32_t J = 0;
-    for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+    for (uint32_t k = 0;; ++k) {
+      const int64_t w = q_fetch_warp(bar->iq, k);
+      if (w >= W) break;
       const CItem it = get_citem<L::NV>(prm, w);
       const CUtensorMap* mo = &prm.mout[prm.pass[it.pass].out];
       __nv_bfloat16* outp = prm.outp[prm.pass[it.pass].out];
@@ -1014,6 +1075,14 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+bool static_items() {
+  static const bool on = [] {
+    const char* s = std::getenv("LASP_STATIC_ITEMS");
+    return s && *s && *s != '0';
+  }();
+  return on;
+}
+
 int sm_count() {
   static int n = 0;
   if (n == 0) {
@@ -1032,9 +1101,9 @@ unsigned persistent_grid(const Plan& p, int per_sm = 1) {
 
 template <int D, Dir DIR>
 cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, cudaStream_t st,
-                       unsigned* gbar_reset) {
+                       unsigned* claim) {
   SegParams prm;
-  prm.gbar_reset = gbar_reset;
+  prm.claim = static_items() ? nullptr : claim;
   cudaError_t e;
   if ((e = make_seq_map(&prm.mx, x, p)) != cudaSuccess) return e;
   if ((e = make_seq_map(&prm.my, y, p)) != cudaSuccess) return e;
@@ -1049,7 +1118,7 @@ cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, 
 
 template <int D>
 cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st,
-                              const PrefixFold* fold) {
+                              const PrefixFold* fold, unsigned* claim, int reserve_sms) {
   CoreParams prm;
   std::memset(&prm, 0, sizeof prm);
   cudaError_t e;
@@ -1092,19 +1161,43 @@ cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const 
   prm.p = p;
   prm.npass = npass;
   prm.status = a[0].status;
+  prm.claim = claim;
   prm.trace = g_trace;
   if (fold) prm.fold = *fold;
   prm.div_nbh = FastDiv(uint32_t(p.B * p.H * CoreLayout<D>::NV));
   prm.div_per = FastDiv(uint32_t(p.B * p.H * CoreLayout<D>::NV * npass));
+  if (static_items()) prm.claim = nullptr;
   auto kern = core_tc_kernel<D>;
   const int smem = int(CoreLayout<D>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
   const int64_t W = p.B * p.H * p.nseg * npass * CoreLayout<D>::NV;
-  const unsigned grid = unsigned(W < sm_count() ? W : sm_count());
+  // reserve_sms: SMs left free for kernels of another stream (the ring's NCCL kernels while a hop is in
+  // flight): a persistent CTA holds an SM's whole register file and shared memory until the launch ends
+  int64_t slots = sm_count() - (reserve_sms > 0 && reserve_sms < sm_count() ? reserve_sms : 0);
+  const unsigned grid = unsigned(W < slots ? W : slots);
   return launch_k(kern, dim3(grid), dim3(512), smem, st, prm);
 }
 
+// Debug / experiments (lasp_debug_occupy): `ctas` CTAs that each hold most of an SM's shared memory and spin
+// for `ns` nanoseconds -- a stand-in for kernels of another stream (NCCL) that occupy SMs while a persistent
+// kernel of this library runs.
+__global__ void occupy_kernel(unsigned long long ns) {
+  extern __shared__ uint8_t sm_hog[];
+  const unsigned long long t0 = globaltimer();
+  while (globaltimer() - t0 < ns) {
+    if (threadIdx.x == 0) sm_hog[0] = 1;
+    __nanosleep(500);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_occupy(int ctas, int smem, double us, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(occupy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  occupy_kernel<<<ctas, 32, smem, st>>>((unsigned long long)(us * 1e3));
+  return cudaGetLastError();
+}
 
 const char* tc_last_error() { return g_tc_err; }
 
@@ -1131,20 +1224,22 @@ bool tc_supported(const Plan& p) {
 
 cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st,
                                 unsigned* r) {
+  if (r == nullptr) return cudaErrorInvalidValue;  // the work-claim counter is required
   if (p.D == 64) return dir == Dir::FWD ? launch_seg<64, Dir::FWD>(p, x, y, out, st, r) : launch_seg<64, Dir::REV>(p, x, y, out, st, r);
   if (p.D == 128) return dir == Dir::FWD ? launch_seg<128, Dir::FWD>(p, x, y, out, st, r) : launch_seg<128, Dir::REV>(p, x, y, out, st, r);
   return cudaErrorNotSupported;
 }
 
-cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st) {
-  return launch_core_tc_multi(p, 1, &a, &dir, st);
+cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st, unsigned* claim,
+                           int reserve_sms) {
+  return launch_core_tc_multi(p, 1, &a, &dir, st, nullptr, claim, reserve_sms);
 }
 
 cudaError_t launch_core_tc_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st,
-                                 const PrefixFold* fold) {
-  if (npass < 1 || npass > 3) return cudaErrorInvalidValue;
-  if (p.D == 64) return launch_core_multi<64>(p, npass, a, dirs, st, fold);
-  if (p.D == 128) return launch_core_multi<128>(p, npass, a, dirs, st, fold);
+                                 const PrefixFold* fold, unsigned* claim, int reserve_sms) {
+  if (npass < 1 || npass > 3 || claim == nullptr) return cudaErrorInvalidValue;
+  if (p.D == 64) return launch_core_multi<64>(p, npass, a, dirs, st, fold, claim, reserve_sms);
+  if (p.D == 128) return launch_core_multi<128>(p, npass, a, dirs, st, fold, claim, reserve_sms);
   return cudaErrorNotSupported;
 }
 

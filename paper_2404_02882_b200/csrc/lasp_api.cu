@@ -121,12 +121,14 @@ size_t seg_state_elems(const Plan& p) { return size_t(p.B * p.H * p.nseg * p.D *
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Workspace {
-  unsigned* gbar;   // [0..1]: counters of the fused prefix fold; [2]: cache-tag status of the call
+  unsigned* gbar;   // control block (16 words, zeroed by the call's entry kernel): [0..1] fused prefix
+                    // fold counters, [2] cache-tag status of the call, [3..5] work-claim counters
   float* seg;       // [B][H][nseg][D][D]
   float* local;     // [B][H][D][D] local total (ring)
   float* in;        // received state
   float* out;       // state to send
   unsigned* status() const { return gbar + 2; }
+  unsigned* claim(int i) const { return gbar + 3 + i; }  // 0: segment states, 1: first core, 2: second core
 };
 
 // the 256-byte control block sits at the start, so lasp_workspace_status needs no shape
@@ -263,14 +265,14 @@ cudaError_t staged(const char* name, cudaStream_t st, F&& launch) {
   return e;
 }
 
-// entry kernel of a call: write (forward) or check (backward) the cache tag; launched without the
-// programmatic attribute, so the call's later kernels (PDL) only ever overlap kernels of the same call
+// entry kernel of a call: write (forward) or check (backward) the cache tag; it waits for the completion of
+// all preceding work before it triggers, so the call's later kernels (PDL) only ever overlap kernels of the
+// same call
 cudaError_t entry_tag(const Plan& p, const void* cache, const Workspace& w, int rank, int world, bool check,
                       bool check_rank, cudaStream_t st) {
   const CacheTag t = make_tag(p, rank, world);
   return staged(check ? "tag_check" : "tag_write", st, [&] {
-    g_entry_launch = true;
-    return launch_tag(t, cache_tag_ptr(p, cache), check ? tag_mask(check_rank) : 0u, w.status(), st);
+    return launch_tag(t, cache_tag_ptr(p, cache), check ? tag_mask(check_rank) : 0u, w.gbar, st);
   });
 }
 
@@ -295,11 +297,11 @@ struct ProfSpan {
 
 // ---- stage dispatch: tcgen05 for covered bf16 shapes, CUDA cores otherwise ---------------------
 cudaError_t seg_state(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st,
-                      unsigned* gbar_reset = nullptr) {
+                      unsigned* claim) {
   const bool tc = tc_supported(p);
   return staged(dir == Dir::FWD ? (tc ? "seg_state_fwd_tc" : "seg_state_fwd_simt")
                                 : (tc ? "seg_state_rev_tc" : "seg_state_rev_simt"), st, [&] {
-    return tc ? launch_seg_state_tc(p, dir, x, y, out, st, gbar_reset) : launch_seg_state_simt(p, dir, x, y, out, st);
+    return tc ? launch_seg_state_tc(p, dir, x, y, out, st, claim) : launch_seg_state_simt(p, dir, x, y, out, st);
   });
 }
 
@@ -315,11 +317,22 @@ bool fused_fold(const Plan& p) {
 }
 
 cudaError_t core(const Plan& p, Dir dir, const void* a, const void* b, const void* c, void* out,
-                 const float* state, int trans, cudaStream_t st, const unsigned* status = nullptr) {
+                 const float* state, int trans, cudaStream_t st, unsigned* claim, const unsigned* status = nullptr,
+                 int reserve_sms = 0) {
   SeqArgs args{a, b, c, out, state, trans, status};
   const bool tc = tc_supported(p);
   return staged(dir == Dir::FWD ? (tc ? "core_fwd_tc" : "core_fwd_simt") : (tc ? "core_rev_tc" : "core_rev_simt"),
-                st, [&] { return tc ? launch_core_tc(p, dir, args, st) : launch_core_simt(p, dir, args, st); });
+                st, [&] {
+                  return tc ? launch_core_tc(p, dir, args, st, claim, reserve_sms) : launch_core_simt(p, dir, args, st);
+                });
+}
+
+// SMs the ring's dQ launch leaves free for the dKV hop's NCCL kernels on the comm stream (P:296 overlap):
+// a persistent core CTA holds an SM's whole register file and shared memory, so without free SMs the hop
+// could only start once dQ has finished. LASP_COMM_SMS overrides (0 disables).
+int comm_sms() {
+  static const int n = int(env_i64("LASP_COMM_SMS", 4));
+  return n;
 }
 
 cudaError_t prefix(const Plan& p, Dir dir, const float* init, const float* seg, float* out, float* fin,
@@ -335,10 +348,10 @@ cudaError_t combine(const Plan& p, const float* in, const float* local, float* o
 // several core passes: one persistent tensor-core launch (passes of a segment interleaved, their
 // shared inputs re-read from L2), or one CUDA-core launch per pass
 cudaError_t core_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st,
-                       const PrefixFold* fold = nullptr) {
+                       unsigned* claim, const PrefixFold* fold = nullptr) {
   if (tc_supported(p))
     return staged(npass == 3 ? "core_bwd3_tc" : npass == 1 && dirs[0] == Dir::FWD ? "core_fwd_tc" : "core_multi_tc", st,
-                  [&] { return launch_core_tc_multi(p, npass, a, dirs, st, fold); });
+                  [&] { return launch_core_tc_multi(p, npass, a, dirs, st, fold, claim); });
   for (int x = 0; x < npass; ++x) {
     cudaError_t e = staged(dirs[x] == Dir::FWD ? "core_fwd_simt" : "core_rev_simt", st,
                            [&] { return launch_core_simt(p, dirs[x], a[x], st); });
@@ -358,7 +371,8 @@ lasp_status_t prologue(const lasp_shape_t* shape, const float* lambda, Plan& p) 
 // Forward compute after KV_in is known (F2 prefix + F3 core). `seg` already holds F1's states. gbar:
 // fused-fold counters (zeroed by F1's launch) or nullptr for the separate prefix kernel.
 lasp_status_t fwd_tail(const Plan& p, const void* q, const void* k, const void* v, const float* kv_in,
-                       void* o, float* kv_out, void* cache, float* seg, unsigned* gbar, cudaStream_t st) {
+                       void* o, float* kv_out, void* cache, float* seg, unsigned* gbar, unsigned* claim,
+                       cudaStream_t st) {
   float* P = static_cast<float*>(cache);
   if (p.C == 0) {
     LASP_CUDA(prefix(p, Dir::FWD, kv_in, nullptr, P, kv_out, st));
@@ -368,11 +382,11 @@ lasp_status_t fwd_tail(const Plan& p, const void* q, const void* k, const void* 
     const PrefixFold fold{kv_in, seg, P, kv_out, gbar, int(Dir::FWD)};
     const SeqArgs a{q, k, v, o, P, 0};
     const Dir dir = Dir::FWD;
-    LASP_CUDA(core_multi(p, 1, &a, &dir, st, &fold));
+    LASP_CUDA(core_multi(p, 1, &a, &dir, st, claim, &fold));
     return LASP_OK;
   }
   LASP_CUDA(prefix(p, Dir::FWD, kv_in, seg, P, kv_out, st));
-  LASP_CUDA(core(p, Dir::FWD, q, k, v, o, P, 0, st));
+  LASP_CUDA(core(p, Dir::FWD, q, k, v, o, P, 0, st, claim));
   return LASP_OK;
 }
 
@@ -593,6 +607,12 @@ size_t lasp_cache_bytes(const lasp_shape_t* shape) {
   return cache_bytes(make_plan(shape));
 }
 
+lasp_status_t lasp_debug_occupy(int ctas, int smem_bytes, double microseconds, void* stream) {
+  if (ctas < 1 || smem_bytes < 0 || !(microseconds >= 0)) return fail(LASP_ERR_SHAPE, "bad occupy arguments");
+  LASP_CUDA(launch_occupy(ctas, smem_bytes, microseconds, static_cast<cudaStream_t>(stream)));
+  return LASP_OK;
+}
+
 lasp_status_t lasp_workspace_status(const void* workspace, void* stream) {
   if (!workspace || !aligned16(workspace)) return fail(LASP_ERR_SHAPE, "workspace NULL or not 16-byte aligned");
   unsigned bits = 0;
@@ -629,8 +649,8 @@ lasp_status_t lasp_fwd_local(const lasp_shape_t* shape, const void* q, const voi
   Workspace w = carve(p, workspace);
   unsigned* gbar = p.C > 0 && fused_fold(p) ? w.gbar : nullptr;
   LASP_CUDA(entry_tag(p, cache, w, -1, -1, false, false, st));                            // cache tag
-  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, gbar));                  // F1
-  if ((s = fwd_tail(p, q, k, v, kv_in, o, kv_out, cache, w.seg, gbar, st)) != LASP_OK) return s;  // F2 + F3
+  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, w.claim(0)));            // F1
+  if ((s = fwd_tail(p, q, k, v, kv_in, o, kv_out, cache, w.seg, gbar, w.claim(1), st)) != LASP_OK) return s;  // F2 + F3
   return LASP_OK;
 }
 
@@ -651,14 +671,14 @@ lasp_status_t lasp_bwd_local(const lasp_shape_t* shape, const void* q, const voi
     return LASP_OK;
   }
   const bool fuse = fused_fold(p);
-  LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, fuse ? w.gbar : nullptr));         // B1
+  LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, w.claim(0)));                        // B1
   const PrefixFold fold{dkv_in, w.seg, w.seg, dkv_out, w.gbar, int(Dir::REV)};
   if (!fuse) LASP_CUDA(prefix(p, Dir::REV, dkv_in, w.seg, w.seg, dkv_out, st));         // B2 (in place)
   // B3: dQ (needs only the cache), dV and dK in one launch (with B2 folded in when fused)
   const SeqArgs passes[3] = {{d_o, v, k, dq, P, 1, w.status()}, {k, q, d_o, dv, w.seg, 0, w.status()},
                              {v, d_o, q, dk, w.seg, 1, w.status()}};
   const Dir dirs[3] = {Dir::FWD, Dir::REV, Dir::REV};
-  LASP_CUDA(core_multi(p, 3, passes, dirs, st, fuse ? &fold : nullptr));
+  LASP_CUDA(core_multi(p, 3, passes, dirs, st, w.claim(1), fuse ? &fold : nullptr));
   return LASP_OK;
 }
 
@@ -789,13 +809,13 @@ lasp_status_t lasp_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   lasp_ring_peers(c->rank, c->world, 0, &from, &to);
   unsigned* gbar = p.C > 0 && fused_fold(p) ? w.gbar : nullptr;
   LASP_CUDA(entry_tag(p, cache, w, c->rank, c->world, false, false, st));              // cache tag
-  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, gbar));               // F1
+  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, w.claim(0)));         // F1
   LASP_CUDA(prefix(p, Dir::FWD, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
   if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
     ProfSpan hop("exchange_fwd", st);
     if ((s = exchange_allgather(c, p, w.local, w.in, false, st)) != LASP_OK) return s;
     hop.stop(st);
-    if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, gbar, st)) != LASP_OK) return s;  // F2 + F3
+    if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, gbar, w.claim(1), st)) != LASP_OK) return s;
     return LASP_OK;
   }
   // F2 ring hop: Recv KV_in from r-1 (Alg. 2), combine, Send to r+1
@@ -810,7 +830,7 @@ lasp_status_t lasp_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
     if ((s = ring_send(c, w.out, n, to, st, "ncclSend(KV)")) != LASP_OK) return s;
   }
   hop.stop(st);
-  if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, gbar, st)) != LASP_OK) return s;  // F2 + F3
+  if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, gbar, w.claim(1), st)) != LASP_OK) return s;  // F2+F3
   return LASP_OK;
 }
 
@@ -829,7 +849,7 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   const float* P = static_cast<const float*>(cache);
   const bool fuse = p.C > 0 && fused_fold(p);
   LASP_CUDA(entry_tag(p, cache, w, c->rank, c->world, true, true, st));                 // cache tag check
-  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, fuse ? w.gbar : nullptr));  // B1
+  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, w.claim(0)));       // B1
   LASP_CUDA(prefix(p, Dir::REV, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
   // B2 ring hop on the comm stream: Recv dKV_in from r+1 (Alg. 3), combine, Send to r-1
   LASP_CUDA(cudaEventRecord(c->ev_ready, st));
@@ -837,6 +857,7 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   ProfSpan hop("exchange_bwd", c->comm_stream);
   int from = -1, to = -1;
   lasp_ring_peers(c->rank, c->world, 1, &from, &to);
+  const bool hop_pending = c->world > 1;  // a receive, send or all-gather runs on the comm stream under dQ
   if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
     if ((s = exchange_allgather(c, p, w.local, w.in, true, c->comm_stream)) != LASP_OK) return s;
   } else if (from >= 0) {
@@ -851,7 +872,8 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   hop.stop(c->comm_stream);
   LASP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
   // dQ needs only the cache: it runs while the dKV hop is in flight
-  if (p.C > 0) LASP_CUDA(core(p, Dir::FWD, d_o, v, k, dq, P, 1, st, w.status()));
+  if (p.C > 0)
+    LASP_CUDA(core(p, Dir::FWD, d_o, v, k, dq, P, 1, st, w.claim(1), w.status(), hop_pending ? comm_sms() : 0));
   LASP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
   if (p.C == 0) return LASP_OK;
   if (!fuse) LASP_CUDA(prefix(p, Dir::REV, w.in, w.seg, w.seg, nullptr, st));   // B2
@@ -859,7 +881,7 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
     const SeqArgs passes[2] = {{k, q, d_o, dv, w.seg, 0, w.status()}, {v, d_o, q, dk, w.seg, 1, w.status()}};
     const Dir dirs[2] = {Dir::REV, Dir::REV};
     const PrefixFold fold{w.in, w.seg, w.seg, nullptr, w.gbar, int(Dir::REV)};
-    LASP_CUDA(core_multi(p, 2, passes, dirs, st, fuse ? &fold : nullptr));
+    LASP_CUDA(core_multi(p, 2, passes, dirs, st, w.claim(2), fuse ? &fold : nullptr));
   }
   return LASP_OK;
 }

@@ -21,9 +21,13 @@
 namespace lasp {
 
 // Programmatic dependent launch: every kernel of the path is launched with programmatic stream
-// serialization; a kernel signals its dependents at entry and waits for its prerequisite grid before
-// touching global memory, so a kernel's prologue (TMEM alloc, barrier init, descriptor prefetch) and
-// its CTAs' start overlap the previous kernel's tail. LASP_NO_PDL=1 disables it (debugging).
+// serialization, so a kernel's prologue (TMEM alloc, barrier init, descriptor prefetch) and its CTAs'
+// start overlap the previous kernel's tail. The first kernel of every call (tag_kernel) executes
+// griddepcontrol.wait -- which returns only once the preceding grid has COMPLETED, whether or not it
+// triggered early -- before it triggers the call's next kernel; so every later kernel of the call starts
+// after all work that preceded the call on the stream is complete and visible, whoever produced the
+// inputs, and PDL edges that skip a wait exist only between kernels of one call, where the
+// library controls both sides. LASP_NO_PDL=1 disables PDL (debugging).
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -35,16 +39,8 @@ inline bool pdl_enabled() {
   return on;
 }
 
-// The first kernel of every entry point is launched WITHOUT the programmatic attribute (it starts once
-// everything before it on the stream has completed, whoever produced the call's inputs), so the PDL edges
-// are only ever between kernels of one call, where the library controls both sides. Set by
-// the entry points, consumed by the next launch on this thread.
-inline thread_local bool g_entry_launch = false;
-
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
-  const bool entry = g_entry_launch;
-  g_entry_launch = false;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -54,7 +50,7 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() && !entry ? 1 : 0;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -116,8 +112,9 @@ enum TagWord { kTagMagic = 0, kTagB, kTagC, kTagH, kTagD, kTagSeg, kTagDtype, kT
 struct CacheTag { uint64_t w[kTagWords]; };
 constexpr size_t kCacheTagBytes = 256;
 constexpr uint64_t kTagMagicValue = 0x4c41535043414348ull;  // "LASPCACH"
-// check_mask == 0: write the tag (and clear *status); else compare the masked words into *status
-cudaError_t launch_tag(const CacheTag& t, uint64_t* hdr, unsigned check_mask, unsigned* status, cudaStream_t st);
+// check_mask == 0: write the tag, else compare the masked words; the mismatch bits go to ctrl[2] (the
+// call's status word) and the other 15 words of the call's control block (counters) are zeroed
+cudaError_t launch_tag(const CacheTag& t, uint64_t* hdr, unsigned check_mask, unsigned* ctrl, cudaStream_t st);
 // true (on the device) when the call's entry kernel found a mismatching cache tag
 __device__ __forceinline__ bool tag_poisoned(const unsigned* status) { return status != nullptr && __ldcg(status) != 0u; }
 
@@ -146,14 +143,14 @@ cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local
 
 // Segment-prefix fold (F2 / B2, same arithmetic as prefix_kernel) run by a core launch before its main
 // loop: the 256 state + epilogue threads of each CTA claim chunks of elements (gbar[0]) and fold them;
-// prefix states are read once every chunk is done (gbar[1]). Both counters are zeroed by the preceding
-// segment-state launch.
+// prefix states are read once every chunk is done (gbar[1]). Both counters are zeroed by the call's
+// entry kernel (tag_kernel).
 struct PrefixFold {
   const float* init;  // state entering the rank, or nullptr (zero)
   const float* seg;   // segment states [B][H][nseg][D][D]
   float* out;         // prefix states (may alias seg)
   float* fin;         // state leaving the rank, or nullptr
-  unsigned* gbar;     // [2]: chunks claimed, chunks done; 0 at kernel start
+  unsigned* gbar;     // [2]: chunks claimed, chunks done; zeroed by the call's entry kernel
   int dir;            // Dir
 };
 
@@ -162,13 +159,16 @@ bool tc_supported(const Plan& p);
 bool tc_fold_fusable(const Plan& p);  // fuse the prefix fold into the core launch (small enough state)
 const char* tc_last_error();
 void tc_set_trace(unsigned long long* buf);  // debug: per-block clock64 timeline of CTA 0  // detail of the last tcgen05-path host failure on this thread
-// gbar_reset: if non-null, set to 0 once the preceding kernel has completed (for a following fused fold)
+// claim: the launch's work-claim counter (a workspace word zeroed by the call's entry kernel)
 cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out,
-                                cudaStream_t st, unsigned* gbar_reset = nullptr);
-cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st);
+                                cudaStream_t st, unsigned* claim);
+// reserve_sms: leave that many SMs free for another stream's kernels (ring hop in flight)
+cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st, unsigned* claim,
+                           int reserve_sms = 0);
 // up to 3 core passes in one persistent launch (their segments interleaved: shared inputs hit L2);
 // fold != nullptr: the launch first computes the prefix states its passes read (PrefixFold)
 cudaError_t launch_core_tc_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st,
-                                 const PrefixFold* fold = nullptr);
+                                 const PrefixFold* fold, unsigned* claim, int reserve_sms = 0);
+cudaError_t launch_occupy(int ctas, int smem, double us, cudaStream_t st);  // debug: SM hog on another stream
 
 }  // namespace lasp
