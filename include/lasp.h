@@ -34,12 +34,12 @@
  *   Layout   : every sequence tensor is [batch][n_local][heads][head_dim], contiguous, row-major,
  *              device memory owned by the caller, base address 16-byte aligned. Element type is
  *              bf16 (LASP_BF16) or fp32 (LASP_FP32) for q, k, v, o, d_o, dq, dk, dv alike.
- *   States   : kv_in / kv_out / dkv_in / dkv_out are fp32 [batch][heads][head_dim][head_dim],
+ *   States   : kv_in / kv_out / dkv_in / dkv_out are fp32 [batch][kv_heads][head_dim][head_dim],
  *              row index = the first factor's dimension (KV = sum k v^T: rows index k, columns v;
  *              dKV = sum q do^T: rows index q, columns do). Device memory, caller-owned.
- *   lambda   : HOST pointer to `heads` fp32 decay rates, each in (0, 1] (P:145 gives a single
- *              lambda, heads are independent, P:18 -- reading A7). lambda = 1 is plain linear
- *              attention.
+ *   lambda   : HOST pointer to `kv_heads` (= `heads` unless grouped-query) fp32 decay rates, each in
+ *              (0, 1] (P:145 gives a single lambda, heads are independent, P:18 -- reading A7).
+ *              lambda = 1 is plain linear attention.
  *   Streams  : all device work is enqueued on the caller's stream; calls return after enqueue.
  *              The kernels of a call use programmatic dependent launch among themselves; the first
  *              one waits until all earlier work on the stream has completed before any other kernel of
@@ -87,9 +87,14 @@ typedef enum { LASP_BF16 = 0, LASP_FP32 = 1 } lasp_dtype_t;
 typedef struct {
   int64_t batch;     /* B >= 1                                   */
   int64_t n_local;   /* C = tokens owned by this rank, >= 0       */
-  int64_t heads;     /* H >= 1                                   */
+  int64_t heads;     /* H >= 1 (query heads)                     */
   int64_t head_dim;  /* D = d_k = d_v, one of 32, 64, 128 */
   lasp_dtype_t dtype;
+  int64_t kv_heads;  /* Hk: key/value heads, 0 = H (multi-head). Hk < H is grouped-query (multi-query for
+                      * Hk = 1) attention: H % Hk == 0, query head h reads
+                      * kv-head h / (H/Hk), and each kv-head has ONE shared state (and decay). k, v, dk, dv are
+                      * [B][C][Hk][D]; lambda, the states, the cache and the ring messages are per kv-head.
+                      * Needs bf16 and head_dim 64 or 128 (else LASP_ERR_UNSUPPORTED).          */
 } lasp_shape_t;
 
 /* Opaque ring context: owns the NCCL communicator and nothing else. */

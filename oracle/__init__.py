@@ -9,6 +9,8 @@ this module only builds/loads it and marshals numpy arrays. Functions:
 
 * ``fwd`` / ``bwd`` -- definition mode, the recurrences Eq. 5 and
   Eq. 13-14 (P:257-272).
+* ``fwd_gqa`` / ``bwd_gqa`` -- the same recurrences with H query heads sharing Hk key/value heads
+  (multi-query / grouped-query attention).
 * ``lasp_fwd_sim`` / ``lasp_bwd_sim`` -- Alg. 2 (P:141-176) and Alg. 3 (P:574-653) run
   literally with T simulated ranks, explicit messages and a KV cache.
 * chunk ops (``build_decay``, ``intra_fwd``, ``inter_fwd``, ``kv_update``, ``intra_bwd``,
@@ -56,6 +58,8 @@ def _load():
             lib = ctypes.CDLL(build())
             lib.oracle_fwd.argtypes = [_i64] * 4 + [_dp] * 3 + [_fp, _dp, ctypes.c_int]
             lib.oracle_bwd.argtypes = [_i64] * 4 + [_dp] * 3 + [_fp] + [_dp] * 4 + [ctypes.c_int]
+            lib.oracle_fwd_gqa.argtypes = [_i64] * 5 + [_dp] * 3 + [_fp, _dp, ctypes.c_int]
+            lib.oracle_bwd_gqa.argtypes = [_i64] * 5 + [_dp] * 3 + [_fp] + [_dp] * 4 + [ctypes.c_int]
             lib.oracle_build_decay.argtypes = [_i64, ctypes.c_float, _dp, _dp, _dp, _dp]
             lib.oracle_intra_fwd.argtypes = [_i64, _i64] + [_dp] * 5
             lib.oracle_inter_fwd.argtypes = [_i64, _i64] + [_dp] * 4
@@ -69,7 +73,8 @@ def _load():
                                                                           ctypes.c_int]
             lib.oracle_lasp_bwd_sim.argtypes = [_i64] * 5 + [_dp] * 3 + [_fp, _dp, _dp] + [_dp] * 3 + \
                 [_i64p, _i64p, ctypes.c_int]
-            for fn in ("oracle_fwd", "oracle_bwd", "oracle_build_decay", "oracle_lasp_fwd_sim",
+            for fn in ("oracle_fwd", "oracle_bwd", "oracle_fwd_gqa", "oracle_bwd_gqa", "oracle_build_decay",
+                       "oracle_lasp_fwd_sim",
                        "oracle_lasp_bwd_sim"):
                 getattr(lib, fn).restype = ctypes.c_int
             _lib = lib
@@ -127,6 +132,30 @@ def bwd(q, k, v, lam, do, nthreads=None):
     lam, lp = _lam(lam, H)
     _check(_load().oracle_bwd(B, N, H, D, _ptr(q), _ptr(k), _ptr(v), lp, _ptr(do), _ptr(dq), _ptr(dk),
                               _ptr(dv), _threads(nthreads)))
+    return dq, dk, dv
+
+
+def fwd_gqa(q, k, v, lam, nthreads=None):
+    """Grouped-query O (SURVEY §8(f) NEXT-4, P:18): q [B][N][H][D], k, v [B][N][Hk][D], lam [Hk];
+    q-head h reads kv-head h // (H/Hk), whose state kv_s = lam kv_{s-1} + k_s v_s^T is shared."""
+    B, N, H, D = _shape4(q)
+    Hk = _shape4(k)[2]
+    q, k, v = _f64(q), _f64(k), _f64(v)
+    o = np.zeros_like(q)
+    lam, lp = _lam(lam, Hk)
+    _check(_load().oracle_fwd_gqa(B, N, H, Hk, D, _ptr(q), _ptr(k), _ptr(v), lp, _ptr(o), _threads(nthreads)))
+    return o
+
+
+def bwd_gqa(q, k, v, lam, do, nthreads=None):
+    """(dQ [B][N][H][D], dK, dV [B][N][Hk][D]) of L = sum(O * dO) for fwd_gqa."""
+    B, N, H, D = _shape4(q)
+    Hk = _shape4(k)[2]
+    q, k, v, do = _f64(q), _f64(k), _f64(v), _f64(do)
+    dq, dk, dv = np.zeros_like(q), np.zeros_like(k), np.zeros_like(v)
+    lam, lp = _lam(lam, Hk)
+    _check(_load().oracle_bwd_gqa(B, N, H, Hk, D, _ptr(q), _ptr(k), _ptr(v), lp, _ptr(do), _ptr(dq), _ptr(dk),
+                                  _ptr(dv), _threads(nthreads)))
     return dq, dk, dv
 
 

@@ -186,6 +186,120 @@ int oracle_bwd(int64_t B, int64_t N, int64_t H, int64_t D, const double* q, cons
 }
 
 /* ---------------------------------------------------------------------------------- */
+/* Grouped-query / multi-query attention ("multi-query, and    */
+/* grouped-query attentions"): H query heads share Hk = H/G key/value heads; q-head h    */
+/* reads kv-head h/G. The recurrence Eq. 5 runs once per kv-head (the memory state is   */
+/* shared by the group, so its decay lambda is one per kv-head -- DESIGN.md reading G1): */
+/*   kv_s = lambda kv_{s-1} + k_s v_s^T,  o_{h,s}^T = q_{h,s}^T kv_s  (h in the group).  */
+/* Gradients of L = sum_h sum_s o_{h,s} . do_{h,s}: dq_{h,s} = kv_s do_{h,s}; the       */
+/* reverse state collects every head of the group, dkv_s = lambda dkv_{s+1} +            */
+/* sum_h q_{h,s} do_{h,s}^T, and dk_s = dkv_s v_s, dv_s = dkv_s^T k_s (Eq. 13-14 with    */
+/* the group's sum). Layout: q, o, do, dq [B][N][H][D]; k, v, dk, dv [B][N][Hk][D];     */
+/* lam [Hk].                                                                             */
+/* ---------------------------------------------------------------------------------- */
+typedef struct {
+    int64_t B, N, H, Hk, D;
+    const double *q, *k, *v, *dout;
+    const float* lam;
+    double *o, *dq, *dk, *dv;
+} gqa_ctx_t;
+
+#define QROW(p, c, b, s, h) ((p) + ((((b) * (c)->N + (s)) * (c)->H + (h)) * (c)->D))
+#define KROW(p, c, b, s, h) ((p) + ((((b) * (c)->N + (s)) * (c)->Hk + (h)) * (c)->D))
+
+static void gqa_fwd_item(void* vctx, int64_t item) {
+    gqa_ctx_t* c = (gqa_ctx_t*)vctx;
+    const int64_t b = item / c->Hk, hk = item % c->Hk, D = c->D, G = c->H / c->Hk;
+    const double lam = (double)c->lam[hk];
+    double* kv = (double*)calloc((size_t)(D * D), sizeof(double));
+    for (int64_t s = 0; s < c->N; ++s) {
+        const double* ks = KROW(c->k, c, b, s, hk);
+        const double* vs = KROW(c->v, c, b, s, hk);
+        for (int64_t d = 0; d < D; ++d)
+            for (int64_t e = 0; e < D; ++e) kv[d * D + e] = lam * kv[d * D + e] + ks[d] * vs[e];
+        for (int64_t h = hk * G; h < (hk + 1) * G; ++h) {
+            const double* qs = QROW(c->q, c, b, s, h);
+            double* os = QROW(c->o, c, b, s, h);
+            for (int64_t e = 0; e < D; ++e) os[e] = 0.0;
+            for (int64_t d = 0; d < D; ++d)
+                for (int64_t e = 0; e < D; ++e) os[e] += qs[d] * kv[d * D + e];
+        }
+    }
+    free(kv);
+}
+
+static void gqa_bwd_item(void* vctx, int64_t item) {
+    gqa_ctx_t* c = (gqa_ctx_t*)vctx;
+    const int64_t b = item / c->Hk, hk = item % c->Hk, D = c->D, G = c->H / c->Hk;
+    const double lam = (double)c->lam[hk];
+    double* kv = (double*)calloc((size_t)(D * D), sizeof(double));
+    for (int64_t s = 0; s < c->N; ++s) {          /* sweep 1: kv_s forward, dq_{h,s} = kv_s do_{h,s} */
+        const double* ks = KROW(c->k, c, b, s, hk);
+        const double* vs = KROW(c->v, c, b, s, hk);
+        for (int64_t d = 0; d < D; ++d)
+            for (int64_t e = 0; e < D; ++e) kv[d * D + e] = lam * kv[d * D + e] + ks[d] * vs[e];
+        for (int64_t h = hk * G; h < (hk + 1) * G; ++h) {
+            const double* dos = QROW(c->dout, c, b, s, h);
+            double* dqs = QROW(c->dq, c, b, s, h);
+            for (int64_t d = 0; d < D; ++d) {
+                double acc = 0.0;
+                for (int64_t e = 0; e < D; ++e) acc += kv[d * D + e] * dos[e];
+                dqs[d] = acc;
+            }
+        }
+    }
+    double* dkv = kv;                             /* sweep 2: reverse, the group's shared dkv */
+    memset(dkv, 0, sizeof(double) * (size_t)(D * D));
+    for (int64_t s = c->N - 1; s >= 0; --s) {
+        const double* ks = KROW(c->k, c, b, s, hk);
+        const double* vs = KROW(c->v, c, b, s, hk);
+        double* dks = KROW(c->dk, c, b, s, hk);
+        double* dvs = KROW(c->dv, c, b, s, hk);
+        for (int64_t d = 0; d < D; ++d)
+            for (int64_t e = 0; e < D; ++e) dkv[d * D + e] = lam * dkv[d * D + e];
+        for (int64_t h = hk * G; h < (hk + 1) * G; ++h) {
+            const double* qs = QROW(c->q, c, b, s, h);
+            const double* dos = QROW(c->dout, c, b, s, h);
+            for (int64_t d = 0; d < D; ++d)
+                for (int64_t e = 0; e < D; ++e) dkv[d * D + e] += qs[d] * dos[e];
+        }
+        for (int64_t d = 0; d < D; ++d) {
+            double acc = 0.0;
+            for (int64_t e = 0; e < D; ++e) acc += dkv[d * D + e] * vs[e];
+            dks[d] = acc;
+        }
+        for (int64_t e = 0; e < D; ++e) dvs[e] = 0.0;
+        for (int64_t d = 0; d < D; ++d)
+            for (int64_t e = 0; e < D; ++e) dvs[e] += ks[d] * dkv[d * D + e];
+    }
+    free(kv);
+}
+
+int oracle_fwd_gqa(int64_t B, int64_t N, int64_t H, int64_t Hk, int64_t D, const double* q, const double* k,
+                   const double* v, const float* lam, double* o, int nthreads) {
+    if (B < 0 || N < 0 || H < 1 || Hk < 1 || H % Hk != 0 || D < 1 || !q || !k || !v || !lam || !o)
+        return ORACLE_ERR_SHAPE;
+    int st = check_lams(Hk, lam);
+    if (st) return st;
+    gqa_ctx_t c = {B, N, H, Hk, D, q, k, v, NULL, lam, o, NULL, NULL, NULL};
+    run_items(gqa_fwd_item, &c, B * Hk, nthreads);
+    return ORACLE_OK;
+}
+
+int oracle_bwd_gqa(int64_t B, int64_t N, int64_t H, int64_t Hk, int64_t D, const double* q, const double* k,
+                   const double* v, const float* lam, const double* dout, double* dq, double* dk, double* dv,
+                   int nthreads) {
+    if (B < 0 || N < 0 || H < 1 || Hk < 1 || H % Hk != 0 || D < 1 || !q || !k || !v || !lam || !dout || !dq ||
+        !dk || !dv)
+        return ORACLE_ERR_SHAPE;
+    int st = check_lams(Hk, lam);
+    if (st) return st;
+    gqa_ctx_t c = {B, N, H, Hk, D, q, k, v, dout, lam, NULL, dq, dk, dv};
+    run_items(gqa_bwd_item, &c, B * Hk, nthreads);
+    return ORACLE_OK;
+}
+
+/* ---------------------------------------------------------------------------------- */
 /* Chunk operations of Alg. 2 / Alg. 3, one head, C x D row-major matrices.              */
 /* ---------------------------------------------------------------------------------- */
 

@@ -21,7 +21,7 @@ STATUS = {0: "LASP_OK", 1: "LASP_ERR_SHAPE", 2: "LASP_ERR_DOMAIN", 3: "LASP_ERR_
 
 class lasp_shape_t(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int64), ("n_local", ctypes.c_int64), ("heads", ctypes.c_int64),
-                ("head_dim", ctypes.c_int64), ("dtype", ctypes.c_int)]
+                ("head_dim", ctypes.c_int64), ("dtype", ctypes.c_int), ("kv_heads", ctypes.c_int64)]
 
 
 class LaspError(RuntimeError):
@@ -105,5 +105,5 @@ def check(status: int) -> None:
         raise LaspError(status, lib().lasp_last_error().decode())
 
 
-def shape(batch: int, n_local: int, heads: int, head_dim: int, dtype: int) -> lasp_shape_t:
-    return lasp_shape_t(batch, n_local, heads, head_dim, dtype)
+def shape(batch: int, n_local: int, heads: int, head_dim: int, dtype: int, kv_heads: int = 0) -> lasp_shape_t:
+    return lasp_shape_t(batch, n_local, heads, head_dim, dtype, kv_heads)

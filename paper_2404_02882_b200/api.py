@@ -3,7 +3,8 @@
 PyTorch is used for device memory, streams and process groups. Tensors use the boundary layout
 [batch][n_local][heads][head_dim] (include/lasp.h); states are fp32 [batch][heads][D][D].
 
-* ``fwd_local`` / ``bwd_local`` -- one rank's Alg. 2 / Alg. 3 compute without transport.
+* ``fwd_local`` / ``bwd_local`` -- one rank's Alg. 2 / Alg. 3 compute without transport. k, v (and dk, dv)
+  may have fewer heads than q (grouped-query / multi-query attention; lambda then has one entry per kv-head).
 * ``Ring``                        -- Alg. 2 / Alg. 3 across a torch.distributed world (NCCL P2P).
 * ``LaspAttention``               -- torch.autograd.Function over ``Ring`` or the local path.
 * ``topology`` / ``sp_group`` / ``scatter_sequence`` -- data-sequence hybrid parallelism (Alg. 1): G = W/T
@@ -21,13 +22,15 @@ from . import _native as N
 _DT = {torch.bfloat16: N.LASP_BF16, torch.float32: N.LASP_FP32}
 
 
-def _shape(q: torch.Tensor) -> N.lasp_shape_t:
+def _shape(q: torch.Tensor, k: torch.Tensor | None = None) -> N.lasp_shape_t:
+    """Boundary shape of q [B][C][H][D]; k [B][C][Hk][D] with Hk < H selects grouped-query attention."""
     if q.dim() != 4:
         raise ValueError("expected [batch][n_local][heads][head_dim]")
     if q.dtype not in _DT:
         raise TypeError("dtype must be bfloat16 or float32")
     B, C, H, D = q.shape
-    return N.shape(B, C, H, D, _DT[q.dtype])
+    Hk = 0 if k is None or k.shape[2] == H else int(k.shape[2])
+    return N.shape(B, C, H, D, _DT[q.dtype], Hk)
 
 
 def _lam(lam, heads: int):
@@ -53,8 +56,18 @@ def _check_seq(*ts):
             raise ValueError("sequence tensors must be contiguous CUDA tensors of equal shape and dtype")
 
 
+def _check_qkv(q, k, v, do=None):
+    """q (and do) [B][C][H][D]; k, v [B][C][Hk][D] with Hk dividing H (Hk = H: multi-head)."""
+    _check_seq(q, do)
+    _check_seq(k, v)
+    if (k.dim() != 4 or k.shape[:2] != q.shape[:2] or k.shape[3] != q.shape[3] or k.dtype != q.dtype
+            or q.shape[2] % k.shape[2] != 0 or k.device != q.device):
+        raise ValueError("k, v must be [B][C][Hk][D] like q with Hk dividing H (grouped-query attention)")
+
+
 def _check_state(t, q, name):
-    """kv_in / kv_out / dkv_in / dkv_out: fp32 [B][H][D][D], contiguous, on q's device (include/lasp.h)."""
+    """kv_in / kv_out / dkv_in / dkv_out: fp32 [B][Hk][D][D], contiguous, on the device (include/lasp.h);
+    ``q`` here is a tensor with the state's head count (k)."""
     if t is None:
         return
     B, _, H, D = q.shape
@@ -94,34 +107,34 @@ def segment_len(shape: N.lasp_shape_t) -> int:
     return int(N.lib().lasp_segment_len(ctypes.byref(shape)))
 
 
-def alloc_cache(q: torch.Tensor) -> torch.Tensor:
-    """Caller-owned KV cache for q's shape (one per layer)."""
-    return torch.empty(max(cache_bytes(_shape(q)), 16), dtype=torch.uint8, device=q.device)
+def alloc_cache(q: torch.Tensor, k: torch.Tensor | None = None) -> torch.Tensor:
+    """Caller-owned KV cache for q's shape (one per layer); pass k for grouped-query shapes."""
+    return torch.empty(max(cache_bytes(_shape(q, k)), 16), dtype=torch.uint8, device=q.device)
 
 
-def alloc_workspace(q: torch.Tensor) -> torch.Tensor:
-    return torch.empty(max(workspace_bytes(_shape(q)), 16), dtype=torch.uint8, device=q.device)
+def alloc_workspace(q: torch.Tensor, k: torch.Tensor | None = None) -> torch.Tensor:
+    return torch.empty(max(workspace_bytes(_shape(q, k)), 16), dtype=torch.uint8, device=q.device)
 
 
-def _state_like(q: torch.Tensor) -> torch.Tensor:
-    B, _, H, D = q.shape
-    return torch.empty((B, H, D, D), dtype=torch.float32, device=q.device)
+def _state_like(k: torch.Tensor) -> torch.Tensor:
+    B, _, Hk, D = k.shape
+    return torch.empty((B, Hk, D, D), dtype=torch.float32, device=k.device)
 
 
 def fwd_local(q, k, v, lam, kv_in=None, *, o=None, kv_out=True, cache=None, workspace=None):
     """Alg. 2 for one rank -> (o, kv_out or None, cache)."""
-    _check_seq(q, k, v)
-    s = _shape(q)
+    _check_qkv(q, k, v)
+    s = _shape(q, k)
     o = torch.empty_like(q) if o is None else o
-    kv_out_t = _state_like(q) if kv_out is True else (kv_out if isinstance(kv_out, torch.Tensor) else None)
-    cache = alloc_cache(q) if cache is None else cache
-    workspace = alloc_workspace(q) if workspace is None else workspace
+    kv_out_t = _state_like(k) if kv_out is True else (kv_out if isinstance(kv_out, torch.Tensor) else None)
+    cache = alloc_cache(q, k) if cache is None else cache
+    workspace = alloc_workspace(q, k) if workspace is None else workspace
     _check_like(o, q, "o")
-    _check_state(kv_in, q, "kv_in")
-    _check_state(kv_out_t, q, "kv_out")
+    _check_state(kv_in, k, "kv_in")
+    _check_state(kv_out_t, k, "kv_out")
     _check_buf(cache, cache_bytes(s), "cache", q.device)
     _check_buf(workspace, workspace_bytes(s), "workspace", q.device)
-    _, lp = _lam(lam, s.heads)
+    _, lp = _lam(lam, k.shape[2])
     N.check(N.lib().lasp_fwd_local(ctypes.byref(s), _p(q), _p(k), _p(v), lp, _p(kv_in), _p(o), _p(kv_out_t),
                                    _p(cache), _p(workspace), _stream(q.device)))
     return o, kv_out_t, cache
@@ -131,20 +144,20 @@ def bwd_local(q, k, v, lam, do, cache, dkv_in=None, *, dq=None, dk=None, dv=None
               check_state=False):
     """Alg. 3 for one rank -> (dq, dk, dv, dkv_out or None). ``check_state``: synchronize and raise
     LaspError(LASP_ERR_STATE) if the cache's tag did not match (else a mismatch shows as NaN outputs)."""
-    _check_seq(q, k, v, do)
-    s = _shape(q)
+    _check_qkv(q, k, v, do)
+    s = _shape(q, k)
     dq = torch.empty_like(q) if dq is None else dq
-    dk = torch.empty_like(q) if dk is None else dk
-    dv = torch.empty_like(q) if dv is None else dv
-    dkv_out_t = _state_like(q) if dkv_out is True else (dkv_out if isinstance(dkv_out, torch.Tensor) else None)
-    workspace = alloc_workspace(q) if workspace is None else workspace
-    for t, n in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
-        _check_like(t, q, n)
-    _check_state(dkv_in, q, "dkv_in")
-    _check_state(dkv_out_t, q, "dkv_out")
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    dkv_out_t = _state_like(k) if dkv_out is True else (dkv_out if isinstance(dkv_out, torch.Tensor) else None)
+    workspace = alloc_workspace(q, k) if workspace is None else workspace
+    for t, n, ref in ((dq, "dq", q), (dk, "dk", k), (dv, "dv", v)):
+        _check_like(t, ref, n)
+    _check_state(dkv_in, k, "dkv_in")
+    _check_state(dkv_out_t, k, "dkv_out")
     _check_buf(cache, cache_bytes(s), "cache", q.device)
     _check_buf(workspace, workspace_bytes(s), "workspace", q.device)
-    _, lp = _lam(lam, s.heads)
+    _, lp = _lam(lam, k.shape[2])
     N.check(N.lib().lasp_bwd_local(ctypes.byref(s), _p(q), _p(k), _p(v), lp, _p(do), _p(cache), _p(dkv_in),
                                    _p(dq), _p(dk), _p(dv), _p(dkv_out_t), _p(workspace), _stream(q.device)))
     if check_state:
@@ -249,39 +262,39 @@ class Ring:
         except Exception:
             pass
 
-    def protocol(self, q) -> tuple[int, int, int]:
-        s = _shape(q)
+    def protocol(self, q, k=None) -> tuple[int, int, int]:
+        s = _shape(q, k)
         a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         N.check(N.lib().lasp_ctx_protocol(self._ctx, ctypes.byref(s), ctypes.byref(a), ctypes.byref(b),
                                           ctypes.byref(c)))
         return a.value, b.value, c.value
 
     def fwd(self, q, k, v, lam, *, o=None, cache=None, workspace=None):
-        _check_seq(q, k, v)
-        s = _shape(q)
+        _check_qkv(q, k, v)
+        s = _shape(q, k)
         o = torch.empty_like(q) if o is None else o
-        cache = alloc_cache(q) if cache is None else cache
-        workspace = alloc_workspace(q) if workspace is None else workspace
+        cache = alloc_cache(q, k) if cache is None else cache
+        workspace = alloc_workspace(q, k) if workspace is None else workspace
         _check_like(o, q, "o")
         _check_buf(cache, cache_bytes(s), "cache", q.device)
         _check_buf(workspace, workspace_bytes(s), "workspace", q.device)
-        _, lp = _lam(lam, s.heads)
+        _, lp = _lam(lam, k.shape[2])
         N.check(N.lib().lasp_fwd(self._ctx, ctypes.byref(s), _p(q), _p(k), _p(v), lp, _p(o), _p(cache),
                                  _p(workspace), _stream(q.device)))
         return o, cache
 
     def bwd(self, q, k, v, lam, do, cache, *, dq=None, dk=None, dv=None, workspace=None, check_state=False):
-        _check_seq(q, k, v, do)
-        s = _shape(q)
+        _check_qkv(q, k, v, do)
+        s = _shape(q, k)
         dq = torch.empty_like(q) if dq is None else dq
-        dk = torch.empty_like(q) if dk is None else dk
-        dv = torch.empty_like(q) if dv is None else dv
-        workspace = alloc_workspace(q) if workspace is None else workspace
-        for t, n in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
-            _check_like(t, q, n)
+        dk = torch.empty_like(k) if dk is None else dk
+        dv = torch.empty_like(v) if dv is None else dv
+        workspace = alloc_workspace(q, k) if workspace is None else workspace
+        for t, n, ref in ((dq, "dq", q), (dk, "dk", k), (dv, "dv", v)):
+            _check_like(t, ref, n)
         _check_buf(cache, cache_bytes(s), "cache", q.device)
         _check_buf(workspace, workspace_bytes(s), "workspace", q.device)
-        _, lp = _lam(lam, s.heads)
+        _, lp = _lam(lam, k.shape[2])
         N.check(N.lib().lasp_bwd(self._ctx, ctypes.byref(s), _p(q), _p(k), _p(v), lp, _p(do), _p(cache), _p(dq),
                                  _p(dk), _p(dv), _p(workspace), _stream(q.device)))
         if check_state:

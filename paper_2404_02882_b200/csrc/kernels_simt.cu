@@ -102,8 +102,8 @@ __global__ void __launch_bounds__(64) prefix_kernel(Plan p, Dir dir, const float
   // thread loads every segment of a batch before it stores any of them.
   const int64_t DD = p.D * p.D;
   const int64_t idx4 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over B*H*D*D/4
-  if (idx4 * 4 >= p.B * p.H * DD) return;
-  const int64_t bh = (idx4 * 4) / DD, e = (idx4 * 4) % DD, h = bh % p.H;
+  if (idx4 * 4 >= p.B * p.Hk * DD) return;
+  const int64_t bh = (idx4 * 4) / DD, e = (idx4 * 4) % DD, h = bh % p.Hk;
   // every segment has seg_len tokens except possibly the last one (both directions)
   const int64_t last_len = p.C - (p.nseg - 1) * p.seg_len;
   // lam^len = exp2(len * log2(lam)) with log2(lam) from the host in fp64 (relative error ~1e-6 at len ~ 1e3)
@@ -143,8 +143,8 @@ __global__ void combine_kernel(Plan p, const float* __restrict__ kv_in,
   pdl_trigger();
   const int64_t DD = p.D * p.D;
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= p.B * p.H * DD) return;
-  const int64_t h = (idx / DD) % p.H;
+  if (idx >= p.B * p.Hk * DD) return;
+  const int64_t h = (idx / DD) % p.Hk;
   const float in = kv_in ? kv_in[idx] : 0.f;
   kv_out[idx] = fmaf(powk(p.lam[h], double(p.C)), in, local[idx]);
 }
@@ -297,7 +297,7 @@ cudaError_t launch_core_simt(const Plan& p, Dir dir, const SeqArgs& a, cudaStrea
 
 cudaError_t launch_prefix(const Plan& p, Dir dir, const float* init, const float* seg_states, float* prefix_out,
                           float* final_out, cudaStream_t st) {
-  const int64_t n = p.B * p.H * p.D * p.D / 4;  // D*D is a multiple of 4
+  const int64_t n = p.B * p.Hk * p.D * p.D / 4;  // D*D is a multiple of 4
   const int threads = 64;
   return launch_k(prefix_kernel, dim3((unsigned)((n + threads - 1) / threads)), dim3(threads), 0, st, p, dir, init,
                   seg_states, prefix_out, final_out);
@@ -313,10 +313,10 @@ __global__ void fold_ranks_kernel(Plan p, const float* __restrict__ g, int64_t s
                                   float* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
-  const int64_t n = p.B * p.H * p.D * p.D;
+  const int64_t n = p.B * p.Hk * p.D * p.D;
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= n) return;
-  const int64_t h = (idx / (p.D * p.D)) % p.H;
+  const int64_t h = (idx / (p.D * p.D)) % p.Hk;
   float cur = 0.f;
   for (int t = 0; t < count; ++t) {
     const float* gj = g + int64_t(j0 + t * step) * stride;
@@ -328,7 +328,7 @@ __global__ void fold_ranks_kernel(Plan p, const float* __restrict__ g, int64_t s
 
 cudaError_t launch_fold_ranks(const Plan& p, const float* gathered, int64_t stride, int j0, int step, int count,
                               float* out, cudaStream_t st) {
-  const int64_t n = p.B * p.H * p.D * p.D;
+  const int64_t n = p.B * p.Hk * p.D * p.D;
   const int threads = 256;
   return launch_k(fold_ranks_kernel, dim3((unsigned)((n + threads - 1) / threads)), dim3(threads), 0, st, p, gathered,
                   stride, j0, step, count, out);
@@ -344,7 +344,7 @@ __global__ void pack_state_kernel(int64_t n, int64_t C, const float* __restrict_
 }
 
 cudaError_t launch_pack_state(const Plan& p, const float* src, float* dst, cudaStream_t st) {
-  const int64_t n = p.B * p.H * p.D * p.D;
+  const int64_t n = p.B * p.Hk * p.D * p.D;
   const int threads = 256;
   return launch_k(pack_state_kernel, dim3((unsigned)((n + threads - 1) / threads)), dim3(threads), 0, st, n, p.C, src,
                   dst);
@@ -373,7 +373,7 @@ cudaError_t launch_tag(const CacheTag& t, uint64_t* hdr, unsigned check_mask, un
 }
 
 cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local, float* kv_out, cudaStream_t st) {
-  const int64_t n = p.B * p.H * p.D * p.D;
+  const int64_t n = p.B * p.Hk * p.D * p.D;
   const int threads = 256;
   return launch_k(combine_kernel, dim3((unsigned)((n + threads - 1) / threads)), dim3(threads), 0, st, p, kv_in, local,
                   kv_out);

@@ -57,14 +57,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 thread_local char g_tc_err[256];
 unsigned long long* g_trace = nullptr;  // debug timeline buffer (lasp_debug_trace)
 
-cudaError_t make_seq_map(CUtensorMap* m, const void* base, const Plan& p) {
+// heads: the tensor's head count (H for q, o, do, dq; Hk for k, v, dk, dv)
+cudaError_t make_seq_map(CUtensorMap* m, const void* base, const Plan& p, int64_t heads) {
   auto fn = encode_fn();
   if (!fn) {
     snprintf(g_tc_err, sizeof g_tc_err, "cuTensorMapEncodeTiled entry point unavailable");
     return cudaErrorNotSupported;
   }
-  cuuint64_t dims[4] = {cuuint64_t(p.D), cuuint64_t(p.H), cuuint64_t(p.C), cuuint64_t(p.B)};
-  cuuint64_t strides[3] = {cuuint64_t(p.D * 2), cuuint64_t(p.H * p.D * 2), cuuint64_t(p.C * p.H * p.D * 2)};
+  cuuint64_t dims[4] = {cuuint64_t(p.D), cuuint64_t(heads), cuuint64_t(p.C), cuuint64_t(p.B)};
+  cuuint64_t strides[3] = {cuuint64_t(p.D * 2), cuuint64_t(heads * p.D * 2), cuuint64_t(p.C * heads * p.D * 2)};
   cuuint32_t box[4] = {64, 1, BT, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
@@ -72,7 +73,7 @@ cudaError_t make_seq_map(CUtensorMap* m, const void* base, const Plan& p) {
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     snprintf(g_tc_err, sizeof g_tc_err, "cuTensorMapEncodeTiled failed (CUresult %d) for ptr=%p dims=[%lld,%lld,%lld,%lld]",
-             int(r), base, (long long)p.D, (long long)p.H, (long long)p.C, (long long)p.B);
+             int(r), base, (long long)p.D, (long long)heads, (long long)p.C, (long long)p.B);
     return cudaErrorInvalidValue;
   }
   return cudaSuccess;
@@ -107,7 +108,7 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
 cudaError_t make_state_map(CUtensorMap* m, const float* base, const Plan& p) {
   auto fn = encode_fn();
   if (!fn) return cudaErrorNotSupported;
-  cuuint64_t dims[2] = {cuuint64_t(p.D), cuuint64_t(p.B * p.H * p.nseg * p.D)};
+  cuuint64_t dims[2] = {cuuint64_t(p.D), cuuint64_t(p.B * p.Hk * p.nseg * p.D)};
   cuuint64_t strides[1] = {cuuint64_t(p.D * 4)};
   cuuint32_t box[2] = {32, cuuint32_t(p.D)};
   cuuint32_t es[2] = {1, 1};
@@ -163,7 +164,7 @@ __device__ __forceinline__ int64_t q_fetch_warp(ItemQueue& q, uint32_t k) {
 }
 
 // ================================================================================================
-// work items: (batch, head, segment), claimed dynamically by a persistent grid
+// work items: (batch, state head, segment), claimed dynamically by a persistent grid
 // ================================================================================================
 struct Item {
   int64_t b, h, seg, beg, end;
@@ -175,11 +176,11 @@ __device__ __noinline__ Item get_item(const Plan& p, Dir dir, int64_t w) {  // o
   // (batch, head) pairs, so the 128-byte head slices of each [H][D] token row are fetched together
   // (DRAM page locality, L2 sector promotion shared by neighbouring heads).
   Item it;  // 32-bit decode (the host guarantees B*H*nseg < 2^31): keeps the hot loops small
-  const uint32_t wu = uint32_t(w), nbh = uint32_t(p.B * p.H), nh = uint32_t(p.H);
-  it.seg = p.div_bh.div(wu);
+  const uint32_t wu = uint32_t(w), nbh = uint32_t(p.B * p.Hk), nh = uint32_t(p.Hk);
+  it.seg = p.div_bhk.div(wu);
   const uint32_t bh = wu - uint32_t(it.seg) * nbh;
-  it.b = p.div_h.div(bh);
-  it.h = bh - uint32_t(it.b) * nh;
+  it.b = p.div_hk.div(bh);
+  it.h = bh - uint32_t(it.b) * nh;  // state (kv-) head
   it.beg = seg_begin(dir, it.seg, p.seg_len, p.C);
   it.end = seg_end(dir, it.seg, p.seg_len, p.C);
   it.nblk = int((it.end - it.beg + BT - 1) / BT);
@@ -223,6 +224,7 @@ struct SegParams {
   float* out;
   unsigned long long* trace;
   unsigned* claim;       // work-claim counter (ItemQueue), 0 at launch
+  int sub;               // X, Y heads summed per state head (B1 with grouped queries: G; else 1)
 };
 
 // debug timeline: event ev (0..15) of block J (< 64) of CTA 0 -> trace[ev * 64 + J] = clock64()
@@ -260,7 +262,8 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
   const uint32_t sbase = smem_u32(sm);
 
   const Plan& p = prm.p;
-  const int64_t W = p.B * p.H * p.nseg;
+  const int64_t W = p.B * p.Hk * p.nseg;
+  const int sub = prm.sub;
   const uint32_t warp = warp_id(), lane = lane_id();
 
   if (threadIdx.x == 0) {
@@ -288,16 +291,17 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
         const int64_t w = q_claim(*iq, k, prm.claim);
         if (w >= W) break;
         const Item it = get_item(p, DIR, w);
-        for (int j = 0; j < it.nblk; ++j, ++J) {
+        for (int jj = 0; jj < it.nblk * sub; ++jj, ++J) {  // block j = jj / sub, summed head u = jj % sub
           const int s = J % ST;
           mbar_wait(&empty[s], ((J / ST) & 1) ^ 1);
           LASP_TRACE(0, J);
           mbar_expect_tx(&full[s], 2 * L::TILE);
-          const int t0 = int(block_row(DIR, it, j));
+          const int t0 = int(block_row(DIR, it, jj / sub));
+          const int hh = int(it.h) * sub + jj % sub;
 #pragma unroll
           for (int x = 0; x < L::NBOX; ++x) {
-            tma_load_4d(sm + L::X(s) + x * BOX, &prm.mx, &full[s], x * 64, int(it.h), t0, int(it.b));
-            tma_load_4d(sm + L::Y(s) + x * BOX, &prm.my, &full[s], x * 64, int(it.h), t0, int(it.b));
+            tma_load_4d(sm + L::X(s) + x * BOX, &prm.mx, &full[s], x * 64, hh, t0, int(it.b));
+            tma_load_4d(sm + L::Y(s) + x * BOX, &prm.my, &full[s], x * 64, hh, t0, int(it.b));
           }
         }
       }
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
         const uint32_t acc = tmem + (k & 1) * D;
         mbar_wait(&acc_empty[k & 1], ((k >> 1) & 1) ^ 1);
         tc_fence_after();
-        for (int j = 0; j < it.nblk; ++j, ++J) {
+        for (int jj = 0; jj < it.nblk * sub; ++jj, ++J) {
           const int s = J % ST;
           mbar_wait(&scaled[s], (J / ST) & 1);
           LASP_TRACE(3, J);
@@ -325,7 +329,7 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
 #pragma unroll
           for (int kk = 0; kk < BT / 16; ++kk)
             mma_bf16(acc, desc_mn(sbase + L::X(s) + kk * 2048, BOX), desc_mn(sbase + L::Y(s) + kk * 2048, BOX), idesc,
-                     (j | kk) != 0);
+                     (jj | kk) != 0);
           mma_commit(&empty[s]);
         }
         mma_commit(&acc_full[k & 1]);
@@ -340,11 +344,11 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
       if (w >= W) break;
       const Item it = get_item(p, DIR, w);
       const float l2 = p.l2lam[it.h];
-      for (int j = 0; j < it.nblk; ++j, ++J) {
+      for (int jj = 0; jj < it.nblk * sub; ++jj, ++J) {
         const int s = J % ST;
         mbar_wait(&full[s], (J / ST) & 1);
         if (g == 0) LASP_TRACE(1, J);
-        const int64_t pos = block_row(DIR, it, j) + g;
+        const int64_t pos = block_row(DIR, it, jj / sub) + g;
         float wgt = 0.f;
         if (pos >= it.beg && pos < it.end)
           wgt = exp2f(float(DIR == Dir::FWD ? (it.end - 1 - pos) : (pos - it.beg + 1)) * l2);
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
       const Item it = get_item(p, DIR, w);
       mbar_wait(&acc_full[k & 1], (k >> 1) & 1);
       tc_fence_after();
-      float* o = prm.out + ((it.b * p.H + it.h) * p.nseg + it.seg) * D * D + int64_t(row) * D;
+      float* o = prm.out + ((it.b * p.Hk + it.h) * p.nseg + it.seg) * D * D + int64_t(row) * D;
       const uint32_t ta = tmem + ((q4 * 32) << 16) + (k & 1) * D;
 #pragma unroll
       for (int c = 0; c < D / 16; ++c) {
@@ -439,6 +443,10 @@ struct CorePass {
   int a, b, c;    // indices into CoreParams::min
   int out;        // index into CoreParams::mout / outp
   int state;      // index into CoreParams::mst
+  int kvp;        // 1: kv-head pass (items over Hk, G query heads summed per block), 0: query-head pass
+  int nh;         // item heads (H or Hk) = heads of a and out
+  uint32_t off;   // first item of this pass inside a segment row
+  FastDiv div_nh; // / nh
 };
 
 struct CoreParams {
@@ -453,7 +461,9 @@ struct CoreParams {
   int npass;
   const unsigned* status;     // cache-tag status of a backward call (nonzero: NaN states), or nullptr
   unsigned* claim;            // work-claim counter (ItemQueue), 0 at launch
-  FastDiv div_per, div_nbh;   // / (B*H*NV*npass), / (B*H*NV) (work-item decode)
+  FastDiv div_per;            // / (items per segment row) (work-item decode)
+  uint32_t per;               // items per segment row (sum over the passes of B * nh * NV)
+  int uniform;                // every pass has the same item count (head_dim 128 interleaved order)
   PrefixFold fold;            // fold.gbar != nullptr: compute the prefix states first (fused F2 / B2)
 };
 
@@ -470,7 +480,7 @@ __device__ __forceinline__ void fold_prefix(const Plan& p, const PrefixFold& f, 
   const int64_t step = fwd ? D2 : -D2;        // float2 elements between consecutive folded segments
   const int64_t last_len = p.C - (p.nseg - 1) * p.seg_len;
   const int64_t bh = i2 / D2, e2 = i2 - bh * D2;
-  const float l2 = p.l2lam[bh % p.H];
+  const float l2 = p.l2lam[bh % p.Hk];
   const float dec_full = exp2f(float(p.seg_len) * l2), dec_last = exp2f(float(last_len) * l2);
   float2 cur = f.init ? __ldcg(reinterpret_cast<const float2*>(f.init) + i2) : make_float2(0.f, 0.f);
   // segment 0 (FWD) or nseg - 1 (REV) of this element
@@ -514,38 +524,53 @@ __device__ __forceinline__ void grid_wait(const unsigned* ctr, unsigned target) 
 }
 
 struct CItem {
-  int64_t b, h, seg, beg, end;
+  int64_t b, h, seg, beg, end;  // h: item head (of a and out)
   int nblk, pass, v;  // v: 64-wide value slice
+  int sh, sub, bh0;   // state / decay head; query heads summed per block (1 or G); b, c head of sub-block 0
   Dir dir;
 };
 
 // item w -> (segment, pass, batch*head, value slice) at head_dim 64, (segment, batch*head, pass, value slice)
-// at head_dim 128: segment-major, value slice innermost
+// at head_dim 128 when every pass has the same item count: segment-major, value slice innermost.
+// Grouped queries: a query-head pass (O, dQ) reads b, c and the state of kv-head h / G; a kv-head pass
+// (dV, dK) reads b, c of the G query heads h G + u, u = 0..G-1 (sub-blocks summed into one output block).
 template <int NV>
 __device__ __noinline__ CItem get_citem(const CoreParams& prm, int64_t w) {
   const Plan& p = prm.p;
   CItem it;
-  const uint32_t nbh = uint32_t(p.B * p.H) * uint32_t(NV), per = nbh * uint32_t(prm.npass), nh = uint32_t(p.H);
   const uint32_t wu = uint32_t(w);
   it.seg = prm.div_per.div(wu);
-  const uint32_t rem = wu - uint32_t(it.seg) * per;
-  uint32_t bhv;
-  if constexpr (NV > 1) {
+  const uint32_t rem = wu - uint32_t(it.seg) * prm.per;
+  uint32_t bh;
+  if (NV > 1 && prm.uniform) {
     // head_dim 128: (batch x head, pass, value slice) inside a segment row, so that the items re-reading one
     // (segment, batch x head)'s a / b tiles run on adjacent CTAs (fused backward 342 -> 336.5 us at TNL-1B;
     // at head_dim 64 the pass-major order is faster, 124.5 vs 125.8 us)
-    const uint32_t pv = uint32_t(prm.npass) * uint32_t(NV), bh0 = rem / pv, r2 = rem - bh0 * pv;
+    const uint32_t pv = uint32_t(prm.npass) * uint32_t(NV), b0 = rem / pv, r2 = rem - b0 * pv;
     it.pass = int(r2 / uint32_t(NV));
-    bhv = bh0 * uint32_t(NV) + (r2 - uint32_t(it.pass) * uint32_t(NV));
+    it.v = int(r2 - uint32_t(it.pass) * uint32_t(NV));
+    bh = b0;
   } else {
-    it.pass = int(prm.div_nbh.div(rem));
-    bhv = rem - uint32_t(it.pass) * nbh;
+    int ps = 0;
+    while (ps + 1 < prm.npass && rem >= prm.pass[ps + 1].off) ++ps;
+    it.pass = ps;
+    const uint32_t bhv = rem - prm.pass[ps].off;
+    bh = bhv / uint32_t(NV);
+    it.v = int(bhv - bh * uint32_t(NV));
   }
-  const uint32_t bh = bhv / uint32_t(NV);
-  it.v = int(bhv - bh * uint32_t(NV));
-  it.b = p.div_h.div(bh);
-  it.h = bh - uint32_t(it.b) * nh;
-  it.dir = Dir(prm.pass[it.pass].dir);
+  const CorePass& ps = prm.pass[it.pass];
+  it.b = ps.div_nh.div(bh);
+  it.h = bh - uint32_t(it.b) * uint32_t(ps.nh);
+  if (ps.kvp) {
+    it.sh = int(it.h);
+    it.sub = int(p.G);
+    it.bh0 = int(it.h * p.G);
+  } else {
+    it.sh = int(it.h / p.G);
+    it.sub = 1;
+    it.bh0 = it.sh;
+  }
+  it.dir = Dir(ps.dir);
   it.beg = seg_begin(it.dir, it.seg, p.seg_len, p.C);
   it.end = seg_end(it.dir, it.seg, p.seg_len, p.C);
   it.nblk = int((it.end - it.beg + BT - 1) / BT);
@@ -556,7 +581,7 @@ __device__ __forceinline__ int64_t cblock_row(const CItem& it, int j) {
 }
 struct CoreBars {
   uint64_t full[3], empty[3], s_full[2], s_empty[2];
-  uint64_t p_full[2], ku_full, ds_full, ds_empty, st_full[2], st_empty[2], o_full, o_empty;
+  uint64_t p_full[2], ku_full, ku_empty, ds_full, ds_empty, st_full[2], st_empty[2], o_full, o_empty;
   uint64_t stg_full, stg_empty;
   ItemQueue iq;
   uint32_t tmem_slot;
@@ -565,7 +590,7 @@ struct CoreBars {
 static_assert(sizeof(CoreBars) <= 256, "CoreBars must fit its 256-byte slot");
 constexpr int kFoldChunk = 256;  // float2 elements per claimed fold chunk (one per fold thread)
 __device__ __forceinline__ unsigned fold_chunks(const Plan& p) {
-  return unsigned((p.B * p.H * p.D * p.D / 2 + kFoldChunk - 1) / kFoldChunk);
+  return unsigned((p.B * p.Hk * p.D * p.D / 2 + kFoldChunk - 1) / kFoldChunk);
 }
 
 
@@ -580,7 +605,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   const uint32_t sbase = smem_u32(sm);
 
   const Plan& p = prm.p;
-  const int64_t W = p.B * p.H * p.nseg * prm.npass * L::NV;
+  const int64_t W = p.nseg * int64_t(prm.per);
   const uint32_t warp = warp_id(), lane = lane_id();
 #ifdef LASP_TRACE_BUILD
   if (prm.trace != nullptr && threadIdx.x == 0) prm.trace[2 * 1024 + blockIdx.x * 2] = globaltimer();
@@ -594,7 +619,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     for (int s = 0; s < ST; ++s) { mbar_init(&bar->full[s], 1); mbar_init(&bar->empty[s], 2); }
     for (int s = 0; s < 2; ++s) { mbar_init(&bar->s_full[s], 1); mbar_init(&bar->s_empty[s], 1); }
     mbar_init(&bar->p_full[0], 128); mbar_init(&bar->p_full[1], 128);
-    mbar_init(&bar->ku_full, 128);
+    mbar_init(&bar->ku_full, 128); mbar_init(&bar->ku_empty, 1);
     mbar_init(&bar->ds_full, 1); mbar_init(&bar->ds_empty, 128);
     for (int b2 = 0; b2 < L::NSB; ++b2) { mbar_init(&bar->st_full[b2], 128); mbar_init(&bar->st_empty[b2], 1); }
     mbar_init(&bar->o_full, 1); mbar_init(&bar->o_empty, 128);
@@ -619,7 +644,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
   if (prm.fold.gbar != nullptr && warp >= 8) {
     const unsigned n_chunks = fold_chunks(p);
     pdl_wait();
-    const int64_t n2 = p.B * p.H * p.D * p.D / 2;
+    const int64_t n2 = p.B * p.Hk * p.D * p.D / 2;
     for (;;) {
       if (threadIdx.x == 256) bar->fold_chunk = atomicAdd(&prm.fold.gbar[0], 1u);
       named_bar_sync(2, 256);
@@ -652,7 +677,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             if (k == 0 && prm.fold.gbar != nullptr) grid_wait(&prm.fold.gbar[1], fold_chunks(p));
             mbar_wait(&bar->stg_empty, (k & 1) ^ 1);
             mbar_expect_tx(&bar->stg_full, 4 * D * D);
-            const int srow = int(((it.b * p.H + it.h) * p.nseg + it.seg) * D);
+            const int srow = int(((it.b * p.Hk + it.sh) * p.nseg + it.seg) * D);
 #pragma unroll
             for (int x = 0; x < D / 32; ++x)
               tma_load_2d(sm + L::STG + x * (D * 128), &prm.mst[ps.state], &bar->stg_full, x * 32, srow);
@@ -662,8 +687,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         const CUtensorMap* ma = &prm.min[ps.a];
         const CUtensorMap* mb = &prm.min[ps.b];
         const CUtensorMap* mc = &prm.min[ps.c];
-        for (int j = 0; j < it.nblk; ++j, ++J) {
-          if (!waited && j == (it.nblk < ST ? it.nblk : ST)) {
+        const int nsb = it.nblk * it.sub;  // sub-blocks: block j = jj / sub, summed query head u = jj % sub
+        for (int jj = 0; jj < nsb; ++jj, ++J) {
+          if (!waited && jj == (nsb < ST ? nsb : ST)) {
             pdl_wait();
             pdl_trigger();
             waited = true;
@@ -673,13 +699,14 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           mbar_wait(&bar->empty[s], ((J / ST) & 1) ^ 1);
           LASP_TRACE(0, J);
           mbar_expect_tx(&bar->full[s], L::STAGE);
-          const int t0 = int(cblock_row(it, j));
+          const int j = it.sub == 1 ? jj : jj / it.sub;
+          const int t0 = int(cblock_row(it, j)), hb = it.bh0 + (jj - j * it.sub);
 #pragma unroll
           for (int x = 0; x < L::NBOX; ++x) {
             tma_load_4d(sm + L::A(s) + x * BOX, ma, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
-            tma_load_4d(sm + L::B_(s) + x * BOX, mb, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
+            tma_load_4d(sm + L::B_(s) + x * BOX, mb, &bar->full[s], x * 64, hb, t0, int(it.b));
           }
-          tma_load_4d(sm + L::C_(s), mc, &bar->full[s], it.v * 64, int(it.h), t0, int(it.b));
+          tma_load_4d(sm + L::C_(s), mc, &bar->full[s], it.v * 64, hb, t0, int(it.b));
         }
         if (!waited) {  // first item shorter than the ring
           pdl_wait();
@@ -702,13 +729,15 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       constexpr uint32_t id_pv = idesc_bf16(128, 64, 0, 1);
       constexpr uint32_t id_x = idesc_bf16(128, 64, 0, 1);
       auto koff = [](int kk) -> uint32_t { return uint32_t(kk >> 2) * BOX + uint32_t(kk & 3) * 32; };
-      uint32_t J = 0, kd = 0;
+      uint32_t J = 0, Jb = 0, kd = 0, nku = 0;  // J: sub-blocks (ring, S buffers), Jb: blocks (outputs, state)
       for (uint32_t k = 0;; ++k) {
         const int64_t w = q_fetch(bar->iq, k);
         q_release(bar->iq, k);
         if (w >= W) break;
-        const int nblk = get_citem<L::NV>(prm, w).nblk;
-        for (int j = 0; j < nblk; ++j, ++J) {
+        const CItem itm = get_citem<L::NV>(prm, w);
+        const int nblk = itm.nblk, sub = itm.sub;
+        for (int jj = 0; jj < nblk * sub; ++jj, ++J) {
+          const int j = sub == 1 ? jj : jj / sub, u = jj - j * sub;
           const int s = int(J % ST);
           if (warp == 2) {
             // S = a b^T (double-buffered in TMEM; buffer J & 1 is free once out(J-2) has read its P)
@@ -723,48 +752,57 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             mma_commit(&bar->s_full[J & 1]);
             LASP_TRACE(1, J);
           } else if (warp == 3) {
-            // dS = b^T (u . c), only for blocks that are not the last of their segment
+            // dS = sum_u b_u^T (u . c_u), only for blocks that are not the last of their segment
             if (j + 1 < nblk) {
-              mbar_wait(&bar->ku_full, kd & 1);
-              mbar_wait(&bar->ds_empty, (kd & 1) ^ 1);
+              mbar_wait(&bar->ku_full, nku & 1);
+              if (u == 0) mbar_wait(&bar->ds_empty, (kd & 1) ^ 1);
               tc_fence_after();
 #pragma unroll
               for (int kk = 0; kk < BT / 16; ++kk)
                 mma_bf16(tmem + L::T_DS, desc_mn(sbase + L::B_(s) + kk * 2048, BOX),
-                         desc_mn(sbase + L::KU + kk * 2048, BOX), id_ds, kk != 0);
-              mma_commit(&bar->ds_full);
+                         desc_mn(sbase + L::KU + kk * 2048, BOX), id_ds, (kk | u) != 0);
+              mma_commit(&bar->ku_empty);  // the u . c buffer is free once this MMA has read it
+              if (u + 1 == sub) {
+                mma_commit(&bar->ds_full);
+                ++kd;
+              }
               mma_commit(&bar->empty[s]);
               LASP_TRACE(2, J);
-              ++kd;
+              ++nku;
             }
           } else {
             // O_inter = a (S_hi + S_lo) first: it does not depend on the mask, so the tensor pipe runs it
             // while the mask warps build P; then O_intra = P c. (This issuer waits on the ring slot itself for
             // the a tile; it also releases the slot, so the parity wait stays within one phase.)
             mbar_wait(&bar->full[s], (J / ST) & 1);
-            mbar_wait(&bar->o_empty, (J & 1) ^ 1);
-            LASP_TRACE(12, J);
-            mbar_wait(&bar->st_full[J % L::NSB], (J / L::NSB) & 1);
-            tc_fence_after();
-            const int sb = int(J % L::NSB);
+            const int sb = int(Jb % L::NSB);
+            if (u == 0) {  // once per block: the inter term of the block's rows
+              mbar_wait(&bar->o_empty, (Jb & 1) ^ 1);
+              LASP_TRACE(12, J);
+              mbar_wait(&bar->st_full[sb], (Jb / L::NSB) & 1);
+              tc_fence_after();
 #pragma unroll
-            for (int kk = 0; kk < L::DK / 16; ++kk)
-              mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SBF(sb) + kk * 2048, BOX),
-                       id_x, kk != 0);
+              for (int kk = 0; kk < L::DK / 16; ++kk)
+                mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SBF(sb) + kk * 2048, BOX),
+                         id_x, kk != 0);
 #pragma unroll
-            for (int kk = 0; kk < L::DK / 16; ++kk)
-              mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SLO(sb) + kk * 2048, BOX),
-                       id_x, 1);
+              for (int kk = 0; kk < L::DK / 16; ++kk)
+                mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SLO(sb) + kk * 2048, BOX),
+                         id_x, 1);
+            }
             mbar_wait(&bar->p_full[J & 1], (J >> 1) & 1);
             LASP_TRACE(11, J);
             tc_fence_after();
             const uint32_t pt = tmem + ((J & 1) ? L::T_S1 : L::T_S0);  // P in TMEM (2 bf16 / column)
 #pragma unroll
             for (int kk = 0; kk < BT / 16; ++kk)
-              mma_bf16_ts(tmem + L::T_OI, pt + kk * 8, desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv, kk != 0);
-            mma_commit(&bar->o_full);
+              mma_bf16_ts(tmem + L::T_OI, pt + kk * 8, desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv, (kk | u) != 0);
+            if (u + 1 == sub) {
+              mma_commit(&bar->o_full);
+              mma_commit(&bar->st_empty[sb]);
+              ++Jb;
+            }
             mma_commit(&bar->s_empty[J & 1]);  // S/P buffer reusable once P c has been read
-            mma_commit(&bar->st_empty[J % L::NSB]);
             mma_commit(&bar->empty[s]);
             if (j + 1 == nblk) mma_commit(&bar->empty[s]);  // no dS for the segment's last block
             LASP_TRACE(3, J);
@@ -781,7 +819,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       if (w >= W) break;
       const CItem it = get_citem<L::NV>(prm, w);
       const bool fwd = it.dir == Dir::FWD;
-      const float l2 = p.l2lam[it.h];
+      const float l2 = p.l2lam[it.sh];
       // Per-thread decay factors of its row, kept in registers for the whole item. With e(u) = lane - u
       // (FWD) or u - lane (REV), column u of chunk c4 has M = lam^(32 |c4 - q4| + e(u)) on the live side:
       //   diagonal chunk (c4 = q4):  dm[u] = lam^e(u) for e(u) >= 0, else 0 (the causal cut)
@@ -800,7 +838,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         t[u] = fast_exp2(x + x32);
       }
       const float sc2 = fast_exp2(32.f * l2), sc3 = fast_exp2(64.f * l2);  // off-diagonal distance 2, 3
-      for (int j = 0; j < it.nblk; ++j, ++J) {
+      for (int jj = 0; jj < it.nblk * it.sub; ++jj, ++J) {  // every sub-block has its own S / P
         const int sb = J & 1;
         mbar_wait(&bar->s_full[sb], (J >> 1) & 1);
         if (lane == 0 && q4 == 3) LASP_TRACE(4, J);
@@ -893,7 +931,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             __syncwarp();
           }
         }
-        const float* st = prm.stp[state] + ((it.b * p.H + it.h) * p.nseg + it.seg) * D * D;
+        const float* st = prm.stp[state] + ((it.b * p.Hk + it.sh) * p.nseg + it.seg) * D * D;
         // states of the preceding kernel: read-only here (ld.global.nc); states folded by this launch: plain
         // (L1-allocating) loads after the acquire in grid_wait -- the fold read them with ld.global.cg, so
         // this SM's L1 holds no copy older than the fold's writes. (Each thread's 16 float4 row loads share
@@ -919,20 +957,22 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         for (int e = 0; e < 64; ++e) S[e] = __int_as_float(0x7fc00000);
       }
     };
-    uint32_t J = 0, kd = 0;
+    uint32_t J = 0, Js = 0, kd = 0, nku = 0;  // J: blocks (state copies), Js: sub-blocks (ring), nku: u.c fills
     for (uint32_t k = 0;; ++k) {
       const int64_t w = q_fetch_warp(bar->iq, k);
       if (w >= W) break;
       const CItem it = get_citem<L::NV>(prm, w);
       const CorePass& ps = prm.pass[it.pass];
       load_state(k, it, ps.trans != 0, ps.state);
-      const float l2 = p.l2lam[it.h];
+      const float l2 = p.l2lam[it.sh];
       const uint32_t u2 = bf16x2_splat(exp2f(float(it.dir == Dir::FWD ? (BT - 1 - g) : (g + 1)) * l2));
       const float decay = exp2f(float(BT) * l2);
-      // u (.) c for dS = b^T (u . c) of block JJ (the Ku buffer is free once dS of the previous block
-      // has been loaded), done early so the dS MMA is never waiting on it
+      // u (.) c for dS = b^T (u . c) of sub-block JJ (the Ku buffer is free once the dS MMA of the previous
+      // sub-block has read it: ku_empty), done early so the dS MMA is never waiting on it
       auto scale_ku = [&](uint32_t JJ) {
         const int s = JJ % ST;
+        mbar_wait(&bar->ku_empty, (nku & 1) ^ 1);
+        ++nku;
         mbar_wait(&bar->full[s], (JJ / ST) & 1);
 #ifdef LASP_EXPERIMENT_NOSTATE
         if (false)
@@ -945,7 +985,8 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         fence_async_smem();
         mbar_arrive(&bar->ku_full);
       };
-      if (it.nblk > 1) scale_ku(J);
+      const int sub = it.sub;
+      if (it.nblk > 1) scale_ku(Js);
       for (int j = 0;; ++j, ++J) {
         // bf16 hi/lo copy of the state entering block J into buffer J % NSB (free once the output MMAs
         // of block J - NSB are done)
@@ -973,7 +1014,11 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         fence_async_smem();
         mbar_arrive(&bar->st_full[sb]);
         if (g == 0) LASP_TRACE(7, J);
-        if (j + 1 == it.nblk) break;  // no state leaves the last block of a segment
+        if (j + 1 == it.nblk) {  // no state leaves the last block of a segment
+          Js += sub;
+          break;
+        }
+        for (int u = 1; u < sub; ++u) scale_ku(Js + u);  // the block's other summed query heads
         // S_{J+1} = lam^128 S_J + dS_J
         mbar_wait(&bar->ds_full, kd & 1);
         if (g == 0) LASP_TRACE(6, J);
@@ -993,7 +1038,8 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         tc_fence_before();
         mbar_arrive(&bar->ds_empty);
         ++kd;
-        if (j + 2 < it.nblk) scale_ku(J + 1);
+        Js += sub;
+        if (j + 2 < it.nblk) scale_ku(Js);
       }
       ++J;  // the break skipped the increment of the last block
     }
@@ -1009,7 +1055,8 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       const CItem it = get_citem<L::NV>(prm, w);
       const CUtensorMap* mo = &prm.mout[prm.pass[it.pass].out];
       __nv_bfloat16* outp = prm.outp[prm.pass[it.pass].out];
-      const float r = exp2f(float(it.dir == Dir::FWD ? (i + 1) : (BT - 1 - i)) * p.l2lam[it.h]);
+      const int64_t oh = prm.pass[it.pass].nh;  // heads of the output tensor
+      const float r = exp2f(float(it.dir == Dir::FWD ? (i + 1) : (BT - 1 - i)) * p.l2lam[it.sh]);
       for (int j = 0; j < it.nblk; ++j, ++J) {
         mbar_wait(&bar->o_full, J & 1);
         if (i == 0) LASP_TRACE(8, J);
@@ -1042,7 +1089,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           // coordinates), so only this segment's rows are written, directly from registers (ADVICE r1:
           // a full-tile store raced with the previous segment's store of the same rows)
           if (t0 + i >= it.beg) {
-            uint4* dst = reinterpret_cast<uint4*>(outp + ((it.b * p.C + (t0 + i)) * p.H + it.h) * D + it.v * 64);
+            uint4* dst = reinterpret_cast<uint4*>(outp + ((it.b * p.C + (t0 + i)) * oh + it.h) * D + it.v * 64);
 #pragma unroll
             for (int c = 0; c < 8; ++c) dst[c] = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
           }
@@ -1094,7 +1141,7 @@ int sm_count() {
 }
 
 unsigned persistent_grid(const Plan& p, int per_sm = 1) {
-  const int64_t W = p.B * p.H * p.nseg;
+  const int64_t W = p.B * p.Hk * p.nseg;
   const int64_t g = W < int64_t(sm_count()) * per_sm ? W : int64_t(sm_count()) * per_sm;
   return unsigned(g > 0 ? g : 1);
 }
@@ -1104,9 +1151,12 @@ cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, 
                        unsigned* claim) {
   SegParams prm;
   prm.claim = static_items() ? nullptr : claim;
+  // F1 reads k, v (Hk heads); B1 reads q, do (H heads), summing the G query heads of each state head
+  prm.sub = DIR == Dir::FWD ? 1 : int(p.G);
+  const int64_t heads = DIR == Dir::FWD ? p.Hk : p.H;
   cudaError_t e;
-  if ((e = make_seq_map(&prm.mx, x, p)) != cudaSuccess) return e;
-  if ((e = make_seq_map(&prm.my, y, p)) != cudaSuccess) return e;
+  if ((e = make_seq_map(&prm.mx, x, p, heads)) != cudaSuccess) return e;
+  if ((e = make_seq_map(&prm.my, y, p, heads)) != cudaSuccess) return e;
   prm.p = p;
   prm.out = out;
   prm.trace = g_trace ? g_trace + 16 * 64 : nullptr;  // second trace region: segment-state kernel
@@ -1132,17 +1182,30 @@ cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const 
   };
   const float* sts[2];
   int nst = 0;
+  int64_t in_heads[4] = {0, 0, 0, 0};
+  uint32_t off = 0;
+  constexpr int NV = CoreLayout<D>::NV;
   for (int x = 0; x < npass; ++x) {
     CorePass& ps = prm.pass[x];
     ps.dir = int(dirs[x]);
     ps.trans = a[x].trans_state;
+    ps.kvp = a[x].kv_pass;
+    // heads of a and out, and of b and c (grouped queries: a kv-head pass reads query-side b, c)
+    const int64_t ha = ps.kvp ? p.Hk : p.H, hbc = ps.kvp ? p.H : p.Hk;
     ps.a = in_index(a[x].a);
+    in_heads[ps.a] = ha;
     ps.b = in_index(a[x].b);
+    in_heads[ps.b] = hbc;
     ps.c = in_index(a[x].c);
+    in_heads[ps.c] = hbc;
     if (nin > 4) return cudaErrorInvalidValue;
+    ps.nh = int(ha);
+    ps.div_nh = FastDiv(uint32_t(ha));
+    ps.off = off;
+    off += uint32_t(p.B * ha * NV);
     ps.out = x;
     prm.outp[x] = static_cast<__nv_bfloat16*>(a[x].out);
-    if ((e = make_seq_map(&prm.mout[x], a[x].out, p)) != cudaSuccess) return e;
+    if ((e = make_seq_map(&prm.mout[x], a[x].out, p, ha)) != cudaSuccess) return e;
     ps.state = -1;
     for (int y = 0; y < nst; ++y)
       if (sts[y] == a[x].state) ps.state = y;
@@ -1155,7 +1218,7 @@ cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const 
     }
   }
   for (int x = 0; x < nin; ++x)
-    if ((e = make_seq_map(&prm.min[x], ins[x], p)) != cudaSuccess) return e;
+    if ((e = make_seq_map(&prm.min[x], ins[x], p, in_heads[x])) != cudaSuccess) return e;
   for (int x = nin; x < 4; ++x) prm.min[x] = prm.min[0];
   if (nst < 2) { prm.mst[1] = prm.mst[0]; prm.stp[1] = prm.stp[0]; }
   prm.p = p;
@@ -1164,13 +1227,15 @@ cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const 
   prm.claim = claim;
   prm.trace = g_trace;
   if (fold) prm.fold = *fold;
-  prm.div_nbh = FastDiv(uint32_t(p.B * p.H * CoreLayout<D>::NV));
-  prm.div_per = FastDiv(uint32_t(p.B * p.H * CoreLayout<D>::NV * npass));
+  prm.per = off;
+  prm.div_per = FastDiv(off);
+  prm.uniform = 1;
+  for (int x = 1; x < npass; ++x) prm.uniform &= prm.pass[x].nh == prm.pass[0].nh;
   if (static_items()) prm.claim = nullptr;
   auto kern = core_tc_kernel<D>;
   const int smem = int(CoreLayout<D>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
-  const int64_t W = p.B * p.H * p.nseg * npass * CoreLayout<D>::NV;
+  const int64_t W = p.nseg * int64_t(off);
   // reserve_sms: SMs left free for kernels of another stream (the ring's NCCL kernels while a hop is in
   // flight): a persistent CTA holds an SM's whole register file and shared memory until the launch ends
   int64_t slots = sm_count() - (reserve_sms > 0 && reserve_sms < sm_count() ? reserve_sms : 0);
@@ -1209,7 +1274,7 @@ bool tc_fold_fusable(const Plan& p) {
     const char* s = std::getenv("LASP_FOLD_MAX_ROUNDS");
     return s && *s ? std::atoll(s) : int64_t(2);
   }();
-  return tc_supported(p) && p.B * p.H * p.D * p.D / 2 <= rounds * sm_count() * kFoldChunk;
+  return tc_supported(p) && p.B * p.Hk * p.D * p.D / 2 <= rounds * sm_count() * kFoldChunk;
 }
 
 void tc_set_trace(unsigned long long* buf) { g_trace = buf; }

@@ -79,31 +79,39 @@ int64_t choose_seg_len(int64_t B, int64_t C, int64_t H, int64_t D) {
   return seg_blocks * q;
 }
 
+int64_t kv_heads(const lasp_shape_t* s) { return s->kv_heads > 0 ? s->kv_heads : s->heads; }
+
 lasp_status_t validate_shape(const lasp_shape_t* s) {
   if (!s) return fail(LASP_ERR_SHAPE, "shape is NULL");
-  if (s->batch < 1 || s->n_local < 0 || s->heads < 1)
-    return fail(LASP_ERR_SHAPE, "need batch >= 1, n_local >= 0, heads >= 1");
+  if (s->batch < 1 || s->n_local < 0 || s->heads < 1 || s->kv_heads < 0)
+    return fail(LASP_ERR_SHAPE, "need batch >= 1, n_local >= 0, heads >= 1, kv_heads >= 0");
   if (s->heads > kMaxHeads) return fail(LASP_ERR_UNSUPPORTED, "heads > 256 not supported");
   if (s->head_dim != 32 && s->head_dim != 64 && s->head_dim != 128)
     return fail(LASP_ERR_UNSUPPORTED, "head_dim must be 32, 64 or 128");
   if (s->dtype != LASP_BF16 && s->dtype != LASP_FP32) return fail(LASP_ERR_SHAPE, "bad dtype");
+  if (s->heads % kv_heads(s) != 0) return fail(LASP_ERR_SHAPE, "kv_heads must divide heads (grouped-query attention)");
+  if (kv_heads(s) != s->heads && !(s->dtype == LASP_BF16 && (s->head_dim == 64 || s->head_dim == 128)))
+    return fail(LASP_ERR_UNSUPPORTED, "grouped-query attention (kv_heads < heads) needs bf16 and head_dim 64 or 128");
   return LASP_OK;
 }
 
 Plan make_plan(const lasp_shape_t* s) {
   Plan p{};
   p.B = s->batch; p.C = s->n_local; p.H = s->heads; p.D = s->head_dim;
+  p.Hk = kv_heads(s);
+  p.G = p.H / p.Hk;
   p.dtype = s->dtype == LASP_BF16 ? 0 : 1;
   p.seg_len = choose_seg_len(p.B, p.C, p.H, p.D);
   p.nseg = p.C > 0 ? (p.C + p.seg_len - 1) / p.seg_len : 1;
-  p.div_bh = FastDiv(uint32_t(p.B * p.H));
-  p.div_h = FastDiv(uint32_t(p.H));
+  p.div_bhk = FastDiv(uint32_t(p.B * p.Hk));
+  p.div_hk = FastDiv(uint32_t(p.Hk));
   return p;
 }
 
+// one decay per state head (kv-head): the state of a query group is shared, so is its decay (reading G1)
 lasp_status_t load_lambda(Plan& p, const float* lambda) {
   if (!lambda) return fail(LASP_ERR_SHAPE, "lambda is NULL");
-  for (int64_t h = 0; h < p.H; ++h) {
+  for (int64_t h = 0; h < p.Hk; ++h) {
     const float l = lambda[h];
     if (!(l > 0.f && l <= 1.f)) {
       char buf[96];
@@ -116,8 +124,8 @@ lasp_status_t load_lambda(Plan& p, const float* lambda) {
   return LASP_OK;
 }
 
-size_t state_elems(const Plan& p) { return size_t(p.B * p.H * p.D * p.D); }
-size_t seg_state_elems(const Plan& p) { return size_t(p.B * p.H * p.nseg * p.D * p.D); }
+size_t state_elems(const Plan& p) { return size_t(p.B * p.Hk * p.D * p.D); }
+size_t seg_state_elems(const Plan& p) { return size_t(p.B * p.Hk * p.nseg * p.D * p.D); }
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Workspace {
@@ -200,7 +208,7 @@ lasp_status_t check_device() {
 // judged by its contents) and records mismatching words in the call's status word.
 uint64_t hash_lam(const Plan& p) {
   uint64_t h = 1469598103934665603ull;
-  for (int64_t i = 0; i < p.H; ++i) {
+  for (int64_t i = 0; i < p.Hk; ++i) {
     uint32_t bits;
     std::memcpy(&bits, &p.lam[i], 4);
     h = (h ^ bits) * 1099511628211ull;
@@ -219,6 +227,7 @@ CacheTag make_tag(const Plan& p, int rank, int world) {
   t.w[kTagLam] = hash_lam(p);
   t.w[kTagRank] = uint64_t(int64_t(rank));
   t.w[kTagWorld] = uint64_t(int64_t(world));
+  t.w[kTagHk] = uint64_t(p.Hk);
   t.w[kTagGen] = ++g_generation;  // diagnostics only (not compared)
   return t;
 }
@@ -226,6 +235,7 @@ CacheTag make_tag(const Plan& p, int rank, int world) {
 unsigned tag_mask(bool check_rank) {
   unsigned m = 0;
   for (int i = kTagMagic; i <= kTagLam; ++i) m |= 1u << i;
+  m |= 1u << kTagHk;
   if (check_rank) m |= (1u << kTagRank) | (1u << kTagWorld);
   return m;
 }
@@ -528,7 +538,7 @@ lasp_status_t exchange_allgather(lasp_ctx* c, const Plan& p, const float* local,
                                  cudaStream_t st) {
   // each rank contributes [state (n floats) | its n_local (int64) | pad] so that ranks of different lengths
   // fold correctly (fold_ranks_kernel decays rank j's contribution with its own lam^(C_j))
-  const size_t n = size_t(p.B * p.H * p.D * p.D);
+  const size_t n = state_elems(p);
   const size_t stride = n + 64;  // 256-byte trailer
   if (c->gather_elems < stride * size_t(c->world + 1)) {
     if (c->gather) LASP_CUDA(cudaFree(c->gather));
@@ -620,7 +630,8 @@ lasp_status_t lasp_workspace_status(const void* workspace, void* stream) {
   LASP_CUDA(cudaMemcpy(&bits, static_cast<const unsigned*>(workspace) + 2, sizeof bits, cudaMemcpyDeviceToHost));
   if (bits == 0) return LASP_OK;
   static const char* names[kTagWords] = {"magic (not a cache written by lasp_fwd*)", "batch", "n_local", "heads",
-                                         "head_dim", "segment length", "dtype", "lambda", "rank", "world"};
+                                         "head_dim", "segment length", "dtype", "lambda", "rank", "world",
+                                         "kv_heads"};
   std::string msg = "cache tag mismatch (backward without a matching forward, S:411):";
   for (int i = 0; i < kTagWords; ++i)
     if ((bits >> i) & 1u) msg += std::string(" ") + (names[i] ? names[i] : "?");
@@ -675,8 +686,8 @@ lasp_status_t lasp_bwd_local(const lasp_shape_t* shape, const void* q, const voi
   const PrefixFold fold{dkv_in, w.seg, w.seg, dkv_out, w.gbar, int(Dir::REV)};
   if (!fuse) LASP_CUDA(prefix(p, Dir::REV, dkv_in, w.seg, w.seg, dkv_out, st));         // B2 (in place)
   // B3: dQ (needs only the cache), dV and dK in one launch (with B2 folded in when fused)
-  const SeqArgs passes[3] = {{d_o, v, k, dq, P, 1, w.status()}, {k, q, d_o, dv, w.seg, 0, w.status()},
-                             {v, d_o, q, dk, w.seg, 1, w.status()}};
+  const SeqArgs passes[3] = {{d_o, v, k, dq, P, 1, w.status(), 0}, {k, q, d_o, dv, w.seg, 0, w.status(), 1},
+                             {v, d_o, q, dk, w.seg, 1, w.status(), 1}};
   const Dir dirs[3] = {Dir::FWD, Dir::REV, Dir::REV};
   LASP_CUDA(core_multi(p, 3, passes, dirs, st, w.claim(1), fuse ? &fold : nullptr));
   return LASP_OK;
@@ -790,7 +801,7 @@ lasp_status_t lasp_ctx_protocol(lasp_ctx_t c, const lasp_shape_t* shape, int64_t
     if (sends_fwd) *sends_fwd = c->world > 1 ? 1 : 0;
     if (sends_bwd) *sends_bwd = c->world > 1 ? 1 : 0;
   }
-  if (elems_per_msg) *elems_per_msg = shape->batch * shape->heads * shape->head_dim * shape->head_dim;
+  if (elems_per_msg) *elems_per_msg = shape->batch * kv_heads(shape) * shape->head_dim * shape->head_dim;
   return LASP_OK;
 }
 
@@ -878,7 +889,7 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   if (p.C == 0) return LASP_OK;
   if (!fuse) LASP_CUDA(prefix(p, Dir::REV, w.in, w.seg, w.seg, nullptr, st));   // B2
   {  // dV and dK in one launch (with B2 folded in when fused)
-    const SeqArgs passes[2] = {{k, q, d_o, dv, w.seg, 0, w.status()}, {v, d_o, q, dk, w.seg, 1, w.status()}};
+    const SeqArgs passes[2] = {{k, q, d_o, dv, w.seg, 0, w.status(), 1}, {v, d_o, q, dk, w.seg, 1, w.status(), 1}};
     const Dir dirs[2] = {Dir::REV, Dir::REV};
     const PrefixFold fold{w.in, w.seg, w.seg, nullptr, w.gbar, int(Dir::REV)};
     LASP_CUDA(core_multi(p, 2, passes, dirs, st, w.claim(2), fuse ? &fold : nullptr));

@@ -80,12 +80,13 @@ struct FastDiv {
 };
 
 struct Plan {
-  int64_t B, C, H, D;  // batch, n_local, heads, head_dim
+  int64_t B, C, H, D;  // batch, n_local, (query) heads, head_dim
+  int64_t Hk, G;       // key/value heads = state heads, and query heads per kv-head (G = H / Hk; MHA: Hk = H)
   int dtype;           // 0 = bf16, 1 = fp32
   int64_t seg_len;     // multiple of kSegQuantum
   int64_t nseg;        // >= 1
-  FastDiv div_bh, div_h;  // / (B*H), / H (work-item decode)
-  float lam[256];      // per-head decay (fp32, the boundary's precision; reading A8), by value
+  FastDiv div_bhk, div_hk;  // / (B*Hk), / Hk (work-item decode of the state kernels)
+  float lam[256];      // per-state-head decay (fp32, the boundary's precision; reading A8), by value, [Hk]
   float l2lam[256];    // log2(lam) computed in fp64 on the host, rounded once (tcgen05 path: exp2 powers)
 };
 constexpr int64_t kMaxHeads = 256;
@@ -108,7 +109,7 @@ __host__ __device__ inline int64_t seg_end(Dir, int64_t p, int64_t L, int64_t C)
 // call's status word (workspace). A backward whose status is nonzero poisons every state it loads with
 // NaN, so all its outputs are NaN (loud), and lasp_workspace_status() reports LASP_ERR_STATE.
 enum TagWord { kTagMagic = 0, kTagB, kTagC, kTagH, kTagD, kTagSeg, kTagDtype, kTagLam, kTagRank, kTagWorld,
-               kTagGen, kTagWords = 16 };
+               kTagHk, kTagGen, kTagWords = 16 };
 struct CacheTag { uint64_t w[kTagWords]; };
 constexpr size_t kCacheTagBytes = 256;
 constexpr uint64_t kTagMagicValue = 0x4c41535043414348ull;  // "LASPCACH"
@@ -119,13 +120,18 @@ cudaError_t launch_tag(const CacheTag& t, uint64_t* hdr, unsigned check_mask, un
 __device__ __forceinline__ bool tag_poisoned(const unsigned* status) { return status != nullptr && __ldcg(status) != 0u; }
 
 // Kernel launch interfaces (kernels_simt.cu, kernels_tc.cu). All return cudaGetLastError().
-// Sequence tensors are [B][C][H][D]; state arrays are [B][H][nseg][D][D] fp32.
+// Sequence tensors are [B][C][H][D] (queries-side: q, o, do, dq) or [B][C][Hk][D] (k, v, dk, dv); state
+// arrays are [B][Hk][nseg][D][D] fp32.
 struct SeqArgs {
   const void* a; const void* b; const void* c;  // core: out rows from a, keys b, values c
   void* out;
-  const float* state;     // device [B][H][nseg][D][D] (state entering each segment)
+  const float* state;     // device [B][Hk][nseg][D][D] (state entering each segment)
   int trans_state;        // use S^T of the stored state
   const unsigned* status = nullptr;  // cache-tag status of the call (backward), nullptr = unchecked
+  // grouped-query passes (NEXT-4): 0 = a query-head pass (O, dQ: items over the H query heads, a and out
+  // have H heads, b, c and the state are those of kv-head h / G); 1 = a kv-head pass (dV, dK: items over
+  // the Hk kv-heads, a and out have Hk heads, and every block sums the G query heads h = hk G + u of b, c)
+  int kv_pass = 0;
 };
 
 cudaError_t launch_seg_state_simt(const Plan& p, Dir dir, const void* x, const void* y,

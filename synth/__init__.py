@@ -125,9 +125,12 @@ def head_lambdas(heads: int, scalar: float | None = None) -> np.ndarray:
 
 def problem(seed: int, batch: int, n_global: int, heads: int, head_dim: int,
             dtype: str = "bf16", lam: float | None = None, token_lo: int = 0,
-            token_hi: int | None = None, with_do: bool = True) -> dict:
-    """Convenience: q, k, v (and do) shards plus the float32 per-head lambda vector."""
-    t = {nm: draw(nm, seed, batch, n_global, heads, head_dim, dtype, token_lo, token_hi)
+            token_hi: int | None = None, with_do: bool = True, kv_heads: int | None = None) -> dict:
+    """Convenience: q, k, v (and do) shards plus the float32 per-head lambda vector. ``kv_heads``
+    (grouped-query attention): k, v are drawn with that many heads and lambda has one entry per kv-head."""
+    hk = heads if kv_heads is None else kv_heads
+    t = {nm: draw(nm, seed, batch, n_global, hk if nm in ("k", "v") else heads, head_dim, dtype, token_lo,
+                  token_hi)
          for nm in (("q", "k", "v", "do") if with_do else ("q", "k", "v"))}
-    t["lam"] = head_lambdas(heads, lam)
+    t["lam"] = head_lambdas(hk, lam)
     return t

@@ -516,3 +516,68 @@ def test_concurrent_streams_fused_fold(L):
         for got, want in zip(outs, ref):
             for a, b in zip(got, want):
                 assert torch.equal(a, b)
+
+
+# ---- grouped-query / multi-query attention ---------------------------------
+def run_sim_ring_gqa(L, p, T, n_global):
+    """As run_sim_ring, with k, v (dk, dv, the states and lambda) on Hk < H heads."""
+    C = n_global // T
+    dev = {k: to_dev(p[k], torch.bfloat16) for k in ("q", "k", "v", "do")}
+    lam = p["lam"]
+    outs, caches, kv = [], [], None
+    for r in range(T):
+        sl = slice(r * C, (r + 1) * C)
+        q, k, v = (dev[x][:, sl].contiguous() for x in ("q", "k", "v"))
+        o, kv, cache = L.fwd_local(q, k, v, lam, kv_in=kv)
+        outs.append(o)
+        caches.append(cache)
+    grads, dkv = [None] * T, None
+    for r in range(T - 1, -1, -1):
+        sl = slice(r * C, (r + 1) * C)
+        q, k, v, do = (dev[x][:, sl].contiguous() for x in ("q", "k", "v", "do"))
+        dq, dk, dv, dkv = L.bwd_local(q, k, v, lam, do, caches[r], dkv_in=dkv, check_state=True)
+        grads[r] = (dq, dk, dv)
+    torch.cuda.synchronize()
+    cat = lambda ts: torch.cat(ts, dim=1).float().cpu().numpy()
+    return cat(outs), cat([g[0] for g in grads]), cat([g[1] for g in grads]), cat([g[2] for g in grads])
+
+
+@pytest.mark.parametrize("B,N,H,Hk,D,T", [(1, 1536, 4, 2, 64, 2),     # GQA, 2 ranks
+                                          (1, 1000, 8, 1, 128, 1),    # MQA, ragged, head_dim 128
+                                          (2, 2048, 6, 3, 64, 4),     # batch 2, 4 ranks
+                                          (1, 3000, 8, 2, 128, 3),    # ragged ranks, several segments
+                                          (1, 640, 4, 4, 64, 2)])     # Hk = H through the GQA API (= MHA)
+def test_gqa_sim_ring_matches_oracle(L, oracle_mod, B, N, H, Hk, D, T):
+    p = synth.problem(60 + H + Hk, B, N, H, D, dtype="bf16", kv_heads=Hk)
+    got = run_sim_ring_gqa(L, p, T, N)
+    refs = [oracle_mod.fwd_gqa(p["q"], p["k"], p["v"], p["lam"])] + \
+        list(oracle_mod.bwd_gqa(p["q"], p["k"], p["v"], p["lam"], p["do"]))
+    errs = {n: per_head_err(x, r) for n, x, r in zip(("o", "dq", "dk", "dv"), got, refs)}
+    assert max(errs.values()) <= BF16_TOL, errs
+
+
+@pytest.mark.parametrize("H,Hk,D", [(16, 4, 64), (16, 4, 128)])
+def test_gqa_tnl_shapes_full_size(L, oracle_mod, H, Hk, D):
+    """TNL-0.4B / TNL-1B layer shapes (32K tokens) with 4 kv-heads (G = 4), every element against the
+    oracle's grouped-query recurrence."""
+    N = 32768
+    p = synth.problem(7, 1, N, H, D, dtype="bf16", kv_heads=Hk)
+    got = run_sim_ring_gqa(L, p, 1, N)
+    refs = [oracle_mod.fwd_gqa(p["q"], p["k"], p["v"], p["lam"])] + \
+        list(oracle_mod.bwd_gqa(p["q"], p["k"], p["v"], p["lam"], p["do"]))
+    errs = {n: per_head_err(x, r) for n, x, r in zip(("o", "dq", "dk", "dv"), got, refs)}
+    assert max(errs.values()) <= BF16_TOL, errs
+
+
+def test_gqa_deterministic_and_rejects_unsupported(L):
+    from paper_2404_02882_b200._native import LaspError
+    p = synth.problem(61, 1, 2000, 8, 64, dtype="bf16", kv_heads=2)
+    a = run_sim_ring_gqa(L, p, 2, 2000)
+    b = run_sim_ring_gqa(L, p, 2, 2000)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    q = torch.zeros((1, 128, 4, 32), dtype=torch.bfloat16, device="cuda")   # head_dim 32: CUDA-core path
+    k = torch.zeros((1, 128, 2, 32), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(LaspError) as e:
+        L.fwd_local(q, k, k, [0.9, 0.9])
+    assert e.value.name == "LASP_ERR_UNSUPPORTED"

@@ -118,8 +118,8 @@ def _run_loopback(p, world, n_global, dtype, group, exchange="ring", bounds=None
                 o, cache = ring.fwd(q, k, v, p["lam"])
                 dq, dk, dv = ring.bwd(q, k, v, p["lam"], do, cache)
             stream.synchronize()
-            B, Cr, H, D = q.shape
-            seg = lasp.segment_len(lasp.api._shape(q))
+            B, Cr, H, D = k.shape   # states are per kv-head
+            seg = lasp.segment_len(lasp.api._shape(q, k))
             nseg = (Cr + seg - 1) // seg
             # cache [B][H][nseg][D][D]; entry 0 of each (b, h) = KV_in(r), the state entering the rank
             kv_in = cache.view(torch.float32)[:B * H * nseg * D * D].view(B, H, nseg, D, D)[:, :, 0]
@@ -155,6 +155,19 @@ def test_loopback_ring_bf16_matches_oracle(oracle_mod, world, exchange):
     got, _ = _run_loopback(p, world, N, torch.bfloat16, f"bf16-w{world}-{exchange}", exchange)
     refs = [oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])] + \
         list(oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"]))
+    for x, r in zip(got, refs):
+        assert oracle_mod.normwise_err(x, r) <= 2e-2
+
+
+@pytest.mark.parametrize("exchange", ["ring", "allgather"])
+def test_loopback_gqa_ring(oracle_mod, exchange):
+    """Grouped-query attention across a 3-rank ring: the messages are the Hk = 2 shared kv-head states."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    p = synth.problem(48, 1, 3 * 768, 8, 128, dtype="bf16", kv_heads=2)
+    got, _ = _run_loopback(p, 3, 3 * 768, torch.bfloat16, f"gqa-{exchange}", exchange)
+    refs = [oracle_mod.fwd_gqa(p["q"], p["k"], p["v"], p["lam"])] + \
+        list(oracle_mod.bwd_gqa(p["q"], p["k"], p["v"], p["lam"], p["do"]))
     for x, r in zip(got, refs):
         assert oracle_mod.normwise_err(x, r) <= 2e-2
 

@@ -393,3 +393,66 @@ def test_dkv_chain_matches_definition(oracle_mod):
         dkv = oracle_mod.dkv_update(dkv, Q[t * C:(t + 1) * C], dO[t * C:(t + 1) * C], lf, lc)
         ref = sum(l64 ** (g - t * C + 1) * np.outer(Q[g], dO[g]) for g in range(t * C, N))
         assert rel(dkv, ref) <= 1e-13
+
+
+# ---- grouped-query / multi-query attention (reading G1) -------------
+def dense_torch_gqa(q, k, v, lam, do):
+    """Dense masked form per query head with the group's key/value head (k, v expanded along heads by
+    torch.repeat_interleave), O and the fp64 autograd gradients -- the expansion makes autograd sum dK, dV
+    over the group's query heads. lam is per kv-head."""
+    B, N, H, D = q.shape
+    Hk = k.shape[2]
+    G = H // Hk
+    tq, tk, tv = (torch.tensor(x, dtype=torch.float64, requires_grad=True) for x in (q, k, v))
+    ke, ve = tk.repeat_interleave(G, dim=2), tv.repeat_interleave(G, dim=2)
+    outs = []
+    for h in range(H):
+        M = torch.tensor(dense_mask(N, float(np.float64(np.float32(lam[h // G])))))
+        s = torch.einsum("bid,bjd->bij", tq[:, :, h], ke[:, :, h]) * M
+        outs.append(torch.einsum("bij,bjd->bid", s, ve[:, :, h]))
+    o = torch.stack(outs, dim=2)
+    (o * torch.tensor(do)).sum().backward()
+    return o.detach().numpy(), tq.grad.numpy(), tk.grad.numpy(), tv.grad.numpy()
+
+
+@pytest.mark.parametrize("H,Hk", [(4, 2), (6, 1), (8, 4)])
+def test_gqa_matches_dense_autograd(oracle_mod, H, Hk):
+    rng = np.random.default_rng(H * 10 + Hk)
+    B, N, D = 2, 96, 8
+    q, do = (rng.standard_normal((B, N, H, D)) for _ in range(2))
+    k, v = (rng.standard_normal((B, N, Hk, D)) for _ in range(2))
+    lam = rng.uniform(0.5, 1.0, Hk).astype(np.float32)
+    lam[0] = 1.0
+    o_ref, dq_ref, dk_ref, dv_ref = dense_torch_gqa(q, k, v, lam, do)
+    o = oracle_mod.fwd_gqa(q, k, v, lam)
+    dq, dk, dv = oracle_mod.bwd_gqa(q, k, v, lam, do)
+    for x, r in ((o, o_ref), (dq, dq_ref), (dk, dk_ref), (dv, dv_ref)):
+        assert x.shape == r.shape and rel(x, r) <= 1e-12
+
+
+def test_gqa_one_group_is_mha_bitwise(oracle_mod):
+    """G = 1 (Hk = H) is the pinned MHA recurrence, operation for operation."""
+    p = rand_problem(12, 2, 70, 3, 5)
+    o = oracle_mod.fwd_gqa(p["q"], p["k"], p["v"], p["lam"])
+    g = oracle_mod.bwd_gqa(p["q"], p["k"], p["v"], p["lam"], p["do"])
+    assert np.array_equal(o, oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"]))
+    for a, b in zip(g, oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"])):
+        assert np.array_equal(a, b)
+
+
+def test_mqa_is_mha_with_repeated_kv(oracle_mod):
+    """Hk = 1: O equals the MHA oracle with k, v repeated for every head; dK, dV equal the MHA gradients
+    summed over the heads (linearity of L in the shared k, v)."""
+    rng = np.random.default_rng(5)
+    B, N, H, D = 1, 130, 4, 6
+    q, do = (rng.standard_normal((B, N, H, D)) for _ in range(2))
+    k, v = (rng.standard_normal((B, N, 1, D)) for _ in range(2))
+    lam = np.array([0.93], dtype=np.float32)
+    kr, vr = np.repeat(k, H, axis=2), np.repeat(v, H, axis=2)
+    o = oracle_mod.fwd_gqa(q, k, v, lam)
+    dq, dk, dv = oracle_mod.bwd_gqa(q, k, v, lam, do)
+    o_m = oracle_mod.fwd(q, kr, vr, np.repeat(lam, H))
+    dq_m, dk_m, dv_m = oracle_mod.bwd(q, kr, vr, np.repeat(lam, H), do)
+    assert rel(o, o_m) <= 1e-13 and rel(dq, dq_m) <= 1e-13
+    assert rel(dk, dk_m.sum(axis=2, keepdims=True)) <= 1e-12
+    assert rel(dv, dv_m.sum(axis=2, keepdims=True)) <= 1e-12
