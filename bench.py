@@ -226,19 +226,24 @@ class ThreadComm:
         return m
 
 
-def closed_form_check(lasp, dev, B, C, H, D, lam, rank, T, run):
+def closed_form_check(lasp, dev, B, C, H, D, lam, rank, T, run, Hk=None):
     """Self-check of the timed configuration before timing (every rank, every exchange): constant inputs
     q_s = q, k_s = k, v_s = v, do_s = do per head have closed forms derived from Eq. 4 (SURVEY §8(c) pin 5,
     the same forms tests/test_gpu_parity.py checks): with s the GLOBAL 1-based position and N = T*C,
       o_s = (q.k) v g(s),  dq_s = (v.do) k g(s),  dk_s = (v.do) q g(N-s+1),  dv_s = (q.k) do g(N-s+1),
-    g(n) = (1 - lam^n) / (1 - lam) (n for lam = 1). Returns the worst normwise error at sampled positions."""
+    g(n) = (1 - lam^n) / (1 - lam) (n for lam = 1). Grouped queries (Hk < H): query head h uses kv-head
+    h // (H/Hk) and its lambda; dk, dv of a kv-head sum the terms of its query heads.
+    Returns the worst normwise error at sampled positions."""
     import numpy as np
     import torch
+    Hk = Hk or H
+    G = H // Hk
     rng = np.random.default_rng(123)
-    vecs = [rng.standard_normal((H, D)).astype(np.float32) * 0.3 for _ in range(4)]
+    shapes = [(H, D), (Hk, D), (Hk, D), (H, D)]
+    vecs = [rng.standard_normal(sh).astype(np.float32) * 0.3 for sh in shapes]
     vecs = [torch.from_numpy(v).to(torch.bfloat16).float().numpy().astype(np.float64) for v in vecs]
     qv, kv_, vv, dov = vecs
-    mk = lambda a: torch.from_numpy(np.broadcast_to(a.astype(np.float32), (B, C, H, D)).copy()).to(
+    mk = lambda a: torch.from_numpy(np.broadcast_to(a.astype(np.float32), (B, C) + a.shape).copy()).to(
         device=dev, dtype=torch.bfloat16)
     o, dq, dk, dv = run(mk(qv), mk(kv_), mk(vv), mk(dov))
     torch.cuda.synchronize(dev)
@@ -246,15 +251,24 @@ def closed_form_check(lasp, dev, B, C, H, D, lam, rank, T, run):
     idx = np.unique(np.clip(np.array([0, 1, 2, 127, 128, 1000, C // 2, C - 2, C - 1]), 0, C - 1))
     s = (rank * C + idx + 1).astype(np.float64)
     worst = 0.0
+
+    def geo(l):
+        return (lambda n: n) if l == 1.0 else (lambda n: (1 - l ** n) / (1 - l))
+
+    def err(got, h, ref):
+        x = got[0, idx, h].float().cpu().numpy().astype(np.float64)
+        return float(np.max(np.abs(x - ref)) / max(np.max(np.abs(ref)), 1e-30))
+
     for h in range(H):
-        l = float(np.float64(np.float32(lam[h])))
-        g = (lambda n: n) if l == 1.0 else (lambda n: (1 - l ** n) / (1 - l))
-        qk, vd = float(qv[h] @ kv_[h]), float(vv[h] @ dov[h])
-        for got, ref in ((o, qk * np.outer(g(s), vv[h])), (dq, vd * np.outer(g(s), kv_[h])),
-                         (dk, vd * np.outer(g(N - s + 1), qv[h])), (dv, qk * np.outer(g(N - s + 1), dov[h]))):
-            x = got[0, idx, h].float().cpu().numpy().astype(np.float64)
-            den = max(np.max(np.abs(ref)), 1e-30)
-            worst = max(worst, float(np.max(np.abs(x - ref)) / den))
+        hk = h // G
+        g = geo(float(np.float64(np.float32(lam[hk]))))
+        qk, vd = float(qv[h] @ kv_[hk]), float(vv[hk] @ dov[h])
+        worst = max(worst, err(o, h, qk * np.outer(g(s), vv[hk])), err(dq, h, vd * np.outer(g(s), kv_[hk])))
+    for hk in range(Hk):
+        g = geo(float(np.float64(np.float32(lam[hk]))))
+        rk = sum(float(vv[hk] @ dov[h]) * qv[h] for h in range(hk * G, (hk + 1) * G))
+        rv = sum(float(qv[h] @ kv_[hk]) * dov[h] for h in range(hk * G, (hk + 1) * G))
+        worst = max(worst, err(dk, hk, np.outer(g(N - s + 1), rk)), err(dv, hk, np.outer(g(N - s + 1), rv)))
     return worst
 
 
@@ -283,6 +297,9 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
     H, D, C, desc = CONFIGS[args.config]
     if args.tokens:
         C = args.tokens
+    Hk = args.kv_heads or H
+    if Hk != H:
+        desc = f"{desc} [grouped-query: {Hk} kv-heads]"
     B = 1
     lib = N.lib()
     T = args.sp_size or world
@@ -290,13 +307,15 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
     G = world // T
     stream = torch.cuda.current_stream(dev)
     # inputs: this rank's shard [t*C, (t+1)*C) of its group's sequence (seed = group id)
-    p = synth.problem(grp_id, B, C * T, H, D, dtype="bf16", token_lo=grank * C, token_hi=(grank + 1) * C)
+    p = synth.problem(grp_id, B, C * T, H, D, dtype="bf16", token_lo=grank * C, token_hi=(grank + 1) * C,
+                      kv_heads=Hk)
     lam = p["lam"]
     host = {k: torch.from_numpy(p[k]) for k in ("q", "k", "v", "do")}
     d_in = {k: v.to(dev, torch.bfloat16) for k, v in host.items()}
     q, k, v, do = d_in["q"], d_in["k"], d_in["v"], d_in["do"]
-    o, dq, dk, dv = (torch.empty_like(q) for _ in range(4))
-    cache, ws = lasp.alloc_cache(q), lasp.alloc_workspace(q)
+    o, dq = torch.empty_like(q), torch.empty_like(q)
+    dk, dv = torch.empty_like(k), torch.empty_like(v)
+    cache, ws = lasp.alloc_cache(q, k), lasp.alloc_workspace(q, k)
     # N > 1: time the paper's ring and the all-gather exchange (NEXT-2) in the same run; `value` is the ring
     if T > 1:
         exchanges = ["ring", "allgather"] if args.exchange == "both" else [args.exchange]
@@ -328,10 +347,10 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
         if ring is not None:
             ring.set_exchange(ex)
         # (0) parity gate through this exact code path (closed forms, every rank), before any timing
-        cws, ccache = lasp.alloc_workspace(q), lasp.alloc_cache(q)
+        cws, ccache = lasp.alloc_workspace(q, k), lasp.alloc_cache(q, k)
 
         def run_const(a, b, c, d):
-            oo, dd = torch.empty_like(a), [torch.empty_like(a) for _ in range(3)]
+            oo, dd = torch.empty_like(a), [torch.empty_like(a), torch.empty_like(b), torch.empty_like(c)]
             if ring is None:
                 lasp.fwd_local(a, b, c, lam, o=oo, kv_out=False, cache=ccache, workspace=cws)
                 lasp.bwd_local(a, b, c, lam, d, ccache, dq=dd[0], dk=dd[1], dv=dd[2], dkv_out=False, workspace=cws)
@@ -339,7 +358,7 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
                 ring.fwd(a, b, c, lam, o=oo, cache=ccache, workspace=cws)
                 ring.bwd(a, b, c, lam, d, ccache, dq=dd[0], dk=dd[1], dv=dd[2], workspace=cws)
             return [oo] + dd
-        err = closed_form_check(lasp, dev, B, C, H, D, lam, grank, T, run_const)
+        err = closed_form_check(lasp, dev, B, C, H, D, lam, grank, T, run_const, Hk)
         err = comm.max(err, rank) if loopback else comm.max(err)
         del cws, ccache
         step = step_fn(ex)
@@ -425,11 +444,11 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
         if ring is not None:
             ring.set_exchange(main_ex)
         pin = {kk: vv.to(torch.bfloat16).pin_memory() for kk, vv in host.items()}
-        outs_h = [torch.empty(q.shape, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
+        outs_h = [torch.empty(t.shape, dtype=torch.bfloat16).pin_memory() for t in (q, q, k, v)]
         n_e2e = max(3, min(args.steps, 20))
         h2d = sum(int(x.numel()) * 2 for x in pin.values())
         d2h = sum(int(x.numel()) * 2 for x in outs_h)
-        bufs = [({kk: torch.empty_like(d_in[kk]) for kk in d_in}, [torch.empty_like(q) for _ in range(4)])
+        bufs = [({kk: torch.empty_like(d_in[kk]) for kk in d_in}, [torch.empty_like(t) for t in (q, q, k, v)])
                 for _ in range(2)]
         s_up, s_dn = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         ev_in = [torch.cuda.Event() for _ in range(2)]
@@ -499,23 +518,24 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
         a_[1] += ms_
     dom_name, (dom_n, dom_ms) = max(fam.items(), key=lambda kv: kv[1][1]) if fam else ("none", (1, 0.0))
     per_launch_ms = dom_ms / max(dom_n, 1)
-    seg_len = lasp.segment_len(N.shape(B, C, H, D, N.LASP_BF16))
+    seg_len = lasp.segment_len(N.shape(B, C, H, D, N.LASP_BF16, Hk if Hk != H else 0))
     nseg = -(-C // seg_len)
-    st_bytes = 4 * B * H * D * D                        # one fp32 D x D state per (batch, head)
+    st_bytes = 4 * B * Hk * D * D                       # one fp32 D x D state per (batch, kv-head)
+    hq = (H + Hk) / 2                                   # mean heads per tensor (q-side H, kv-side Hk)
     if dom_name.startswith("core_bwd3"):
         # the B3 row reads Q, K, V, dO and writes dQ, dK, dV once (14D B per token-head) plus
         # 2 states per pass (the cached KV_in and the received dKV_in)
-        bytes_per_launch = 7 * 2 * D * B * C * H + 2 * st_bytes
+        bytes_per_launch = int(2 * D * B * C * (3 * H + 4 * Hk)) + 2 * st_bytes  # Q, dO, dQ: H heads; K, V, dK, dV: Hk
         unit_note = "14*D bytes per token-head (Q,K,V,dO bf16 reads + dQ,dK,dV bf16 writes; B3 row) + 2*B*H*D^2*4"
         # this design's extra state traffic: the 3 passes read one prefix state per segment, and (fused B2)
         # the fold reads and writes the nseg segment states
         overhead = 3 * nseg * st_bytes - 2 * st_bytes + (2 * nseg * st_bytes if "prefix_rev" not in stages else 0)
     elif dom_name.startswith("core"):
-        bytes_per_launch = 4 * 2 * D * B * C * H + 2 * st_bytes  # a, b, c read + out written, 8D B/token-head
+        bytes_per_launch = int(2 * D * B * C * (2 * H + 2 * Hk)) + 2 * st_bytes  # Q, K, V read + O written
         unit_note = "8*D bytes per token-head (3 bf16 reads + 1 bf16 write) + 2*B*H*D^2*4"
         overhead = nseg * st_bytes - 2 * st_bytes + (2 * nseg * st_bytes if "prefix" not in stages else 0)
     elif dom_name.startswith("seg_state"):
-        bytes_per_launch = 2 * 2 * D * B * C * H          # reads two bf16 tensors: 4D B/token-head
+        bytes_per_launch = int(2 * 2 * D * B * C * hq)    # reads two bf16 tensors: 4D B/token-head
         unit_note = "4*D bytes per token-head (2 bf16 reads)"
         overhead = nseg * st_bytes
     else:
@@ -536,7 +556,7 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
                 "overhead_bytes_per_launch": overhead, "overhead_frac": (bytes_per_launch + overhead) / max(
                     per_launch_ms / 1e3, 1e-12) / 1e9 / hbm, "bytes_rule": unit_note, "peak_source": peak_src,
                 "duration_us": per_launch_ms * 1e3}
-    path_bytes = 22 * D * B * C * H
+    path_bytes = int(2 * D * B * C * (5 * H + 6 * Hk))  # 22D per token-head at Hk = H
     path = {"bytes_per_step": path_bytes, "achieved_gbs": path_bytes / (ms_step / 1e3) / 1e9,
             "frac_of_hbm": path_bytes / (ms_step / 1e3) / 1e9 / hbm,
             "tc_peak_frac": B * C * H * alg_flops_per_token_head(D) / (ms_step / 1e3) / (tflops * 1e12),
@@ -557,7 +577,7 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (synth/, seed 0; bf16 inputs)",
             "config": {"workload": desc if not args.tokens else f"{desc} [n_local overridden: {C}]",
                        "global_batch": B * G, "seq_len": C * T, "n_local": C, "heads": H,
-                       "head_dim": D, "lambda": "per-head 1-2^-(1+14h/(H-1))", "segment_len": seg_len,
+                       "head_dim": D, "kv_heads": Hk, "lambda": "per-head 1-2^-(1+14h/(H-1))", "segment_len": seg_len,
                        "l2": "flushed between timed steps (256 MiB read outside the step events); inputs 4x"
                              f" {B * C * H * D * 2 >> 20} MiB", "parallelism": f"dp{G}xsp{T}" if G > 1 else f"sp{T}",
                        "launch": ex_report[main_ex]["launch"], "exchange": main_ex},
@@ -647,6 +667,8 @@ def main():
                     help="run N ranks as threads on ONE GPU with the in-process loopback transport (the whole N>1 "
                          "code path incl. the closed-form parity gate; not a scaling measurement)")
     ap.add_argument("--tokens", type=int, default=0, help="override n_local (tokens per GPU) of --config")
+    ap.add_argument("--kv-heads", type=int, default=0,
+                    help="grouped-query attention: key/value heads (default: the config's heads, i.e. multi-head)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

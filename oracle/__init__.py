@@ -11,6 +11,9 @@ this module only builds/loads it and marshals numpy arrays. Functions:
   Eq. 13-14 (P:257-272).
 * ``fwd_gqa`` / ``bwd_gqa`` -- the same recurrences with H query heads sharing Hk key/value heads
   (multi-query / grouped-query attention).
+* ``norm_fwd`` / ``norm_bwd`` / ``layer_fwd`` / ``layer_bwd`` -- the steps either side of the path
+  (SURVEY §8(f) NEXT-3): Q, K, V = X W (Alg. 2) and Norm(.) of Eq. 2 read as per-head RMS
+  normalization (reading N1).
 * ``lasp_fwd_sim`` / ``lasp_bwd_sim`` -- Alg. 2 (P:141-176) and Alg. 3 (P:574-653) run
   literally with T simulated ranks, explicit messages and a KV cache.
 * chunk ops (``build_decay``, ``intra_fwd``, ``inter_fwd``, ``kv_update``, ``intra_bwd``,
@@ -46,7 +49,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
         tmp = _LIB_PATH + f".{os.getpid()}.tmp"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math",
-                               "-ffp-contract=off", "-o", tmp, _SRC, "-lpthread"])
+                               "-ffp-contract=off", "-o", tmp, _SRC, "-lpthread", "-lm"])
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
 
@@ -58,6 +61,10 @@ def _load():
             lib = ctypes.CDLL(build())
             lib.oracle_fwd.argtypes = [_i64] * 4 + [_dp] * 3 + [_fp, _dp, ctypes.c_int]
             lib.oracle_bwd.argtypes = [_i64] * 4 + [_dp] * 3 + [_fp] + [_dp] * 4 + [ctypes.c_int]
+            lib.oracle_norm_fwd.argtypes = [_i64, _i64, ctypes.c_double, _dp, _dp, _dp]
+            lib.oracle_norm_bwd.argtypes = [_i64, _i64, _dp, _dp, _dp, _dp]
+            lib.oracle_norm_fwd.restype = ctypes.c_int
+            lib.oracle_norm_bwd.restype = ctypes.c_int
             lib.oracle_fwd_gqa.argtypes = [_i64] * 5 + [_dp] * 3 + [_fp, _dp, ctypes.c_int]
             lib.oracle_bwd_gqa.argtypes = [_i64] * 5 + [_dp] * 3 + [_fp] + [_dp] * 4 + [ctypes.c_int]
             lib.oracle_build_decay.argtypes = [_i64, ctypes.c_float, _dp, _dp, _dp, _dp]
@@ -157,6 +164,60 @@ def bwd_gqa(q, k, v, lam, do, nthreads=None):
     _check(_load().oracle_bwd_gqa(B, N, H, Hk, D, _ptr(q), _ptr(k), _ptr(v), lp, _ptr(do), _ptr(dq), _ptr(dk),
                                   _ptr(dv), _threads(nthreads)))
     return dq, dk, dv
+
+
+NORM_EPS = 1e-6  # DESIGN.md reading N1
+
+
+def norm_fwd(o, eps=NORM_EPS):
+    """Norm(O) of Eq. 2 read as per-head RMS normalization (reading N1): o [..][D] ->
+    (y = o r, r = (mean_c o_c^2 + eps)^-1/2 with shape o.shape[:-1])."""
+    o = _f64(o)
+    D = o.shape[-1]
+    rows = o.size // D if D else 0
+    y, r = np.zeros_like(o), np.zeros(o.shape[:-1])
+    _check(_load().oracle_norm_fwd(rows, D, float(eps), _ptr(o), _ptr(y), _ptr(r)))
+    return y, r
+
+
+def norm_bwd(y, r, dy):
+    """dO = r (dY - y (y . dY) / D) per row, the gradient of norm_fwd."""
+    y, r, dy = _f64(y), _f64(r), _f64(dy)
+    D = y.shape[-1]
+    out = np.zeros_like(y)
+    _check(_load().oracle_norm_bwd(y.size // D, D, _ptr(y), _ptr(r), _ptr(dy), _ptr(out)))
+    return out
+
+
+def layer_fwd(x, w_q, w_k, w_v, lam, H, Hk=None, eps=NORM_EPS, nthreads=None):
+    """NEXT-3 layer: Alg. 2 line 'Calculate Q = X W_Q, K = X W_K, V = X W_V' (numpy matmul as the
+    library step), LASP O (fwd / fwd_gqa), then Norm (reading N1). x [B][N][d], w_* [d][heads * D].
+    Returns dict with q, k, v [B][N][heads][D], o, y, r."""
+    x = _f64(x)
+    B, N, d = x.shape
+    Hk = Hk or H
+    q = (x @ _f64(w_q)).reshape(B, N, H, -1)
+    k = (x @ _f64(w_k)).reshape(B, N, Hk, -1)
+    v = (x @ _f64(w_v)).reshape(B, N, Hk, -1)
+    o = fwd_gqa(q, k, v, lam, nthreads) if Hk != H else fwd(q, k, v, lam, nthreads)
+    y, r = norm_fwd(o, eps)
+    return {"q": q, "k": k, "v": v, "o": o, "y": y, "r": r}
+
+
+def layer_bwd(x, w_q, w_k, w_v, lam, fw, dy, nthreads=None):
+    """Gradients of sum(Y * dY) for layer_fwd: (dX [B][N][d], dW_Q, dW_K, dW_V [d][heads * D], dO)."""
+    x = _f64(x)
+    B, N, d = x.shape
+    q, k, v = fw["q"], fw["k"], fw["v"]
+    do = norm_bwd(fw["y"], fw["r"], dy)
+    if k.shape[2] != q.shape[2]:
+        dq, dk, dv = bwd_gqa(q, k, v, lam, do, nthreads)
+    else:
+        dq, dk, dv = bwd(q, k, v, lam, do, nthreads)
+    dq2, dk2, dv2 = (t.reshape(B * N, -1) for t in (dq, dk, dv))
+    x2 = x.reshape(B * N, d)
+    dx = (dq2 @ _f64(w_q).T + dk2 @ _f64(w_k).T + dv2 @ _f64(w_v).T).reshape(B, N, d)
+    return dx, x2.T @ dq2, x2.T @ dk2, x2.T @ dv2, do
 
 
 def lasp_fwd_sim(q, k, v, lam, T, nthreads=None):

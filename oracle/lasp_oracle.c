@@ -26,6 +26,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 
 #define ORACLE_OK 0
 #define ORACLE_ERR_SHAPE 1
@@ -296,6 +297,39 @@ int oracle_bwd_gqa(int64_t B, int64_t N, int64_t H, int64_t Hk, int64_t D, const
     if (st) return st;
     gqa_ctx_t c = {B, N, H, Hk, D, q, k, v, dout, lam, NULL, dq, dk, dv};
     run_items(gqa_bwd_item, &c, B * Hk, nthreads);
+    return ORACLE_OK;
+}
+
+/* ---------------------------------------------------------------------------------- */
+/* Norm(.) of Eq. 2 (the paper omits it from the derivation, and does not   */
+/* define it). DESIGN.md reading N1: per-head RMS normalization (TransNormerLLM's        */
+/* SRMSNorm applied to each head's d-vector, no learnable gain -- a gain folds into the  */
+/* output projection):  y = o * r,  r = (sum_c o_c^2 / D + eps)^(-1/2), per (b, s, h).   */
+/* Backward: do = r * (dy - y * (y . dy) / D).                                            */
+/* o, y, dy, do: [B][N][H][D]; r: [B][N][H].                                              */
+/* ---------------------------------------------------------------------------------- */
+int oracle_norm_fwd(int64_t rows, int64_t D, double eps, const double* o, double* y, double* r) {
+    if (rows < 0 || D < 1 || !(eps >= 0.0) || !o || !y || !r) return ORACLE_ERR_SHAPE;
+    for (int64_t i = 0; i < rows; ++i) {
+        const double* oi = o + i * D;
+        double ss = 0.0;
+        for (int64_t c = 0; c < D; ++c) ss += oi[c] * oi[c];
+        const double ri = 1.0 / sqrt(ss / (double)D + eps);
+        for (int64_t c = 0; c < D; ++c) y[i * D + c] = oi[c] * ri;
+        r[i] = ri;
+    }
+    return ORACLE_OK;
+}
+
+int oracle_norm_bwd(int64_t rows, int64_t D, const double* y, const double* r, const double* dy, double* dout) {
+    if (rows < 0 || D < 1 || !y || !r || !dy || !dout) return ORACLE_ERR_SHAPE;
+    for (int64_t i = 0; i < rows; ++i) {
+        const double* yi = y + i * D;
+        const double* gi = dy + i * D;
+        double dot = 0.0;
+        for (int64_t c = 0; c < D; ++c) dot += yi[c] * gi[c];
+        for (int64_t c = 0; c < D; ++c) dout[i * D + c] = r[i] * (gi[c] - yi[c] * dot / (double)D);
+    }
     return ORACLE_OK;
 }
 

@@ -456,3 +456,64 @@ def test_mqa_is_mha_with_repeated_kv(oracle_mod):
     assert rel(o, o_m) <= 1e-13 and rel(dq, dq_m) <= 1e-13
     assert rel(dk, dk_m.sum(axis=2, keepdims=True)) <= 1e-12
     assert rel(dv, dv_m.sum(axis=2, keepdims=True)) <= 1e-12
+
+
+# ---- NEXT-3: Norm(.) (Eq. 2; reading N1) and the projection prologue (Alg. 2) ----------------
+def test_norm_known_values_and_invariants(oracle_mod):
+    o = np.array([[3.0, 4.0], [0.0, 0.0], [-1.0, 1.0]])
+    y, r = oracle_mod.norm_fwd(o, eps=0.0 + 1e-300)
+    np.testing.assert_allclose(y[0], [3 / np.sqrt(12.5), 4 / np.sqrt(12.5)], rtol=1e-15)
+    np.testing.assert_allclose(y[2], [-1.0, 1.0], rtol=1e-15)      # mean square 1 already
+    assert np.all(y[1] == 0.0)                                      # eps keeps the zero row finite
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((50, 64))
+    y, r = oracle_mod.norm_fwd(x, eps=0.0)
+    np.testing.assert_allclose(np.mean(y * y, axis=1), 1.0, rtol=1e-13)          # unit RMS
+    y2, _ = oracle_mod.norm_fwd(7.5 * x, eps=0.0)
+    np.testing.assert_allclose(y2, y, rtol=1e-13, atol=1e-15)                      # scale invariance
+    dy = rng.standard_normal((50, 64))
+    do = oracle_mod.norm_bwd(y, r, dy)
+    np.testing.assert_allclose(np.sum(do * x, axis=1), 0.0, atol=1e-11)            # d/dc Norm(c x) = 0
+
+
+def test_norm_matches_torch_rms_norm(oracle_mod):
+    """The reading N1 normalization is exactly torch.nn.functional.rms_norm over the head dimension (a
+    library routine), forward and backward (fp64 autograd)."""
+    rng = np.random.default_rng(4)
+    o = rng.standard_normal((2, 33, 3, 16))
+    dy = rng.standard_normal(o.shape)
+    y, r = oracle_mod.norm_fwd(o)
+    t = torch.tensor(o, requires_grad=True)
+    ty = torch.nn.functional.rms_norm(t, (16,), eps=oracle_mod.NORM_EPS)
+    (ty * torch.tensor(dy)).sum().backward()
+    assert rel(y, ty.detach().numpy()) <= 1e-14
+    assert rel(oracle_mod.norm_bwd(y, r, dy), t.grad.numpy()) <= 1e-13
+
+
+@pytest.mark.parametrize("H,Hk", [(2, 2), (4, 2)])
+def test_layer_matches_dense_autograd(oracle_mod, H, Hk):
+    """The NEXT-3 layer Y = Norm(LASP(X W_Q, X W_K, X W_V)) and its gradients (dX, dW_*) against torch fp64
+    autograd of the dense masked form (Eq. 2 with the reading-N1 Norm)."""
+    rng = np.random.default_rng(H + Hk)
+    B, N, D = 2, 48, 8
+    d = H * D
+    x = rng.standard_normal((B, N, d))
+    wq, wk, wv = (rng.standard_normal((d, h * D)) * d ** -0.5 for h in (H, Hk, Hk))
+    dy = rng.standard_normal((B, N, H, D))
+    lam = rng.uniform(0.6, 1.0, Hk).astype(np.float32)
+    fw = oracle_mod.layer_fwd(x, wq, wk, wv, lam, H, Hk)
+    dx, dwq, dwk, dwv, _ = oracle_mod.layer_bwd(x, wq, wk, wv, lam, fw, dy)
+    tx, tq, tk, tv = (torch.tensor(a, requires_grad=True) for a in (x, wq, wk, wv))
+    q = (tx @ tq).reshape(B, N, H, D)
+    k = (tx @ tk).reshape(B, N, Hk, D).repeat_interleave(H // Hk, dim=2)
+    v = (tx @ tv).reshape(B, N, Hk, D).repeat_interleave(H // Hk, dim=2)
+    outs = []
+    for h in range(H):
+        M = torch.tensor(dense_mask(N, float(np.float64(np.float32(lam[h // (H // Hk)])))))
+        outs.append(torch.einsum("bij,bjd->bid", torch.einsum("bid,bjd->bij", q[:, :, h], k[:, :, h]) * M,
+                                 v[:, :, h]))
+    y = torch.nn.functional.rms_norm(torch.stack(outs, dim=2), (D,), eps=oracle_mod.NORM_EPS)
+    (y * torch.tensor(dy)).sum().backward()
+    assert rel(fw["y"], y.detach().numpy()) <= 1e-12
+    for a, b in ((dx, tx.grad), (dwq, tq.grad), (dwk, tk.grad), (dwv, tv.grad)):
+        assert rel(a, b.numpy()) <= 1e-11
