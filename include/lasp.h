@@ -229,6 +229,35 @@ lasp_status_t lasp_bwd(lasp_ctx_t ctx, const lasp_shape_t* shape, const void* q,
                        const void* v, const float* lambda, const void* d_o, const void* cache,
                        void* dq, void* dk, void* dv, void* workspace, void* stream);
 
+/* ---- the steps either side of the path: one attention layer ----
+ *
+ *   Q = X W_Q, K = X W_K, V = X W_V          (Alg. 2; X is this rank's chunk, [B][C][d_model])
+ *   O = LASP(Q, K, V; lambda)                (as lasp_fwd_local / lasp_fwd)
+ *   Y = Norm(O)                              (Eq. 2; the paper leaves Norm undefined, P:180 --
+ *                                             DESIGN.md reading N1: per-head RMS normalization
+ *                                             y = o r, r = (mean_c o_c^2 + 1e-6)^(-1/2) per (b, s, h))
+ * ctx == NULL: a single rank (no ring; the state entering the rank is zero); else the ring of ctx.
+ * Layouts: x [B][C][d_model] bf16; w_q [d_model][H*D], w_k, w_v [d_model][Hk*D] bf16 (row-major, so
+ * X W_Q is the [B][C][H][D] layout of q); q, y, d_o, dq [B][C][H][D] bf16; k, v, dk, dv [B][C][Hk][D]
+ * bf16; rnorm [B][C][H] fp32; dx bf16 like x; dw_* fp32 like w_*. Needs bf16 and head_dim 64 or 128.
+ * Fusion: the projections are plain tensor-core GEMMs (cuBLAS, loaded at first use; LASP_CUBLAS_LIB
+ * overrides the library path); the Norm runs in the epilogue of the forward core kernel (head_dim 64:
+ * y and r written directly; head_dim 128: the two value-slice items of a row meet in a second, elementwise
+ * phase), and its backward dO = r (dY - y (y . dY) / D) runs inside the B1 kernel (dKV-state
+ * accumulation), which writes dO to d_o for the B3 passes. workspace: lasp_layer_workspace_bytes. */
+size_t lasp_layer_workspace_bytes(const lasp_shape_t* shape);
+lasp_status_t lasp_layer_fwd(lasp_ctx_t ctx, const lasp_shape_t* shape, int64_t d_model, const void* x,
+                             const void* w_q, const void* w_k, const void* w_v, const float* lambda,
+                             void* q, void* k, void* v, void* y, float* rnorm, void* cache, void* workspace,
+                             void* stream);
+/* Gradients of sum(Y * dY): dx, dw_q, dw_k, dw_v (and the intermediates d_o = dL/dO, dq, dk, dv, which
+ * the caller provides as scratch). q, k, v, y, rnorm and cache come from lasp_layer_fwd. */
+lasp_status_t lasp_layer_bwd(lasp_ctx_t ctx, const lasp_shape_t* shape, int64_t d_model, const void* x,
+                             const void* w_q, const void* w_k, const void* w_v, const float* lambda,
+                             const void* q, const void* k, const void* v, const void* y, const float* rnorm,
+                             const void* dy, const void* cache, void* d_o, void* dq, void* dk, void* dv,
+                             void* dx, float* dw_q, float* dw_k, float* dw_v, void* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

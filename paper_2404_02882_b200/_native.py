@@ -63,6 +63,10 @@ _SIGS = {
     "lasp_topology": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                        ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "lasp_fwd": ([_vp, _sp, _vp, _vp, _vp, _fp, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "lasp_layer_workspace_bytes": ([_sp], ctypes.c_size_t),
+    "lasp_layer_fwd": ([_vp, _sp, ctypes.c_int64] + [_vp] * 4 + [_fp] + [_vp] * 4 + [_vp] * 4, ctypes.c_int),
+    "lasp_layer_bwd": ([_vp, _sp, ctypes.c_int64] + [_vp] * 4 + [_fp] + [_vp] * 5 + [_vp] * 2 + [_vp] * 4 +
+                       [_vp] * 4 + [_vp, _vp], ctypes.c_int),
     "lasp_bwd": ([_vp, _sp, _vp, _vp, _vp, _fp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
 }
 
@@ -82,6 +86,15 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                               "(the LASP path has no CPU fallback)")
+        if not os.environ.get("LASP_CUBLAS_LIB"):
+            # the layer entry points' projection GEMMs: torch's bundled cuBLAS (already loaded by torch)
+            try:
+                import nvidia.cublas
+                cand = os.path.join(list(nvidia.cublas.__path__)[0], "lib", "libcublas.so.12")
+                if os.path.exists(cand):
+                    os.environ["LASP_CUBLAS_LIB"] = cand
+            except ImportError:
+                pass
         if not os.environ.get("LASP_NCCL_LIB"):
             # the ring loads NCCL lazily (dlopen): point it at torch's bundled copy, the one torch.distributed uses
             try:
@@ -93,6 +106,8 @@ def lib():
                 pass
         L = ctypes.CDLL(LIB_PATH)
         for name, (args, res) in _SIGS.items():
+            if os.environ.get("LASP_LIB") and not hasattr(L, name):
+                continue  # an older build loaded for a same-box A/B (tools/cmp_libs.sh)
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = res

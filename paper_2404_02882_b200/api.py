@@ -331,3 +331,65 @@ class LaspAttention(torch.autograd.Function):
 
 def lasp_attention(q, k, v, lam, ring=None):
     return LaspAttention.apply(q, k, v, lam, ring)
+
+
+# ---- NEXT-3: the layer around the path (include/lasp.h lasp_layer_fwd / lasp_layer_bwd) ----------------------
+def layer_workspace_bytes(shape: N.lasp_shape_t) -> int:
+    return int(N.lib().lasp_layer_workspace_bytes(ctypes.byref(shape)))
+
+
+def layer_fwd(x, w_q, w_k, w_v, lam, heads, ring=None, *, out=None, workspace=None):
+    """Y = Norm(LASP(X W_Q, X W_K, X W_V)) for this rank's chunk x [B][C][d_model] (bf16); w_q [d][H*D],
+    w_k, w_v [d][Hk*D]. Norm is the per-head RMS normalization of DESIGN.md reading N1. ``ring``: a Ring
+    (the state arrives over the ring) or None (single rank). Returns a dict with q, k, v, y, rnorm, cache
+    (all needed by layer_bwd)."""
+    B, C, d = x.shape
+    D = w_q.shape[1] // heads
+    Hk = w_k.shape[1] // D
+    if w_q.shape != (d, heads * D) or w_k.shape != (d, Hk * D) or w_v.shape != w_k.shape:
+        raise ValueError("w_q must be [d_model][heads*D], w_k and w_v [d_model][kv_heads*D]")
+    for t in (x, w_q, w_k, w_v):
+        if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("layer tensors must be contiguous bf16 CUDA tensors")
+    o = out or {}
+    q = o.get("q") if o.get("q") is not None else torch.empty((B, C, heads, D), dtype=x.dtype, device=x.device)
+    k = o.get("k") if o.get("k") is not None else torch.empty((B, C, Hk, D), dtype=x.dtype, device=x.device)
+    v = o.get("v") if o.get("v") is not None else torch.empty_like(k)
+    y = o.get("y") if o.get("y") is not None else torch.empty_like(q)
+    rnorm = o.get("rnorm") if o.get("rnorm") is not None else torch.empty((B, C, heads), dtype=torch.float32,
+                                                                           device=x.device)
+    s = _shape(q, k)
+    cache = o.get("cache") if o.get("cache") is not None else alloc_cache(q, k)
+    if workspace is None:
+        workspace = torch.empty(max(layer_workspace_bytes(s), 16), dtype=torch.uint8, device=x.device)
+    _check_buf(workspace, layer_workspace_bytes(s), "workspace", x.device)
+    _check_buf(cache, cache_bytes(s), "cache", x.device)
+    _, lp = _lam(lam, Hk)
+    ctx = ring._ctx if ring is not None else None
+    N.check(N.lib().lasp_layer_fwd(ctx, ctypes.byref(s), d, _p(x), _p(w_q), _p(w_k), _p(w_v), lp, _p(q), _p(k),
+                                   _p(v), _p(y), _p(rnorm), _p(cache), _p(workspace), _stream(x.device)))
+    return {"q": q, "k": k, "v": v, "y": y, "rnorm": rnorm, "cache": cache, "workspace": workspace}
+
+
+def layer_bwd(x, w_q, w_k, w_v, lam, fw, dy, ring=None, *, out=None):
+    """Gradients of sum(Y * dY) for layer_fwd: returns dict dx, dw_q, dw_k, dw_v (fp32) and the intermediates
+    d_o (= dL/dO, formed by the Norm backward inside the B1 kernel), dq, dk, dv."""
+    q, k = fw["q"], fw["k"]
+    B, C, d = x.shape
+    o = out or {}
+    d_o = o.get("d_o") if o.get("d_o") is not None else torch.empty_like(q)
+    dq = o.get("dq") if o.get("dq") is not None else torch.empty_like(q)
+    dk = o.get("dk") if o.get("dk") is not None else torch.empty_like(k)
+    dv = o.get("dv") if o.get("dv") is not None else torch.empty_like(k)
+    dx = o.get("dx") if o.get("dx") is not None else torch.empty_like(x)
+    dws = [o.get(n) if o.get(n) is not None else torch.empty(w.shape, dtype=torch.float32, device=x.device)
+           for n, w in (("dw_q", w_q), ("dw_k", w_k), ("dw_v", w_v))]
+    _check_like(dy, q, "dy")
+    s = _shape(q, k)
+    _, lp = _lam(lam, k.shape[2])
+    ctx = ring._ctx if ring is not None else None
+    N.check(N.lib().lasp_layer_bwd(ctx, ctypes.byref(s), d, _p(x), _p(w_q), _p(w_k), _p(w_v), lp, _p(q), _p(k),
+                                   _p(fw["v"]), _p(fw["y"]), _p(fw["rnorm"]), _p(dy), _p(fw["cache"]), _p(d_o),
+                                   _p(dq), _p(dk), _p(dv), _p(dx), _p(dws[0]), _p(dws[1]), _p(dws[2]),
+                                   _p(fw["workspace"]), _stream(x.device)))
+    return {"dx": dx, "dw_q": dws[0], "dw_k": dws[1], "dw_v": dws[2], "d_o": d_o, "dq": dq, "dk": dk, "dv": dv}

@@ -350,6 +350,38 @@ cudaError_t launch_pack_state(const Plan& p, const float* src, float* dst, cudaS
                   dst);
 }
 
+// Norm epilogue, second phase at head_dim 128 (the two 64-wide value slices of a head row are separate core
+// items): r = (mean o^2 + eps)^-1/2 from the slices' sums of squares, y = o r in place, r stored for the
+// backward. One thread per 8 elements (16 B), 16 threads per (token, head) row.
+__global__ void norm_apply_kernel(int64_t rows, float eps, __nv_bfloat16* __restrict__ y, const float* __restrict__ nsum,
+                                  float* __restrict__ rnorm) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t row = idx >> 4;
+  if (row >= rows) return;
+  const float rn = 1.f / sqrtf((nsum[2 * row] + nsum[2 * row + 1]) * (1.f / 128.f) + eps);
+  uint4* ptr = reinterpret_cast<uint4*>(y) + idx;
+  uint4 v = *ptr;
+  uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 h2 = *reinterpret_cast<__nv_bfloat162*>(&w[i]);
+    float2 f = __bfloat1622float2(h2);
+    h2 = __floats2bfloat162_rn(f.x * rn, f.y * rn);
+    w[i] = *reinterpret_cast<uint32_t*>(&h2);
+  }
+  *ptr = v;
+  if ((idx & 15) == 0) rnorm[row] = rn;
+}
+
+cudaError_t launch_norm_apply(const Plan& p, void* y, const NormArgs& n, cudaStream_t st) {
+  const int64_t rows = p.B * p.C * p.H;
+  const int64_t threads = rows * 16;
+  return launch_k(norm_apply_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, rows, n.eps,
+                  static_cast<__nv_bfloat16*>(y), (const float*)n.nsum, n.rnorm);
+}
+
 // Entry kernel of every call: waits until everything before the call has completed (griddepcontrol.wait),
 // only then lets the call's next kernel start (lasp_common.cuh, PDL), writes (forward) or checks (backward)
 // the cache tag into the call's status word ctrl[2], and zeroes the call's counters (ctrl[0..1]: fused

@@ -198,10 +198,12 @@ __device__ __forceinline__ int64_t block_row(Dir dir, const Item& it, int j) {
 // seg_state_tc (persistent): warp 0 TMA, warp 1 UMMA, warps 4-7 scale X rows, warps 8-11 drain
 // the (double-buffered) TMEM accumulator of finished items to global memory.
 // ================================================================================================
-template <int D>
+// NORM (B1 with the Norm backward fused, NEXT-3): a third tile per stage holds the forward output y
+template <int D, bool NORM = false>
 struct SegLayout {
   static constexpr int NBOX = D / 64;
   static constexpr uint32_t TILE = NBOX * BOX;
+  static constexpr int NT = NORM ? 3 : 2;  // tiles per stage
 #ifndef LASP_SEG_STAGES64
 #define LASP_SEG_STAGES64 2  // 2 x 2 beat 3 x 2, 4 x 1 and 6 x 1 (stages x CTAs/SM) by ~1 % (round 1 sweep)
 #define LASP_SEG_CTAS64 2
@@ -209,11 +211,12 @@ struct SegLayout {
 #ifndef LASP_SEG_STAGES128
 #define LASP_SEG_STAGES128 3  // 3 x 64 KB stages, 1 CTA/SM: seg F 61.4 -> 58.0 us at TNL-1B
 #endif
-  static constexpr int STAGES = D == 64 ? LASP_SEG_STAGES64 : LASP_SEG_STAGES128;
+  static constexpr int STAGES = NORM ? 2 : D == 64 ? LASP_SEG_STAGES64 : LASP_SEG_STAGES128;
   static constexpr int CTAS_PER_SM = D == 64 ? LASP_SEG_CTAS64 : 1;  // 2 x (96 KB smem, 128 TMEM columns) per SM
-  static constexpr uint32_t X(int s) { return uint32_t(s) * 2 * TILE; }
-  static constexpr uint32_t Y(int s) { return uint32_t(s) * 2 * TILE + TILE; }
-  static constexpr uint32_t BARS = STAGES * 2 * TILE;
+  static constexpr uint32_t X(int s) { return uint32_t(s) * NT * TILE; }
+  static constexpr uint32_t Y(int s) { return uint32_t(s) * NT * TILE + TILE; }
+  static constexpr uint32_t Y2(int s) { return uint32_t(s) * NT * TILE + 2 * TILE; }
+  static constexpr uint32_t BARS = STAGES * NT * TILE;
   static constexpr uint32_t BYTES = BARS + 512 + 1024;  // barriers + item queue + tmem slot + alignment slack
   static constexpr uint32_t TCOLS = 2 * D;             // two accumulators
 };
@@ -225,6 +228,11 @@ struct SegParams {
   unsigned long long* trace;
   unsigned* claim;       // work-claim counter (ItemQueue), 0 at launch
   int sub;               // X, Y heads summed per state head (B1 with grouped queries: G; else 1)
+  // fused Norm backward (NORM instantiation, B1 only): Y is dY, the third tile is the forward output y;
+  // the scaler warps turn dY into dO = r (dY - y (y . dY) / D) in shared memory and write it to dout
+  CUtensorMap my2;
+  const float* rnorm;    // [B][C][H]
+  __nv_bfloat16* dout;   // [B][C][H][D]
 };
 
 // debug timeline: event ev (0..15) of block J (< 64) of CTA 0 -> trace[ev * 64 + J] = clock64()
@@ -246,9 +254,9 @@ struct SegParams {
 #define LASP_TRACE2(ev, J) do { } while (0)
 #endif
 
-template <int D, Dir DIR>
+template <int D, Dir DIR, bool NORM>
 __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_constant__ SegParams prm) {
-  using L = SegLayout<D>;
+  using L = SegLayout<D, NORM>;
   constexpr int ST = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -269,6 +277,7 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
   if (threadIdx.x == 0) {
     tma_prefetch(&prm.mx);
     tma_prefetch(&prm.my);
+    if (NORM) tma_prefetch(&prm.my2);
     for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&scaled[s], 128); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], 128); }
     q_init(*iq, 1 + 4 + 4);  // consumers: the UMMA thread, 4 scaler warps, 4 drain warps
@@ -295,13 +304,14 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
           const int s = J % ST;
           mbar_wait(&empty[s], ((J / ST) & 1) ^ 1);
           LASP_TRACE(0, J);
-          mbar_expect_tx(&full[s], 2 * L::TILE);
+          mbar_expect_tx(&full[s], L::NT * L::TILE);
           const int t0 = int(block_row(DIR, it, jj / sub));
           const int hh = int(it.h) * sub + jj % sub;
 #pragma unroll
           for (int x = 0; x < L::NBOX; ++x) {
             tma_load_4d(sm + L::X(s) + x * BOX, &prm.mx, &full[s], x * 64, hh, t0, int(it.b));
             tma_load_4d(sm + L::Y(s) + x * BOX, &prm.my, &full[s], x * 64, hh, t0, int(it.b));
+            if (NORM) tma_load_4d(sm + L::Y2(s) + x * BOX, &prm.my2, &full[s], x * 64, hh, t0, int(it.b));
           }
         }
       }
@@ -352,6 +362,49 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
         float wgt = 0.f;
         if (pos >= it.beg && pos < it.end)
           wgt = exp2f(float(DIR == Dir::FWD ? (it.end - 1 - pos) : (pos - it.beg + 1)) * l2);
+        if constexpr (NORM) {
+          // Norm backward of this row (reading N1): dO = r (dY - y (y . dY) / D) in fp32, rounded once to bf16,
+          // into the Y tile (the MMA's operand) and to dout (read by the B3 passes)
+          const int hh = int(it.h) * sub + jj % sub;
+          const bool live = pos >= it.beg && pos < it.end;
+          const int64_t row = (it.b * p.C + pos) * p.H + hh;
+          const float rr = live ? prm.rnorm[row] : 0.f;
+          float dot = 0.f;
+#pragma unroll
+          for (int x = 0; x < L::NBOX; ++x)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint32_t o = x * BOX + uint32_t(g) * 128 + ((uint32_t(c) ^ (uint32_t(g) & 7)) << 4);
+              const uint4 gy = lds128(sbase + L::Y(s) + o), yy = lds128(sbase + L::Y2(s) + o);
+              const uint32_t* a = reinterpret_cast<const uint32_t*>(&gy);
+              const uint32_t* b = reinterpret_cast<const uint32_t*>(&yy);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                dot = fmaf(__uint_as_float(a[q] << 16), __uint_as_float(b[q] << 16), dot);
+                dot = fmaf(__uint_as_float(a[q] & 0xFFFF0000u), __uint_as_float(b[q] & 0xFFFF0000u), dot);
+              }
+            }
+          const float coef = dot * (1.f / float(D));
+          uint4* dst = reinterpret_cast<uint4*>(prm.dout + row * D);
+#pragma unroll
+          for (int x = 0; x < L::NBOX; ++x)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint32_t o = x * BOX + uint32_t(g) * 128 + ((uint32_t(c) ^ (uint32_t(g) & 7)) << 4);
+              uint4 gy = lds128(sbase + L::Y(s) + o);
+              const uint4 yy = lds128(sbase + L::Y2(s) + o);
+              uint32_t* a = reinterpret_cast<uint32_t*>(&gy);
+              const uint32_t* b = reinterpret_cast<const uint32_t*>(&yy);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float lo = rr * fmaf(-__uint_as_float(b[q] << 16), coef, __uint_as_float(a[q] << 16));
+                const float hi = rr * fmaf(-__uint_as_float(b[q] & 0xFFFF0000u), coef, __uint_as_float(a[q] & 0xFFFF0000u));
+                a[q] = pack_bf16(lo, hi);
+              }
+              sts128(sbase + L::Y(s) + o, gy);
+              if (live) dst[x * 8 + c] = gy;
+            }
+        }
 #ifdef LASP_EXPERIMENT_SEG_NOSCALE  // timing experiment only (tools/cmp_variants.sh): unweighted X
         if (false)
 #endif
@@ -463,8 +516,17 @@ struct CoreParams {
   unsigned* claim;            // work-claim counter (ItemQueue), 0 at launch
   FastDiv div_per;            // / (items per segment row) (work-item decode)
   uint32_t per;               // items per segment row (sum over the passes of B * nh * NV)
+  FastDiv div_nbh, div_h;     // multi-head decode: / (B*H*NV), / H
   int uniform;                // every pass has the same item count (head_dim 128 interleaved order)
   PrefixFold fold;            // fold.gbar != nullptr: compute the prefix states first (fused F2 / B2)
+  // Norm epilogue (NEXT-3, reading N1; the forward O pass of a NORM instantiation): head_dim 64 writes
+  // y = o r and r = (mean o^2 + eps)^-1/2 into rnorm [B][C][H]; head_dim 128 (two value-slice items per
+  // head row) writes o and each slice's sum of squares into nsum [B][C][H][2] for norm_apply_kernel.
+  float* rnorm;
+  float* nsum;
+  float norm_eps;
+  int late_inputs;            // 1: an input tensor is written by the preceding kernel (fused Norm
+                              // backward): the producer waits for it before the first load
 };
 
 // Fused F2 / B2 (Alg. 2, Alg. 3 P:648 between segments; the arithmetic of prefix_kernel): per
@@ -534,13 +596,37 @@ struct CItem {
 // at head_dim 128 when every pass has the same item count: segment-major, value slice innermost.
 // Grouped queries: a query-head pass (O, dQ) reads b, c and the state of kv-head h / G; a kv-head pass
 // (dV, dK) reads b, c of the G query heads h G + u, u = 0..G-1 (sub-blocks summed into one output block).
-template <int NV>
+template <int NV, bool GQ>
 __device__ __noinline__ CItem get_citem(const CoreParams& prm, int64_t w) {
   const Plan& p = prm.p;
   CItem it;
   const uint32_t wu = uint32_t(w);
   it.seg = prm.div_per.div(wu);
   const uint32_t rem = wu - uint32_t(it.seg) * prm.per;
+  if constexpr (!GQ) {  // multi-head: every pass has B * H * NV items per segment row (round-1 decode)
+    const uint32_t nbh = uint32_t(p.B * p.H) * uint32_t(NV), nh = uint32_t(p.H);
+    uint32_t bhv;
+    if constexpr (NV > 1) {
+      const uint32_t pv = uint32_t(prm.npass) * uint32_t(NV), bh0 = rem / pv, r2 = rem - bh0 * pv;
+      it.pass = int(r2 / uint32_t(NV));
+      bhv = bh0 * uint32_t(NV) + (r2 - uint32_t(it.pass) * uint32_t(NV));
+    } else {
+      it.pass = int(prm.div_nbh.div(rem));
+      bhv = rem - uint32_t(it.pass) * nbh;
+    }
+    const uint32_t bh = bhv / uint32_t(NV);
+    it.v = int(bhv - bh * uint32_t(NV));
+    it.b = prm.div_h.div(bh);
+    it.h = bh - uint32_t(it.b) * nh;
+    it.sh = int(it.h);
+    it.sub = 1;
+    it.bh0 = int(it.h);
+    it.dir = Dir(prm.pass[it.pass].dir);
+    it.beg = seg_begin(it.dir, it.seg, p.seg_len, p.C);
+    it.end = seg_end(it.dir, it.seg, p.seg_len, p.C);
+    it.nblk = int((it.end - it.beg + BT - 1) / BT);
+    return it;
+  }
   uint32_t bh;
   if (NV > 1 && prm.uniform) {
     // head_dim 128: (batch x head, pass, value slice) inside a segment row, so that the items re-reading one
@@ -595,7 +681,9 @@ __device__ __forceinline__ unsigned fold_chunks(const Plan& p) {
 
 
 
-template <int D>
+// GQ: grouped queries (G > 1) -- a separate instantiation, so that the multi-head kernel keeps sub = 1 as a
+// compile-time constant (no sub-block arithmetic, no u . c release barrier: measured -8 % otherwise)
+template <int D, bool GQ, bool NORM>
 __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__ CoreParams prm) {
   using L = CoreLayout<D>;
   constexpr int ST = L::STAGES;
@@ -665,11 +753,16 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     // ------------------------------------------------------------------ TMA producer
     if (elect_one()) {
       bool waited = false;
+      if (prm.late_inputs) {  // the inputs are not complete before the preceding kernel has finished
+        pdl_wait();
+        pdl_trigger();
+        waited = true;
+      }
       uint32_t J = 0, k = 0;
       for (;; ++k) {
         const int64_t w = q_claim(bar->iq, k, prm.claim);
         if (w >= W) break;
-        const CItem it = get_citem<L::NV>(prm, w);
+        const CItem it = get_citem<L::NV, GQ>(prm, w);
         const CorePass& ps = prm.pass[it.pass];
         // the segment's prefix state -> STG (single buffer, released by the state warps)
         auto load_stg = [&]() {
@@ -687,7 +780,8 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         const CUtensorMap* ma = &prm.min[ps.a];
         const CUtensorMap* mb = &prm.min[ps.b];
         const CUtensorMap* mc = &prm.min[ps.c];
-        const int nsb = it.nblk * it.sub;  // sub-blocks: block j = jj / sub, summed query head u = jj % sub
+        const int isub = GQ ? it.sub : 1;
+        const int nsb = it.nblk * isub;  // sub-blocks: block j = jj / sub, summed query head u = jj % sub
         for (int jj = 0; jj < nsb; ++jj, ++J) {
           if (!waited && jj == (nsb < ST ? nsb : ST)) {
             pdl_wait();
@@ -699,8 +793,8 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           mbar_wait(&bar->empty[s], ((J / ST) & 1) ^ 1);
           LASP_TRACE(0, J);
           mbar_expect_tx(&bar->full[s], L::STAGE);
-          const int j = it.sub == 1 ? jj : jj / it.sub;
-          const int t0 = int(cblock_row(it, j)), hb = it.bh0 + (jj - j * it.sub);
+          const int j = GQ ? jj / isub : jj;
+          const int t0 = int(cblock_row(it, j)), hb = it.bh0 + (jj - j * isub);
 #pragma unroll
           for (int x = 0; x < L::NBOX; ++x) {
             tma_load_4d(sm + L::A(s) + x * BOX, ma, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
@@ -734,10 +828,10 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         const int64_t w = q_fetch(bar->iq, k);
         q_release(bar->iq, k);
         if (w >= W) break;
-        const CItem itm = get_citem<L::NV>(prm, w);
-        const int nblk = itm.nblk, sub = itm.sub;
+        const CItem itm = get_citem<L::NV, GQ>(prm, w);
+        const int nblk = itm.nblk, sub = GQ ? itm.sub : 1;
         for (int jj = 0; jj < nblk * sub; ++jj, ++J) {
-          const int j = sub == 1 ? jj : jj / sub, u = jj - j * sub;
+          const int j = GQ ? jj / sub : jj, u = jj - j * sub;
           const int s = int(J % ST);
           if (warp == 2) {
             // S = a b^T (double-buffered in TMEM; buffer J & 1 is free once out(J-2) has read its P)
@@ -761,7 +855,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
               for (int kk = 0; kk < BT / 16; ++kk)
                 mma_bf16(tmem + L::T_DS, desc_mn(sbase + L::B_(s) + kk * 2048, BOX),
                          desc_mn(sbase + L::KU + kk * 2048, BOX), id_ds, (kk | u) != 0);
-              mma_commit(&bar->ku_empty);  // the u . c buffer is free once this MMA has read it
+              if (GQ) mma_commit(&bar->ku_empty);  // the u . c buffer is free once this MMA has read it
               if (u + 1 == sub) {
                 mma_commit(&bar->ds_full);
                 ++kd;
@@ -817,7 +911,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     for (uint32_t k = 0;; ++k) {
       const int64_t w = q_fetch_warp(bar->iq, k);
       if (w >= W) break;
-      const CItem it = get_citem<L::NV>(prm, w);
+      const CItem it = get_citem<L::NV, GQ>(prm, w);
       const bool fwd = it.dir == Dir::FWD;
       const float l2 = p.l2lam[it.sh];
       // Per-thread decay factors of its row, kept in registers for the whole item. With e(u) = lane - u
@@ -838,7 +932,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         t[u] = fast_exp2(x + x32);
       }
       const float sc2 = fast_exp2(32.f * l2), sc3 = fast_exp2(64.f * l2);  // off-diagonal distance 2, 3
-      for (int jj = 0; jj < it.nblk * it.sub; ++jj, ++J) {  // every sub-block has its own S / P
+      for (int jj = 0; jj < it.nblk * (GQ ? it.sub : 1); ++jj, ++J) {  // every sub-block has its own S / P
         const int sb = J & 1;
         mbar_wait(&bar->s_full[sb], (J >> 1) & 1);
         if (lane == 0 && q4 == 3) LASP_TRACE(4, J);
@@ -961,7 +1055,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     for (uint32_t k = 0;; ++k) {
       const int64_t w = q_fetch_warp(bar->iq, k);
       if (w >= W) break;
-      const CItem it = get_citem<L::NV>(prm, w);
+      const CItem it = get_citem<L::NV, GQ>(prm, w);
       const CorePass& ps = prm.pass[it.pass];
       load_state(k, it, ps.trans != 0, ps.state);
       const float l2 = p.l2lam[it.sh];
@@ -971,8 +1065,10 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       // sub-block has read it: ku_empty), done early so the dS MMA is never waiting on it
       auto scale_ku = [&](uint32_t JJ) {
         const int s = JJ % ST;
-        mbar_wait(&bar->ku_empty, (nku & 1) ^ 1);
-        ++nku;
+        if (GQ) {  // (one u . c per block: the ds_full wait before it already implies the buffer is free)
+          mbar_wait(&bar->ku_empty, (nku & 1) ^ 1);
+          ++nku;
+        }
         mbar_wait(&bar->full[s], (JJ / ST) & 1);
 #ifdef LASP_EXPERIMENT_NOSTATE
         if (false)
@@ -985,7 +1081,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         fence_async_smem();
         mbar_arrive(&bar->ku_full);
       };
-      const int sub = it.sub;
+      const int sub = GQ ? it.sub : 1;
       if (it.nblk > 1) scale_ku(Js);
       for (int j = 0;; ++j, ++J) {
         // bf16 hi/lo copy of the state entering block J into buffer J % NSB (free once the output MMAs
@@ -1052,7 +1148,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     for (uint32_t k = 0;; ++k) {
       const int64_t w = q_fetch_warp(bar->iq, k);
       if (w >= W) break;
-      const CItem it = get_citem<L::NV>(prm, w);
+      const CItem it = get_citem<L::NV, GQ>(prm, w);
       const CUtensorMap* mo = &prm.mout[prm.pass[it.pass].out];
       __nv_bfloat16* outp = prm.outp[prm.pass[it.pass].out];
       const int64_t oh = prm.pass[it.pass].nh;  // heads of the output tensor
@@ -1069,6 +1165,23 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         const uint32_t ti = tmem + ((q4 * 32) << 16) + L::T_OI;
         const uint32_t tx = tmem + ((q4 * 32) << 16) + L::T_OX;
         uint32_t pk[32];
+        float rn = 1.f, ss = 0.f;
+        if constexpr (NORM && L::NV == 1) {
+          // Norm epilogue, whole head row in this thread: a first TMEM pass for the row's sum of squares
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float a[16], x[16];
+            tmem_ld16(ti + c * 16, a);
+            tmem_ld16(tx + c * 16, x);
+            tmem_ld_wait();
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              const float o = fmaf(r, x[u], a[u]);
+              ss = fmaf(o, o, ss);
+            }
+          }
+          rn = 1.f / sqrtf(ss * (1.f / 64.f) + prm.norm_eps);
+        }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           float a[16], x[16];
@@ -1080,9 +1193,22 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             mbar_arrive(&bar->o_empty);
           }
 #pragma unroll
-          for (int u = 0; u < 16; u += 2) pk[c * 8 + u / 2] = pack_bf16(fmaf(r, x[u], a[u]), fmaf(r, x[u + 1], a[u + 1]));
+          for (int u = 0; u < 16; u += 2) {
+            float o0 = fmaf(r, x[u], a[u]), o1 = fmaf(r, x[u + 1], a[u + 1]);
+            if constexpr (NORM && L::NV > 1) ss = fmaf(o0, o0, fmaf(o1, o1, ss));
+            if constexpr (NORM && L::NV == 1) { o0 *= rn; o1 *= rn; }
+            pk[c * 8 + u / 2] = pack_bf16(o0, o1);
+          }
         }
         const int t0 = int(cblock_row(it, j));
+        if constexpr (NORM) {  // per-row statistics of the forward O pass (rows of this segment only)
+          const int64_t t = t0 + i;
+          if (t >= it.beg && t < it.end) {
+            const int64_t row = (it.b * p.C + t) * p.H + it.h;
+            if constexpr (L::NV == 1) prm.rnorm[row] = rn;
+            else prm.nsum[row * 2 + it.v] = ss;
+          }
+        }
         if (t0 < it.beg) {
           // ragged block of a REV pass, which starts before its segment: rows before the segment belong
           // to the previous segment's item (or precede the rank start, where TMA stores reject negative
@@ -1146,10 +1272,18 @@ unsigned persistent_grid(const Plan& p, int per_sm = 1) {
   return unsigned(g > 0 ? g : 1);
 }
 
-template <int D, Dir DIR>
+template <int D, Dir DIR, bool NORM>
 cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, cudaStream_t st,
-                       unsigned* claim) {
+                       unsigned* claim, const NormBwdArgs* nb) {
   SegParams prm;
+  std::memset(&prm, 0, sizeof prm);
+  if (NORM) {
+    if (nb == nullptr || DIR != Dir::REV) return cudaErrorInvalidValue;
+    cudaError_t e2 = make_seq_map(&prm.my2, nb->y, p, p.H);
+    if (e2 != cudaSuccess) return e2;
+    prm.rnorm = nb->rnorm;
+    prm.dout = static_cast<__nv_bfloat16*>(nb->dout);
+  }
   prm.claim = static_items() ? nullptr : claim;
   // F1 reads k, v (Hk heads); B1 reads q, do (H heads), summing the G query heads of each state head
   prm.sub = DIR == Dir::FWD ? 1 : int(p.G);
@@ -1160,15 +1294,16 @@ cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, 
   prm.p = p;
   prm.out = out;
   prm.trace = g_trace ? g_trace + 16 * 64 : nullptr;  // second trace region: segment-state kernel
-  auto kern = seg_state_tc_kernel<D, DIR>;
-  const int smem = int(SegLayout<D>::BYTES);
+  auto kern = seg_state_tc_kernel<D, DIR, NORM>;
+  const int smem = int(SegLayout<D, NORM>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
-  return launch_k(kern, dim3(persistent_grid(p, SegLayout<D>::CTAS_PER_SM)), dim3(384), smem, st, prm);
+  return launch_k(kern, dim3(persistent_grid(p, SegLayout<D, NORM>::CTAS_PER_SM)), dim3(384), smem, st, prm);
 }
 
 template <int D>
 cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st,
-                              const PrefixFold* fold, unsigned* claim, int reserve_sms) {
+                              const PrefixFold* fold, unsigned* claim, int reserve_sms, const NormArgs* norm,
+                              bool late_inputs) {
   CoreParams prm;
   std::memset(&prm, 0, sizeof prm);
   cudaError_t e;
@@ -1229,10 +1364,20 @@ cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const 
   if (fold) prm.fold = *fold;
   prm.per = off;
   prm.div_per = FastDiv(off);
+  prm.div_nbh = FastDiv(uint32_t(p.B * p.H * NV));
+  prm.div_h = FastDiv(uint32_t(p.H));
   prm.uniform = 1;
   for (int x = 1; x < npass; ++x) prm.uniform &= prm.pass[x].nh == prm.pass[0].nh;
   if (static_items()) prm.claim = nullptr;
-  auto kern = core_tc_kernel<D>;
+  auto kern = norm != nullptr ? (p.G > 1 ? core_tc_kernel<D, true, true> : core_tc_kernel<D, false, true>)
+                               : (p.G > 1 ? core_tc_kernel<D, true, false> : core_tc_kernel<D, false, false>);
+  if (norm != nullptr) {
+    if (npass != 1 || dirs[0] != Dir::FWD) return cudaErrorInvalidValue;
+    prm.rnorm = norm->rnorm;
+    prm.nsum = norm->nsum;
+    prm.norm_eps = norm->eps;
+  }
+  prm.late_inputs = late_inputs ? 1 : 0;
   const int smem = int(CoreLayout<D>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
   const int64_t W = p.nseg * int64_t(off);
@@ -1288,23 +1433,34 @@ bool tc_supported(const Plan& p) {
 }
 
 cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st,
-                                unsigned* r) {
+                                unsigned* r, const NormBwdArgs* nb) {
   if (r == nullptr) return cudaErrorInvalidValue;  // the work-claim counter is required
-  if (p.D == 64) return dir == Dir::FWD ? launch_seg<64, Dir::FWD>(p, x, y, out, st, r) : launch_seg<64, Dir::REV>(p, x, y, out, st, r);
-  if (p.D == 128) return dir == Dir::FWD ? launch_seg<128, Dir::FWD>(p, x, y, out, st, r) : launch_seg<128, Dir::REV>(p, x, y, out, st, r);
+  if (nb != nullptr) {
+    if (dir != Dir::REV) return cudaErrorInvalidValue;
+    if (p.D == 64) return launch_seg<64, Dir::REV, true>(p, x, y, out, st, r, nb);
+    if (p.D == 128) return launch_seg<128, Dir::REV, true>(p, x, y, out, st, r, nb);
+    return cudaErrorNotSupported;
+  }
+  if (p.D == 64)
+    return dir == Dir::FWD ? launch_seg<64, Dir::FWD, false>(p, x, y, out, st, r, nullptr)
+                           : launch_seg<64, Dir::REV, false>(p, x, y, out, st, r, nullptr);
+  if (p.D == 128)
+    return dir == Dir::FWD ? launch_seg<128, Dir::FWD, false>(p, x, y, out, st, r, nullptr)
+                           : launch_seg<128, Dir::REV, false>(p, x, y, out, st, r, nullptr);
   return cudaErrorNotSupported;
 }
 
 cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st, unsigned* claim,
-                           int reserve_sms) {
-  return launch_core_tc_multi(p, 1, &a, &dir, st, nullptr, claim, reserve_sms);
+                           int reserve_sms, const NormArgs* norm, bool late_inputs) {
+  return launch_core_tc_multi(p, 1, &a, &dir, st, nullptr, claim, reserve_sms, norm, late_inputs);
 }
 
 cudaError_t launch_core_tc_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st,
-                                 const PrefixFold* fold, unsigned* claim, int reserve_sms) {
+                                 const PrefixFold* fold, unsigned* claim, int reserve_sms, const NormArgs* norm,
+                                 bool late_inputs) {
   if (npass < 1 || npass > 3 || claim == nullptr) return cudaErrorInvalidValue;
-  if (p.D == 64) return launch_core_multi<64>(p, npass, a, dirs, st, fold, claim, reserve_sms);
-  if (p.D == 128) return launch_core_multi<128>(p, npass, a, dirs, st, fold, claim, reserve_sms);
+  if (p.D == 64) return launch_core_multi<64>(p, npass, a, dirs, st, fold, claim, reserve_sms, norm, late_inputs);
+  if (p.D == 128) return launch_core_multi<128>(p, npass, a, dirs, st, fold, claim, reserve_sms, norm, late_inputs);
   return cudaErrorNotSupported;
 }
 

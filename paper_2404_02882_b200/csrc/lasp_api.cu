@@ -10,6 +10,7 @@
 #include "../../include/lasp.h"
 #include "lasp_common.cuh"
 
+#include <cublas_v2.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -307,11 +308,12 @@ struct ProfSpan {
 
 // ---- stage dispatch: tcgen05 for covered bf16 shapes, CUDA cores otherwise ---------------------
 cudaError_t seg_state(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st,
-                      unsigned* claim) {
+                      unsigned* claim, const NormBwdArgs* nb = nullptr) {
   const bool tc = tc_supported(p);
+  if (nb && !tc) return cudaErrorNotSupported;
   return staged(dir == Dir::FWD ? (tc ? "seg_state_fwd_tc" : "seg_state_fwd_simt")
-                                : (tc ? "seg_state_rev_tc" : "seg_state_rev_simt"), st, [&] {
-    return tc ? launch_seg_state_tc(p, dir, x, y, out, st, claim) : launch_seg_state_simt(p, dir, x, y, out, st);
+                                : (tc ? (nb ? "seg_state_rev_norm_tc" : "seg_state_rev_tc") : "seg_state_rev_simt"), st, [&] {
+    return tc ? launch_seg_state_tc(p, dir, x, y, out, st, claim, nb) : launch_seg_state_simt(p, dir, x, y, out, st);
   });
 }
 
@@ -328,12 +330,14 @@ bool fused_fold(const Plan& p) {
 
 cudaError_t core(const Plan& p, Dir dir, const void* a, const void* b, const void* c, void* out,
                  const float* state, int trans, cudaStream_t st, unsigned* claim, const unsigned* status = nullptr,
-                 int reserve_sms = 0) {
+                 int reserve_sms = 0, const NormArgs* norm = nullptr, bool late_inputs = false) {
   SeqArgs args{a, b, c, out, state, trans, status};
   const bool tc = tc_supported(p);
+  if (norm && !tc) return cudaErrorNotSupported;
   return staged(dir == Dir::FWD ? (tc ? "core_fwd_tc" : "core_fwd_simt") : (tc ? "core_rev_tc" : "core_rev_simt"),
                 st, [&] {
-                  return tc ? launch_core_tc(p, dir, args, st, claim, reserve_sms) : launch_core_simt(p, dir, args, st);
+                  return tc ? launch_core_tc(p, dir, args, st, claim, reserve_sms, norm, late_inputs)
+                            : launch_core_simt(p, dir, args, st);
                 });
 }
 
@@ -358,10 +362,12 @@ cudaError_t combine(const Plan& p, const float* in, const float* local, float* o
 // several core passes: one persistent tensor-core launch (passes of a segment interleaved, their
 // shared inputs re-read from L2), or one CUDA-core launch per pass
 cudaError_t core_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st,
-                       unsigned* claim, const PrefixFold* fold = nullptr) {
+                       unsigned* claim, const PrefixFold* fold = nullptr, const NormArgs* norm = nullptr,
+                       bool late_inputs = false) {
   if (tc_supported(p))
     return staged(npass == 3 ? "core_bwd3_tc" : npass == 1 && dirs[0] == Dir::FWD ? "core_fwd_tc" : "core_multi_tc", st,
-                  [&] { return launch_core_tc_multi(p, npass, a, dirs, st, fold, claim); });
+                  [&] { return launch_core_tc_multi(p, npass, a, dirs, st, fold, claim, 0, norm, late_inputs); });
+  if (norm) return cudaErrorNotSupported;
   for (int x = 0; x < npass; ++x) {
     cudaError_t e = staged(dirs[x] == Dir::FWD ? "core_fwd_simt" : "core_rev_simt", st,
                            [&] { return launch_core_simt(p, dirs[x], a[x], st); });
@@ -382,7 +388,7 @@ lasp_status_t prologue(const lasp_shape_t* shape, const float* lambda, Plan& p) 
 // fused-fold counters (zeroed by F1's launch) or nullptr for the separate prefix kernel.
 lasp_status_t fwd_tail(const Plan& p, const void* q, const void* k, const void* v, const float* kv_in,
                        void* o, float* kv_out, void* cache, float* seg, unsigned* gbar, unsigned* claim,
-                       cudaStream_t st) {
+                       cudaStream_t st, const NormArgs* norm = nullptr) {
   float* P = static_cast<float*>(cache);
   if (p.C == 0) {
     LASP_CUDA(prefix(p, Dir::FWD, kv_in, nullptr, P, kv_out, st));
@@ -392,11 +398,13 @@ lasp_status_t fwd_tail(const Plan& p, const void* q, const void* k, const void* 
     const PrefixFold fold{kv_in, seg, P, kv_out, gbar, int(Dir::FWD)};
     const SeqArgs a{q, k, v, o, P, 0};
     const Dir dir = Dir::FWD;
-    LASP_CUDA(core_multi(p, 1, &a, &dir, st, claim, &fold));
-    return LASP_OK;
+    LASP_CUDA(core_multi(p, 1, &a, &dir, st, claim, &fold, norm));
+  } else {
+    LASP_CUDA(prefix(p, Dir::FWD, kv_in, seg, P, kv_out, st));
+    LASP_CUDA(core(p, Dir::FWD, q, k, v, o, P, 0, st, claim, nullptr, 0, norm));
   }
-  LASP_CUDA(prefix(p, Dir::FWD, kv_in, seg, P, kv_out, st));
-  LASP_CUDA(core(p, Dir::FWD, q, k, v, o, P, 0, st, claim));
+  if (norm && p.D == 128)  // two value-slice items per head row: the row statistics meet in a second phase
+    LASP_CUDA(staged("norm_apply", st, [&] { return launch_norm_apply(p, o, *norm, st); }));
   return LASP_OK;
 }
 
@@ -442,6 +450,77 @@ lasp_status_t nccl_fail(ncclResult_t r, const char* what, int rank, int peer) {
   std::snprintf(buf, sizeof buf, "%s failed on rank %d (peer %d): %s", what, rank, peer,
                 nccl().GetErrorString ? nccl().GetErrorString(r) : "?");
   return fail(LASP_ERR_COMM, buf);
+}
+
+// ---- cuBLAS, loaded lazily (the projection GEMMs of the NEXT-3 layer entry points only) -------------
+// The Q / K / V projections and their gradients are plain dense GEMMs (M = B*C tokens, K or N = d_model):
+// tensor-core bound, nothing of LASP to fuse into them, so they run on the library GEMM (the task's rule for
+// plain GEMMs); every LASP step around them stays in this library's kernels.
+struct CublasApi {
+  bool loaded = false;
+  std::string why;
+  cublasStatus_t (*Create)(cublasHandle_t*) = nullptr;
+  cublasStatus_t (*SetStream)(cublasHandle_t, cudaStream_t) = nullptr;
+  cublasStatus_t (*GemmEx)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int, const void*,
+                           const void*, cudaDataType, int, const void*, cudaDataType, int, const void*, void*,
+                           cudaDataType, int, cublasComputeType_t, cublasGemmAlgo_t) = nullptr;
+};
+
+CublasApi& cublas() {
+  static CublasApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* cands[] = {std::getenv("LASP_CUBLAS_LIB"), "libcublas.so.12"};
+    void* h = nullptr;
+    for (const char* c : cands)
+      if (c && (h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) { api.why = "libcublas.so.12 not found (set LASP_CUBLAS_LIB)"; return; }
+    api.Create = (decltype(api.Create))dlsym(h, "cublasCreate_v2");
+    api.SetStream = (decltype(api.SetStream))dlsym(h, "cublasSetStream_v2");
+    api.GemmEx = (decltype(api.GemmEx))dlsym(h, "cublasGemmEx");
+    api.loaded = api.Create && api.SetStream && api.GemmEx;
+    if (!api.loaded) api.why = "libcublas.so.12 lacks cublasGemmEx";
+  });
+  return api;
+}
+
+// one handle per (thread, device)
+lasp_status_t cublas_handle(cudaStream_t st, cublasHandle_t* out) {
+  CublasApi& cb = cublas();
+  if (!cb.loaded) return fail(LASP_ERR_UNSUPPORTED, cb.why);
+  thread_local std::unordered_map<int, cublasHandle_t> handles;
+  int dev = 0;
+  LASP_CUDA(cudaGetDevice(&dev));
+  auto it = handles.find(dev);
+  if (it == handles.end()) {
+    cublasHandle_t h = nullptr;
+    if (cb.Create(&h) != CUBLAS_STATUS_SUCCESS) return fail(LASP_ERR_CUDA, "cublasCreate failed");
+    it = handles.emplace(dev, h).first;
+  }
+  if (cb.SetStream(it->second, st) != CUBLAS_STATUS_SUCCESS) return fail(LASP_ERR_CUDA, "cublasSetStream failed");
+  *out = it->second;
+  return LASP_OK;
+}
+
+// Row-major C[M][N] (=|+=) op(A) op(B), bf16 operands, fp32 accumulation; C bf16 or fp32. In cuBLAS's
+// column-major terms this is C^T = op(B)^T op(A)^T.
+//   ta == false: A is [M][K] row-major; true: A is [K][M] row-major (A^T used).
+//   tb == false: B is [K][N] row-major; true: B is [N][K] row-major (B^T used).
+lasp_status_t gemm_rm(cublasHandle_t h, int64_t M, int64_t N, int64_t K, const void* A, bool ta, const void* B, bool tb,
+                      void* C, bool c_fp32, float beta) {
+  const float alpha = 1.f;
+  const cublasOperation_t opa = tb ? CUBLAS_OP_T : CUBLAS_OP_N;  // first cuBLAS operand = B^T (N x K col-major)
+  const cublasOperation_t opb = ta ? CUBLAS_OP_T : CUBLAS_OP_N;
+  const int lda = int(tb ? K : N), ldb = int(ta ? M : K);
+  cublasStatus_t r = cublas().GemmEx(h, opa, opb, int(N), int(M), int(K), &alpha, B, CUDA_R_16BF, lda, A, CUDA_R_16BF,
+                                     ldb, &beta, C, c_fp32 ? CUDA_R_32F : CUDA_R_16BF, int(N), CUBLAS_COMPUTE_32F,
+                                     CUBLAS_GEMM_DEFAULT);
+  if (r != CUBLAS_STATUS_SUCCESS) {
+    char b[96];
+    std::snprintf(b, sizeof b, "cublasGemmEx failed (status %d)", int(r));
+    return fail(LASP_ERR_CUDA, b);
+  }
+  return LASP_OK;
 }
 
 // ---- loopback transport: the ring's ranks as threads of one process on one GPU (testing) ------
@@ -569,6 +648,105 @@ lasp_status_t exchange_allgather(lasp_ctx* c, const Plan& p, const float* local,
              ? LASP_OK : cuda_fail(cudaGetLastError(), "fold_ranks");
 }
 
+// Alg. 2 for one rank after validation. c == nullptr: the communication-free local path (kv_in given, kv_out
+// optional); otherwise the ring / all-gather of ctx c (KV_in received). norm: the Norm epilogue (NEXT-3).
+lasp_status_t fwd_body(lasp_ctx* c, const Plan& p, const void* q, const void* k, const void* v, const float* kv_in,
+                       void* o, float* kv_out, void* cache, void* workspace, cudaStream_t st, const NormArgs* norm) {
+  Workspace w = carve(p, workspace);
+  lasp_status_t s;
+  unsigned* gbar = p.C > 0 && fused_fold(p) ? w.gbar : nullptr;
+  LASP_CUDA(entry_tag(p, cache, w, c ? c->rank : -1, c ? c->world : -1, false, false, st));   // cache tag
+  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, w.claim(0)));                  // F1
+  if (c == nullptr)
+    return fwd_tail(p, q, k, v, kv_in, o, kv_out, cache, w.seg, gbar, w.claim(1), st, norm);  // F2 + F3
+  const size_t n = state_elems(p);
+  int from = -1, to = -1;
+  lasp_ring_peers(c->rank, c->world, 0, &from, &to);
+  LASP_CUDA(prefix(p, Dir::FWD, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
+  ProfSpan hop("exchange_fwd", st);
+  if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
+    if ((s = exchange_allgather(c, p, w.local, w.in, false, st)) != LASP_OK) return s;
+  } else {
+    // F2 ring hop: Recv KV_in from r-1 (Alg. 2), combine, Send to r+1
+    if (from >= 0) {
+      if ((s = ring_recv(c, w.in, n, from, st, "ncclRecv(KV)")) != LASP_OK) return s;
+    } else {
+      LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), st));
+    }
+    if (to >= 0) {
+      LASP_CUDA(combine(p, w.in, w.local, w.out, st));
+      if ((s = ring_send(c, w.out, n, to, st, "ncclSend(KV)")) != LASP_OK) return s;
+    }
+  }
+  hop.stop(st);
+  return fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, gbar, w.claim(1), st, norm);     // F2 + F3
+}
+
+// Alg. 3 for one rank after validation (c == nullptr: local path). nb: the Norm backward fused into B1 --
+// d_o is then dY, and dO = Norm'(dY) is written to nb->dout, which the B3 passes read.
+lasp_status_t bwd_body(lasp_ctx* c, const Plan& p, const void* q, const void* k, const void* v, const void* d_o,
+                       const void* cache, const float* dkv_in, void* dq, void* dk, void* dv, float* dkv_out,
+                       void* workspace, cudaStream_t st, const NormBwdArgs* nb) {
+  Workspace w = carve(p, workspace);
+  lasp_status_t s;
+  const float* P = static_cast<const float*>(cache);
+  const bool fuse = p.C > 0 && fused_fold(p);
+  const void* g = nb ? nb->dout : d_o;  // the dO the B3 passes read
+  LASP_CUDA(entry_tag(p, cache, w, c ? c->rank : -1, c ? c->world : -1, true, c != nullptr, st));  // tag check
+  if (c == nullptr) {
+    if (p.C == 0) {
+      LASP_CUDA(prefix(p, Dir::REV, dkv_in, nullptr, nullptr, dkv_out, st));
+      return LASP_OK;
+    }
+    LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, w.claim(0), nb));                      // B1
+    const PrefixFold fold{dkv_in, w.seg, w.seg, dkv_out, w.gbar, int(Dir::REV)};
+    if (!fuse) LASP_CUDA(prefix(p, Dir::REV, dkv_in, w.seg, w.seg, dkv_out, st));          // B2 (in place)
+    // B3: dQ (needs only the cache), dV and dK in one launch (with B2 folded in when fused)
+    const SeqArgs passes[3] = {{g, v, k, dq, P, 1, w.status(), 0}, {k, q, g, dv, w.seg, 0, w.status(), 1},
+                               {v, g, q, dk, w.seg, 1, w.status(), 1}};
+    const Dir dirs[3] = {Dir::FWD, Dir::REV, Dir::REV};
+    // with the fused fold B1 immediately precedes this launch: dO (written by B1) must be waited for
+    LASP_CUDA(core_multi(p, 3, passes, dirs, st, w.claim(1), fuse ? &fold : nullptr, nullptr, nb && fuse));
+    return LASP_OK;
+  }
+  const size_t n = state_elems(p);
+  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, w.claim(0), nb));         // B1
+  LASP_CUDA(prefix(p, Dir::REV, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
+  // B2 ring hop on the comm stream: Recv dKV_in from r+1 (Alg. 3 P:629), combine, Send to r-1
+  LASP_CUDA(cudaEventRecord(c->ev_ready, st));
+  LASP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+  ProfSpan hop("exchange_bwd", c->comm_stream);
+  int from = -1, to = -1;
+  lasp_ring_peers(c->rank, c->world, 1, &from, &to);
+  const bool hop_pending = c->world > 1;  // a receive, send or all-gather runs on the comm stream under dQ
+  if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
+    if ((s = exchange_allgather(c, p, w.local, w.in, true, c->comm_stream)) != LASP_OK) return s;
+  } else if (from >= 0) {
+    if ((s = ring_recv(c, w.in, n, from, c->comm_stream, "ncclRecv(dKV)")) != LASP_OK) return s;
+  } else {
+    LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), c->comm_stream));                   // P:585
+  }
+  if (to >= 0 && c->exchange != LASP_EXCHANGE_ALLGATHER) {
+    LASP_CUDA(combine(p, w.in, w.local, w.out, c->comm_stream));
+    if ((s = ring_send(c, w.out, n, to, c->comm_stream, "ncclSend(dKV)")) != LASP_OK) return s;
+  }
+  hop.stop(c->comm_stream);
+  LASP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
+  // dQ needs only the cache: it runs while the dKV hop is in flight, on all SMs but comm_sms()
+  if (p.C > 0)
+    LASP_CUDA(core(p, Dir::FWD, g, v, k, dq, P, 1, st, w.claim(1), w.status(), hop_pending ? comm_sms() : 0));
+  LASP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
+  if (p.C == 0) return LASP_OK;
+  if (!fuse) LASP_CUDA(prefix(p, Dir::REV, w.in, w.seg, w.seg, nullptr, st));   // B2
+  {  // dV and dK in one launch (with B2 folded in when fused)
+    const SeqArgs passes[2] = {{k, q, g, dv, w.seg, 0, w.status(), 1}, {v, g, q, dk, w.seg, 1, w.status(), 1}};
+    const Dir dirs[2] = {Dir::REV, Dir::REV};
+    const PrefixFold fold{w.in, w.seg, w.seg, nullptr, w.gbar, int(Dir::REV)};
+    LASP_CUDA(core_multi(p, 2, passes, dirs, st, w.claim(2), fuse ? &fold : nullptr));
+  }
+  return LASP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -656,13 +834,7 @@ lasp_status_t lasp_fwd_local(const lasp_shape_t* shape, const void* q, const voi
   if (s != LASP_OK) return s;
   if ((s = check_ptrs(p, {q, k, v, o}, cache, workspace)) != LASP_OK) return s;
   if ((s = check_device()) != LASP_OK) return s;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  Workspace w = carve(p, workspace);
-  unsigned* gbar = p.C > 0 && fused_fold(p) ? w.gbar : nullptr;
-  LASP_CUDA(entry_tag(p, cache, w, -1, -1, false, false, st));                            // cache tag
-  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, w.claim(0)));            // F1
-  if ((s = fwd_tail(p, q, k, v, kv_in, o, kv_out, cache, w.seg, gbar, w.claim(1), st)) != LASP_OK) return s;  // F2 + F3
-  return LASP_OK;
+  return fwd_body(nullptr, p, q, k, v, kv_in, o, kv_out, cache, workspace, static_cast<cudaStream_t>(stream), nullptr);
 }
 
 lasp_status_t lasp_bwd_local(const lasp_shape_t* shape, const void* q, const void* k, const void* v,
@@ -673,24 +845,8 @@ lasp_status_t lasp_bwd_local(const lasp_shape_t* shape, const void* q, const voi
   if (s != LASP_OK) return s;
   if ((s = check_ptrs(p, {q, k, v, d_o, dq, dk, dv}, cache, workspace)) != LASP_OK) return s;
   if ((s = check_device()) != LASP_OK) return s;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  Workspace w = carve(p, workspace);
-  const float* P = static_cast<const float*>(cache);
-  LASP_CUDA(entry_tag(p, cache, w, -1, -1, true, false, st));                             // cache tag check
-  if (p.C == 0) {
-    LASP_CUDA(prefix(p, Dir::REV, dkv_in, nullptr, nullptr, dkv_out, st));
-    return LASP_OK;
-  }
-  const bool fuse = fused_fold(p);
-  LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, w.claim(0)));                        // B1
-  const PrefixFold fold{dkv_in, w.seg, w.seg, dkv_out, w.gbar, int(Dir::REV)};
-  if (!fuse) LASP_CUDA(prefix(p, Dir::REV, dkv_in, w.seg, w.seg, dkv_out, st));         // B2 (in place)
-  // B3: dQ (needs only the cache), dV and dK in one launch (with B2 folded in when fused)
-  const SeqArgs passes[3] = {{d_o, v, k, dq, P, 1, w.status(), 0}, {k, q, d_o, dv, w.seg, 0, w.status(), 1},
-                             {v, d_o, q, dk, w.seg, 1, w.status(), 1}};
-  const Dir dirs[3] = {Dir::FWD, Dir::REV, Dir::REV};
-  LASP_CUDA(core_multi(p, 3, passes, dirs, st, w.claim(1), fuse ? &fold : nullptr));
-  return LASP_OK;
+  return bwd_body(nullptr, p, q, k, v, d_o, cache, dkv_in, dq, dk, dv, dkv_out, workspace,
+                  static_cast<cudaStream_t>(stream), nullptr);
 }
 
 lasp_status_t lasp_unique_id(uint8_t id[128]) {
@@ -813,36 +969,7 @@ lasp_status_t lasp_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   if (s != LASP_OK) return s;
   if ((s = check_ptrs(p, {q, k, v, o}, cache, workspace)) != LASP_OK) return s;
   if ((s = check_device()) != LASP_OK) return s;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  Workspace w = carve(p, workspace);
-  const size_t n = state_elems(p);
-  int from = -1, to = -1;
-  lasp_ring_peers(c->rank, c->world, 0, &from, &to);
-  unsigned* gbar = p.C > 0 && fused_fold(p) ? w.gbar : nullptr;
-  LASP_CUDA(entry_tag(p, cache, w, c->rank, c->world, false, false, st));              // cache tag
-  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, w.claim(0)));         // F1
-  LASP_CUDA(prefix(p, Dir::FWD, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
-  if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
-    ProfSpan hop("exchange_fwd", st);
-    if ((s = exchange_allgather(c, p, w.local, w.in, false, st)) != LASP_OK) return s;
-    hop.stop(st);
-    if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, gbar, w.claim(1), st)) != LASP_OK) return s;
-    return LASP_OK;
-  }
-  // F2 ring hop: Recv KV_in from r-1 (Alg. 2), combine, Send to r+1
-  ProfSpan hop("exchange_fwd", st);
-  if (from >= 0) {
-    if ((s = ring_recv(c, w.in, n, from, st, "ncclRecv(KV)")) != LASP_OK) return s;
-  } else {
-    LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), st));
-  }
-  if (to >= 0) {
-    LASP_CUDA(combine(p, w.in, w.local, w.out, st));
-    if ((s = ring_send(c, w.out, n, to, st, "ncclSend(KV)")) != LASP_OK) return s;
-  }
-  hop.stop(st);
-  if ((s = fwd_tail(p, q, k, v, w.in, o, nullptr, cache, w.seg, gbar, w.claim(1), st)) != LASP_OK) return s;  // F2+F3
-  return LASP_OK;
+  return fwd_body(c, p, q, k, v, nullptr, o, nullptr, cache, workspace, static_cast<cudaStream_t>(stream), nullptr);
 }
 
 lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, const void* k, const void* v,
@@ -854,45 +981,68 @@ lasp_status_t lasp_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const void* q, c
   if (s != LASP_OK) return s;
   if ((s = check_ptrs(p, {q, k, v, d_o, dq, dk, dv}, cache, workspace)) != LASP_OK) return s;
   if ((s = check_device()) != LASP_OK) return s;
+  return bwd_body(c, p, q, k, v, d_o, cache, nullptr, dq, dk, dv, nullptr, workspace,
+                  static_cast<cudaStream_t>(stream), nullptr);
+}
+
+// ---- NEXT-3: the layer around the path (projection prologue, Norm epilogue) --------------------------------
+size_t lasp_layer_workspace_bytes(const lasp_shape_t* shape) {
+  if (validate_shape(shape) != LASP_OK) return 0;
+  const Plan p = make_plan(shape);
+  return workspace_bytes(p) + align256(size_t(p.B * p.C * p.H) * 2 * sizeof(float));  // + Norm slice sums
+}
+
+lasp_status_t lasp_layer_fwd(lasp_ctx_t c, const lasp_shape_t* shape, int64_t d_model, const void* x,
+                             const void* w_q, const void* w_k, const void* w_v, const float* lambda, void* q, void* k,
+                             void* v, void* y, float* rnorm, void* cache, void* workspace, void* stream) {
+  Plan p;
+  lasp_status_t s = prologue(shape, lambda, p);
+  if (s != LASP_OK) return s;
+  if (d_model < 1 || (p.C > 0 && (!x || !w_q || !w_k || !w_v || !rnorm)))
+    return fail(LASP_ERR_SHAPE, "layer: d_model >= 1 and non-NULL x, w_q, w_k, w_v, rnorm required");
+  if (!tc_supported(p)) return fail(LASP_ERR_UNSUPPORTED, "layer: the Norm epilogue needs bf16 and head_dim 64 or 128");
+  if ((s = check_ptrs(p, {q, k, v, y}, cache, workspace)) != LASP_OK) return s;
+  if ((s = check_device()) != LASP_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  Workspace w = carve(p, workspace);
-  const size_t n = state_elems(p);
-  const float* P = static_cast<const float*>(cache);
-  const bool fuse = p.C > 0 && fused_fold(p);
-  LASP_CUDA(entry_tag(p, cache, w, c->rank, c->world, true, true, st));                 // cache tag check
-  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, w.claim(0)));       // B1
-  LASP_CUDA(prefix(p, Dir::REV, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
-  // B2 ring hop on the comm stream: Recv dKV_in from r+1 (Alg. 3 P:629), combine, Send to r-1
-  LASP_CUDA(cudaEventRecord(c->ev_ready, st));
-  LASP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
-  ProfSpan hop("exchange_bwd", c->comm_stream);
-  int from = -1, to = -1;
-  lasp_ring_peers(c->rank, c->world, 1, &from, &to);
-  const bool hop_pending = c->world > 1;  // a receive, send or all-gather runs on the comm stream under dQ
-  if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
-    if ((s = exchange_allgather(c, p, w.local, w.in, true, c->comm_stream)) != LASP_OK) return s;
-  } else if (from >= 0) {
-    if ((s = ring_recv(c, w.in, n, from, c->comm_stream, "ncclRecv(dKV)")) != LASP_OK) return s;
-  } else {
-    LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), c->comm_stream));            // P:585
+  if (p.C > 0) {  // Alg. 2: Q = X W_Q, K = X W_K, V = X W_V (the rank's own chunk)
+    cublasHandle_t h;
+    if ((s = cublas_handle(st, &h)) != LASP_OK) return s;
+    const int64_t M = p.B * p.C;
+    if ((s = gemm_rm(h, M, p.H * p.D, d_model, x, false, w_q, false, q, false, 0.f)) != LASP_OK) return s;
+    if ((s = gemm_rm(h, M, p.Hk * p.D, d_model, x, false, w_k, false, k, false, 0.f)) != LASP_OK) return s;
+    if ((s = gemm_rm(h, M, p.Hk * p.D, d_model, x, false, w_v, false, v, false, 0.f)) != LASP_OK) return s;
   }
-  if (to >= 0 && c->exchange != LASP_EXCHANGE_ALLGATHER) {
-    LASP_CUDA(combine(p, w.in, w.local, w.out, c->comm_stream));
-    if ((s = ring_send(c, w.out, n, to, c->comm_stream, "ncclSend(dKV)")) != LASP_OK) return s;
-  }
-  hop.stop(c->comm_stream);
-  LASP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
-  // dQ needs only the cache: it runs while the dKV hop is in flight
-  if (p.C > 0)
-    LASP_CUDA(core(p, Dir::FWD, d_o, v, k, dq, P, 1, st, w.claim(1), w.status(), hop_pending ? comm_sms() : 0));
-  LASP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
-  if (p.C == 0) return LASP_OK;
-  if (!fuse) LASP_CUDA(prefix(p, Dir::REV, w.in, w.seg, w.seg, nullptr, st));   // B2
-  {  // dV and dK in one launch (with B2 folded in when fused)
-    const SeqArgs passes[2] = {{k, q, d_o, dv, w.seg, 0, w.status(), 1}, {v, d_o, q, dk, w.seg, 1, w.status(), 1}};
-    const Dir dirs[2] = {Dir::REV, Dir::REV};
-    const PrefixFold fold{w.in, w.seg, w.seg, nullptr, w.gbar, int(Dir::REV)};
-    LASP_CUDA(core_multi(p, 2, passes, dirs, st, w.claim(2), fuse ? &fold : nullptr));
+  const NormArgs norm{rnorm, reinterpret_cast<float*>(static_cast<char*>(workspace) + workspace_bytes(p)),
+                      kNormEps};
+  return fwd_body(c, p, q, k, v, nullptr, y, nullptr, cache, workspace, st, &norm);
+}
+
+lasp_status_t lasp_layer_bwd(lasp_ctx_t c, const lasp_shape_t* shape, int64_t d_model, const void* x,
+                             const void* w_q, const void* w_k, const void* w_v, const float* lambda, const void* q,
+                             const void* k, const void* v, const void* y, const float* rnorm, const void* dy,
+                             const void* cache, void* d_o, void* dq, void* dk, void* dv, void* dx, float* dw_q,
+                             float* dw_k, float* dw_v, void* workspace, void* stream) {
+  Plan p;
+  lasp_status_t s = prologue(shape, lambda, p);
+  if (s != LASP_OK) return s;
+  if (d_model < 1 || (p.C > 0 && (!x || !w_q || !w_k || !w_v || !rnorm || !dx || !dw_q || !dw_k || !dw_v)))
+    return fail(LASP_ERR_SHAPE, "layer: d_model >= 1 and non-NULL x, w_*, rnorm, dx, dw_* required");
+  if (!tc_supported(p)) return fail(LASP_ERR_UNSUPPORTED, "layer: the Norm backward needs bf16 and head_dim 64 or 128");
+  if ((s = check_ptrs(p, {q, k, v, y, dy, d_o, dq, dk, dv}, cache, workspace)) != LASP_OK) return s;
+  if ((s = check_device()) != LASP_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const NormBwdArgs nb{y, rnorm, d_o};
+  if ((s = bwd_body(c, p, q, k, v, dy, cache, nullptr, dq, dk, dv, nullptr, workspace, st, &nb)) != LASP_OK) return s;
+  if (p.C > 0) {  // dX = dQ W_Q^T + dK W_K^T + dV W_V^T; dW_* = X^T d* (fp32)
+    cublasHandle_t h;
+    if ((s = cublas_handle(st, &h)) != LASP_OK) return s;
+    const int64_t M = p.B * p.C, NQ = p.H * p.D, NK = p.Hk * p.D;
+    if ((s = gemm_rm(h, M, d_model, NQ, dq, false, w_q, true, dx, false, 0.f)) != LASP_OK) return s;
+    if ((s = gemm_rm(h, M, d_model, NK, dk, false, w_k, true, dx, false, 1.f)) != LASP_OK) return s;
+    if ((s = gemm_rm(h, M, d_model, NK, dv, false, w_v, true, dx, false, 1.f)) != LASP_OK) return s;
+    if ((s = gemm_rm(h, d_model, NQ, M, x, true, dq, false, dw_q, true, 0.f)) != LASP_OK) return s;
+    if ((s = gemm_rm(h, d_model, NK, M, x, true, dk, false, dw_k, true, 0.f)) != LASP_OK) return s;
+    if ((s = gemm_rm(h, d_model, NK, M, x, true, dv, false, dw_v, true, 0.f)) != LASP_OK) return s;
   }
   return LASP_OK;
 }

@@ -165,16 +165,34 @@ bool tc_supported(const Plan& p);
 bool tc_fold_fusable(const Plan& p);  // fuse the prefix fold into the core launch (small enough state)
 const char* tc_last_error();
 void tc_set_trace(unsigned long long* buf);  // debug: per-block clock64 timeline of CTA 0  // detail of the last tcgen05-path host failure on this thread
+// Norm backward fused into B1 (NEXT-3): y here is dY; dO = r (dY - y_fwd (y_fwd . dY) / D) is formed per row
+// in shared memory, used as the MMA operand and written to dout for the B3 passes
+struct NormBwdArgs {
+  const void* y;       // forward output Norm(O) [B][C][H][D] bf16
+  const float* rnorm;  // [B][C][H]
+  void* dout;          // [B][C][H][D] bf16, written
+};
 // claim: the launch's work-claim counter (a workspace word zeroed by the call's entry kernel)
 cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out,
-                                cudaStream_t st, unsigned* claim);
-// reserve_sms: leave that many SMs free for another stream's kernels (ring hop in flight)
+                                cudaStream_t st, unsigned* claim, const NormBwdArgs* norm_bwd = nullptr);
+// Norm(.) of Eq. 2 (NEXT-3, reading N1: per-head RMS normalization) fused into the forward core's epilogue
+constexpr float kNormEps = 1e-6f;  // reading N1
+struct NormArgs {
+  float* rnorm;   // [B][C][H] fp32: r = (mean_c o_c^2 + eps)^-1/2 (head_dim 64: written by the core epilogue)
+  float* nsum;    // [B][C][H][2] fp32: per-value-slice sums of squares (head_dim 128; norm_apply finishes)
+  float eps;
+};
+// reserve_sms: leave that many SMs free for another stream's kernels (ring hop in flight); norm: the
+// forward O pass writes Norm(O) (NormArgs); late_inputs: an input is produced by the preceding kernel
 cudaError_t launch_core_tc(const Plan& p, Dir dir, const SeqArgs& a, cudaStream_t st, unsigned* claim,
-                           int reserve_sms = 0);
+                           int reserve_sms = 0, const NormArgs* norm = nullptr, bool late_inputs = false);
 // up to 3 core passes in one persistent launch (their segments interleaved: shared inputs hit L2);
 // fold != nullptr: the launch first computes the prefix states its passes read (PrefixFold)
 cudaError_t launch_core_tc_multi(const Plan& p, int npass, const SeqArgs* a, const Dir* dirs, cudaStream_t st,
-                                 const PrefixFold* fold, unsigned* claim, int reserve_sms = 0);
+                                 const PrefixFold* fold, unsigned* claim, int reserve_sms = 0,
+                                 const NormArgs* norm = nullptr, bool late_inputs = false);
+// head_dim 128 second phase of the Norm epilogue: y = o r in place from the two slice sums (nsum)
+cudaError_t launch_norm_apply(const Plan& p, void* y, const NormArgs& n, cudaStream_t st);
 cudaError_t launch_occupy(int ctas, int smem, double us, cudaStream_t st);  // debug: SM hog on another stream
 
 }  // namespace lasp

@@ -30,7 +30,7 @@ __all__ = [
 ]
 
 # Fixed tensor ids (part of the recipe: changing them changes every fixture).
-TENSOR_IDS = {"q": 1, "k": 2, "v": 3, "do": 4}
+TENSOR_IDS = {"q": 1, "k": 2, "v": 3, "do": 4, "x": 5, "wq": 6, "wk": 7, "wv": 8, "dy": 9}
 
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
 
@@ -133,4 +133,31 @@ def problem(seed: int, batch: int, n_global: int, heads: int, head_dim: int,
                   token_hi)
          for nm in (("q", "k", "v", "do") if with_do else ("q", "k", "v"))}
     t["lam"] = head_lambdas(hk, lam)
+    return t
+
+
+def _draw2(name: str, seed: int, rows: int, cols: int, scale: float, dtype: str, row_lo: int = 0,
+           row_hi: int | None = None, row_total: int | None = None) -> np.ndarray:
+    """A [rows][cols] matrix (rows [row_lo, row_hi) of a [row_total][cols] one) with the same generator."""
+    row_hi = rows if row_hi is None else row_hi
+    a = draw(name, seed, 1, row_total or rows, 1, cols, dtype, row_lo, row_hi, scale=scale)
+    return a.reshape(row_hi - row_lo, cols)
+
+
+def layer_problem(seed: int, batch: int, n_global: int, heads: int, kv_heads: int, head_dim: int, d_model: int,
+                  token_lo: int = 0, token_hi: int | None = None, lam: float | None = None) -> dict:
+    """Inputs of the NEXT-3 layer (projection + LASP + Norm): x [B][tokens][d_model] (unit variance),
+    w_q [d][H*D], w_k, w_v [d][Hk*D] with scales d^-1/2 * D^-1/4 (q . k of unit variance, as the q, k recipe)
+    and d^-1/2 (v), dy [B][tokens][H][D] (unit variance), all bf16-valued float32; lambda per kv-head."""
+    token_hi = n_global if token_hi is None else token_hi
+    n = token_hi - token_lo
+    x = np.stack([_draw2("x", seed, n_global, d_model, 1.0, "bf16", b * n_global + token_lo,
+                         b * n_global + token_hi, batch * n_global) for b in range(batch)])
+    sq = d_model ** -0.5 * head_dim ** -0.25
+    t = {"x": x.reshape(batch, n, d_model),
+         "w_q": _draw2("wq", seed, d_model, heads * head_dim, sq, "bf16"),
+         "w_k": _draw2("wk", seed, d_model, kv_heads * head_dim, sq, "bf16"),
+         "w_v": _draw2("wv", seed, d_model, kv_heads * head_dim, d_model ** -0.5, "bf16"),
+         "dy": draw("dy", seed, batch, n_global, heads, head_dim, "bf16", token_lo, token_hi),
+         "lam": head_lambdas(kv_heads, lam)}
     return t
