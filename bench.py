@@ -272,6 +272,53 @@ def closed_form_check(lasp, dev, B, C, H, D, lam, rank, T, run, Hk=None):
     return worst
 
 
+def layer_bench(args, lasp, dev, stream, B, C, H, Hk, D, l2_flush):
+    """one whole attention layer, Y = Norm(LASP(X W_Q, X W_K, X W_V)) forward and its
+    backward (dX, dW_Q, dW_K, dW_V) through lasp_layer_fwd / lasp_layer_bwd (cuBLAS projections, Norm fused
+    into the core epilogue / the B1 kernel), d_model = H * D, graph-replayed like the main line, L2 flushed
+    between steps. Reported next to the attention-only number, not instead of it."""
+    import torch
+
+    import synth
+    d = H * D
+    t = synth.layer_problem(0, B, C, H, Hk, D, d)
+    x, wq, wk, wv, dy = (torch.from_numpy(t[n]).to(dev, torch.bfloat16) for n in ("x", "w_q", "w_k", "w_v", "dy"))
+    fw = lasp.layer_fwd(x, wq, wk, wv, t["lam"], H)
+    g = lasp.layer_bwd(x, wq, wk, wv, t["lam"], fw, dy)
+    outs_f = {n: fw[n] for n in ("q", "k", "v", "y", "rnorm", "cache")}
+    outs_b = dict(g)
+
+    def step():
+        lasp.layer_fwd(x, wq, wk, wv, t["lam"], H, out=outs_f, workspace=fw["workspace"])
+        lasp.layer_bwd(x, wq, wk, wv, t["lam"], fw, dy, out=outs_b)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    graph = None
+    if args.graph:
+        try:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                step()
+            gr.replay()
+            torch.cuda.synchronize(dev)
+            graph = gr
+        except Exception:  # noqa: BLE001 - eager fallback, reported
+            torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        l2_flush()
+        ev[i][0].record(stream)
+        graph.replay() if graph is not None else step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    flops = 2 * 3 * B * C * d * (H + 2 * Hk) * D  # projection GEMMs: fwd X W, bwd dX and dW; 2 flop per MAC
+    return {"metric": "layer fwd+bwd tokens/sec (projections + LASP + Norm)", "value": B * C / (ms / 1e3),
+            "unit": "tokens/s", "ms_per_step": ms, "d_model": d, "launch": "cuda-graph replay" if graph else "eager",
+            "projection_gflop_per_step": flops / 1e9}
+
+
 def cpu_info():
     model = "unknown"
     try:
@@ -563,6 +610,10 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
             "stages_ms_per_step": {kk: vv[1] / args.steps for kk, vv in stages.items()},
             "profiled_ms_per_step": R["prof_ms"] / args.steps}
 
+    layer = None
+    if world == 1 and not loopback and not args.no_layer:
+        layer = layer_bench(args, lasp, dev, stream, B, C, H, Hk, D, l2_flush)
+
     cpu = None
     if world == 1 and not loopback and not args.no_cpu_baseline:
         cpu = cpu_baseline(H, D, C, desc)
@@ -583,7 +634,7 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
                        "launch": ex_report[main_ex]["launch"], "exchange": main_ex},
             "parity_ok": all(r["parity_ok"] for r in ex_report.values()),
             "gpu_launches": int(R["launches"]), "clocks": clk_summary, "e2e": e2e, "roofline": roofline,
-            "path": path, "cpu_baseline": cpu}
+            "path": path, "cpu_baseline": cpu, "layer": layer}
     if T > 1:
         line["exchanges"] = ex_report
     else:
@@ -670,6 +721,7 @@ def main():
     ap.add_argument("--kv-heads", type=int, default=0,
                     help="grouped-query attention: key/value heads (default: the config's heads, i.e. multi-head)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-layer", action="store_true", help="skip the NEXT-3 whole-layer line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -189,35 +189,53 @@ def norm_bwd(y, r, dy):
     return out
 
 
-def layer_fwd(x, w_q, w_k, w_v, lam, H, Hk=None, eps=NORM_EPS, nthreads=None):
+def round_bf16(a):
+    """Round to bfloat16 (ties to even), returned as float64: the precision of a tensor the bf16 path
+    materializes (reading N2). fp64 -> fp32 (RNE) -> bf16 (RNE on the fp32 bits), the same two
+    steps as a kernel that accumulates in fp32 and stores bf16 (the double rounding can differ from a direct
+    fp64 -> bf16 rounding only when the fp32 step lands on a bf16 tie)."""
+    f = np.ascontiguousarray(np.asarray(a, np.float64).astype(np.float32))
+    u = f.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16 << 16  # RNE on the low 16 bits (finite inputs)
+    return u.astype(np.uint32).view(np.float32).astype(np.float64).reshape(np.shape(a))
+
+
+def layer_fwd(x, w_q, w_k, w_v, lam, H, Hk=None, eps=NORM_EPS, nthreads=None, bf16_points=False):
     """NEXT-3 layer: Alg. 2 line 'Calculate Q = X W_Q, K = X W_K, V = X W_V' (numpy matmul as the
     library step), LASP O (fwd / fwd_gqa), then Norm (reading N1). x [B][N][d], w_* [d][heads * D].
+    bf16_points: Q, K, V (and in layer_bwd Y, dO, dQ, dK, dV) are rounded to bf16 where the bf16 path
+    materializes them (reading N2); everything else stays fp64.
     Returns dict with q, k, v [B][N][heads][D], o, y, r."""
     x = _f64(x)
     B, N, d = x.shape
     Hk = Hk or H
-    q = (x @ _f64(w_q)).reshape(B, N, H, -1)
-    k = (x @ _f64(w_k)).reshape(B, N, Hk, -1)
-    v = (x @ _f64(w_v)).reshape(B, N, Hk, -1)
+    rnd = round_bf16 if bf16_points else (lambda t: t)
+    q = rnd(x @ _f64(w_q)).reshape(B, N, H, -1)
+    k = rnd(x @ _f64(w_k)).reshape(B, N, Hk, -1)
+    v = rnd(x @ _f64(w_v)).reshape(B, N, Hk, -1)
     o = fwd_gqa(q, k, v, lam, nthreads) if Hk != H else fwd(q, k, v, lam, nthreads)
     y, r = norm_fwd(o, eps)
-    return {"q": q, "k": k, "v": v, "o": o, "y": y, "r": r}
+    return {"q": q, "k": k, "v": v, "o": o, "y": y, "r": r, "bf16_points": bf16_points}
 
 
 def layer_bwd(x, w_q, w_k, w_v, lam, fw, dy, nthreads=None):
-    """Gradients of sum(Y * dY) for layer_fwd: (dX [B][N][d], dW_Q, dW_K, dW_V [d][heads * D], dO)."""
+    """Gradients of sum(Y * dY) for layer_fwd: (dX [B][N][d], dW_Q, dW_K, dW_V [d][heads * D], dO, dQ, dK, dV).
+    With fw from layer_fwd(bf16_points=True) the stored Y, the formed dO and dQ, dK, dV are rounded to bf16
+    (reading N2), as the bf16 path stores them."""
     x = _f64(x)
     B, N, d = x.shape
     q, k, v = fw["q"], fw["k"], fw["v"]
-    do = norm_bwd(fw["y"], fw["r"], dy)
+    rnd = round_bf16 if fw.get("bf16_points") else (lambda t: t)
+    do = rnd(norm_bwd(rnd(fw["y"]), fw["r"], dy))
     if k.shape[2] != q.shape[2]:
         dq, dk, dv = bwd_gqa(q, k, v, lam, do, nthreads)
     else:
         dq, dk, dv = bwd(q, k, v, lam, do, nthreads)
+    dq, dk, dv = rnd(dq), rnd(dk), rnd(dv)
     dq2, dk2, dv2 = (t.reshape(B * N, -1) for t in (dq, dk, dv))
     x2 = x.reshape(B * N, d)
     dx = (dq2 @ _f64(w_q).T + dk2 @ _f64(w_k).T + dv2 @ _f64(w_v).T).reshape(B, N, d)
-    return dx, x2.T @ dq2, x2.T @ dk2, x2.T @ dv2, do
+    return dx, x2.T @ dq2, x2.T @ dk2, x2.T @ dv2, do, dq, dk, dv
 
 
 def lasp_fwd_sim(q, k, v, lam, T, nthreads=None):

@@ -502,7 +502,7 @@ def test_layer_matches_dense_autograd(oracle_mod, H, Hk):
     dy = rng.standard_normal((B, N, H, D))
     lam = rng.uniform(0.6, 1.0, Hk).astype(np.float32)
     fw = oracle_mod.layer_fwd(x, wq, wk, wv, lam, H, Hk)
-    dx, dwq, dwk, dwv, _ = oracle_mod.layer_bwd(x, wq, wk, wv, lam, fw, dy)
+    dx, dwq, dwk, dwv = oracle_mod.layer_bwd(x, wq, wk, wv, lam, fw, dy)[:4]
     tx, tq, tk, tv = (torch.tensor(a, requires_grad=True) for a in (x, wq, wk, wv))
     q = (tx @ tq).reshape(B, N, H, D)
     k = (tx @ tk).reshape(B, N, Hk, D).repeat_interleave(H // Hk, dim=2)
@@ -517,3 +517,36 @@ def test_layer_matches_dense_autograd(oracle_mod, H, Hk):
     assert rel(fw["y"], y.detach().numpy()) <= 1e-12
     for a, b in ((dx, tx.grad), (dwq, tq.grad), (dwk, tk.grad), (dwv, tv.grad)):
         assert rel(a, b.numpy()) <= 1e-11
+
+
+def test_round_bf16_matches_torch_conversion(oracle_mod):
+    """oracle.round_bf16 (reading N2) is torch's fp32 -> bf16 round-to-nearest-even (a library routine) after
+    fp64 -> fp32, including ties, negative values, subnormal-range and large magnitudes."""
+    rng = np.random.default_rng(11)
+    a = np.concatenate([rng.standard_normal(20000) * 10.0 ** rng.integers(-30, 30, 20000),
+                        [0.0, -0.0, 1.0, 1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, -(1.0 + 2 ** -8), 3e38, 1e-40]])
+    ref = torch.tensor(a, dtype=torch.float64).to(torch.float32).to(torch.bfloat16).to(torch.float64).numpy()
+    got = oracle_mod.round_bf16(a)
+    assert np.array_equal(got, ref)
+    assert got[-5] == 1.0 and got[-4] == 1.0 + 2 ** -6  # ties to even: 1 + 2^-8 -> 1, 1 + 3*2^-8 -> 1 + 2^-6
+
+
+def test_layer_bf16_points_round_exactly_the_materialized_tensors(oracle_mod):
+    """bf16_points=True (reading N2) changes only the rounding of Q, K, V / Y, dO, dQ, dK, dV: with inputs whose
+    projections are already bf16-exact (X, W with few significant bits), both modes agree to fp64 rounding."""
+    rng = np.random.default_rng(5)
+    B, N, H, D = 1, 40, 2, 8
+    d = H * D
+    x = rng.integers(-2, 3, (B, N, d)).astype(np.float64)
+    wq, wk, wv = (rng.integers(-1, 2, (d, H * D)).astype(np.float64) / 8 for _ in range(3))
+    dy = oracle_mod.round_bf16(rng.standard_normal((B, N, H, D)))
+    lam = np.full(H, 0.75, np.float32)
+    fa = oracle_mod.layer_fwd(x, wq, wk, wv, lam, H)
+    fb = oracle_mod.layer_fwd(x, wq, wk, wv, lam, H, bf16_points=True)
+    for n in ("q", "k", "v", "o", "y", "r"):
+        assert np.array_equal(fa[n], fb[n]), n          # projections exact in bf16: identical forward
+    ga = oracle_mod.layer_bwd(x, wq, wk, wv, lam, fa, dy)
+    gb = oracle_mod.layer_bwd(x, wq, wk, wv, lam, fb, dy)
+    assert np.array_equal(gb[4], oracle_mod.round_bf16(gb[4]))           # dO is bf16-valued
+    assert rel(gb[4], ga[4]) <= 2 ** -8 and rel(gb[0], ga[0]) <= 5e-2   # the rounding of the fp64 chain (dX: cancellation)
+    assert not np.array_equal(gb[4], ga[4])                              # ... but rounded

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_gpu_layer.py -x -q 2>&1 | tail -25 > gpurun_out/r2f_layer.txt
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -30 > gpurun_out/r2f_pytest.txt
+timeout 300 python bench.py --steps 20 --warmup 5 > gpurun_out/r2f_bench.json 2> gpurun_out/r2f_bench.err
+timeout 300 python bench.py --steps 20 --warmup 5 --config tnl1b --no-e2e --no-cpu-baseline > gpurun_out/r2f_bench_tnl1b.json 2>> gpurun_out/r2f_bench.err
+timeout 300 python __graft_entry__.py smoke > gpurun_out/r2f_smoke.txt 2>&1
