@@ -586,7 +586,7 @@ __device__ __forceinline__ void grid_wait(const unsigned* ctr, unsigned target) 
 }
 
 struct CItem {
-  int64_t b, h, seg, beg, end;  // h: item head (of a and out)
+  int32_t b, h, seg, beg, end;  // h: item head (of a and out); token indices < 2^30 (tc_supported)
   int nblk, pass, v;  // v: 64-wide value slice
   int sh, sub, bh0;   // state / decay head; query heads summed per block (1 or G); b, c head of sub-block 0
   Dir dir;
@@ -883,6 +883,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
               for (int kk = 0; kk < L::DK / 16; ++kk)
                 mma_bf16(tmem + L::T_OX, desc_k(sbase + L::A(s) + koff(kk)), desc_mn(sbase + L::SLO(sb) + kk * 2048, BOX),
                          id_x, 1);
+              mma_commit(&bar->st_empty[sb]);  // the state copy is free once the inter MMAs have read it
             }
             mbar_wait(&bar->p_full[J & 1], (J >> 1) & 1);
             LASP_TRACE(11, J);
@@ -893,7 +894,6 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
               mma_bf16_ts(tmem + L::T_OI, pt + kk * 8, desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv, (kk | u) != 0);
             if (u + 1 == sub) {
               mma_commit(&bar->o_full);
-              mma_commit(&bar->st_empty[sb]);
               ++Jb;
             }
             mma_commit(&bar->s_empty[J & 1]);  // S/P buffer reusable once P c has been read
@@ -1429,7 +1429,9 @@ bool tc_supported(const Plan& p) {
     const char* s = std::getenv("LASP_DISABLE_TC");
     return s && *s && *s != '0';
   }();
-  return !disabled && p.dtype == 0 && (p.D == 64 || p.D == 128) && p.C > 0;
+  // 32-bit token coordinates (TMA boxes, work items) and item indices (B * H * nseg * passes * slices)
+  return !disabled && p.dtype == 0 && (p.D == 64 || p.D == 128) && p.C > 0 && p.C < (int64_t(1) << 30) &&
+         p.B * p.H * p.nseg * 6 < (int64_t(1) << 31);
 }
 
 cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st,
