@@ -525,6 +525,8 @@ struct CoreParams {
   float* rnorm;
   float* nsum;
   float norm_eps;
+  int seg_desc;               // 1: items in descending segment order (the segment-state launch before this one
+                              // ascended, so its last-read tiles are still in L2)
   int late_inputs;            // 1: an input tensor is written by the preceding kernel (fused Norm
                               // backward): the producer waits for it before the first load
 };
@@ -601,8 +603,9 @@ __device__ __noinline__ CItem get_citem(const CoreParams& prm, int64_t w) {
   const Plan& p = prm.p;
   CItem it;
   const uint32_t wu = uint32_t(w);
-  it.seg = prm.div_per.div(wu);
-  const uint32_t rem = wu - uint32_t(it.seg) * prm.per;
+  const uint32_t sg = prm.div_per.div(wu);
+  const uint32_t rem = wu - sg * prm.per;
+  it.seg = prm.seg_desc ? int32_t(p.nseg - 1 - sg) : int32_t(sg);
   if constexpr (!GQ) {  // multi-head: every pass has B * H * NV items per segment row (round-1 decode)
     const uint32_t nbh = uint32_t(p.B * p.H) * uint32_t(NV), nh = uint32_t(p.H);
     uint32_t bhv;
@@ -1378,6 +1381,15 @@ cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const 
     prm.norm_eps = norm->eps;
   }
   prm.late_inputs = late_inputs ? 1 : 0;
+  // descending segments: the preceding segment-state launch ascended, so the tiles it read last (K, V for
+  // F3; Q, and for B3 also dO) are the first this launch needs, and this launch ends on the segments the next
+  // ascending segment-state launch starts with (F3 -> B1 share Q). Same-box A/B: TNL-0.4B 228.0 -> 226.5 us
+  // (B1 35.2 -> 33.4 us), TNL-1B 560.4 -> 559.7 us. LASP_CORE_SEG_DESC=0 restores ascending order.
+  static const int seg_desc = [] {
+    const char* e = std::getenv("LASP_CORE_SEG_DESC");
+    return e && *e ? std::atoi(e) : 1;
+  }();
+  prm.seg_desc = seg_desc;
   const int smem = int(CoreLayout<D>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
   const int64_t W = p.nseg * int64_t(off);
