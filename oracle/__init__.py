@@ -11,6 +11,9 @@ this module only builds/loads it and marshals numpy arrays. Functions:
   Eq. 13-14 (P:257-272).
 * ``fwd_gqa`` / ``bwd_gqa`` -- the same recurrences with H query heads sharing Hk key/value heads
   (multi-query / grouped-query attention).
+* ``gla_fwd`` / ``gla_bwd`` -- generalised (per-token, per-channel) decay: the GLA / GateLoop row of
+  Table 3 (App. A.4); recurrence and its reverse, the decay
+  gradient from its definition.
 * ``norm_fwd`` / ``norm_bwd`` / ``layer_fwd`` / ``layer_bwd`` -- the steps either side of the path
   (SURVEY §8(f) NEXT-3): Q, K, V = X W (Alg. 2) and Norm(.) of Eq. 2 read as per-head RMS
   normalization (reading N1).
@@ -80,7 +83,10 @@ def _load():
                                                                           ctypes.c_int]
             lib.oracle_lasp_bwd_sim.argtypes = [_i64] * 5 + [_dp] * 3 + [_fp, _dp, _dp] + [_dp] * 3 + \
                 [_i64p, _i64p, ctypes.c_int]
+            lib.oracle_gla_fwd.argtypes = [_i64] * 4 + [_dp] * 5 + [ctypes.c_int]
+            lib.oracle_gla_bwd.argtypes = [_i64] * 4 + [_dp] * 9 + [ctypes.c_int]
             for fn in ("oracle_fwd", "oracle_bwd", "oracle_fwd_gqa", "oracle_bwd_gqa", "oracle_build_decay",
+                       "oracle_gla_fwd", "oracle_gla_bwd",
                        "oracle_lasp_fwd_sim",
                        "oracle_lasp_bwd_sim"):
                 getattr(lib, fn).restype = ctypes.c_int
@@ -164,6 +170,28 @@ def bwd_gqa(q, k, v, lam, do, nthreads=None):
     _check(_load().oracle_bwd_gqa(B, N, H, Hk, D, _ptr(q), _ptr(k), _ptr(v), lp, _ptr(do), _ptr(dq), _ptr(dk),
                                   _ptr(dv), _threads(nthreads)))
     return dq, dk, dv
+
+
+def gla_fwd(q, k, v, lg, nthreads=None):
+    """Generalised decay (NEXT-4; Table 3 GLA / GateLoop row, App. A.4): O of the recurrence
+    kv_t = Diag(exp(lg_t)) kv_{t-1} + k_t v_t^T, o_t = kv_t^T q_t. All inputs [B][N][H][D]; lg <= 0 is the
+    log of the per-token, per-key-channel decay."""
+    B, N, H, D = _shape4(q)
+    q, k, v, lg = _f64(q), _f64(k), _f64(v), _f64(lg)
+    o = np.zeros_like(q)
+    _check(_load().oracle_gla_fwd(B, N, H, D, _ptr(q), _ptr(k), _ptr(v), _ptr(lg), _ptr(o), _threads(nthreads)))
+    return o
+
+
+def gla_bwd(q, k, v, lg, do, nthreads=None):
+    """(dQ, dK, dV, dlg) of L = sum(O * dO) for gla_fwd; dlg_t[d] = g_t[d] sum_e dkv_t[d][e] kv_{t-1}[d][e] (the
+    definition of the gradient through kv_t = Diag(g_t) kv_{t-1} + ...)."""
+    B, N, H, D = _shape4(q)
+    q, k, v, lg, do = _f64(q), _f64(k), _f64(v), _f64(lg), _f64(do)
+    dq, dk, dv, dlg = (np.zeros_like(q) for _ in range(4))
+    _check(_load().oracle_gla_bwd(B, N, H, D, _ptr(q), _ptr(k), _ptr(v), _ptr(lg), _ptr(do), _ptr(dq), _ptr(dk),
+                                  _ptr(dv), _ptr(dlg), _threads(nthreads)))
+    return dq, dk, dv, dlg
 
 
 NORM_EPS = 1e-6  # DESIGN.md reading N1

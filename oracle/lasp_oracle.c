@@ -642,3 +642,138 @@ int oracle_lasp_bwd_sim(int64_t B, int64_t N, int64_t H, int64_t D, int64_t T, c
     free(m);
     return ORACLE_OK;
 }
+
+/* ---------------------------------------------------------------------------------- */
+/* Generalised decay: the GLA / GateLoop row of Table 3 (App. A.4,   */
+/* P:671-713 general form m_t = o_t m_{t-1} + e_t i_t^T; GLA/GateLoop P:735):              */
+/*   kv_t = Diag(g_t) kv_{t-1} + k_t v_t^T,  o_t^T = q_t^T kv_t,  g_t = exp(lg_t) in (0,1]^D  */
+/* per token and key channel (data-dependent decay; a per-channel constant decay is        */
+/* lg_t = log lambda for every t). Definition mode: the recurrence, token by token.          */
+/* Backward of L = sum(O * dO): dkv_t = q_t do_t^T + Diag(g_{t+1}) dkv_{t+1} (dkv_N = 0),    */
+/* dq_t = kv_t do_t, dk_t = dkv_t v_t, dv_t = dkv_t^T k_t, and the decay gradient from its    */
+/* definition dL/dlg_t[d] = g_t[d] sum_e dkv_t[d][e] kv_{t-1}[d][e] (kv_{-1} = 0). The        */
+/* reverse sweep needs kv_{t-1}: the forward states are recomputed per 64-token chunk from   */
+/* checkpoints (kv entering each chunk), nothing is divided by a decay.                      */
+/* ---------------------------------------------------------------------------------- */
+typedef struct {
+    int64_t B, N, H, D;
+    const double *q, *k, *v, *lg, *dout;
+    double *o, *dq, *dk, *dv, *dlg;
+} gla_ctx_t;
+
+#define GROW(p, c, b, s, h) ((p) + ((((b) * (c)->N + (s)) * (c)->H + (h)) * (c)->D))
+
+/* kv <- Diag(exp(lg_s)) kv + k_s v_s^T */
+static void gla_step(int64_t D, double* kv, const double* lgs, const double* ks, const double* vs) {
+    for (int64_t d = 0; d < D; ++d) {
+        const double g = exp(lgs[d]);
+        for (int64_t e = 0; e < D; ++e) kv[d * D + e] = g * kv[d * D + e] + ks[d] * vs[e];
+    }
+}
+
+static void gla_fwd_item(void* vctx, int64_t item) {
+    gla_ctx_t* c = (gla_ctx_t*)vctx;
+    const int64_t b = item / c->H, h = item % c->H, D = c->D;
+    double* kv = (double*)calloc((size_t)(D * D), sizeof(double));
+    for (int64_t s = 0; s < c->N; ++s) {
+        gla_step(D, kv, GROW(c->lg, c, b, s, h), GROW(c->k, c, b, s, h), GROW(c->v, c, b, s, h));
+        const double* qs = GROW(c->q, c, b, s, h);
+        double* os = GROW(c->o, c, b, s, h);
+        for (int64_t e = 0; e < D; ++e) os[e] = 0.0;
+        for (int64_t d = 0; d < D; ++d)
+            for (int64_t e = 0; e < D; ++e) os[e] += qs[d] * kv[d * D + e];
+    }
+    free(kv);
+}
+
+#define GLA_CK 64
+static void gla_bwd_item(void* vctx, int64_t item) {
+    gla_ctx_t* c = (gla_ctx_t*)vctx;
+    const int64_t b = item / c->H, h = item % c->H, D = c->D, N = c->N, DD = D * D;
+    const int64_t nck = (N + GLA_CK - 1) / GLA_CK;
+    double* ck = (double*)calloc((size_t)((nck > 0 ? nck : 1) * DD), sizeof(double)); /* kv entering chunk j */
+    double* st = (double*)malloc(sizeof(double) * (size_t)((GLA_CK + 1) * DD));       /* kv_{t-1}, kv_t, ... */
+    double* kv = (double*)calloc((size_t)DD, sizeof(double));
+    double* dkv = (double*)calloc((size_t)DD, sizeof(double));
+    for (int64_t s = 0; s < N; ++s) {
+        if (s % GLA_CK == 0) memcpy(ck + (s / GLA_CK) * DD, kv, sizeof(double) * (size_t)DD);
+        gla_step(D, kv, GROW(c->lg, c, b, s, h), GROW(c->k, c, b, s, h), GROW(c->v, c, b, s, h));
+    }
+    for (int64_t j = nck - 1; j >= 0; --j) {
+        const int64_t s0 = j * GLA_CK, s1 = (s0 + GLA_CK < N) ? s0 + GLA_CK : N;
+        /* st[i] = kv_{s0 + i - 1} for i = 0 .. s1 - s0 */
+        memcpy(st, ck + j * DD, sizeof(double) * (size_t)DD);
+        for (int64_t s = s0; s < s1; ++s) {
+            memcpy(st + (s - s0 + 1) * DD, st + (s - s0) * DD, sizeof(double) * (size_t)DD);
+            gla_step(D, st + (s - s0 + 1) * DD, GROW(c->lg, c, b, s, h), GROW(c->k, c, b, s, h),
+                     GROW(c->v, c, b, s, h));
+        }
+        for (int64_t s = s1 - 1; s >= s0; --s) {
+            const double* qs = GROW(c->q, c, b, s, h);
+            const double* ks = GROW(c->k, c, b, s, h);
+            const double* vs = GROW(c->v, c, b, s, h);
+            const double* dos = GROW(c->dout, c, b, s, h);
+            const double* kvs = st + (s - s0 + 1) * DD;  /* kv_s */
+            const double* kvp = st + (s - s0) * DD;      /* kv_{s-1} */
+            /* dkv_s = q_s do_s^T + Diag(g_{s+1}) dkv_{s+1} */
+            if (s + 1 < N) {
+                const double* lgn = GROW(c->lg, c, b, s + 1, h);
+                for (int64_t d = 0; d < D; ++d) {
+                    const double g = exp(lgn[d]);
+                    for (int64_t e = 0; e < D; ++e) dkv[d * D + e] *= g;
+                }
+            }
+            for (int64_t d = 0; d < D; ++d)
+                for (int64_t e = 0; e < D; ++e) dkv[d * D + e] += qs[d] * dos[e];
+            double* dqs = GROW(c->dq, c, b, s, h);
+            double* dks = GROW(c->dk, c, b, s, h);
+            double* dvs = GROW(c->dv, c, b, s, h);
+            double* dls = GROW(c->dlg, c, b, s, h);
+            const double* lgs = GROW(c->lg, c, b, s, h);
+            for (int64_t d = 0; d < D; ++d) {
+                double aq = 0.0, ak = 0.0, al = 0.0;
+                for (int64_t e = 0; e < D; ++e) {
+                    aq += kvs[d * D + e] * dos[e];
+                    ak += dkv[d * D + e] * vs[e];
+                    al += dkv[d * D + e] * kvp[d * D + e];
+                }
+                dqs[d] = aq;
+                dks[d] = ak;
+                dls[d] = exp(lgs[d]) * al;
+            }
+            for (int64_t e = 0; e < D; ++e) {
+                double av = 0.0;
+                for (int64_t d = 0; d < D; ++d) av += dkv[d * D + e] * ks[d];
+                dvs[e] = av;
+            }
+        }
+    }
+    free(ck); free(st); free(kv); free(dkv);
+}
+
+static int check_lg(int64_t n, const double* lg) {
+    for (int64_t i = 0; i < n; ++i)
+        if (!(lg[i] <= 0.0)) return ORACLE_ERR_DOMAIN; /* g = exp(lg) in (0, 1] */
+    return ORACLE_OK;
+}
+
+int oracle_gla_fwd(int64_t B, int64_t N, int64_t H, int64_t D, const double* q, const double* k, const double* v,
+                   const double* lg, double* o, int nthreads) {
+    if (B < 0 || N < 0 || H < 1 || D < 1) return ORACLE_ERR_SHAPE;
+    int st = check_lg(B * N * H * D, lg);
+    if (st) return st;
+    gla_ctx_t c = {B, N, H, D, q, k, v, lg, NULL, o, NULL, NULL, NULL, NULL};
+    run_items(gla_fwd_item, &c, B * H, nthreads);
+    return ORACLE_OK;
+}
+
+int oracle_gla_bwd(int64_t B, int64_t N, int64_t H, int64_t D, const double* q, const double* k, const double* v,
+                   const double* lg, const double* dout, double* dq, double* dk, double* dv, double* dlg,
+                   int nthreads) {
+    if (B < 0 || N < 0 || H < 1 || D < 1) return ORACLE_ERR_SHAPE;
+    int st = check_lg(B * N * H * D, lg);
+    if (st) return st;
+    gla_ctx_t c = {B, N, H, D, q, k, v, lg, dout, NULL, dq, dk, dv, dlg};
+    run_items(gla_bwd_item, &c, B * H, nthreads);
+    return ORACLE_OK;
+}

@@ -550,3 +550,91 @@ def test_layer_bf16_points_round_exactly_the_materialized_tensors(oracle_mod):
     assert np.array_equal(gb[4], oracle_mod.round_bf16(gb[4]))           # dO is bf16-valued
     assert rel(gb[4], ga[4]) <= 2 ** -8 and rel(gb[0], ga[0]) <= 5e-2   # the rounding of the fp64 chain (dX: cancellation)
     assert not np.array_equal(gb[4], ga[4])                              # ... but rounded
+
+
+# ---- NEXT-4: generalised decay (Table 3 GLA / GateLoop row, App. A.4) --------------------
+def _gla_inputs(seed, B, N, H, D, lo=0.0, hi=1.0):
+    rng = np.random.default_rng(seed)
+    q, k, v, do = (rng.standard_normal((B, N, H, D)) for _ in range(4))
+    lg = -rng.uniform(lo, hi, (B, N, H, D))
+    return q, k, v, lg, do
+
+
+def test_gla_constant_decay_is_the_scalar_lambda_path(oracle_mod):
+    """lg_t = log(lambda_h) for every token and channel is the TNL / RetNet row (Eq. 5): gla_fwd / gla_bwd
+    equal the scalar-lambda oracle, and the decay gradient summed over a head's tokens and channels is
+    dL/dlog(lambda), checked by finite differences of the (constant-decay) forward."""
+    B, N, H, D = 2, 37, 3, 5
+    q, k, v, _, do = _gla_inputs(1, B, N, H, D)
+    lam = np.array([0.9, 0.5, 1.0], np.float32)
+    lg = np.broadcast_to(np.log(lam.astype(np.float64))[None, None, :, None], (B, N, H, D)).copy()
+    o = oracle_mod.gla_fwd(q, k, v, lg)
+    assert rel(o, oracle_mod.fwd(q, k, v, lam)) <= 1e-13
+    dq, dk, dv, dlg = oracle_mod.gla_bwd(q, k, v, lg, do)
+    for a, b in zip((dq, dk, dv), oracle_mod.bwd(q, k, v, lam, do)):
+        assert rel(a, b) <= 1e-13
+    L = lambda x: np.sum(oracle_mod.gla_fwd(q, k, v, x) * do)
+    for h in range(H):
+        # one-sided second-order difference towards smaller log-decay (lambda = 1 has no room above)
+        eps = 1e-5
+        l1, l2 = lg.copy(), lg.copy()
+        l1[:, :, h] -= eps
+        l2[:, :, h] -= 2 * eps
+        fd = (3 * L(lg) - 4 * L(l1) + L(l2)) / (2 * eps)
+        assert abs(dlg[:, :, h].sum() - fd) <= 1e-6 * max(1.0, abs(fd)), (h, dlg[:, :, h].sum(), fd)
+
+
+def _gla_dense_torch(q, k, v, lg):
+    """Dense form of the GLA recurrence: o_t = sum_{i<=t} sum_d q_t[d] k_i[d] exp(sum_{s=i+1..t} lg_s[d]) v_i."""
+    c = torch.cumsum(lg, dim=1)                                        # [B][N][H][D]
+    N = q.shape[1]
+    dec = torch.exp(c[:, :, None] - c[:, None, :])                     # [B][t][i][H][D] = exp(c_t - c_i)
+    causal = torch.tril(torch.ones(N, N, dtype=q.dtype))[None, :, :, None, None]
+    A = torch.einsum("bthd,bihd,btihd->bhti", q, k, dec * causal)      # exp(c_t - c_i) only for i <= t
+    return torch.einsum("bhti,bihe->bthe", A, v)
+
+
+def test_gla_matches_dense_form_and_fp64_autograd(oracle_mod):
+    """Forward against the dense decay-product form; dQ, dK, dV and the decay gradient against torch fp64
+    autograd of that dense form (a different evaluation order and a different gradient derivation)."""
+    B, N, H, D = 2, 29, 2, 4
+    q, k, v, lg, do = _gla_inputs(2, B, N, H, D, 0.0, 2.0)
+    o = oracle_mod.gla_fwd(q, k, v, lg)
+    tq, tk, tv, tl = (torch.tensor(a, requires_grad=True) for a in (q, k, v, lg))
+    to = _gla_dense_torch(tq, tk, tv, tl)
+    assert rel(o, to.detach().numpy()) <= 1e-12
+    (to * torch.tensor(do)).sum().backward()
+    got = oracle_mod.gla_bwd(q, k, v, lg, do)
+    for a, t in zip(got, (tq, tk, tv, tl)):
+        assert rel(a, t.grad.numpy()) <= 1e-11
+
+
+def test_gla_decay_gradient_finite_differences(oracle_mod):
+    """d L / d lg at single (token, head, channel) entries by central differences of the forward."""
+    B, N, H, D = 1, 70, 1, 3      # spans two 64-token checkpoint chunks of the oracle's reverse sweep
+    q, k, v, lg, do = _gla_inputs(3, B, N, H, D)
+    dlg = oracle_mod.gla_bwd(q, k, v, lg, do)[3]
+    eps = 1e-6
+    for (t, d) in ((0, 0), (1, 2), (63, 1), (64, 0), (69, 2), (35, 1)):
+        lp, lm = lg.copy(), lg.copy()
+        lp[0, t, 0, d] += eps
+        lm[0, t, 0, d] -= eps
+        fd = (np.sum(oracle_mod.gla_fwd(q, k, v, lp) * do) - np.sum(oracle_mod.gla_fwd(q, k, v, lm) * do)) / (2 * eps)
+        assert abs(dlg[0, t, 0, d] - fd) <= 1e-6 * max(1.0, abs(fd)), (t, d, dlg[0, t, 0, d], fd)
+    assert np.all(dlg[0, 0] == 0.0)   # kv_{-1} = 0: the first token's decay multiplies nothing
+
+
+def test_gla_causality_and_no_decay_is_linear_attention(oracle_mod):
+    """lg = 0 (g = 1) is plain linear attention tril(Q K^T) V; changing tokens after t never changes o_t."""
+    B, N, H, D = 1, 20, 2, 3
+    q, k, v, lg, _ = _gla_inputs(4, B, N, H, D)
+    o0 = oracle_mod.gla_fwd(q, k, v, np.zeros_like(lg))
+    for h in range(H):
+        ref = np.tril(q[0, :, h] @ k[0, :, h].T) @ v[0, :, h]
+        assert rel(o0[0, :, h], ref) <= 1e-13
+    o = oracle_mod.gla_fwd(q, k, v, lg)
+    k2, lg2 = k.copy(), lg.copy()
+    k2[:, 12:] += 1.0
+    lg2[:, 12:] -= 0.5
+    o2 = oracle_mod.gla_fwd(q, k2, v, lg2)
+    assert np.array_equal(o[:, :12], o2[:, :12]) and not np.array_equal(o[:, 12:], o2[:, 12:])
