@@ -258,6 +258,40 @@ lasp_status_t lasp_layer_bwd(lasp_ctx_t ctx, const lasp_shape_t* shape, int64_t 
                              const void* dy, const void* cache, void* d_o, void* dq, void* dk, void* dv,
                              void* dx, float* dw_q, float* dw_k, float* dw_v, void* workspace, void* stream);
 
+/* ---- generalised decay: the GLA / GateLoop row of Table 3 ----
+ *
+ *   kv_t = Diag(g_t) kv_{t-1} + k_t v_t^T,   o_t = kv_t^T q_t,   g_t = exp(log_g_t) in (0, 1]^head_dim
+ *
+ * (App. A.4, the general form m_t = o_t m_{t-1} + e_t i_t^T with o_t = g_t 1^T, GLA / GateLoop
+ * P:735; readings D1-D3). The decay is data-dependent: one value per token, head and key channel;
+ * a per-channel constant decay is log_g_t = log(lambda) for every t, and lambda = exp(log_g) per head is the
+ * scalar path. The paper claims LASP covers this row without giving the chunk form; this path
+ * uses: segment state L_p (recurrence from zero), segment decay exp(sum log_g) per key row, the fold
+ * P_{p+1} = Diag(exp(ls_p)) P_p + L_p, and the same one-state-per-head ring messages as Alg. 2 / 3 (KV r -> r+1,
+ * dKV r+1 -> r; dKV = gradient of the later ranks' loss w.r.t. the state leaving the rank).
+ * Tensors: fp32 (shape->dtype = LASP_FP32), kv_heads = heads (or 0), head_dim 32, 64 or 128; q, k, v, log_g,
+ * o, d_o, dq, dk, dv, dlog_g are [batch][n_local][heads][head_dim]; states fp32 [batch][heads][head_dim]^2.
+ * log_g must be <= 0 (not checked on the device). dlog_g = dL/dlog_g, L = sum(O * dO).
+ * Cache / workspace: caller-owned, lasp_gla_cache_bytes / lasp_gla_workspace_bytes; the cache holds the state
+ * entering every segment and the state leaving the rank, plus a tag (a backward whose cache was not written by
+ * a matching lasp_gla_fwd* gets NaN outputs and lasp_workspace_status = LASP_ERR_STATE). Errors: LASP_ERR_SHAPE
+ * (NULL / misaligned pointers, bad sizes), LASP_ERR_UNSUPPORTED (dtype, head_dim, kv_heads), LASP_ERR_COMM. */
+size_t lasp_gla_cache_bytes(const lasp_shape_t* shape);
+size_t lasp_gla_workspace_bytes(const lasp_shape_t* shape);
+int64_t lasp_gla_segment_len(const lasp_shape_t* shape);
+lasp_status_t lasp_gla_fwd_local(const lasp_shape_t* shape, const float* q, const float* k, const float* v,
+                                 const float* log_g, const float* kv_in, float* o, float* kv_out, void* cache,
+                                 void* workspace, void* stream);
+lasp_status_t lasp_gla_bwd_local(const lasp_shape_t* shape, const float* q, const float* k, const float* v,
+                                 const float* log_g, const float* d_o, const void* cache, const float* dkv_in,
+                                 float* dq, float* dk, float* dv, float* dlog_g, float* dkv_out, void* workspace,
+                                 void* stream);
+lasp_status_t lasp_gla_fwd(lasp_ctx_t ctx, const lasp_shape_t* shape, const float* q, const float* k,
+                           const float* v, const float* log_g, float* o, void* cache, void* workspace, void* stream);
+lasp_status_t lasp_gla_bwd(lasp_ctx_t ctx, const lasp_shape_t* shape, const float* q, const float* k,
+                           const float* v, const float* log_g, const float* d_o, const void* cache, float* dq,
+                           float* dk, float* dv, float* dlog_g, void* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,13 @@ _SIGS = {
     "lasp_layer_bwd": ([_vp, _sp, ctypes.c_int64] + [_vp] * 4 + [_fp] + [_vp] * 5 + [_vp] * 2 + [_vp] * 4 +
                        [_vp] * 4 + [_vp, _vp], ctypes.c_int),
     "lasp_bwd": ([_vp, _sp, _vp, _vp, _vp, _fp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "lasp_gla_cache_bytes": ([_sp], ctypes.c_size_t),
+    "lasp_gla_workspace_bytes": ([_sp], ctypes.c_size_t),
+    "lasp_gla_segment_len": ([_sp], ctypes.c_int64),
+    "lasp_gla_fwd_local": ([_sp] + [_vp] * 10, ctypes.c_int),
+    "lasp_gla_bwd_local": ([_sp] + [_vp] * 14, ctypes.c_int),
+    "lasp_gla_fwd": ([_vp, _sp] + [_vp] * 8, ctypes.c_int),
+    "lasp_gla_bwd": ([_vp, _sp] + [_vp] * 12, ctypes.c_int),
 }
 
 _lib = None

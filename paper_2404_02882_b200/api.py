@@ -7,6 +7,8 @@ PyTorch is used for device memory, streams and process groups. Tensors use the b
   may have fewer heads than q (grouped-query / multi-query attention; lambda then has one entry per kv-head).
 * ``Ring``                        -- Alg. 2 / Alg. 3 across a torch.distributed world (NCCL P2P).
 * ``LaspAttention``               -- torch.autograd.Function over ``Ring`` or the local path.
+* ``gla_fwd_local`` / ``gla_bwd_local`` / ``Ring.gla_fwd`` / ``Ring.gla_bwd`` -- generalised decay (SURVEY §8(f)
+  NEXT-4, the GLA / GateLoop row of Table 3): per-token, per-key-channel decay exp(log_g), fp32.
 * ``topology`` / ``sp_group`` / ``scatter_sequence`` -- data-sequence hybrid parallelism (Alg. 1): G = W/T
   sequence-parallel groups, one ring per group.
 """
@@ -300,6 +302,106 @@ class Ring:
         if check_state:
             workspace_status(workspace)
         return dq, dk, dv
+
+
+# ---- NEXT-4: generalised decay (include/lasp.h lasp_gla_*) ------------------------------------------------------
+def _gla_check(q, *ts):
+    if q.dim() != 4 or q.dtype != torch.float32 or not q.is_cuda or not q.is_contiguous():
+        raise ValueError("generalised decay: q must be a contiguous float32 CUDA tensor [B][C][H][D]")
+    _check_seq(q, *ts)
+
+
+def gla_cache_bytes(q) -> int:
+    return int(N.lib().lasp_gla_cache_bytes(ctypes.byref(_shape(q))))
+
+
+def gla_workspace_bytes(q) -> int:
+    return int(N.lib().lasp_gla_workspace_bytes(ctypes.byref(_shape(q))))
+
+
+def gla_alloc(q):
+    """(cache, workspace) for the generalised-decay path at q's shape."""
+    return (torch.empty(max(gla_cache_bytes(q), 16), dtype=torch.uint8, device=q.device),
+            torch.empty(max(gla_workspace_bytes(q), 16), dtype=torch.uint8, device=q.device))
+
+
+def gla_fwd_local(q, k, v, log_g, kv_in=None, *, o=None, kv_out=True, cache=None, workspace=None):
+    """kv_t = Diag(exp(log_g_t)) kv_{t-1} + k_t v_t^T, o_t = kv_t^T q_t for one rank -> (o, kv_out or None, cache).
+    All tensors float32 [B][C][H][D]; log_g <= 0."""
+    _gla_check(q, k, v, log_g)
+    s = _shape(q)
+    o = torch.empty_like(q) if o is None else o
+    kv_out_t = _state_like(k) if kv_out is True else (kv_out if isinstance(kv_out, torch.Tensor) else None)
+    if cache is None or workspace is None:
+        c2, w2 = gla_alloc(q)
+        cache = c2 if cache is None else cache
+        workspace = w2 if workspace is None else workspace
+    _check_like(o, q, "o")
+    _check_state(kv_in, k, "kv_in")
+    _check_state(kv_out_t, k, "kv_out")
+    _check_buf(cache, gla_cache_bytes(q), "cache", q.device)
+    _check_buf(workspace, gla_workspace_bytes(q), "workspace", q.device)
+    N.check(N.lib().lasp_gla_fwd_local(ctypes.byref(s), _p(q), _p(k), _p(v), _p(log_g), _p(kv_in), _p(o),
+                                       _p(kv_out_t), _p(cache), _p(workspace), _stream(q.device)))
+    return o, kv_out_t, cache
+
+
+def gla_bwd_local(q, k, v, log_g, do, cache, dkv_in=None, *, dq=None, dk=None, dv=None, dlog_g=None, dkv_out=True,
+                  workspace=None, check_state=False):
+    """Gradients of sum(O * dO) for gla_fwd_local -> (dq, dk, dv, dlog_g, dkv_out or None)."""
+    _gla_check(q, k, v, log_g, do)
+    s = _shape(q)
+    dq, dk, dv, dlog_g = (torch.empty_like(q) if t is None else t for t in (dq, dk, dv, dlog_g))
+    dkv_out_t = _state_like(k) if dkv_out is True else (dkv_out if isinstance(dkv_out, torch.Tensor) else None)
+    workspace = gla_alloc(q)[1] if workspace is None else workspace
+    for t, n in ((dq, "dq"), (dk, "dk"), (dv, "dv"), (dlog_g, "dlog_g")):
+        _check_like(t, q, n)
+    _check_state(dkv_in, k, "dkv_in")
+    _check_state(dkv_out_t, k, "dkv_out")
+    _check_buf(cache, gla_cache_bytes(q), "cache", q.device)
+    _check_buf(workspace, gla_workspace_bytes(q), "workspace", q.device)
+    N.check(N.lib().lasp_gla_bwd_local(ctypes.byref(s), _p(q), _p(k), _p(v), _p(log_g), _p(do), _p(cache),
+                                       _p(dkv_in), _p(dq), _p(dk), _p(dv), _p(dlog_g), _p(dkv_out_t), _p(workspace),
+                                       _stream(q.device)))
+    if check_state:
+        workspace_status(workspace)
+    return dq, dk, dv, dlog_g, dkv_out_t
+
+
+def _ring_gla_fwd(self, q, k, v, log_g, *, o=None, cache=None, workspace=None):
+    """Generalised-decay Alg. 2 across the ring (KV r -> r+1) -> (o, cache)."""
+    _gla_check(q, k, v, log_g)
+    s = _shape(q)
+    o = torch.empty_like(q) if o is None else o
+    if cache is None or workspace is None:
+        c2, w2 = gla_alloc(q)
+        cache = c2 if cache is None else cache
+        workspace = w2 if workspace is None else workspace
+    _check_like(o, q, "o")
+    _check_buf(cache, gla_cache_bytes(q), "cache", q.device)
+    _check_buf(workspace, gla_workspace_bytes(q), "workspace", q.device)
+    N.check(N.lib().lasp_gla_fwd(self._ctx, ctypes.byref(s), _p(q), _p(k), _p(v), _p(log_g), _p(o), _p(cache),
+                                 _p(workspace), _stream(q.device)))
+    return o, cache
+
+
+def _ring_gla_bwd(self, q, k, v, log_g, do, cache, *, workspace=None, check_state=False):
+    """Generalised-decay Alg. 3 across the ring (dKV r+1 -> r) -> (dq, dk, dv, dlog_g)."""
+    _gla_check(q, k, v, log_g, do)
+    s = _shape(q)
+    dq, dk, dv, dlg = (torch.empty_like(q) for _ in range(4))
+    workspace = gla_alloc(q)[1] if workspace is None else workspace
+    _check_buf(cache, gla_cache_bytes(q), "cache", q.device)
+    _check_buf(workspace, gla_workspace_bytes(q), "workspace", q.device)
+    N.check(N.lib().lasp_gla_bwd(self._ctx, ctypes.byref(s), _p(q), _p(k), _p(v), _p(log_g), _p(do), _p(cache),
+                                 _p(dq), _p(dk), _p(dv), _p(dlg), _p(workspace), _stream(q.device)))
+    if check_state:
+        workspace_status(workspace)
+    return dq, dk, dv, dlg
+
+
+Ring.gla_fwd = _ring_gla_fwd
+Ring.gla_bwd = _ring_gla_bwd
 
 
 class LaspAttention(torch.autograd.Function):

@@ -9,8 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblasp.so")
-SOURCES = ["lasp_api.cu", "kernels_simt.cu", "kernels_tc.cu"]
-HEADERS = ["lasp_common.cuh", "sm100.cuh"]
+SOURCES = ["lasp_api.cu", "kernels_simt.cu", "kernels_tc.cu", "kernels_gla.cu"]
+HEADERS = ["lasp_common.cuh", "sm100.cuh", "gla.cuh"]
 
 
 def _nccl_include() -> str:

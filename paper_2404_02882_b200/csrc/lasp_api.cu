@@ -8,6 +8,7 @@
 // The KV-independent local parts (F1/B1) are hoisted in front of the ring hop, so the hop carries
 // lambda^C * received + local (Alg. 2, Alg. 3), and dQ overlaps the dKV ring.
 #include "../../include/lasp.h"
+#include "gla.cuh"
 #include "lasp_common.cuh"
 
 #include <cublas_v2.h>
@@ -749,6 +750,170 @@ lasp_status_t bwd_body(lasp_ctx* c, const Plan& p, const void* q, const void* k,
 
 }  // namespace
 
+// ---- NEXT-4: generalised decay (kernels_gla.cu) --------------------------------------------------------
+namespace {
+
+constexpr uint64_t kGlaTagMagic = 0x4c415350474c4121ull;  // "LASPGLA!": a GLA cache, never a scalar-path one
+
+lasp_status_t gla_plan(const lasp_shape_t* s, GlaPlan& g) {
+  if (!s) return fail(LASP_ERR_SHAPE, "shape is NULL");
+  if (s->batch < 1 || s->n_local < 0 || s->heads < 1 || s->kv_heads < 0)
+    return fail(LASP_ERR_SHAPE, "need batch >= 1, n_local >= 0, heads >= 1, kv_heads >= 0");
+  if (s->dtype != LASP_FP32) return fail(LASP_ERR_UNSUPPORTED, "generalised decay: fp32 tensors only");
+  if (s->head_dim != 32 && s->head_dim != 64 && s->head_dim != 128)
+    return fail(LASP_ERR_UNSUPPORTED, "head_dim must be 32, 64 or 128");
+  if (s->kv_heads != 0 && s->kv_heads != s->heads)
+    return fail(LASP_ERR_UNSUPPORTED, "generalised decay: kv_heads must equal heads");
+  g.B = s->batch; g.C = s->n_local; g.H = s->heads; g.D = s->head_dim;
+  // ~8 items (CTAs) per SM, segments a multiple of the 16-token tile
+  const int64_t forced = env_i64("LASP_GLA_SEG_LEN", 0);
+  int64_t L;
+  if (forced > 0) {
+    L = (forced + 15) / 16 * 16;
+  } else {
+    const int64_t target = 8 * 148;
+    int64_t nseg = (target + g.B * g.H - 1) / (g.B * g.H);
+    if (nseg < 1) nseg = 1;
+    L = g.C > 0 ? ((g.C + nseg - 1) / nseg + 15) / 16 * 16 : 16;
+    if (L < 64) L = 64;
+  }
+  g.seg_len = L;
+  g.nseg = g.C > 0 ? (g.C + L - 1) / L : 1;
+  if (g.B * g.H * g.nseg >= (int64_t(1) << 31)) return fail(LASP_ERR_UNSUPPORTED, "too many segments");
+  return LASP_OK;
+}
+
+size_t gla_state_elems(const GlaPlan& g) { return size_t(g.B * g.H * g.D * g.D); }
+size_t gla_cache_bytes(const GlaPlan& g) {
+  return align256(size_t(g.B * g.H * (g.nseg + 1) * g.D * g.D) * 4) + kCacheTagBytes;
+}
+struct GlaWs {
+  unsigned* ctrl;  // 16 words (entry kernel zeroes; [2] = cache-tag status)
+  float* seg;      // [B][H][nseg][D][D]
+  float* ls;       // [B][H][nseg][D]
+  float* local;    // [B][H][D][D]
+  float* in;
+  float* out;
+  float* lsum;     // [B][H][D]
+};
+GlaWs gla_carve(const GlaPlan& g, void* ws) {
+  char* c = static_cast<char*>(ws);
+  GlaWs w;
+  w.ctrl = reinterpret_cast<unsigned*>(c); c += 256;
+  w.seg = reinterpret_cast<float*>(c); c += align256(size_t(g.B * g.H * g.nseg * g.D * g.D) * 4);
+  w.ls = reinterpret_cast<float*>(c); c += align256(size_t(g.B * g.H * g.nseg * g.D) * 4);
+  w.local = reinterpret_cast<float*>(c); c += align256(gla_state_elems(g) * 4);
+  w.in = reinterpret_cast<float*>(c); c += align256(gla_state_elems(g) * 4);
+  w.out = reinterpret_cast<float*>(c); c += align256(gla_state_elems(g) * 4);
+  w.lsum = reinterpret_cast<float*>(c);
+  return w;
+}
+size_t gla_ws_bytes(const GlaPlan& g) {
+  return 256 + align256(size_t(g.B * g.H * g.nseg * g.D * g.D) * 4) + align256(size_t(g.B * g.H * g.nseg * g.D) * 4) +
+         3 * align256(gla_state_elems(g) * 4) + align256(size_t(g.B * g.H * g.D) * 4);
+}
+
+cudaError_t gla_entry(const GlaPlan& g, const void* cache, const GlaWs& w, int rank, int world, bool check,
+                      cudaStream_t st) {
+  CacheTag t{};
+  t.w[kTagMagic] = kGlaTagMagic;
+  t.w[kTagB] = uint64_t(g.B); t.w[kTagC] = uint64_t(g.C); t.w[kTagH] = uint64_t(g.H); t.w[kTagD] = uint64_t(g.D);
+  t.w[kTagSeg] = uint64_t(g.seg_len);
+  t.w[kTagDtype] = 1;
+  t.w[kTagRank] = uint64_t(int64_t(rank));
+  t.w[kTagWorld] = uint64_t(int64_t(world));
+  t.w[kTagHk] = uint64_t(g.H);
+  t.w[kTagGen] = ++g_generation;
+  unsigned mask = 0;
+  if (check) {
+    for (int i = kTagMagic; i <= kTagDtype; ++i) mask |= 1u << i;
+    if (rank >= 0) mask |= (1u << kTagRank) | (1u << kTagWorld);
+  }
+  uint64_t* hdr = reinterpret_cast<uint64_t*>(static_cast<char*>(const_cast<void*>(cache)) +
+                                              align256(size_t(g.B * g.H * (g.nseg + 1) * g.D * g.D) * 4));
+  return staged(check ? "gla_tag_check" : "gla_tag_write", st,
+                [&] { return launch_tag(t, hdr, mask, w.ctrl, st); });
+}
+
+lasp_status_t gla_check(const GlaPlan& g, std::initializer_list<const void*> seq, const void* cache, const void* ws) {
+  if (g.C > 0)
+    for (const void* x : seq)
+      if (!x || !aligned16(x)) return fail(LASP_ERR_SHAPE, "sequence tensor NULL or not 16-byte aligned");
+  if (!cache || !aligned16(cache)) return fail(LASP_ERR_SHAPE, "cache NULL or not 16-byte aligned");
+  if (!ws || !aligned16(ws)) return fail(LASP_ERR_SHAPE, "workspace NULL or not 16-byte aligned");
+  return check_device();
+}
+
+// Alg. 2 / Alg. 3 with the generalised decay, one rank (c == nullptr: the local path with kv_in / kv_out).
+// Ring: receive the neighbour's state, fold this rank's segments with it (the fold's final value is the
+// message for the next rank: KV_out = Diag(prod_t g_t) KV_in + L_rank; dKV_out = G'_rank + Diag(...) dKV_in),
+// send, then the per-token passes.
+lasp_status_t gla_hop_in(lasp_ctx* c, const GlaPlan& g, float* in, bool backward, cudaStream_t st) {
+  int from = -1, to = -1;
+  lasp_ring_peers(c->rank, c->world, backward ? 1 : 0, &from, &to);
+  const size_t n = gla_state_elems(g);
+  if (from >= 0) return ring_recv(c, in, n, from, st, backward ? "ncclRecv(dKV, gla)" : "ncclRecv(KV, gla)");
+  LASP_CUDA(cudaMemsetAsync(in, 0, n * sizeof(float), st));
+  return LASP_OK;
+}
+lasp_status_t gla_hop_out(lasp_ctx* c, const GlaPlan& g, const float* out, bool backward, cudaStream_t st) {
+  int from = -1, to = -1;
+  lasp_ring_peers(c->rank, c->world, backward ? 1 : 0, &from, &to);
+  if (to < 0) return LASP_OK;
+  return ring_send(c, out, gla_state_elems(g), to, st, backward ? "ncclSend(dKV, gla)" : "ncclSend(KV, gla)");
+}
+
+lasp_status_t gla_fwd_body(lasp_ctx* c, const GlaPlan& g, const float* q, const float* k, const float* v,
+                           const float* lg, const float* kv_in, float* o, float* kv_out, void* cache, void* ws,
+                           cudaStream_t st) {
+  GlaWs w = gla_carve(g, ws);
+  float* P = static_cast<float*>(cache);
+  lasp_status_t s;
+  LASP_CUDA(gla_entry(g, cache, w, c ? c->rank : -1, c ? c->world : -1, false, st));
+  if (g.C > 0) LASP_CUDA(staged("gla_state_fwd", st, [&] { return gla_launch_state(g, 0, k, v, lg, w.seg, w.ls, st); }));
+  const float* init = kv_in;
+  float* fin = kv_out;
+  ProfSpan hop("exchange_fwd", st);
+  if (c != nullptr) {
+    if ((s = gla_hop_in(c, g, w.in, false, st)) != LASP_OK) return s;
+    init = w.in;
+    fin = w.out;
+  }
+  LASP_CUDA(staged("gla_fold_fwd", st, [&] { return gla_launch_fold(g, 0, init, w.seg, w.ls, P, fin, nullptr, st); }));
+  if (c != nullptr && (s = gla_hop_out(c, g, w.out, false, st)) != LASP_OK) return s;
+  hop.stop(st);
+  if (g.C > 0) LASP_CUDA(staged("gla_out", st, [&] { return gla_launch_out(g, q, k, v, lg, P, o, st); }));
+  return LASP_OK;
+}
+
+lasp_status_t gla_bwd_body(lasp_ctx* c, const GlaPlan& g, const float* q, const float* k, const float* v,
+                           const float* lg, const float* d_o, const void* cache, const float* dkv_in, float* dq,
+                           float* dk, float* dv, float* dlg, float* dkv_out, void* ws, cudaStream_t st) {
+  GlaWs w = gla_carve(g, ws);
+  const float* P = static_cast<const float*>(cache);
+  lasp_status_t s;
+  LASP_CUDA(gla_entry(g, cache, w, c ? c->rank : -1, c ? c->world : -1, true, st));
+  if (g.C > 0) LASP_CUDA(staged("gla_state_rev", st, [&] { return gla_launch_state(g, 1, q, d_o, lg, w.seg, w.ls, st); }));
+  const float* init = dkv_in;
+  float* fin = dkv_out;
+  ProfSpan hop("exchange_bwd", st);
+  if (c != nullptr) {
+    if ((s = gla_hop_in(c, g, w.in, true, st)) != LASP_OK) return s;
+    init = w.in;
+    fin = w.out;
+  }
+  LASP_CUDA(staged("gla_fold_rev", st, [&] { return gla_launch_fold(g, 1, init, w.seg, w.ls, nullptr, fin, nullptr, st); }));
+  if (c != nullptr && (s = gla_hop_out(c, g, w.out, true, st)) != LASP_OK) return s;
+  hop.stop(st);
+  if (g.C > 0)
+    LASP_CUDA(staged("gla_bwd", st, [&] {
+      return gla_launch_bwd(g, q, k, v, lg, d_o, P, w.seg, dq, dk, dv, dlg, w.ctrl + 2, st);
+    }));
+  return LASP_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* lasp_last_error(void) { return g_err.c_str(); }
@@ -1045,6 +1210,66 @@ lasp_status_t lasp_layer_bwd(lasp_ctx_t c, const lasp_shape_t* shape, int64_t d_
     if ((s = gemm_rm(h, d_model, NK, M, x, true, dv, false, dw_v, true, 0.f)) != LASP_OK) return s;
   }
   return LASP_OK;
+}
+
+// ---- NEXT-4: generalised decay (the GLA / GateLoop row of Table 3) ---------------------------------------
+size_t lasp_gla_cache_bytes(const lasp_shape_t* shape) {
+  GlaPlan g;
+  return gla_plan(shape, g) == LASP_OK ? gla_cache_bytes(g) : 0;
+}
+
+size_t lasp_gla_workspace_bytes(const lasp_shape_t* shape) {
+  GlaPlan g;
+  return gla_plan(shape, g) == LASP_OK ? gla_ws_bytes(g) : 0;
+}
+
+int64_t lasp_gla_segment_len(const lasp_shape_t* shape) {
+  GlaPlan g;
+  return gla_plan(shape, g) == LASP_OK ? g.seg_len : 0;
+}
+
+lasp_status_t lasp_gla_fwd_local(const lasp_shape_t* shape, const float* q, const float* k, const float* v,
+                                 const float* log_g, const float* kv_in, float* o, float* kv_out, void* cache,
+                                 void* workspace, void* stream) {
+  GlaPlan g;
+  lasp_status_t s = gla_plan(shape, g);
+  if (s != LASP_OK) return s;
+  if ((s = gla_check(g, {q, k, v, log_g, o}, cache, workspace)) != LASP_OK) return s;
+  return gla_fwd_body(nullptr, g, q, k, v, log_g, kv_in, o, kv_out, cache, workspace, static_cast<cudaStream_t>(stream));
+}
+
+lasp_status_t lasp_gla_bwd_local(const lasp_shape_t* shape, const float* q, const float* k, const float* v,
+                                 const float* log_g, const float* d_o, const void* cache, const float* dkv_in,
+                                 float* dq, float* dk, float* dv, float* dlog_g, float* dkv_out, void* workspace,
+                                 void* stream) {
+  GlaPlan g;
+  lasp_status_t s = gla_plan(shape, g);
+  if (s != LASP_OK) return s;
+  if ((s = gla_check(g, {q, k, v, log_g, d_o, dq, dk, dv, dlog_g}, cache, workspace)) != LASP_OK) return s;
+  return gla_bwd_body(nullptr, g, q, k, v, log_g, d_o, cache, dkv_in, dq, dk, dv, dlog_g, dkv_out, workspace,
+                      static_cast<cudaStream_t>(stream));
+}
+
+lasp_status_t lasp_gla_fwd(lasp_ctx_t c, const lasp_shape_t* shape, const float* q, const float* k, const float* v,
+                           const float* log_g, float* o, void* cache, void* workspace, void* stream) {
+  if (!c) return fail(LASP_ERR_SHAPE, "ctx is NULL");
+  GlaPlan g;
+  lasp_status_t s = gla_plan(shape, g);
+  if (s != LASP_OK) return s;
+  if ((s = gla_check(g, {q, k, v, log_g, o}, cache, workspace)) != LASP_OK) return s;
+  return gla_fwd_body(c, g, q, k, v, log_g, nullptr, o, nullptr, cache, workspace, static_cast<cudaStream_t>(stream));
+}
+
+lasp_status_t lasp_gla_bwd(lasp_ctx_t c, const lasp_shape_t* shape, const float* q, const float* k, const float* v,
+                           const float* log_g, const float* d_o, const void* cache, float* dq, float* dk, float* dv,
+                           float* dlog_g, void* workspace, void* stream) {
+  if (!c) return fail(LASP_ERR_SHAPE, "ctx is NULL");
+  GlaPlan g;
+  lasp_status_t s = gla_plan(shape, g);
+  if (s != LASP_OK) return s;
+  if ((s = gla_check(g, {q, k, v, log_g, d_o, dq, dk, dv, dlog_g}, cache, workspace)) != LASP_OK) return s;
+  return gla_bwd_body(c, g, q, k, v, log_g, d_o, cache, nullptr, dq, dk, dv, dlog_g, nullptr, workspace,
+                      static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

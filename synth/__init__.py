@@ -26,11 +26,11 @@ import numpy as np
 
 __all__ = [
     "TENSOR_IDS", "splitmix64", "uniform", "draw", "round_bf16", "bf16_bits",
-    "bits_to_f32", "head_lambdas", "problem",
+    "bits_to_f32", "head_lambdas", "problem", "head_decay_rates", "gla_problem",
 ]
 
 # Fixed tensor ids (part of the recipe: changing them changes every fixture).
-TENSOR_IDS = {"q": 1, "k": 2, "v": 3, "do": 4, "x": 5, "wq": 6, "wk": 7, "wv": 8, "dy": 9}
+TENSOR_IDS = {"q": 1, "k": 2, "v": 3, "do": 4, "x": 5, "wq": 6, "wk": 7, "wv": 8, "dy": 9, "lg": 10}
 
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
 
@@ -160,4 +160,31 @@ def layer_problem(seed: int, batch: int, n_global: int, heads: int, kv_heads: in
          "w_v": _draw2("wv", seed, d_model, kv_heads * head_dim, d_model ** -0.5, "bf16"),
          "dy": draw("dy", seed, batch, n_global, heads, head_dim, "bf16", token_lo, token_hi),
          "lam": head_lambdas(kv_heads, lam)}
+    return t
+
+
+def head_decay_rates(heads: int) -> np.ndarray:
+    """Mean per-token log-decay magnitude a_h of head h for the generalised-decay inputs: 2^-(1 + 9 h/(H-1))
+    (0.5 .. ~0.001: from a few tokens of memory to ~1000; GLA-style gates sigmoid(x)^(1/16) sit near 0.05)."""
+    if heads == 1:
+        return np.array([0.05])
+    return 2.0 ** -(1.0 + 9.0 * np.arange(heads, dtype=np.float64) / (heads - 1))
+
+
+def gla_problem(seed: int, batch: int, n_global: int, heads: int, head_dim: int, token_lo: int = 0,
+                token_hi: int | None = None) -> dict:
+    """Inputs of the generalised-decay path (NEXT-4), all float32 [B][tokens][H][D]: q, k, v, do as ``draw``
+    (fp32), and the log decay lg = -2 a_h u (u uniform in [0, 1), per token, head and key channel; mean -a_h)."""
+    token_hi = n_global if token_hi is None else token_hi
+    t = {nm: draw(nm, seed, batch, n_global, heads, head_dim, "fp32", token_lo, token_hi)
+         for nm in ("q", "k", "v", "do")}
+    n = token_hi - token_lo
+    inner = heads * head_dim
+    lg = np.empty((batch, n, heads, head_dim), dtype=np.float32)
+    rate = head_decay_rates(heads)[None, :, None]
+    for b in range(batch):
+        base = (b * n_global + token_lo) * inner
+        u = uniform(seed, TENSOR_IDS["lg"], np.arange(base, base + n * inner, dtype=np.uint64))
+        lg[b] = (-2.0 * rate * u.reshape(n, heads, head_dim)).astype(np.float32)
+    t["lg"] = lg
     return t

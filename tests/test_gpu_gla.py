@@ -1,0 +1,175 @@
+"""GPU parity of the generalised-decay path (the GLA / GateLoop row of Table 3, App. A.4
+P:671-713) through lasp_gla_* against the fp64 oracle (oracle.gla_fwd / gla_bwd) on synth.gla_problem.
+
+Tolerance (reading D3): fp32 in / fp32 out, fp32 arithmetic in a different order than the oracle;
+normwise per tensor and head (max|x - ref| / max|ref|) 1e-5 for O, dQ, dK, dV (north_star's fp32 bar), 1e-4 for
+the decay gradient, which the kernels form as a suffix sum over the sequence of q . dq - k . dk (terms that
+cancel: the sum over the whole sequence is exactly 0)."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+TOL, TOL_DLG = 1e-5, 1e-4
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2404_02882_b200 as lasp
+    return lasp
+
+
+def per_head_err(x, ref):
+    x, ref = np.asarray(x, np.float64), np.asarray(ref, np.float64)
+    worst = 0.0
+    for h in range(ref.shape[2]):
+        den = np.max(np.abs(ref[:, :, h]))
+        num = np.max(np.abs(x[:, :, h] - ref[:, :, h]))
+        worst = max(worst, num / den if den > 0 else num)
+    return worst
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run_chain(L, t, T):
+    """T ranks simulated by chaining kv_out -> kv_in (forward) and dkv_out -> dkv_in (backward)."""
+    N = t["q"].shape[1]
+    C = N // T
+    d = {k: dev(v) for k, v in t.items()}
+    sl = [slice(r * C, (r + 1) * C if r < T - 1 else N) for r in range(T)]
+    outs, caches, kv = [], [], None
+    for r in range(T):
+        q, k, v, lg = (d[x][:, sl[r]].contiguous() for x in ("q", "k", "v", "lg"))
+        o, kv, cache = L.gla_fwd_local(q, k, v, lg, kv_in=kv)
+        outs.append(o)
+        caches.append(cache)
+    grads, dkv = [None] * T, None
+    for r in reversed(range(T)):
+        q, k, v, lg, do = (d[x][:, sl[r]].contiguous() for x in ("q", "k", "v", "lg", "do"))
+        dq, dk, dv, dlg, dkv = L.gla_bwd_local(q, k, v, lg, do, caches[r], dkv_in=dkv)
+        grads[r] = (dq, dk, dv, dlg)
+    torch.cuda.synchronize()
+    cat = lambda ts: torch.cat(ts, 1).cpu().numpy()
+    return [cat(outs)] + [cat([g[i] for g in grads]) for i in range(4)]
+
+
+def check(oracle_mod, t, got):
+    ref = [oracle_mod.gla_fwd(t["q"], t["k"], t["v"], t["lg"])]
+    ref += list(oracle_mod.gla_bwd(t["q"], t["k"], t["v"], t["lg"], t["do"]))
+    errs = {n: per_head_err(g, r) for n, g, r in zip(("o", "dq", "dk", "dv", "dlg"), got, ref)}
+    assert max(errs[n] for n in ("o", "dq", "dk", "dv")) <= TOL, errs
+    assert errs["dlg"] <= TOL_DLG, errs
+    return errs
+
+
+@pytest.mark.parametrize("B,N,H,D,T,seg", [(1, 1000, 2, 64, 1, 0),      # default plan, ragged last segment
+                                           (2, 777, 3, 32, 1, 64),      # batch 2, head_dim 32, 13 segments
+                                           (1, 600, 2, 128, 1, 96),     # head_dim 128 (two threads per column)
+                                           (1, 1200, 2, 64, 3, 80),     # 3 chained ranks, ragged segments
+                                           (1, 5, 1, 64, 1, 0),         # fewer tokens than one tile
+                                           (1, 2048, 4, 64, 2, 0)])
+def test_gla_matches_oracle(L, oracle_mod, monkeypatch, B, N, H, D, T, seg):
+    if seg:
+        monkeypatch.setenv("LASP_GLA_SEG_LEN", str(seg))
+    t = synth.gla_problem(B + N + D, B, N, H, D)
+    check(oracle_mod, t, run_chain(L, t, T))
+
+
+def test_gla_constant_decay_is_the_scalar_path(L, oracle_mod):
+    """log_g = log(lambda_h) everywhere reproduces the scalar-lambda recurrence (Eq. 5 / Eq. 13-14)."""
+    B, N, H, D = 1, 900, 3, 64
+    t = synth.gla_problem(5, B, N, H, D)
+    lam = np.array([0.5, 0.9, 1.0], np.float32)
+    t["lg"] = np.broadcast_to(np.log(lam)[None, None, :, None], t["q"].shape).astype(np.float32).copy()
+    got = run_chain(L, t, 1)
+    lam64 = np.exp(t["lg"][0, 0, :, 0].astype(np.float64)).astype(np.float32)
+    assert per_head_err(got[0], oracle_mod.fwd(t["q"], t["k"], t["v"], lam64)) <= 5 * TOL
+    for g, r in zip(got[1:4], oracle_mod.bwd(t["q"], t["k"], t["v"], lam64, t["do"])):
+        assert per_head_err(g, r) <= 5 * TOL
+
+
+def test_gla_loopback_ring(L, oracle_mod):
+    """lasp_gla_fwd / lasp_gla_bwd across a 3-rank ring (in-process loopback transport, threads on one GPU)."""
+    import threading
+    B, N, H, D, T = 1, 1536, 2, 64, 3
+    t = synth.gla_problem(11, B, N, H, D)
+    C = N // T
+    res, errs = [None] * T, []
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                ring = L.Ring.loopback(r, T, "gla-test")
+                sl = slice(r * C, (r + 1) * C)
+                q, k, v, lg, do = (dev(t[x][:, sl]) for x in ("q", "k", "v", "lg", "do"))
+                o, cache = ring.gla_fwd(q, k, v, lg)
+                g = ring.gla_bwd(q, k, v, lg, do, cache)
+                s.synchronize()
+                res[r] = [o.cpu().numpy()] + [x.cpu().numpy() for x in g]
+                ring.close()
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+    ths = [threading.Thread(target=rank, args=(r,)) for r in range(T)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert not errs, errs
+    got = [np.concatenate([res[r][i] for r in range(T)], 1) for i in range(5)]
+    check(oracle_mod, t, got)
+
+
+def test_gla_full_size_closed_form(L):
+    """At the TNL-0.4B bench shape (16 x 64, 32K tokens) with per-token, per-channel decay and constant q, k, v per
+    head: o_s[e] = v[e] sum_d q[d] k[d] w_s[d], w_s = g_s w_{s-1} + 1 (a per-channel scalar recurrence), and
+    dq_s[d] = (v . do) k[d] w_s[d] for constant do; checked at sampled positions of every head. Tolerance 1e-4: the
+    fp32 recurrence's rounding grows with the memory length 1 / (1 - g) (up to ~1000 tokens for the slowest head
+    here, n u ~ 6e-5; reading D3)."""
+    B, N, H, D = 1, 32768, 16, 64
+    t = synth.gla_problem(3, B, N, H, D)
+    rng = np.random.default_rng(0)
+    qv, kv_, vv, dov = (rng.standard_normal((H, D)).astype(np.float32) * 0.3 for _ in range(4))
+    full = lambda a: dev(np.broadcast_to(a, (B, N, H, D)).copy())
+    q, k, v, do, lg = full(qv), full(kv_), full(vv), full(dov), dev(t["lg"])
+    o, _, cache = L.gla_fwd_local(q, k, v, lg)
+    dq, dk, dv, dlg, _ = L.gla_bwd_local(q, k, v, lg, do, cache)
+    torch.cuda.synchronize()
+    g = np.exp(t["lg"][0].astype(np.float64))  # [N][H][D]
+    w = np.empty((N, H, D))
+    acc = np.zeros((H, D))
+    for s in range(N):
+        acc = g[s] * acc + 1.0
+        w[s] = acc
+    idx = np.array([0, 1, 127, 128, 5000, 16383, 16384, 32766, 32767])
+    o_ref = np.einsum("hd,shd,he->she", qv.astype(np.float64) * kv_, w[idx], vv.astype(np.float64))
+    dq_ref = np.einsum("h,hd,shd->shd", np.einsum("he,he->h", vv.astype(np.float64), dov), kv_.astype(np.float64),
+                       w[idx])
+    o_got, dq_got = o[0, idx].cpu().numpy(), dq[0, idx].cpu().numpy()
+    for h in range(H):
+        assert np.max(np.abs(o_got[:, h] - o_ref[:, h])) <= 1e-4 * np.max(np.abs(o_ref[:, h])), h
+        assert np.max(np.abs(dq_got[:, h] - dq_ref[:, h])) <= 1e-4 * np.max(np.abs(dq_ref[:, h])), h
+
+
+def test_gla_backward_without_forward_is_state_error(L):
+    B, N, H, D = 1, 256, 2, 64
+    t = synth.gla_problem(1, B, N, H, D)
+    q, k, v, lg, do = (dev(t[x]) for x in ("q", "k", "v", "lg", "do"))
+    cache, ws = L.gla_alloc(q)
+    cache.zero_()
+    with pytest.raises(L._native.LaspError) as e:
+        L.gla_bwd_local(q, k, v, lg, do, cache, workspace=ws, check_state=True)
+    assert e.value.name == "LASP_ERR_STATE"
+
+
+def test_gla_rejects_bf16_and_grouped_queries(L):
+    q = torch.zeros(1, 64, 2, 64, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(ValueError):
+        L.gla_fwd_local(q, q, q, q)
