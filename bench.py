@@ -319,6 +319,76 @@ def layer_bench(args, lasp, dev, stream, B, C, H, Hk, D, l2_flush):
             "projection_gflop_per_step": flops / 1e9}
 
 
+def gla_bench(args, lasp, lib, dev, stream, B, C, H, D, l2_flush):
+    """the generalised-decay path (GLA / GateLoop row of Table 3) at the same shape, fp32
+    inputs (q, k, v, do, log decay), fwd + bwd (dQ, dK, dV, dlog_g) through lasp_gla_fwd_local / _bwd_local,
+    graph-replayed, L2 flushed between steps. Roofline: CUDA-core ALU issue (the kernels are FP32-pipe
+    recurrences): 16 D^2 FP32 lane-instructions per token-head (F1 2, F3 3, B1 2, dQ 3, dV 3, dK 3) against
+    148 SMs x 128 FP32 lanes x the max SM clock."""
+    import ctypes
+    import json as _json
+
+    import torch
+
+    import synth
+    t = synth.gla_problem(0, B, C, H, D)
+    q, k, v, do, lg = (torch.from_numpy(t[n]).to(dev) for n in ("q", "k", "v", "do", "lg"))
+    cache, ws = lasp.gla_alloc(q)
+    o, dq, dk, dv, dlg = (torch.empty_like(q) for _ in range(5))
+
+    def step():
+        lasp.gla_fwd_local(q, k, v, lg, o=o, kv_out=False, cache=cache, workspace=ws)
+        lasp.gla_bwd_local(q, k, v, lg, do, cache, dq=dq, dk=dk, dv=dv, dlog_g=dlg, dkv_out=False, workspace=ws)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    graph = None
+    if args.graph:
+        try:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                step()
+            gr.replay()
+            torch.cuda.synchronize(dev)
+            graph = gr
+        except Exception:  # noqa: BLE001 - eager, reported
+            torch.cuda.synchronize(dev)
+    n = max(3, min(args.steps, 10))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    for i in range(n):
+        l2_flush()
+        ev[i][0].record(stream)
+        graph.replay() if graph is not None else step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    ms = sum(a.elapsed_time(b) for a, b in ev) / n
+    # per-kernel times (profiled eager pass)
+    lib.lasp_profile_enable(1)
+    for _ in range(n):
+        step()
+    torch.cuda.synchronize(dev)
+    lib.lasp_profile_enable(0)
+    buf = ctypes.create_string_buffer(1 << 16)
+    lib.lasp_profile_read(buf, len(buf))
+    stages = {kk: vv[1] / n for kk, vv in _json.loads(buf.value.decode() or "{}").items()}
+    ops = 16 * D * D * B * C * H
+    clk = peaks_clock()
+    peak = 148 * 128 * clk * 1e6 / 1e9  # G lane-ops / s
+    return {"metric": "generalised-decay (GLA) fwd+bwd tokens/sec", "value": B * C / (ms / 1e3), "unit": "tokens/s",
+            "ms_per_step": ms, "dtype": "fp32", "launch": "cuda-graph replay" if graph else "eager",
+            "stages_ms_per_step": stages,
+            "roofline": {"bound": "alu", "achieved": ops / (ms / 1e3) / 1e9, "peak": peak, "unit": "G FP32 lane-ops/s",
+                         "frac": ops / (ms / 1e3) / 1e9 / peak, "ops_rule": "16 D^2 FP32 lane-instructions per token-head",
+                         "peak_rule": "148 SMs x 128 FP32 lanes x sm_max_mhz"}}
+
+
+def peaks_clock():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0))
+    except Exception:  # noqa: BLE001
+        return 1965.0
+
+
 def cpu_info():
     model = "unknown"
     try:
@@ -613,6 +683,9 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
     layer = None
     if world == 1 and not loopback and not args.no_layer:
         layer = layer_bench(args, lasp, dev, stream, B, C, H, Hk, D, l2_flush)
+    gla = None
+    if world == 1 and not loopback and not args.no_gla and Hk == H:
+        gla = gla_bench(args, lasp, lib, dev, stream, B, C, H, D, l2_flush)
 
     cpu = None
     if world == 1 and not loopback and not args.no_cpu_baseline:
@@ -634,7 +707,7 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
                        "launch": ex_report[main_ex]["launch"], "exchange": main_ex},
             "parity_ok": all(r["parity_ok"] for r in ex_report.values()),
             "gpu_launches": int(R["launches"]), "clocks": clk_summary, "e2e": e2e, "roofline": roofline,
-            "path": path, "cpu_baseline": cpu, "layer": layer}
+            "path": path, "cpu_baseline": cpu, "layer": layer, "gla": gla}
     if T > 1:
         line["exchanges"] = ex_report
     else:
@@ -722,6 +795,7 @@ def main():
                     help="grouped-query attention: key/value heads (default: the config's heads, i.e. multi-head)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-layer", action="store_true", help="skip the NEXT-3 whole-layer line")
+    ap.add_argument("--no-gla", action="store_true", help="skip the NEXT-4 generalised-decay line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

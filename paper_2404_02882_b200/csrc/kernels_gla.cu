@@ -32,7 +32,7 @@
 namespace lasp {
 namespace {
 
-constexpr int GT = 16;  // tokens per shared-memory tile
+constexpr int GT = 16;  // tokens per shared-memory tile (double-buffered with cp.async)
 
 template <int D>
 struct GlaCfg {
@@ -58,22 +58,24 @@ __device__ __forceinline__ size_t row_off(const GlaPlan& p, int64_t b, int64_t t
   return size_t(((b * p.C + t) * p.H + h) * p.D);
 }
 
-// stage tokens [t0, t0 + GT) of up to 5 tensors into sm[x][GT][D] (zeros past the segment end; lg -> g)
+// async copy of 16 bytes global -> shared (zero-filled when !valid)
+__device__ __forceinline__ void cp16(float* dst, const float* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// issue the async copies of tokens [t0, t0 + GT) of NX tensors into buf[NX][GT][D] (zeros outside [s0, s1))
 template <int D, int NX>
-__device__ __forceinline__ void load_tile(const GlaPlan& p, int64_t b, int64_t h, int64_t t0, int64_t tend,
-                                          const float* const (&src)[NX], const int (&is_lg)[NX],
-                                          float (*sm)[GT][D], float (*lgs)[D]) {
+__device__ __forceinline__ void stage_tile(const GlaPlan& p, int64_t b, int64_t h, int64_t t0, int64_t s0, int64_t s1,
+                                           const float* const (&src)[NX], float* buf) {
   constexpr int NT = GlaCfg<D>::NT, V4 = D / 4;
   for (int i = threadIdx.x; i < NX * GT * V4; i += NT) {
     const int x = i / (GT * V4), r = (i / V4) % GT, c4 = i % V4;
     const int64_t t = t0 + r;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (t < tend && t >= 0) v = *reinterpret_cast<const float4*>(src[x] + row_off(p, b, t, h) + c4 * 4);
-    if (is_lg[x]) {
-      if (lgs) *reinterpret_cast<float4*>(&lgs[r][c4 * 4]) = v;  // raw log decay (0 past the end)
-      v = make_float4(__expf(v.x), __expf(v.y), __expf(v.z), __expf(v.w));
-    }
-    *reinterpret_cast<float4*>(&sm[x][r][c4 * 4]) = v;
+    const bool ok = t >= s0 && t < s1;
+    cp16(buf + (size_t(x) * GT + r) * D + c4 * 4, ok ? src[x] + row_off(p, b, t, h) + c4 * 4 : src[x], ok);
   }
 }
 
@@ -83,16 +85,30 @@ __device__ __forceinline__ float pair_sum(float x) {
   return x;
 }
 
+// staged tensors per mode (the log decay is always index LGX; dK also stages dq and k)
+template <int MODE> struct GlaTensors;
+template <> struct GlaTensors<0> { static constexpr int NX = 3, LGX = 2; };  // F1: k, v, lg
+template <> struct GlaTensors<1> { static constexpr int NX = 4, LGX = 3; };  // F3: q, k, v, lg
+template <> struct GlaTensors<2> { static constexpr int NX = 3, LGX = 2; };  // B1: q, do, lg
+template <> struct GlaTensors<3> { static constexpr int NX = 4, LGX = 3; };  // DQ: k, v, do, lg
+template <> struct GlaTensors<4> { static constexpr int NX = 4, LGX = 3; };  // DV: q, do, k, lg
+template <> struct GlaTensors<5> { static constexpr int NX = 6, LGX = 3; };  // DK: q, do, v, lg, dq, k
+
+template <int D, int MODE>
+constexpr size_t gla_smem_bytes() {
+  return (2 * size_t(GlaTensors<MODE>::NX) + 1) * GT * D * sizeof(float);
+}
+
 template <int D, int MODE>
 __global__ void __launch_bounds__(GlaCfg<D>::NT) gla_kernel(const GlaArgs a) {
   using Cfg = GlaCfg<D>;
   constexpr int RPT = Cfg::RPT, TPC = Cfg::TPC;
   constexpr bool REV = MODE == G_B1 || MODE == G_DV || MODE == G_DK;
   constexpr bool ROWS = MODE == G_DQ || MODE == G_DK;  // thread owns a state row (else a column)
-  // tensors staged per tile (index into sm): see the mode comments below
-  constexpr int NX = MODE == G_DK ? 5 : MODE == G_F1 || MODE == G_B1 ? 3 : 4;
-  __shared__ __align__(16) float sm[NX][GT][D];
-  __shared__ __align__(16) float lgs[MODE == G_F1 || MODE == G_B1 ? GT : 1][D];
+  constexpr int NX = GlaTensors<MODE>::NX, LGX = GlaTensors<MODE>::LGX;
+  extern __shared__ __align__(16) float smem[];
+  float* raw = smem;                            // [2][NX][GT][D] double-buffered token tiles
+  float* gb = smem + 2 * NX * GT * D;           // [GT][D] g = exp(lg) of the tile being computed
 
   pdl_wait();  // inputs and states come from the preceding kernels (never triggered early by this path)
   const GlaPlan& p = a.p;
@@ -104,8 +120,22 @@ __global__ void __launch_bounds__(GlaCfg<D>::NT) gla_kernel(const GlaArgs a) {
   const int base = part * RPT;
   const size_t seg_off = (size_t(bh) * size_t(p.nseg) + size_t(seg)) * size_t(p.D) * size_t(p.D);
 
+  const float* srcs[NX];
+  if constexpr (MODE == G_F1) { srcs[0] = a.k; srcs[1] = a.v; srcs[2] = a.lg; }
+  if constexpr (MODE == G_F3) { srcs[0] = a.q; srcs[1] = a.k; srcs[2] = a.v; srcs[3] = a.lg; }
+  if constexpr (MODE == G_B1) { srcs[0] = a.q; srcs[1] = a.d_o; srcs[2] = a.lg; }
+  if constexpr (MODE == G_DQ) { srcs[0] = a.k; srcs[1] = a.v; srcs[2] = a.d_o; srcs[3] = a.lg; }
+  if constexpr (MODE == G_DV) { srcs[0] = a.q; srcs[1] = a.d_o; srcs[2] = a.k; srcs[3] = a.lg; }
+  if constexpr (MODE == G_DK) {
+    srcs[0] = a.q; srcs[1] = a.d_o; srcs[2] = a.v; srcs[3] = a.lg; srcs[4] = a.dq_in; srcs[5] = a.k;
+  }
+  const int64_t ntile = (s1 - s0 + GT - 1) / GT;
+  auto tile_t0 = [&](int64_t ti) { return REV ? s1 - (ti + 1) * GT : s0 + ti * GT; };  // REV tiles end at s1
+  if (ntile > 0) stage_tile<D, NX>(p, b, h, tile_t0(0), s0, s1, srcs, raw);
+  cp_commit();
+
   float st[RPT];
-  // ---- initial state
+  // ---- initial state (loads overlap the first tile's copies)
   if constexpr (MODE == G_F1 || MODE == G_B1) {
 #pragma unroll
     for (int r = 0; r < RPT; ++r) st[r] = 0.f;
@@ -123,7 +153,7 @@ __global__ void __launch_bounds__(GlaCfg<D>::NT) gla_kernel(const GlaArgs a) {
       for (int r = 0; r < RPT; ++r) st[r] = __int_as_float(0x7fc00000);
     }
   }
-  float run = 0.f;  // DK: suffix sum of q . dq - k . dk (this row), F1 / B1: sum of lg (this column index)
+  float run = 0.f;  // DK: suffix sum of q . dq - k . dk (this row); F1 / B1: sum of lg (this column index)
   if constexpr (MODE == G_DK) {
     const float* pn = a.cache + (size_t(bh) * size_t(p.nseg + 1) + size_t(seg + 1)) * size_t(p.D) * size_t(p.D);
     float c = 0.f;
@@ -132,38 +162,33 @@ __global__ void __launch_bounds__(GlaCfg<D>::NT) gla_kernel(const GlaArgs a) {
     run = pair_sum<TPC>(c);  // <R_p[d, :], P_{p+1}[d, :]>: dlg summed over the tokens after this segment
   }
 
-  // staged tensors: F1 (k, v, lg) F3 (q, k, v, lg) B1 (q, do, lg) DQ (k, v, do, lg) DV (q, do, k, lg)
-  //                 DK (q, do, v, lg, dq)
-  const float* srcs[NX];
-  int is_lg[NX];
-#pragma unroll
-  for (int x = 0; x < NX; ++x) is_lg[x] = 0;
-  if constexpr (MODE == G_F1) { srcs[0] = a.k; srcs[1] = a.v; srcs[2] = a.lg; is_lg[2] = 1; }
-  if constexpr (MODE == G_F3) { srcs[0] = a.q; srcs[1] = a.k; srcs[2] = a.v; srcs[3] = a.lg; is_lg[3] = 1; }
-  if constexpr (MODE == G_B1) { srcs[0] = a.q; srcs[1] = a.d_o; srcs[2] = a.lg; is_lg[2] = 1; }
-  if constexpr (MODE == G_DQ) { srcs[0] = a.k; srcs[1] = a.v; srcs[2] = a.d_o; srcs[3] = a.lg; is_lg[3] = 1; }
-  if constexpr (MODE == G_DV) { srcs[0] = a.q; srcs[1] = a.d_o; srcs[2] = a.k; srcs[3] = a.lg; is_lg[3] = 1; }
-  if constexpr (MODE == G_DK) {
-    srcs[0] = a.q; srcs[1] = a.d_o; srcs[2] = a.v; srcs[3] = a.lg; srcs[4] = a.dq_in; is_lg[3] = 1;
-  }
-  constexpr int GX = MODE == G_F1 || MODE == G_B1 ? 2 : 3;  // index of g in sm
-
-  const int64_t ntile = (s1 - s0 + GT - 1) / GT;
   for (int64_t ti = 0; ti < ntile; ++ti) {
-    const int64_t t0 = REV ? s1 - (ti + 1) * GT : s0 + ti * GT;  // REV tiles end at the segment end
-    __syncthreads();  // the previous tile is consumed
-    load_tile<D, NX>(p, b, h, t0, s1, srcs, is_lg, sm, (MODE == G_F1 || MODE == G_B1) ? lgs : nullptr);
+    float* cur = raw + size_t(ti & 1) * NX * GT * D;
+    __syncthreads();  // every thread is done with the other buffer (tile ti - 1) and with gb
+    if (ti + 1 < ntile) stage_tile<D, NX>(p, b, h, tile_t0(ti + 1), s0, s1, srcs, raw + size_t((ti + 1) & 1) * NX * GT * D);
+    cp_commit();
+    cp_wait_prev();   // this thread's copies of tile ti have landed
+    __syncthreads();  // ... and everybody's
+    {
+      const float* lgt = cur + size_t(LGX) * GT * D;
+      for (int i = threadIdx.x; i < GT * D / 4; i += Cfg::NT) {
+        const float4 l4 = reinterpret_cast<const float4*>(lgt)[i];
+        reinterpret_cast<float4*>(gb)[i] = make_float4(__expf(l4.x), __expf(l4.y), __expf(l4.z), __expf(l4.w));
+      }
+    }
     __syncthreads();
+    const int64_t t0 = tile_t0(ti);
+    auto T = [&](int x, int r) -> const float* { return cur + (size_t(x) * GT + r) * D; };
     for (int rr = 0; rr < GT; ++rr) {
       const int r = REV ? GT - 1 - rr : rr;
       const int64_t t = t0 + r;
       if (t < s0 || t >= s1) continue;  // (uniform across the CTA)
-      const float* g = sm[GX][r];
+      const float* g = gb + size_t(r) * D;
       if constexpr (MODE == G_F1 || MODE == G_F3) {
         // kv = Diag(g_t) kv + k_t v_t^T (column `own`), then (F3) o_t[own] = sum_d q_t[d] kv[d][own]
-        const float* kk = sm[MODE == G_F1 ? 0 : 1][r];
-        const float vj = sm[MODE == G_F1 ? 1 : 2][r][own];
-        float acc = 0.f;
+        const float* kk = T(MODE == G_F1 ? 0 : 1, r);
+        const float vj = T(MODE == G_F1 ? 1 : 2, r)[own];
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < RPT; i += 4) {
           const float4 g4 = *reinterpret_cast<const float4*>(g + base + i);
@@ -173,77 +198,88 @@ __global__ void __launch_bounds__(GlaCfg<D>::NT) gla_kernel(const GlaArgs a) {
           st[i + 2] = fmaf(g4.z, st[i + 2], k4.z * vj);
           st[i + 3] = fmaf(g4.w, st[i + 3], k4.w * vj);
           if constexpr (MODE == G_F3) {
-            const float4 q4 = *reinterpret_cast<const float4*>(sm[0][r] + base + i);
-            acc = fmaf(q4.x, st[i], fmaf(q4.y, st[i + 1], fmaf(q4.z, st[i + 2], fmaf(q4.w, st[i + 3], acc))));
+            const float4 q4 = *reinterpret_cast<const float4*>(T(0, r) + base + i);
+            acc[0] = fmaf(q4.x, st[i], acc[0]);
+            acc[1] = fmaf(q4.y, st[i + 1], acc[1]);
+            acc[2] = fmaf(q4.z, st[i + 2], acc[2]);
+            acc[3] = fmaf(q4.w, st[i + 3], acc[3]);
           }
         }
         if constexpr (MODE == G_F3) {
-          acc = pair_sum<TPC>(acc);
-          if (part == 0) a.out[row_off(p, b, t, h) + own] = acc;
+          const float o = pair_sum<TPC>((acc[0] + acc[1]) + (acc[2] + acc[3]));
+          if (part == 0) a.out[row_off(p, b, t, h) + own] = o;
         }
-        if constexpr (MODE == G_F1) if (part == 0) run += lgs[r][own];
+        if constexpr (MODE == G_F1) if (part == 0) run += T(LGX, r)[own];
       } else if constexpr (MODE == G_DQ) {
         // row `own`: kv[own][:] = g_t[own] kv[own][:] + k_t[own] v_t[:], dq_t[own] = sum_e kv[own][e] do_t[e]
-        const float gi = g[own], ki = sm[0][r][own];
-        float acc = 0.f;
+        const float gi = g[own], ki = T(0, r)[own];
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < RPT; i += 4) {
-          const float4 v4 = *reinterpret_cast<const float4*>(sm[1][r] + base + i);
-          const float4 d4 = *reinterpret_cast<const float4*>(sm[2][r] + base + i);
+          const float4 v4 = *reinterpret_cast<const float4*>(T(1, r) + base + i);
+          const float4 d4 = *reinterpret_cast<const float4*>(T(2, r) + base + i);
           st[i] = fmaf(gi, st[i], ki * v4.x);
           st[i + 1] = fmaf(gi, st[i + 1], ki * v4.y);
           st[i + 2] = fmaf(gi, st[i + 2], ki * v4.z);
           st[i + 3] = fmaf(gi, st[i + 3], ki * v4.w);
-          acc = fmaf(st[i], d4.x, fmaf(st[i + 1], d4.y, fmaf(st[i + 2], d4.z, fmaf(st[i + 3], d4.w, acc))));
+          acc[0] = fmaf(st[i], d4.x, acc[0]);
+          acc[1] = fmaf(st[i + 1], d4.y, acc[1]);
+          acc[2] = fmaf(st[i + 2], d4.z, acc[2]);
+          acc[3] = fmaf(st[i + 3], d4.w, acc[3]);
         }
-        acc = pair_sum<TPC>(acc);
-        if (part == 0) a.out[row_off(p, b, t, h) + own] = acc;
+        const float o = pair_sum<TPC>((acc[0] + acc[1]) + (acc[2] + acc[3]));
+        if (part == 0) a.out[row_off(p, b, t, h) + own] = o;
       } else if constexpr (MODE == G_B1 || MODE == G_DV) {
         // column `own`: dkv[:][own] += q_t[:] do_t[own]; (DV) dv_t[own] = sum_d dkv[d][own] k_t[d]; then
         // dkv *= g_t (the decay the next, earlier token sees: dkv_{t-1} = q do^T + Diag(g_t) dkv_t)
-        const float dj = sm[1][r][own];
-        float acc = 0.f;
+        const float dj = T(1, r)[own];
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < RPT; i += 4) {
-          const float4 q4 = *reinterpret_cast<const float4*>(sm[0][r] + base + i);
+          const float4 q4 = *reinterpret_cast<const float4*>(T(0, r) + base + i);
           const float4 g4 = *reinterpret_cast<const float4*>(g + base + i);
           st[i] = fmaf(q4.x, dj, st[i]);
           st[i + 1] = fmaf(q4.y, dj, st[i + 1]);
           st[i + 2] = fmaf(q4.z, dj, st[i + 2]);
           st[i + 3] = fmaf(q4.w, dj, st[i + 3]);
           if constexpr (MODE == G_DV) {
-            const float4 k4 = *reinterpret_cast<const float4*>(sm[2][r] + base + i);
-            acc = fmaf(st[i], k4.x, fmaf(st[i + 1], k4.y, fmaf(st[i + 2], k4.z, fmaf(st[i + 3], k4.w, acc))));
+            const float4 k4 = *reinterpret_cast<const float4*>(T(2, r) + base + i);
+            acc[0] = fmaf(st[i], k4.x, acc[0]);
+            acc[1] = fmaf(st[i + 1], k4.y, acc[1]);
+            acc[2] = fmaf(st[i + 2], k4.z, acc[2]);
+            acc[3] = fmaf(st[i + 3], k4.w, acc[3]);
           }
           st[i] *= g4.x; st[i + 1] *= g4.y; st[i + 2] *= g4.z; st[i + 3] *= g4.w;
         }
         if constexpr (MODE == G_DV) {
-          acc = pair_sum<TPC>(acc);
-          if (part == 0) a.out[row_off(p, b, t, h) + own] = acc;
+          const float o = pair_sum<TPC>((acc[0] + acc[1]) + (acc[2] + acc[3]));
+          if (part == 0) a.out[row_off(p, b, t, h) + own] = o;
         }
-        if constexpr (MODE == G_B1) if (part == 0) run += lgs[r][own];
+        if constexpr (MODE == G_B1) if (part == 0) run += T(LGX, r)[own];
       } else {  // G_DK
         // row `own`: dkv[own][:] += q_t[own] do_t[:]; dk_t[own] = sum_e dkv[own][e] v_t[e];
-        // dlg_t[own] = (suffix) + q_t[own] dq_t[own] - k-side term; dkv[own][:] *= g_t[own]
-        const float qi = sm[0][r][own], gi = g[own];
-        float acc = 0.f;
+        // dlg_t[own] = (suffix) + q_t[own] dq_t[own] - k_t[own] dk_t[own]; dkv[own][:] *= g_t[own]
+        const float qi = T(0, r)[own], gi = g[own];
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < RPT; i += 4) {
-          const float4 d4 = *reinterpret_cast<const float4*>(sm[1][r] + base + i);
-          const float4 v4 = *reinterpret_cast<const float4*>(sm[2][r] + base + i);
+          const float4 d4 = *reinterpret_cast<const float4*>(T(1, r) + base + i);
+          const float4 v4 = *reinterpret_cast<const float4*>(T(2, r) + base + i);
           st[i] = fmaf(qi, d4.x, st[i]);
           st[i + 1] = fmaf(qi, d4.y, st[i + 1]);
           st[i + 2] = fmaf(qi, d4.z, st[i + 2]);
           st[i + 3] = fmaf(qi, d4.w, st[i + 3]);
-          acc = fmaf(st[i], v4.x, fmaf(st[i + 1], v4.y, fmaf(st[i + 2], v4.z, fmaf(st[i + 3], v4.w, acc))));
+          acc[0] = fmaf(st[i], v4.x, acc[0]);
+          acc[1] = fmaf(st[i + 1], v4.y, acc[1]);
+          acc[2] = fmaf(st[i + 2], v4.z, acc[2]);
+          acc[3] = fmaf(st[i + 3], v4.w, acc[3]);
           st[i] *= gi; st[i + 1] *= gi; st[i + 2] *= gi; st[i + 3] *= gi;
         }
-        acc = pair_sum<TPC>(acc);
+        const float dk = pair_sum<TPC>((acc[0] + acc[1]) + (acc[2] + acc[3]));
         if (part == 0) {
           const size_t o = row_off(p, b, t, h) + own;
-          const float ki = a.k[o];
-          run += fmaf(qi, sm[4][r][own], -ki * acc);
-          a.out[o] = acc;
+          run += fmaf(qi, T(4, r)[own], -T(5, r)[own] * dk);
+          a.out[o] = dk;
           a.dlg[o] = run;
         }
       }
@@ -307,7 +343,10 @@ __global__ void gla_combine_kernel(GlaPlan p, const float* __restrict__ in, cons
 template <int D, int MODE>
 cudaError_t launch_mode(const GlaArgs& a, cudaStream_t st) {
   const int64_t items = a.p.B * a.p.H * a.p.nseg;
-  return launch_k(gla_kernel<D, MODE>, dim3(unsigned(items)), dim3(GlaCfg<D>::NT), 0, st, a);
+  constexpr size_t smem = gla_smem_bytes<D, MODE>();
+  cudaError_t e = cudaFuncSetAttribute(gla_kernel<D, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  return launch_k(gla_kernel<D, MODE>, dim3(unsigned(items)), dim3(GlaCfg<D>::NT), smem, st, a);
 }
 
 template <int MODE>
