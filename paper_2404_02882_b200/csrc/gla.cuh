@@ -7,10 +7,12 @@ namespace lasp {
 
 struct GlaPlan {
   int64_t B, C, H, D;   // batch, n_local, heads (= kv heads), head_dim
-  int64_t seg_len;      // multiple of 16 (the kernels' token tile)
+  int64_t seg_len;      // multiple of 8 (the kernels' token tile)
   int64_t nseg;         // >= 1
 };
 
+// co-resident CTAs per SM of the slowest-occupancy pass (the host sizes the segment count to whole waves)
+int gla_slots_per_sm(int D);
 // F1 (rev = 0: x = k, y = v) / B1 (rev = 1: x = q, y = do): per-segment local states into seg
 // [B][H][nseg][D][D] (B1: G'_p) and segment log-decay sums into ls [B][H][nseg][D]
 cudaError_t gla_launch_state(const GlaPlan& p, int rev, const float* x, const float* y, const float* lg, float* seg,

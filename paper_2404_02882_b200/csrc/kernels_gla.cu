@@ -22,23 +22,33 @@
 //       kv_{e_p+1} = Diag(g_{e_p+1}) kv_{e_p} + ...), so no extra exchange is needed.
 //
 // Kernels run the recurrences token by token on CUDA cores (fp32 FFMA, exact: no decay is ever inverted, no
-// exponent-range restriction). One CTA per (batch, head, segment) item; each thread owns one state column
-// (F1, F3, B1, dV: the output / update index is the column) or one state row (dQ, dK), split over two
-// threads at head_dim 128 (64 registers each, partial dot products combined with one shuffle). The tokens'
-// vectors are staged in shared memory 16 at a time and read as warp-broadcasts.
+// exponent-range restriction). One CTA per (batch, head, segment) item; each thread owns a 2-D tile of the state
+// in registers (GlaCfg). The tokens' vectors are staged in shared memory 16 at a time (cp.async, double-buffered)
+// and read as warp broadcasts.
 #include "lasp_common.cuh"
 #include "gla.cuh"
+
+#include <algorithm>
+#include <type_traits>
 
 namespace lasp {
 namespace {
 
-constexpr int GT = 16;  // tokens per shared-memory tile (double-buffered with cp.async)
+constexpr int GT = 8;   // tokens per shared-memory tile (double-buffered with cp.async)
 
+// Each thread owns an OSPAN x RSPAN tile of the D x D state: OSPAN output indices (the value column for the
+// F1 / F3 / B1 / dV passes, the key row for dQ / dK) by RSPAN indices of the dimension the outputs reduce over.
+// The NRED = D / RSPAN threads sharing the same outputs are adjacent lanes and combine their partial dot
+// products with xor-shuffles. A thread's reduce indices are interleaved with its NRED partners' at float4
+// granularity (chunk c of thread rg covers indices 4 (c NRED + rg) .. +3), so the partners' vector loads hit
+// consecutive 16-byte words (no bank conflicts). Per token a thread reads 2-3 RSPAN-vectors and one OSPAN-vector from shared memory
+// (warp broadcasts) for 2-3 x 64 FP32 instructions.
 template <int D>
 struct GlaCfg {
-  static constexpr int RPT = D > 64 ? 64 : D;  // state elements per thread
-  static constexpr int TPC = D / RPT;          // threads per state column / row (1 or 2)
-  static constexpr int NT = D * TPC;           // threads per item
+  static constexpr int OSPAN = D == 128 ? 2 : 4;
+  static constexpr int RSPAN = D == 32 ? 8 : D == 64 ? 16 : 32;
+  static constexpr int NRED = D / RSPAN;                 // 4
+  static constexpr int NT = (D / OSPAN) * NRED;          // 32, 64, 256 threads per item
 };
 
 enum GlaMode : int { G_F1 = 0, G_F3 = 1, G_B1 = 2, G_DQ = 3, G_DV = 4, G_DK = 5 };
@@ -71,17 +81,20 @@ template <int D, int NX>
 __device__ __forceinline__ void stage_tile(const GlaPlan& p, int64_t b, int64_t h, int64_t t0, int64_t s0, int64_t s1,
                                            const float* const (&src)[NX], float* buf) {
   constexpr int NT = GlaCfg<D>::NT, V4 = D / 4;
-  for (int i = threadIdx.x; i < NX * GT * V4; i += NT) {
-    const int x = i / (GT * V4), r = (i / V4) % GT, c4 = i % V4;
-    const int64_t t = t0 + r;
-    const bool ok = t >= s0 && t < s1;
-    cp16(buf + (size_t(x) * GT + r) * D + c4 * 4, ok ? src[x] + row_off(p, b, t, h) + c4 * 4 : src[x], ok);
-  }
+#pragma unroll
+  for (int x = 0; x < NX; ++x)
+    for (int i = threadIdx.x; i < GT * V4; i += NT) {
+      const int r = i / V4, c4 = i % V4;
+      const int64_t t = t0 + r;
+      const bool ok = t >= s0 && t < s1;
+      cp16(buf + (size_t(x) * GT + r) * D + c4 * 4, ok ? src[x] + row_off(p, b, t, h) + c4 * 4 : src[x], ok);
+    }
 }
 
-template <int TPC>
-__device__ __forceinline__ float pair_sum(float x) {
-  if constexpr (TPC == 2) x += __shfl_xor_sync(0xffffffffu, x, 1);
+template <int NRED>
+__device__ __forceinline__ float red_sum(float x) {
+#pragma unroll
+  for (int m = 1; m < NRED; m <<= 1) x += __shfl_xor_sync(0xffffffffu, x, m);
   return x;
 }
 
@@ -102,9 +115,9 @@ constexpr size_t gla_smem_bytes() {
 template <int D, int MODE>
 __global__ void __launch_bounds__(GlaCfg<D>::NT) gla_kernel(const GlaArgs a) {
   using Cfg = GlaCfg<D>;
-  constexpr int RPT = Cfg::RPT, TPC = Cfg::TPC;
+  constexpr int OS = Cfg::OSPAN, RS = Cfg::RSPAN, NRED = Cfg::NRED;
   constexpr bool REV = MODE == G_B1 || MODE == G_DV || MODE == G_DK;
-  constexpr bool ROWS = MODE == G_DQ || MODE == G_DK;  // thread owns a state row (else a column)
+  constexpr bool ROWS = MODE == G_DQ || MODE == G_DK;  // outputs indexed by the key row (else the value column)
   constexpr int NX = GlaTensors<MODE>::NX, LGX = GlaTensors<MODE>::LGX;
   extern __shared__ __align__(16) float smem[];
   float* raw = smem;                            // [2][NX][GT][D] double-buffered token tiles
@@ -115,10 +128,23 @@ __global__ void __launch_bounds__(GlaCfg<D>::NT) gla_kernel(const GlaArgs a) {
   const int64_t item = blockIdx.x;
   const int64_t seg = item % p.nseg, bh = item / p.nseg, b = bh / p.H, h = bh % p.H;
   const int64_t s0 = seg * p.seg_len, s1 = (s0 + p.seg_len < p.C) ? s0 + p.seg_len : p.C;
-  const int own = int(threadIdx.x) / TPC;             // owned column (or row) index
-  const int part = int(threadIdx.x) % TPC;            // which RPT-slice of the other index
-  const int base = part * RPT;
+  const int tid = int(threadIdx.x);
+  const int ob = (tid / NRED) * OS;      // first output index of this thread
+  const int rg = tid % NRED;             // reduce group: indices 4 (c NRED + rg) + u, c < RS / 4, u < 4
+  const bool lead = tid % NRED == 0;     // writes the reduced outputs
   const size_t seg_off = (size_t(bh) * size_t(p.nseg) + size_t(seg)) * size_t(p.D) * size_t(p.D);
+  // state element (output j, reduce i) <-> S[d][e]: column modes d = ridx(i), e = ob + j; row modes d = ob + j,
+  // e = ridx(i)
+  auto ridx = [&](int i) -> int { return ((i >> 2) * NRED + rg) * 4 + (i & 3); };
+  auto sidx = [&](int j, int i) -> size_t {
+    return ROWS ? size_t(ob + j) * D + size_t(ridx(i)) : size_t(ridx(i)) * D + size_t(ob + j);
+  };
+  // RS consecutive reduce-index values of a [D] shared-memory vector into registers
+  auto rvec = [&](float* dst, const float* src) {
+#pragma unroll
+    for (int i = 0; i < RS; i += 4)
+      *reinterpret_cast<float4*>(dst + i) = *reinterpret_cast<const float4*>(src + ridx(i));
+  };
 
   const float* srcs[NX];
   if constexpr (MODE == G_F1) { srcs[0] = a.k; srcs[1] = a.v; srcs[2] = a.lg; }
@@ -134,32 +160,37 @@ __global__ void __launch_bounds__(GlaCfg<D>::NT) gla_kernel(const GlaArgs a) {
   if (ntile > 0) stage_tile<D, NX>(p, b, h, tile_t0(0), s0, s1, srcs, raw);
   cp_commit();
 
-  float st[RPT];
+  float st[OS][RS];
   // ---- initial state (loads overlap the first tile's copies)
   if constexpr (MODE == G_F1 || MODE == G_B1) {
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) st[r] = 0.f;
+    for (int j = 0; j < OS; ++j)
+#pragma unroll
+      for (int i = 0; i < RS; ++i) st[j][i] = 0.f;
   } else {
     const float* init;
     if constexpr (MODE == G_F3 || MODE == G_DQ)
       init = a.cache + (size_t(bh) * size_t(p.nseg + 1) + size_t(seg)) * size_t(p.D) * size_t(p.D);
     else
       init = a.seg + seg_off;  // R_p
+    const bool poison = a.status != nullptr && tag_poisoned(a.status);
 #pragma unroll
-    for (int r = 0; r < RPT; ++r)
-      st[r] = ROWS ? init[size_t(own) * D + base + r] : init[size_t(base + r) * D + own];
-    if (a.status != nullptr && tag_poisoned(a.status)) {
+    for (int j = 0; j < OS; ++j)
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) st[r] = __int_as_float(0x7fc00000);
-    }
+      for (int i = 0; i < RS; ++i) st[j][i] = poison ? __int_as_float(0x7fc00000) : init[sidx(j, i)];
   }
-  float run = 0.f;  // DK: suffix sum of q . dq - k . dk (this row); F1 / B1: sum of lg (this column index)
+  float run[OS];  // DK: suffix sums of q . dq - k . dk (rows ob..ob+OS); F1 / B1: sum of lg (index tid)
+#pragma unroll
+  for (int j = 0; j < OS; ++j) run[j] = 0.f;
   if constexpr (MODE == G_DK) {
     const float* pn = a.cache + (size_t(bh) * size_t(p.nseg + 1) + size_t(seg + 1)) * size_t(p.D) * size_t(p.D);
-    float c = 0.f;
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) c = fmaf(st[r], pn[size_t(own) * D + base + r], c);
-    run = pair_sum<TPC>(c);  // <R_p[d, :], P_{p+1}[d, :]>: dlg summed over the tokens after this segment
+    for (int j = 0; j < OS; ++j) {
+      float c = 0.f;
+#pragma unroll
+      for (int i = 0; i < RS; ++i) c = fmaf(st[j][i], pn[sidx(j, i)], c);
+      run[j] = red_sum<NRED>(c);  // <R_p[d, :], P_{p+1}[d, :]>: dlg summed over the tokens after this segment
+    }
   }
 
   for (int64_t ti = 0; ti < ntile; ++ti) {
@@ -171,7 +202,7 @@ __global__ void __launch_bounds__(GlaCfg<D>::NT) gla_kernel(const GlaArgs a) {
     __syncthreads();  // ... and everybody's
     {
       const float* lgt = cur + size_t(LGX) * GT * D;
-      for (int i = threadIdx.x; i < GT * D / 4; i += Cfg::NT) {
+      for (int i = tid; i < GT * D / 4; i += Cfg::NT) {
         const float4 l4 = reinterpret_cast<const float4*>(lgt)[i];
         reinterpret_cast<float4*>(gb)[i] = make_float4(__expf(l4.x), __expf(l4.y), __expf(l4.z), __expf(l4.w));
       }
@@ -179,120 +210,147 @@ __global__ void __launch_bounds__(GlaCfg<D>::NT) gla_kernel(const GlaArgs a) {
     __syncthreads();
     const int64_t t0 = tile_t0(ti);
     auto T = [&](int x, int r) -> const float* { return cur + (size_t(x) * GT + r) * D; };
+    // vec<N>(ptr): N consecutive floats from shared memory (float4 broadcasts) into registers
     for (int rr = 0; rr < GT; ++rr) {
       const int r = REV ? GT - 1 - rr : rr;
       const int64_t t = t0 + r;
       if (t < s0 || t >= s1) continue;  // (uniform across the CTA)
       const float* g = gb + size_t(r) * D;
+      float o[OS];
       if constexpr (MODE == G_F1 || MODE == G_F3) {
-        // kv = Diag(g_t) kv + k_t v_t^T (column `own`), then (F3) o_t[own] = sum_d q_t[d] kv[d][own]
-        const float* kk = T(MODE == G_F1 ? 0 : 1, r);
-        const float vj = T(MODE == G_F1 ? 1 : 2, r)[own];
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        // S[d][e] = g[d] S[d][e] + k[d] v[e]; (F3) o[e] = sum_d q[d] S[d][e]    (e outputs, d reduce)
+        float gv[RS], kv[RS], vo[OS];
+        rvec(gv, g);
+        rvec(kv, T(MODE == G_F1 ? 0 : 1, r));
 #pragma unroll
-        for (int i = 0; i < RPT; i += 4) {
-          const float4 g4 = *reinterpret_cast<const float4*>(g + base + i);
-          const float4 k4 = *reinterpret_cast<const float4*>(kk + base + i);
-          st[i] = fmaf(g4.x, st[i], k4.x * vj);
-          st[i + 1] = fmaf(g4.y, st[i + 1], k4.y * vj);
-          st[i + 2] = fmaf(g4.z, st[i + 2], k4.z * vj);
-          st[i + 3] = fmaf(g4.w, st[i + 3], k4.w * vj);
-          if constexpr (MODE == G_F3) {
-            const float4 q4 = *reinterpret_cast<const float4*>(T(0, r) + base + i);
-            acc[0] = fmaf(q4.x, st[i], acc[0]);
-            acc[1] = fmaf(q4.y, st[i + 1], acc[1]);
-            acc[2] = fmaf(q4.z, st[i + 2], acc[2]);
-            acc[3] = fmaf(q4.w, st[i + 3], acc[3]);
-          }
-        }
+        for (int j = 0; j < OS; ++j) vo[j] = T(MODE == G_F1 ? 1 : 2, r)[ob + j];
+#pragma unroll
+        for (int j = 0; j < OS; ++j)
+#pragma unroll
+          for (int i = 0; i < RS; ++i) st[j][i] = fmaf(gv[i], st[j][i], kv[i] * vo[j]);
         if constexpr (MODE == G_F3) {
-          const float o = pair_sum<TPC>((acc[0] + acc[1]) + (acc[2] + acc[3]));
-          if (part == 0) a.out[row_off(p, b, t, h) + own] = o;
-        }
-        if constexpr (MODE == G_F1) if (part == 0) run += T(LGX, r)[own];
-      } else if constexpr (MODE == G_DQ) {
-        // row `own`: kv[own][:] = g_t[own] kv[own][:] + k_t[own] v_t[:], dq_t[own] = sum_e kv[own][e] do_t[e]
-        const float gi = g[own], ki = T(0, r)[own];
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+          float qv[RS];
+          rvec(qv, T(0, r));
 #pragma unroll
-        for (int i = 0; i < RPT; i += 4) {
-          const float4 v4 = *reinterpret_cast<const float4*>(T(1, r) + base + i);
-          const float4 d4 = *reinterpret_cast<const float4*>(T(2, r) + base + i);
-          st[i] = fmaf(gi, st[i], ki * v4.x);
-          st[i + 1] = fmaf(gi, st[i + 1], ki * v4.y);
-          st[i + 2] = fmaf(gi, st[i + 2], ki * v4.z);
-          st[i + 3] = fmaf(gi, st[i + 3], ki * v4.w);
-          acc[0] = fmaf(st[i], d4.x, acc[0]);
-          acc[1] = fmaf(st[i + 1], d4.y, acc[1]);
-          acc[2] = fmaf(st[i + 2], d4.z, acc[2]);
-          acc[3] = fmaf(st[i + 3], d4.w, acc[3]);
-        }
-        const float o = pair_sum<TPC>((acc[0] + acc[1]) + (acc[2] + acc[3]));
-        if (part == 0) a.out[row_off(p, b, t, h) + own] = o;
-      } else if constexpr (MODE == G_B1 || MODE == G_DV) {
-        // column `own`: dkv[:][own] += q_t[:] do_t[own]; (DV) dv_t[own] = sum_d dkv[d][own] k_t[d]; then
-        // dkv *= g_t (the decay the next, earlier token sees: dkv_{t-1} = q do^T + Diag(g_t) dkv_t)
-        const float dj = T(1, r)[own];
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int j = 0; j < OS; ++j) {
+            float x0 = 0.f, x1 = 0.f;
 #pragma unroll
-        for (int i = 0; i < RPT; i += 4) {
-          const float4 q4 = *reinterpret_cast<const float4*>(T(0, r) + base + i);
-          const float4 g4 = *reinterpret_cast<const float4*>(g + base + i);
-          st[i] = fmaf(q4.x, dj, st[i]);
-          st[i + 1] = fmaf(q4.y, dj, st[i + 1]);
-          st[i + 2] = fmaf(q4.z, dj, st[i + 2]);
-          st[i + 3] = fmaf(q4.w, dj, st[i + 3]);
-          if constexpr (MODE == G_DV) {
-            const float4 k4 = *reinterpret_cast<const float4*>(T(2, r) + base + i);
-            acc[0] = fmaf(st[i], k4.x, acc[0]);
-            acc[1] = fmaf(st[i + 1], k4.y, acc[1]);
-            acc[2] = fmaf(st[i + 2], k4.z, acc[2]);
-            acc[3] = fmaf(st[i + 3], k4.w, acc[3]);
+            for (int i = 0; i < RS; i += 2) {
+              x0 = fmaf(qv[i], st[j][i], x0);
+              x1 = fmaf(qv[i + 1], st[j][i + 1], x1);
+            }
+            o[j] = red_sum<NRED>(x0 + x1);
           }
-          st[i] *= g4.x; st[i + 1] *= g4.y; st[i + 2] *= g4.z; st[i + 3] *= g4.w;
-        }
-        if constexpr (MODE == G_DV) {
-          const float o = pair_sum<TPC>((acc[0] + acc[1]) + (acc[2] + acc[3]));
-          if (part == 0) a.out[row_off(p, b, t, h) + own] = o;
-        }
-        if constexpr (MODE == G_B1) if (part == 0) run += T(LGX, r)[own];
-      } else {  // G_DK
-        // row `own`: dkv[own][:] += q_t[own] do_t[:]; dk_t[own] = sum_e dkv[own][e] v_t[e];
-        // dlg_t[own] = (suffix) + q_t[own] dq_t[own] - k_t[own] dk_t[own]; dkv[own][:] *= g_t[own]
-        const float qi = T(0, r)[own], gi = g[own];
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+          if (lead) {
+            float* dst = a.out + row_off(p, b, t, h) + ob;
 #pragma unroll
-        for (int i = 0; i < RPT; i += 4) {
-          const float4 d4 = *reinterpret_cast<const float4*>(T(1, r) + base + i);
-          const float4 v4 = *reinterpret_cast<const float4*>(T(2, r) + base + i);
-          st[i] = fmaf(qi, d4.x, st[i]);
-          st[i + 1] = fmaf(qi, d4.y, st[i + 1]);
-          st[i + 2] = fmaf(qi, d4.z, st[i + 2]);
-          st[i + 3] = fmaf(qi, d4.w, st[i + 3]);
-          acc[0] = fmaf(st[i], v4.x, acc[0]);
-          acc[1] = fmaf(st[i + 1], v4.y, acc[1]);
-          acc[2] = fmaf(st[i + 2], v4.z, acc[2]);
-          acc[3] = fmaf(st[i + 3], v4.w, acc[3]);
-          st[i] *= gi; st[i + 1] *= gi; st[i + 2] *= gi; st[i + 3] *= gi;
+            for (int j = 0; j < OS; ++j) dst[j] = o[j];
+          }
         }
-        const float dk = pair_sum<TPC>((acc[0] + acc[1]) + (acc[2] + acc[3]));
-        if (part == 0) {
-          const size_t o = row_off(p, b, t, h) + own;
-          run += fmaf(qi, T(4, r)[own], -T(5, r)[own] * dk);
-          a.out[o] = dk;
-          a.dlg[o] = run;
+      } else if constexpr (MODE == G_DQ) {
+        // S[d][e] = g[d] S[d][e] + k[d] v[e]; dq[d] = sum_e S[d][e] do[e]    (d outputs, e reduce)
+        float vv[RS], dv[RS], gd[OS], kd[OS];
+        rvec(vv, T(1, r));
+        rvec(dv, T(2, r));
+#pragma unroll
+        for (int j = 0; j < OS; ++j) { gd[j] = g[ob + j]; kd[j] = T(0, r)[ob + j]; }
+#pragma unroll
+        for (int j = 0; j < OS; ++j) {
+          float x0 = 0.f, x1 = 0.f;
+#pragma unroll
+          for (int i = 0; i < RS; i += 2) {
+            st[j][i] = fmaf(gd[j], st[j][i], kd[j] * vv[i]);
+            st[j][i + 1] = fmaf(gd[j], st[j][i + 1], kd[j] * vv[i + 1]);
+            x0 = fmaf(st[j][i], dv[i], x0);
+            x1 = fmaf(st[j][i + 1], dv[i + 1], x1);
+          }
+          o[j] = red_sum<NRED>(x0 + x1);
         }
+        if (lead) {
+          float* dst = a.out + row_off(p, b, t, h) + ob;
+#pragma unroll
+          for (int j = 0; j < OS; ++j) dst[j] = o[j];
+        }
+      } else if constexpr (MODE == G_B1 || MODE == G_DV) {
+        // S[d][e] += q[d] do[e]; (DV) dv[e] = sum_d S[d][e] k[d]; S[d][e] *= g[d]    (e outputs, d reduce)
+        float qv[RS], gv[RS], dj[OS];
+        rvec(qv, T(0, r));
+        rvec(gv, g);
+#pragma unroll
+        for (int j = 0; j < OS; ++j) dj[j] = T(1, r)[ob + j];
+#pragma unroll
+        for (int j = 0; j < OS; ++j)
+#pragma unroll
+          for (int i = 0; i < RS; ++i) st[j][i] = fmaf(qv[i], dj[j], st[j][i]);
+        if constexpr (MODE == G_DV) {
+          float kv[RS];
+          rvec(kv, T(2, r));
+#pragma unroll
+          for (int j = 0; j < OS; ++j) {
+            float x0 = 0.f, x1 = 0.f;
+#pragma unroll
+            for (int i = 0; i < RS; i += 2) {
+              x0 = fmaf(st[j][i], kv[i], x0);
+              x1 = fmaf(st[j][i + 1], kv[i + 1], x1);
+            }
+            o[j] = red_sum<NRED>(x0 + x1);
+          }
+          if (lead) {
+            float* dst = a.out + row_off(p, b, t, h) + ob;
+#pragma unroll
+            for (int j = 0; j < OS; ++j) dst[j] = o[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < OS; ++j)
+#pragma unroll
+          for (int i = 0; i < RS; ++i) st[j][i] *= gv[i];
+      } else {  // G_DK
+        // S[d][e] += q[d] do[e]; dk[d] = sum_e S[d][e] v[e]; dlg[d] = run + q[d] dq[d] - k[d] dk[d]; S *= g[d]
+        float dv[RS], vv[RS], qd[OS];
+        rvec(dv, T(1, r));
+        rvec(vv, T(2, r));
+#pragma unroll
+        for (int j = 0; j < OS; ++j) qd[j] = T(0, r)[ob + j];
+#pragma unroll
+        for (int j = 0; j < OS; ++j) {
+          float x0 = 0.f, x1 = 0.f;
+          const float gj = g[ob + j];
+#pragma unroll
+          for (int i = 0; i < RS; i += 2) {
+            st[j][i] = fmaf(qd[j], dv[i], st[j][i]);
+            st[j][i + 1] = fmaf(qd[j], dv[i + 1], st[j][i + 1]);
+            x0 = fmaf(st[j][i], vv[i], x0);
+            x1 = fmaf(st[j][i + 1], vv[i + 1], x1);
+            st[j][i] *= gj;
+            st[j][i + 1] *= gj;
+          }
+          o[j] = red_sum<NRED>(x0 + x1);
+        }
+        if (lead) {
+          const size_t off = row_off(p, b, t, h) + ob;
+#pragma unroll
+          for (int j = 0; j < OS; ++j) {
+            run[j] += fmaf(qd[j], T(4, r)[ob + j], -T(5, r)[ob + j] * o[j]);
+            a.out[off + j] = o[j];
+            a.dlg[off + j] = run[j];
+          }
+        }
+      }
+      if constexpr (MODE == G_F1 || MODE == G_B1) {
+        if (tid < D) run[0] += T(LGX, r)[tid];
       }
     }
   }
   // ---- segment results
   if constexpr (MODE == G_F1 || MODE == G_B1) {
-    // F1: L_p column `own` (rows base..base+RPT); B1: G'_p = Diag(g_{s_p}) dkv_{s_p} (the loop already applied
-    // g of every token down to s_p)
+    // F1: L_p; B1: G'_p = Diag(g_{s_p}) dkv_{s_p} (the loop already applied g of every token down to s_p)
     float* dst = a.seg + seg_off;
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) dst[size_t(base + r) * D + own] = st[r];
-    if (part == 0) a.ls[(size_t(bh) * size_t(p.nseg) + size_t(seg)) * size_t(p.D) + own] = run;
+    for (int j = 0; j < OS; ++j)
+#pragma unroll
+      for (int i = 0; i < RS; ++i) dst[sidx(j, i)] = st[j][i];
+    if (tid < D) a.ls[(size_t(bh) * size_t(p.nseg) + size_t(seg)) * size_t(p.D) + tid] = run[0];
   }
 }
 
@@ -360,6 +418,31 @@ cudaError_t launch_d(const GlaArgs& a, cudaStream_t st) {
 }
 
 }  // namespace
+
+int gla_slots_per_sm(int D) {
+  // the fewest co-resident CTAs per SM over the passes (the segment count is common to all of them)
+  auto occ = [](auto kern, size_t smem, int nt) {
+    int n = 0;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, nt, smem) != cudaSuccess) n = 1;
+    return n > 0 ? n : 1;
+  };
+  auto all = [&](auto dtag) {
+    constexpr int DD = decltype(dtag)::value;
+    constexpr int NT = GlaCfg<DD>::NT;
+    int m = occ(gla_kernel<DD, G_F1>, gla_smem_bytes<DD, G_F1>(), NT);
+    m = std::min(m, occ(gla_kernel<DD, G_F3>, gla_smem_bytes<DD, G_F3>(), NT));
+    m = std::min(m, occ(gla_kernel<DD, G_DQ>, gla_smem_bytes<DD, G_DQ>(), NT));
+    m = std::min(m, occ(gla_kernel<DD, G_DK>, gla_smem_bytes<DD, G_DK>(), NT));
+    return m;
+  };
+  static int cache[3] = {0, 0, 0};
+  const int k = D == 32 ? 0 : D == 64 ? 1 : 2;
+  if (cache[k] == 0)
+    cache[k] = D == 32 ? all(std::integral_constant<int, 32>{}) : D == 64 ? all(std::integral_constant<int, 64>{})
+                                                                          : all(std::integral_constant<int, 128>{});
+  return cache[k];
+}
 
 cudaError_t gla_launch_state(const GlaPlan& p, int rev, const float* x, const float* y, const float* lg, float* seg,
                              float* ls, cudaStream_t st) {

@@ -765,17 +765,23 @@ lasp_status_t gla_plan(const lasp_shape_t* s, GlaPlan& g) {
   if (s->kv_heads != 0 && s->kv_heads != s->heads)
     return fail(LASP_ERR_UNSUPPORTED, "generalised decay: kv_heads must equal heads");
   g.B = s->batch; g.C = s->n_local; g.H = s->heads; g.D = s->head_dim;
-  // ~8 items (CTAs) per SM, segments a multiple of the 16-token tile
+  // segments a multiple of the 8-token tile
   const int64_t forced = env_i64("LASP_GLA_SEG_LEN", 0);
   int64_t L;
   if (forced > 0) {
-    L = (forced + 15) / 16 * 16;
+    L = (forced + 7) / 8 * 8;
   } else {
-    const int64_t target = 8 * 148;
-    int64_t nseg = (target + g.B * g.H - 1) / (g.B * g.H);
+    // whole waves: the items (one CTA per (batch, head, segment), each a long sequential recurrence) are sized
+    // to a multiple of the co-resident CTA slots, so no wave runs partly empty (1184 items on 1036 slots ran
+    // as 2 waves)
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t slots = int64_t(sms) * gla_slots_per_sm(int(g.D));
+    const int64_t waves = env_i64("LASP_GLA_WAVES", 1);  // 1 wave measured best (profiles/r2t_gla_waves.txt)
+    int64_t nseg = (waves * slots) / (g.B * g.H);
     if (nseg < 1) nseg = 1;
-    L = g.C > 0 ? ((g.C + nseg - 1) / nseg + 15) / 16 * 16 : 16;
-    if (L < 64) L = 64;
+    L = g.C > 0 ? ((g.C + nseg - 1) / nseg + 7) / 8 * 8 : 8;
+    if (L < 32) L = 32;
   }
   g.seg_len = L;
   g.nseg = g.C > 0 ? (g.C + L - 1) / L : 1;
