@@ -79,7 +79,10 @@ def full(rep, out, key=None):
         traffic = to_bytes(*got["dram__bytes_read.sum"]) + to_bytes(*got["dram__bytes_write.sum"])
         p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
         d = json.load(open(p)) if os.path.exists(p) else {}
-        d[key] = traffic
+        git = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True,
+                             cwd=os.path.dirname(p)).stdout.strip() or None
+        d[key] = {"bytes": traffic, "report": os.path.basename(rep), "git": git,
+                  "note": "dram__bytes_read.sum + dram__bytes_write.sum of one --set full capture (per launch)"}
         json.dump(d, open(p, "w"), indent=1, sort_keys=True)
 
 
