@@ -470,7 +470,8 @@ struct CoreLayout {
   static constexpr uint32_t TC = BOX;                    // [128][64] bf16 (c, u.c, out)
   static constexpr int STAGES = D == 64 ? 3 : 2;
   static constexpr int NSB = D == 64 ? 2 : 1;            // bf16 state copies (double-buffered if smem allows)
-  static constexpr bool HAS_STG = D == 64;               // TMA-staged prefix state (else read directly)
+  static constexpr bool HAS_STG = D == 64;               // TMA-staged prefix state (else read directly); D = 64 only
+  static_assert(!HAS_STG || D == 64, "the STG reader is the head_dim 64 split-state layout");
   static constexpr uint32_t STAGE = 2 * TA + TC;
   static constexpr uint32_t A(int s) { return uint32_t(s) * STAGE; }
   static constexpr uint32_t B_(int s) { return uint32_t(s) * STAGE + TA; }
@@ -992,28 +993,35 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     // Thread d owns row d (key index) of the [DK][64] state slice (TMEM layout of M = DK for dS).
     const uint32_t q4 = warp & 3;
     const int g = int(threadIdx.x) - 256;  // tile row for the u.c scaling
-    const bool valid = L::DK == 128 || lane < 16;
-    const int d = L::DK == 128 ? int(q4 * 32 + lane) : int(q4 * 16 + lane);
-    float S[64];
+    // head_dim 64 (SPLIT): the M = 64 accumulator occupies lanes 0-15 of each quadrant, so each state row is
+    // spread over 4 threads (tcgen05.ld.16x256b): thread (quadrant q4, lane l) holds rows q4 16 + l / 4 + 8 hr
+    // (hr = 0, 1) at columns 8 r + 2 (l % 4) + f (r < 8, f = 0, 1) as S[4 r + 2 hr + f] -- all 32 lanes work,
+    // 32 state values each. head_dim 128: thread q4 32 + l holds row d of the 64-wide value slice, S[64].
+    constexpr bool SPLIT = L::DK == 64;
+    constexpr int NS = SPLIT ? 32 : 64;
+    const int d = int(q4 * 32 + lane);                               // (head_dim 128)
+    const int r0 = int(q4 * 16) + int(lane >> 2), cq = int(lane & 3);  // (SPLIT)
+    auto srow = [&](int i) { return r0 + 8 * ((i >> 1) & 1); };       // SPLIT: row / column of S[i]
+    auto scol = [&](int i) { return 8 * (i >> 2) + 2 * cq + (i & 1); };
+    float S[NS];
     auto load_state = [&](uint32_t k, const CItem& it, bool trans, int state) {
-      if constexpr (L::HAS_STG) {
-        // segment prefix state from STG (TMA, 128B-swizzled fp32 rows of 32 floats): row d of S, or
-        // column d for S^T; both access patterns are (nearly) bank-conflict free
+      if constexpr (SPLIT) {
+        // segment prefix state from STG (TMA, 128B-swizzled fp32 rows of 32 floats)
         mbar_wait(&bar->stg_full, k & 1);
-        if (valid) {
-          if (trans) {
-            const uint32_t x = uint32_t(d) >> 5, c = (uint32_t(d) & 31) >> 2, wd = uint32_t(d) & 3;
 #pragma unroll
-            for (int e = 0; e < D; ++e)
-              S[e] = *reinterpret_cast<const float*>(sm + L::STG + x * (D * 128) + e * 128 + ((c ^ (e & 7)) << 4) + wd * 4);
-          } else {
+        for (int i = 0; i < NS; i += 2) {
+          const uint32_t rr = uint32_t(srow(i)), cc = uint32_t(scol(i));
+          if (trans) {  // S[rr][cc] = stored[cc][rr], [cc][rr + 1]
 #pragma unroll
-            for (int e = 0; e < D; e += 4) {
-              const uint32_t x = uint32_t(e) >> 5, c = (uint32_t(e) & 31) >> 2;
-              const float4 t = *reinterpret_cast<const float4*>(sm + L::STG + x * (D * 128) + d * 128 +
-                                                                ((c ^ (uint32_t(d) & 7)) << 4));
-              S[e] = t.x; S[e + 1] = t.y; S[e + 2] = t.z; S[e + 3] = t.w;
+            for (int f = 0; f < 2; ++f) {
+              const uint32_t e = cc + f, x = rr >> 5, c = (rr & 31) >> 2, wd = rr & 3;
+              S[i + f] = *reinterpret_cast<const float*>(sm + L::STG + x * (D * 128) + e * 128 + ((c ^ (e & 7)) << 4) + wd * 4);
             }
+          } else {
+            const uint32_t x = cc >> 5, c = (cc & 31) >> 2;
+            const float2 t = *reinterpret_cast<const float2*>(sm + L::STG + x * (D * 128) + rr * 128 +
+                                                              ((c ^ (rr & 7)) << 4) + (cc & 3) * 4);
+            S[i] = t.x; S[i + 1] = t.y;
           }
         }
         mbar_arrive(&bar->stg_empty);
@@ -1051,7 +1059,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       }
       if (tag_poisoned(prm.status)) {  // the call's cache tag did not match: every output becomes NaN
 #pragma unroll
-        for (int e = 0; e < 64; ++e) S[e] = __int_as_float(0x7fc00000);
+        for (int e = 0; e < NS; ++e) S[e] = __int_as_float(0x7fc00000);
       }
     };
     uint32_t J = 0, Js = 0, kd = 0, nku = 0;  // J: blocks (state copies), Js: sub-blocks (ring), nku: u.c fills
@@ -1094,7 +1102,18 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
 #ifdef LASP_EXPERIMENT_NOSTATE  // timing experiment only: no state math
         if (false)
 #endif
-        if (valid) {
+        if constexpr (SPLIT) {
+          // one bf16 pair (4 bytes) per (row, 16-byte chunk): the 32 lanes of a store cover 8 rows x one chunk,
+          // distinct banks under the 128B swizzle
+#pragma unroll
+          for (int i = 0; i < NS; i += 2) {
+            const uint32_t hi = pack_bf16(S[i], S[i + 1]);
+            const uint32_t lo = pack_bf16(S[i] - __uint_as_float(hi << 16), S[i + 1] - __uint_as_float(hi & 0xFFFF0000u));
+            const uint32_t off = sw128_off(uint32_t(srow(i)), uint32_t(i >> 2)) + 4u * uint32_t(cq);
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sbase + L::SBF(sb) + off), "r"(hi) : "memory");
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sbase + L::SLO(sb) + off), "r"(lo) : "memory");
+          }
+        } else {
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const float* v = &S[c * 8];
@@ -1126,13 +1145,21 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
 #ifdef LASP_EXPERIMENT_NOSTATE
         if (false)
 #endif
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float v[16];
-          tmem_ld16(td + c * 16, v);
+        if constexpr (SPLIT) {
+          float v[32];
+          tmem_ld_16x256b_x8(td, v);
           tmem_ld_wait();
 #pragma unroll
-          for (int t = 0; t < 16; ++t) S[c * 16 + t] = fmaf(decay, S[c * 16 + t], v[t]);
+          for (int t = 0; t < 32; ++t) S[t] = fmaf(decay, S[t], v[t]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float v[16];
+            tmem_ld16(td + c * 16, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int t = 0; t < 16; ++t) S[c * 16 + t] = fmaf(decay, S[c * 16 + t], v[t]);
+          }
         }
         tc_fence_before();
         mbar_arrive(&bar->ds_empty);
