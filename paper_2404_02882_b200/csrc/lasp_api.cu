@@ -77,7 +77,12 @@ int64_t choose_seg_len(int64_t B, int64_t C, int64_t H, int64_t D) {
   int64_t nseg_t = (target + B * H * nv - 1) / (B * H * nv);
   if (nseg_t < 1) nseg_t = 1;
   if (nseg_t > nb) nseg_t = nb;
-  const int64_t seg_blocks = (nb + nseg_t - 1) / nseg_t;
+  int64_t seg_blocks = (nb + nseg_t - 1) / nseg_t;
+  // short sequences: a segment of one or two blocks spends most of its item on pipeline fill and the fold;
+  // at least 2 blocks (head_dim 64) / 4 blocks (head_dim 128) per segment (sweep profiles/r2x_short.txt: 2K
+  // tokens 16 x 64 40.1 -> 44.3 M tokens/s, 16 x 128 20.9 -> 23.1 M; 32K unaffected: 7 / 11 blocks already)
+  const int64_t min_blocks = env_i64("LASP_MIN_SEG_BLOCKS", nv > 1 ? 4 : 2);
+  if (seg_blocks < min_blocks) seg_blocks = min_blocks < nb ? min_blocks : nb;
   return seg_blocks * q;
 }
 

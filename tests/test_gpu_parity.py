@@ -212,10 +212,12 @@ def test_state_error_on_reused_cache_address(L):
     assert e.value.name == "LASP_ERR_STATE"
 
 
-def test_ragged_multi_segment_rev_store_deterministic(L, oracle_mod):
+def test_ragged_multi_segment_rev_store_deterministic(L, oracle_mod, monkeypatch):
     """with several segments and a ragged rank length, the REV passes' ragged block starts inside
     the previous segment; only the segment's own rows may be stored (else two CTAs race on those rows with
-    differently rounded values). B=1, H=4, D=64, C=1000: 8 segments of 128 tokens with a 104-token tail."""
+    differently rounded values). B=1, H=4, D=64, C=1000: 8 segments of 128 tokens with a 104-token tail
+    (forced: the plan itself now keeps at least 2 blocks per segment at this length)."""
+    monkeypatch.setenv("LASP_SEG_LEN", "128")
     assert L.segment_len(L.api._shape(torch.empty((1, 1000, 4, 64), dtype=torch.bfloat16, device="meta"))) == 128
     p = synth.problem(11, 1, 1000, 4, 64, dtype="bf16")
     runs = [run_sim_ring(L, p, 1, torch.bfloat16, 1000) for _ in range(6)]
