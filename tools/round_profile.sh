@@ -26,3 +26,5 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:l
 timeout 300 python -m pytest tests -m gpu -q > gpurun_out/${tag}_pytest_gpu.txt 2>&1
 timeout 300 python __graft_entry__.py smoke > gpurun_out/${tag}_smoke.txt 2>&1
 ls -la gpurun_out | tail -12
+timeout 600 python bench.py --loopback 4 --steps 10 --warmup 3 --no-e2e > gpurun_out/${tag}_loop4.json 2> gpurun_out/${tag}_loop4.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${tag}_reference.json 2> gpurun_out/${tag}_reference.err
