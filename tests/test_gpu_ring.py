@@ -57,6 +57,20 @@ def test_ring_world1_fp32(ring, oracle_mod):
         assert oracle_mod.normwise_err(x.cpu().numpy(), r) <= 1e-5
 
 
+def test_ring_world1_generalised_decay(ring, oracle_mod):
+    """The NEXT-4 generalised-decay ring entry points (lasp_gla_fwd / lasp_gla_bwd) through the NCCL ctx at world
+    size 1 against the oracle (fp32: 1e-5, decay gradient 1e-4; reading D3)."""
+    t = synth.gla_problem(23, 1, 1500, 2, 64)
+    q, k, v, lg, do = (torch.from_numpy(t[x]).cuda() for x in ("q", "k", "v", "lg", "do"))
+    o, cache = ring.gla_fwd(q, k, v, lg)
+    dq, dk, dv, dlg = ring.gla_bwd(q, k, v, lg, do, cache)
+    torch.cuda.synchronize()
+    refs = [oracle_mod.gla_fwd(t["q"], t["k"], t["v"], t["lg"])] + \
+        list(oracle_mod.gla_bwd(t["q"], t["k"], t["v"], t["lg"], t["do"]))
+    for x, r, tol in zip((o, dq, dk, dv, dlg), refs, (1e-5, 1e-5, 1e-5, 1e-5, 1e-4)):
+        assert oracle_mod.normwise_err(x.cpu().numpy(), r) <= tol
+
+
 def test_ring_graph_capture_matches_eager(ring):
     """The NCCL-ctx entry points (comm stream fork/join, events, memsets) captured into a CUDA graph
     reproduce the eager results bit for bit (include/lasp.h "Graphs")."""
