@@ -34,7 +34,11 @@
 namespace lasp {
 namespace {
 
-constexpr int GT = 8;   // tokens per shared-memory tile (double-buffered with cp.async)
+// tokens per shared-memory tile (double-buffered with cp.async): smaller tiles leave room for more co-resident
+// CTAs, which wins at head_dim <= 64 (same-box sweep, profiles/r3k / r3l: TNL-0.4B shape 4 / 8 / 16 / 32 tokens
+// 16.4 / 14.5 / 12.1 / 8.5 M tokens/s) while head_dim 128 prefers 8 (3.82 / 3.96 / 3.62 / 3.0)
+template <int D>
+constexpr int gla_gt() { return D <= 64 ? 4 : 8; }
 
 // Each thread owns an OSPAN x RSPAN tile of the D x D state: OSPAN output indices (the value column for the
 // F1 / F3 / B1 / dV passes, the key row for dQ / dK) by RSPAN indices of the dimension the outputs reduce over.
@@ -43,10 +47,15 @@ constexpr int GT = 8;   // tokens per shared-memory tile (double-buffered with c
 // granularity (chunk c of thread rg covers indices 4 (c NRED + rg) .. +3), so the partners' vector loads hit
 // consecutive 16-byte words (no bank conflicts). Per token a thread reads 2-3 RSPAN-vectors and one OSPAN-vector from shared memory
 // (warp broadcasts) for 2-3 x 64 FP32 instructions.
+#ifndef LASP_GLA_OS64
+#define LASP_GLA_OS64 4
+#define LASP_GLA_RS64 16
+#endif
 template <int D>
 struct GlaCfg {
-  static constexpr int OSPAN = D == 128 ? 2 : 4;
-  static constexpr int RSPAN = D == 32 ? 8 : D == 64 ? 16 : 32;
+  static constexpr int GT = gla_gt<D>();
+  static constexpr int OSPAN = D == 128 ? 2 : D == 64 ? LASP_GLA_OS64 : 4;
+  static constexpr int RSPAN = D == 32 ? 8 : D == 64 ? LASP_GLA_RS64 : 32;
   static constexpr int NRED = D / RSPAN;                 // 4
   static constexpr int NT = (D / OSPAN) * NRED;          // 32, 64, 256 threads per item
 };
@@ -80,7 +89,7 @@ __device__ __forceinline__ void cp_wait_prev() { asm volatile("cp.async.wait_gro
 template <int D, int NX>
 __device__ __forceinline__ void stage_tile(const GlaPlan& p, int64_t b, int64_t h, int64_t t0, int64_t s0, int64_t s1,
                                            const float* const (&src)[NX], float* buf) {
-  constexpr int NT = GlaCfg<D>::NT, V4 = D / 4;
+  constexpr int NT = GlaCfg<D>::NT, V4 = D / 4, GT = GlaCfg<D>::GT;
 #pragma unroll
   for (int x = 0; x < NX; ++x)
     for (int i = threadIdx.x; i < GT * V4; i += NT) {
@@ -109,13 +118,13 @@ template <> struct GlaTensors<5> { static constexpr int NX = 6, LGX = 3; };  // 
 
 template <int D, int MODE>
 constexpr size_t gla_smem_bytes() {
-  return (2 * size_t(GlaTensors<MODE>::NX) + 1) * GT * D * sizeof(float);
+  return (2 * size_t(GlaTensors<MODE>::NX) + 1) * GlaCfg<D>::GT * D * sizeof(float);
 }
 
 template <int D, int MODE>
 __global__ void __launch_bounds__(GlaCfg<D>::NT) gla_kernel(const GlaArgs a) {
   using Cfg = GlaCfg<D>;
-  constexpr int OS = Cfg::OSPAN, RS = Cfg::RSPAN, NRED = Cfg::NRED;
+  constexpr int OS = Cfg::OSPAN, RS = Cfg::RSPAN, NRED = Cfg::NRED, GT = Cfg::GT;
   constexpr bool REV = MODE == G_B1 || MODE == G_DV || MODE == G_DK;
   constexpr bool ROWS = MODE == G_DQ || MODE == G_DK;  // outputs indexed by the key row (else the value column)
   constexpr int NX = GlaTensors<MODE>::NX, LGX = GlaTensors<MODE>::LGX;
@@ -223,7 +232,7 @@ __global__ void __launch_bounds__(GlaCfg<D>::NT) gla_kernel(const GlaArgs a) {
         rvec(gv, g);
         rvec(kv, T(MODE == G_F1 ? 0 : 1, r));
 #pragma unroll
-        for (int j = 0; j < OS; ++j) vo[j] = T(MODE == G_F1 ? 1 : 2, r)[ob + j];
+        for (int j = 0; j < OS; ++j) vo[j] = T(MODE == G_F1 ? 1 : 2, r)[ob + j];  // (consecutive: vectorized)
 #pragma unroll
         for (int j = 0; j < OS; ++j)
 #pragma unroll
