@@ -10,7 +10,7 @@ bf16, per-head lambda_h = 1 - 2^-(1 + 14h/15). N>1 keeps 32K tokens per GPU (wea
 NCCL KV/dKV ring (one process per GPU, launched by torchrun). Synthetic inputs from synth/ (seeded).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lasp|reference] [--config tnl04b|tnl1b|tnl7b]
-       [--exchange both|ring|allgather] [--sp-size T] [--loopback N] [--tokens C] [--no-graph] [--no-e2e]
+       [--exchange all|both|ring|allgather|p2p] [--sp-size T] [--loopback N] [--tokens C] [--no-graph] [--no-e2e]
        [--no-cpu-baseline]
 
 Before timing, every rank runs one fwd+bwd of constant per-head inputs through the same code path (ring /
@@ -226,7 +226,7 @@ class ThreadComm:
         return m
 
 
-def closed_form_check(lasp, dev, B, C, H, D, lam, rank, T, run, Hk=None):
+def closed_form_check(lasp, dev, B, C, H, D, lam, rank, T, run, Hk=None, sync=None):
     """Self-check of the timed configuration before timing (every rank, every exchange): constant inputs
     q_s = q, k_s = k, v_s = v, do_s = do per head have closed forms derived from Eq. 4 (SURVEY §8(c) pin 5,
     the same forms tests/test_gpu_parity.py checks): with s the GLOBAL 1-based position and N = T*C,
@@ -246,7 +246,7 @@ def closed_form_check(lasp, dev, B, C, H, D, lam, rank, T, run, Hk=None):
     mk = lambda a: torch.from_numpy(np.broadcast_to(a.astype(np.float32), (B, C) + a.shape).copy()).to(
         device=dev, dtype=torch.bfloat16)
     o, dq, dk, dv = run(mk(qv), mk(kv_), mk(vv), mk(dov))
-    torch.cuda.synchronize(dev)
+    (sync or (lambda: torch.cuda.synchronize(dev)))()
     N = T * C
     idx = np.unique(np.clip(np.array([0, 1, 2, 127, 128, 1000, C // 2, C - 2, C - 1]), 0, C - 1))
     s = (rank * C + idx + 1).astype(np.float64)
@@ -423,6 +423,14 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
     grp_id, grank, _ = lasp.topology(rank, world, T)
     G = world // T
     stream = torch.cuda.current_stream(dev)
+
+    def sync():
+        # loopback ranks are threads sharing one device: a device-wide synchronize from one rank's thread would also
+        # wait for the other ranks' streams, which the P2P exchange's device-side waits make mutually dependent
+        if loopback:
+            stream.synchronize()
+        else:
+            torch.cuda.synchronize(dev)
     # inputs: this rank's shard [t*C, (t+1)*C) of its group's sequence (seed = group id)
     p = synth.problem(grp_id, B, C * T, H, D, dtype="bf16", token_lo=grank * C, token_hi=(grank + 1) * C,
                       kv_heads=Hk)
@@ -435,8 +443,11 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
     cache, ws = lasp.alloc_cache(q, k), lasp.alloc_workspace(q, k)
     # N > 1: time the paper's ring and the all-gather exchange (NEXT-2) in the same run; `value` is the ring
     if T > 1:
-        exchanges = ["ring", "allgather"] if args.exchange == "both" else [args.exchange]
+        exchanges = {"all": ["ring", "allgather", "p2p"], "both": ["ring", "allgather"]}.get(args.exchange,
+                                                                                            [args.exchange])
         ring = make_ring()
+        if "p2p" in exchanges:  # the ring with each hop one kernel over peer memory (CUDA IPC / NVLink)
+            ring.enable_p2p(B * Hk * D * D)
     else:
         exchanges, ring = ["none"], None
 
@@ -475,13 +486,13 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
                 ring.fwd(a, b, c, lam, o=oo, cache=ccache, workspace=cws)
                 ring.bwd(a, b, c, lam, d, ccache, dq=dd[0], dk=dd[1], dv=dd[2], workspace=cws)
             return [oo] + dd
-        err = closed_form_check(lasp, dev, B, C, H, D, lam, grank, T, run_const, Hk)
+        err = closed_form_check(lasp, dev, B, C, H, D, lam, grank, T, run_const, Hk, sync)
         err = comm.max(err, rank) if loopback else comm.max(err)
         del cws, ccache
         step = step_fn(ex)
         for _ in range(args.warmup):
             step()
-        torch.cuda.synchronize(dev)
+        sync()
         # the step's launches captured once into a CUDA graph (programmatic-dependent-launch edges and the
         # NCCL ring kept), replayed in the timed region: same kernels, no per-launch host work
         graph, graph_launches, graph_note = None, 0, None
@@ -494,18 +505,18 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
                     step()
                 graph_launches = lib.lasp_launch_count() - l0
                 g.replay()
-                torch.cuda.synchronize(dev)
+                sync()
                 graph = g
             except Exception as e:  # noqa: BLE001 - reported in the line
                 graph_note = f"capture failed ({type(e).__name__}: {e}); eager"
-                torch.cuda.synchronize(dev)
+                sync()
 
         def timed_loop(n, profile):
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
             if not loopback or rank == 0:
                 lib.lasp_profile_enable(1 if profile else 0)
             comm.barrier()
-            torch.cuda.synchronize(dev)
+            sync()
             comm.barrier()
             for i in range(n):
                 l2_flush()                       # outside the step events
@@ -515,7 +526,7 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
                 else:
                     step()
                 ev[i][1].record(stream)
-            torch.cuda.synchronize(dev)
+            sync()
             comm.barrier()
             if not loopback or rank == 0:
                 lib.lasp_profile_enable(0)
@@ -604,14 +615,14 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
             stream.wait_stream(s_dn)
 
         e2e_run(2)
-        torch.cuda.synchronize(dev)
+        sync()
         comm.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         s_up.wait_event(e0)
         e2e_run(n_e2e)
         e1.record(stream)
-        torch.cuda.synchronize(dev)
+        sync()
         et = comm.max(e0.elapsed_time(e1))
         e2e = {"value": world * B * C * n_e2e / (et / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e,
@@ -784,9 +795,10 @@ def main():
     ap.add_argument("--sp-size", type=int, default=0,
                     help="sequence-parallel size T (default: all ranks in one ring); G = N/T data-parallel groups "
                          "(Alg. 1 data-sequence hybrid, NEXT-1)")
-    ap.add_argument("--exchange", choices=["both", "ring", "allgather"], default="both",
-                    help="state exchange at N > 1: the paper's ring, one all-gather (NEXT-2), or both (default: each "
-                         "timed in the same run; `value` is the ring's, both are reported under `exchanges`)")
+    ap.add_argument("--exchange", choices=["all", "both", "ring", "allgather", "p2p"], default="all",
+                    help="state exchange at N > 1: the paper's ring over NCCL, one all-gather (NEXT-2), the ring with "
+                         "fused P2P hop kernels (p2p), ring + allgather (both), or all three (default: each timed in "
+                         "the same run; `value` is the NCCL ring's, every one is reported under `exchanges`)")
     ap.add_argument("--loopback", type=int, default=0,
                     help="run N ranks as threads on ONE GPU with the in-process loopback transport (the whole N>1 "
                          "code path incl. the closed-form parity gate; not a scaling measurement)")

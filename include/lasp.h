@@ -192,10 +192,33 @@ lasp_status_t lasp_ctx_create_loopback(int rank, int world, const char* group, i
  *     have received: KV_in(r) = sum_{j<r} lam^(C(r-1-j)) L_j, dKV_in(r) = sum_{j>r} lam^(C(j-r-1)) G_j.
  *     Same results up to fp32 summation order. Each rank's n_local travels with its state, so ranks of
  *     different lengths fold correctly (rank j's contribution is decayed with lam^(C_j)).
- * LASP_ERR_DOMAIN for any other value. */
+ *   LASP_EXCHANGE_P2P: the paper's ring, each hop ONE kernel over peer memory (NVLink): it waits for the
+ *     upstream rank's data flag on this rank's receive buffer, copies KV_in out, and stores
+ *     lam^C KV_in + L_r straight into the downstream rank's receive buffer (combine and send fused), then
+ *     publishes a data flag to the downstream and an ack to the upstream (a sender waits for the ack of its
+ *     previous message before overwriting). Flags are epoch counters in device memory, so steps can be
+ *     graph-captured and replayed. Needs lasp_ctx_p2p_setup + lasp_ctx_p2p_connect; scalar-decay path only.
+ *     The waits are on the device: with several ranks on ONE device (a loopback ctx, or processes sharing a
+ *     GPU) no rank may block in a device-wide synchronize before the other ranks have submitted their calls
+ *     (synchronize the rank's own stream instead); across GPUs the ranks are independent.
+ * LASP_ERR_DOMAIN for any other value; LASP_ERR_COMM for RING / ALLGATHER on a P2P-only ctx. */
 #define LASP_EXCHANGE_RING 0
 #define LASP_EXCHANGE_ALLGATHER 1
+#define LASP_EXCHANGE_P2P 2
 lasp_status_t lasp_ctx_set_exchange(lasp_ctx_t ctx, int exchange);
+
+/* A ring ctx without NCCL whose only exchange is LASP_EXCHANGE_P2P (peer buffers through CUDA IPC): rank r of
+ * world ranks on `device` (several processes may share one GPU). Destroy with lasp_ctx_destroy. */
+lasp_status_t lasp_ctx_create_p2p(int rank, int world, int device, lasp_ctx_t* out);
+/* Collective P2P setup, step 1 (every rank): allocate this rank's flag / receive block for states of up to
+ * max_state_elems (= batch * kv_heads * head_dim^2; the same value on every rank) and write its CUDA IPC handle
+ * (64 bytes) to `handle`. The caller gathers the world's handles in rank order (e.g. torch.distributed
+ * all_gather_object). LASP_ERR_STATE if already set up. */
+lasp_status_t lasp_ctx_p2p_setup(lasp_ctx_t ctx, size_t max_state_elems, uint8_t handle[64]);
+/* Step 2: open the blocks of ranks r - 1 and r + 1 from `handles` (world x 64 bytes, rank order), or, on a
+ * loopback ctx, handles = NULL: take them from the loopback group (waits up to 120 s for the peers' setup).
+ * LASP_ERR_COMM if a handle cannot be opened. */
+lasp_status_t lasp_ctx_p2p_connect(lasp_ctx_t ctx, const uint8_t* handles);
 
 /* Ring schedule (host-only, no GPU): the peer this rank receives its state from and sends its state to
  * (-1 = none). Forward (backward = 0): from r-1, to r+1 (Alg. 2); backward: from r+1, to r-1

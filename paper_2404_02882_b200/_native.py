@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("LASP_LIB") or os.path.join(HERE, "liblasp.so")  # LAS
 HEADER = os.path.join(os.path.dirname(HERE), "include", "lasp.h")
 
 LASP_BF16, LASP_FP32 = 0, 1
-LASP_EXCHANGE_RING, LASP_EXCHANGE_ALLGATHER = 0, 1
+LASP_EXCHANGE_RING, LASP_EXCHANGE_ALLGATHER, LASP_EXCHANGE_P2P = 0, 1, 2
 STATUS = {0: "LASP_OK", 1: "LASP_ERR_SHAPE", 2: "LASP_ERR_DOMAIN", 3: "LASP_ERR_PARTITION", 4: "LASP_ERR_STATE",
           5: "LASP_ERR_COMM", 6: "LASP_ERR_CUDA", 7: "LASP_ERR_UNSUPPORTED"}
 
@@ -57,6 +57,9 @@ _SIGS = {
                                  ctypes.c_int),
     "lasp_ctx_destroy": ([_vp], ctypes.c_int),
     "lasp_ctx_set_exchange": ([_vp, ctypes.c_int], ctypes.c_int),
+    "lasp_ctx_create_p2p": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)], ctypes.c_int),
+    "lasp_ctx_p2p_setup": ([_vp, ctypes.c_size_t, ctypes.c_char_p], ctypes.c_int),
+    "lasp_ctx_p2p_connect": ([_vp, ctypes.c_char_p], ctypes.c_int),
     "lasp_ctx_protocol": ([_vp, _sp, _i64p, _i64p, _i64p], ctypes.c_int),
     "lasp_ring_peers": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                          ctypes.POINTER(ctypes.c_int)], ctypes.c_int),

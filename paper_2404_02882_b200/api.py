@@ -225,6 +225,7 @@ class Ring:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self._group = group
         idbuf = ctypes.create_string_buffer(128)
         if self.rank == 0:
             N.check(N.lib().lasp_unique_id(idbuf))
@@ -242,16 +243,50 @@ class Ring:
         self.rank, self.world = rank, world
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self._ctx = ctypes.c_void_p()
+        self._loopback = True
         N.check(N.lib().lasp_ctx_create_loopback(rank, world, group.encode(), self.device.index or 0,
                                                  ctypes.byref(self._ctx)))
         return self
 
     def set_exchange(self, exchange: str) -> "Ring":
-        """'ring' (the paper's T-1 hops, default) or 'allgather' (one all-gather of the local states plus a
-        local fold)."""
-        mode = {"ring": N.LASP_EXCHANGE_RING, "allgather": N.LASP_EXCHANGE_ALLGATHER}[exchange]
+        """'ring' (the paper's T-1 hops, default), 'allgather' (one all-gather of the local states plus a
+        local fold) or 'p2p' (the ring with each hop one kernel over peer memory; needs
+        enable_p2p first)."""
+        mode = {"ring": N.LASP_EXCHANGE_RING, "allgather": N.LASP_EXCHANGE_ALLGATHER,
+                "p2p": N.LASP_EXCHANGE_P2P}[exchange]
         N.check(N.lib().lasp_ctx_set_exchange(self._ctx, mode))
         return self
+
+    def enable_p2p(self, max_state_elems: int, group=None) -> "Ring":
+        """Set up the P2P exchange (include/lasp.h lasp_ctx_p2p_setup / _connect): every rank allocates its flag /
+        receive block for states of up to max_state_elems (batch * kv_heads * head_dim^2, the same on every
+        rank); the CUDA IPC handles are exchanged with torch.distributed (all_gather_object over ``group``), or
+        inside a loopback group without it. Selects the 'p2p' exchange."""
+        h = ctypes.create_string_buffer(64)
+        N.check(N.lib().lasp_ctx_p2p_setup(self._ctx, int(max_state_elems), h))
+        if getattr(self, "_loopback", False):
+            N.check(N.lib().lasp_ctx_p2p_connect(self._ctx, None))
+        else:
+            import torch.distributed as dist
+            allh = [None] * self.world
+            dist.all_gather_object(allh, h.raw, group=group if group is not None else getattr(self, "_group", None))
+            N.check(N.lib().lasp_ctx_p2p_connect(self._ctx, b"".join(allh)))
+        self._p2p = True
+        return self.set_exchange("p2p")
+
+    @classmethod
+    def p2p_only(cls, max_state_elems: int, device=None, group=None) -> "Ring":
+        """A ring over the torch.distributed world (or ``group``) WITHOUT NCCL: the P2P exchange only (CUDA IPC
+        peer buffers; several processes may share one GPU, which NCCL refuses)."""
+        import torch.distributed as dist
+        self = cls.__new__(cls)
+        self.rank = dist.get_rank(group) if group is not None else dist.get_rank()
+        self.world = dist.get_world_size(group) if group is not None else dist.get_world_size()
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self._group = group
+        self._ctx = ctypes.c_void_p()
+        N.check(N.lib().lasp_ctx_create_p2p(self.rank, self.world, self.device.index or 0, ctypes.byref(self._ctx)))
+        return self.enable_p2p(max_state_elems, group)
 
     def close(self):
         if self._ctx:

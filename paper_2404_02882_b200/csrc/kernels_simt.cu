@@ -404,6 +404,72 @@ cudaError_t launch_tag(const CacheTag& t, uint64_t* hdr, unsigned check_mask, un
   return launch_k(tag_kernel, dim3(1), dim3(32), 0, st, t, hdr, check_mask, ctrl);
 }
 
+// ---- P2P exchange (LASP_EXCHANGE_P2P): the ring hop as ONE kernel over peer memory -------------------------
+// Rank r's hop in direction dir (0: forward, KV from r-1 to r+1; 1: backward, dKV from r+1 to r-1):
+//   e = my epoch + 1; wait until the upstream has put epoch e into my receive buffer (flag, acquire.sys);
+//   copy it to the rank's private KV_in (the fold reads that); wait until the downstream has copied my previous
+//   message (ack >= e - 1); store lam^C KV_in + local straight into the downstream rank's receive buffer
+//   (NVLink stores to peer memory: combine and send fused); the last CTA then publishes the data flag to the
+//   downstream (release.sys), the ack to the upstream, and my epoch. Epochs live in device memory, so the launch
+//   can be captured into a CUDA graph and replayed. Flag words: [dir] data epoch, [2 + dir] ack, [4 + dir] my
+//   epoch, [6 + dir] CTA-done counter. A small grid (kP2PCtas) keeps the spinning CTAs off most SMs.
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* a) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* a, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ void spin_until_ge(const uint64_t* a, uint64_t target) {
+  uint32_t n = 0;
+  while (ld_acquire_sys(a) < target) {
+    __nanosleep(128);
+    if (++n == (1u << 28)) __trap();  // a peer that never arrives: fail loudly instead of hanging
+  }
+}
+
+__global__ void p2p_hop_kernel(Plan p, P2PHop h) {
+  // no early trigger: the next kernel (a persistent core launch holding whole SMs) must not start while this
+  // one waits for a peer -- with several ranks on one device its CTAs would starve the peer's kernels
+  pdl_wait();
+  const int dir = h.dir;
+  __shared__ uint64_t e_s;
+  if (threadIdx.x == 0) {
+    const uint64_t e = *reinterpret_cast<volatile uint64_t*>(&h.my_flags[4 + dir]) + 1;
+    if (h.has_up) spin_until_ge(&h.my_flags[dir], e);
+    if (h.peer_recv != nullptr) spin_until_ge(&h.my_flags[2 + dir], e - 1);
+    e_s = e;
+  }
+  __syncthreads();
+  const uint64_t e = e_s;
+  const int64_t DD = p.D * p.D;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < h.n; idx += int64_t(gridDim.x) * blockDim.x) {
+    const float in = h.has_up ? __ldcg(h.my_recv + idx) : 0.f;
+    h.in_priv[idx] = in;
+    if (h.peer_recv != nullptr) {
+      const int64_t hd = (idx / DD) % p.Hk;
+      h.peer_recv[idx] = fmaf(powk(p.lam[hd], double(p.C)), in, h.local[idx]);
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long done = atomicAdd(reinterpret_cast<unsigned long long*>(&h.my_flags[6 + dir]), 1ull) + 1ull;
+    if (done == gridDim.x) {  // every CTA's copies and peer stores are fenced
+      __threadfence_system();
+      if (h.has_up) st_release_sys(&h.up_flags[2 + dir], e);      // ack: epoch e has been copied
+      if (h.peer_recv != nullptr) st_release_sys(&h.peer_flags[dir], e);
+      h.my_flags[6 + dir] = 0;
+      st_release_sys(&h.my_flags[4 + dir], e);
+    }
+  }
+}
+
+cudaError_t launch_p2p_hop(const Plan& p, const P2PHop& h, cudaStream_t st) {
+  return launch_k(p2p_hop_kernel, dim3(kP2PCtas), dim3(256), 0, st, p, h);
+}
+
 cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local, float* kv_out, cudaStream_t st) {
   const int64_t n = p.B * p.Hk * p.D * p.D;
   const int threads = 256;

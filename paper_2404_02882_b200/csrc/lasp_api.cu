@@ -543,6 +543,7 @@ struct LoopGroup {
   std::mutex mu;
   std::condition_variable cv;
   std::map<std::pair<int, int>, std::deque<LoopMsg>> q;  // (src, dst) -> messages in send order
+  std::map<int, char*> p2p;                                // P2P exchange: rank -> its flag / buffer block
 };
 std::mutex g_loop_mu;
 std::unordered_map<std::string, std::weak_ptr<LoopGroup>> g_loops;
@@ -569,6 +570,13 @@ struct lasp_ctx {
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
   float* gather = nullptr;  // all-gather exchange: [world + 1][B*H*D*D + 64] fp32 (ctx-owned, grown on demand)
   size_t gather_elems = 0;
+  // P2P exchange: this rank's block [8 flag words | pad to 256 B | recv fwd (p2p_elems) | recv bwd], and the
+  // blocks of ranks r - 1 and r + 1 (opened CUDA IPC handles, or the loopback group's pointers)
+  char* p2p = nullptr;
+  size_t p2p_elems = 0;
+  char* p2p_prev = nullptr;
+  char* p2p_next = nullptr;
+  bool p2p_ipc = false;  // the peer pointers are opened IPC handles (closed on destroy)
 };
 
 namespace {
@@ -654,6 +662,32 @@ lasp_status_t exchange_allgather(lasp_ctx* c, const Plan& p, const float* local,
              ? LASP_OK : cuda_fail(cudaGetLastError(), "fold_ranks");
 }
 
+// P2P exchange (LASP_EXCHANGE_P2P): the ring hop as one kernel that receives (flag wait on this rank's buffer),
+// combines and stores the result into the downstream rank's buffer over peer memory (kernels_simt.cu).
+size_t p2p_off_recv(const lasp_ctx* c, int dir) { return 256 + size_t(dir) * align256(c->p2p_elems * 4); }
+lasp_status_t p2p_hop(lasp_ctx* c, const Plan& p, const float* local, float* in, bool backward, cudaStream_t st) {
+  const size_t n = state_elems(p);
+  if (!c->p2p || (c->world > 1 && !c->p2p_prev && !c->p2p_next))
+    return fail(LASP_ERR_COMM, "P2P exchange: lasp_ctx_p2p_setup / lasp_ctx_p2p_connect not done");
+  if (n > c->p2p_elems) return fail(LASP_ERR_SHAPE, "P2P exchange: state larger than the setup's max_state_elems");
+  const int dir = backward ? 1 : 0;
+  char* up = backward ? c->p2p_next : c->p2p_prev;     // the rank this one receives from
+  char* down = backward ? c->p2p_prev : c->p2p_next;   // the rank this one sends to
+  P2PHop h{};
+  h.local = local;
+  h.in_priv = in;
+  h.my_recv = reinterpret_cast<const float*>(c->p2p + p2p_off_recv(c, dir));
+  h.my_flags = reinterpret_cast<uint64_t*>(c->p2p);
+  h.peer_recv = down ? reinterpret_cast<float*>(down + p2p_off_recv(c, dir)) : nullptr;
+  h.peer_flags = down ? reinterpret_cast<uint64_t*>(down) : nullptr;
+  h.up_flags = up ? reinterpret_cast<uint64_t*>(up) : nullptr;
+  h.has_up = up != nullptr;
+  h.dir = dir;
+  h.n = int64_t(n);
+  LASP_CUDA(staged(backward ? "p2p_hop_bwd" : "p2p_hop_fwd", st, [&] { return launch_p2p_hop(p, h, st); }));
+  return LASP_OK;
+}
+
 // Alg. 2 for one rank after validation. c == nullptr: the communication-free local path (kv_in given, kv_out
 // optional); otherwise the ring / all-gather of ctx c (KV_in received). norm: the Norm epilogue (NEXT-3).
 lasp_status_t fwd_body(lasp_ctx* c, const Plan& p, const void* q, const void* k, const void* v, const float* kv_in,
@@ -670,7 +704,9 @@ lasp_status_t fwd_body(lasp_ctx* c, const Plan& p, const void* q, const void* k,
   lasp_ring_peers(c->rank, c->world, 0, &from, &to);
   LASP_CUDA(prefix(p, Dir::FWD, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
   ProfSpan hop("exchange_fwd", st);
-  if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
+  if (c->exchange == LASP_EXCHANGE_P2P) {
+    if ((s = p2p_hop(c, p, w.local, w.in, false, st)) != LASP_OK) return s;
+  } else if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
     if ((s = exchange_allgather(c, p, w.local, w.in, false, st)) != LASP_OK) return s;
   } else {
     // F2 ring hop: Recv KV_in from r-1 (Alg. 2), combine, Send to r+1
@@ -725,14 +761,16 @@ lasp_status_t bwd_body(lasp_ctx* c, const Plan& p, const void* q, const void* k,
   int from = -1, to = -1;
   lasp_ring_peers(c->rank, c->world, 1, &from, &to);
   const bool hop_pending = c->world > 1;  // a receive, send or all-gather runs on the comm stream under dQ
-  if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
+  if (c->exchange == LASP_EXCHANGE_P2P) {
+    if ((s = p2p_hop(c, p, w.local, w.in, true, c->comm_stream)) != LASP_OK) return s;
+  } else if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
     if ((s = exchange_allgather(c, p, w.local, w.in, true, c->comm_stream)) != LASP_OK) return s;
   } else if (from >= 0) {
     if ((s = ring_recv(c, w.in, n, from, c->comm_stream, "ncclRecv(dKV)")) != LASP_OK) return s;
   } else {
     LASP_CUDA(cudaMemsetAsync(w.in, 0, n * sizeof(float), c->comm_stream));
   }
-  if (to >= 0 && c->exchange != LASP_EXCHANGE_ALLGATHER) {
+  if (to >= 0 && c->exchange == LASP_EXCHANGE_RING) {
     LASP_CUDA(combine(p, w.in, w.local, w.out, c->comm_stream));
     if ((s = ring_send(c, w.out, n, to, c->comm_stream, "ncclSend(dKV)")) != LASP_OK) return s;
   }
@@ -860,6 +898,8 @@ lasp_status_t gla_check(const GlaPlan& g, std::initializer_list<const void*> seq
 // message for the next rank: KV_out = Diag(prod_t g_t) KV_in + L_rank; dKV_out = G'_rank + Diag(...) dKV_in),
 // send, then the per-token passes.
 lasp_status_t gla_hop_in(lasp_ctx* c, const GlaPlan& g, float* in, bool backward, cudaStream_t st) {
+  if (c->exchange == LASP_EXCHANGE_P2P || (!c->comm && !c->loop))
+    return fail(LASP_ERR_UNSUPPORTED, "generalised decay: the ring exchange only (the P2P hop applies a scalar decay)");
   int from = -1, to = -1;
   lasp_ring_peers(c->rank, c->world, backward ? 1 : 0, &from, &to);
   const size_t n = gla_state_elems(g);
@@ -1076,15 +1116,98 @@ lasp_status_t lasp_ctx_create_loopback(int rank, int world, const char* group, i
 
 lasp_status_t lasp_ctx_set_exchange(lasp_ctx_t c, int exchange) {
   if (!c) return fail(LASP_ERR_SHAPE, "ctx is NULL");
-  if (exchange != LASP_EXCHANGE_RING && exchange != LASP_EXCHANGE_ALLGATHER)
-    return fail(LASP_ERR_DOMAIN, "exchange must be LASP_EXCHANGE_RING or LASP_EXCHANGE_ALLGATHER");
+  if (exchange != LASP_EXCHANGE_RING && exchange != LASP_EXCHANGE_ALLGATHER && exchange != LASP_EXCHANGE_P2P)
+    return fail(LASP_ERR_DOMAIN, "exchange must be LASP_EXCHANGE_RING, _ALLGATHER or _P2P");
+  if (exchange != LASP_EXCHANGE_P2P && !c->comm && !c->loop)
+    return fail(LASP_ERR_COMM, "a P2P-only ctx (lasp_ctx_create_p2p) supports only LASP_EXCHANGE_P2P");
   c->exchange = exchange;
+  return LASP_OK;
+}
+
+lasp_status_t lasp_ctx_create_p2p(int rank, int world, int device, lasp_ctx_t* out) {
+  if (!out) return fail(LASP_ERR_SHAPE, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(LASP_ERR_PARTITION, "rank outside [0, world)");
+  LASP_CUDA(cudaSetDevice(device));
+  lasp_ctx* c = new lasp_ctx;
+  c->rank = rank; c->world = world; c->device = device;
+  c->exchange = LASP_EXCHANGE_P2P;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming);
+  if (e != cudaSuccess) { delete c; return cuda_fail(e, "ctx stream/event"); }
+  *out = c;
+  return LASP_OK;
+}
+
+lasp_status_t lasp_ctx_p2p_setup(lasp_ctx_t c, size_t max_state_elems, uint8_t handle[64]) {
+  if (!c || !handle || max_state_elems == 0) return fail(LASP_ERR_SHAPE, "NULL ctx / handle or zero size");
+  if (c->p2p) return fail(LASP_ERR_STATE, "P2P exchange already set up on this ctx");
+  LASP_CUDA(cudaSetDevice(c->device));
+  c->p2p_elems = max_state_elems;
+  const size_t bytes = 256 + 2 * align256(max_state_elems * 4);
+  LASP_CUDA(cudaMalloc(&c->p2p, bytes));
+  LASP_CUDA(cudaMemset(c->p2p, 0, 256));  // epochs, acks and counters start at 0 on every rank
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  LASP_CUDA(cudaIpcGetMemHandle(&h, c->p2p));
+  std::memcpy(handle, &h, 64);
+  if (c->loop) {
+    {
+      std::lock_guard<std::mutex> g(c->loop->mu);
+      c->loop->p2p[c->rank] = c->p2p;
+    }
+    c->loop->cv.notify_all();
+  }
+  return LASP_OK;
+}
+
+lasp_status_t lasp_ctx_p2p_connect(lasp_ctx_t c, const uint8_t* handles) {
+  if (!c || !c->p2p) return fail(LASP_ERR_STATE, "lasp_ctx_p2p_setup first");
+  LASP_CUDA(cudaSetDevice(c->device));
+  auto open = [&](int peer, char** dst) -> lasp_status_t {
+    if (peer < 0 || peer >= c->world) return LASP_OK;
+    if (handles == nullptr) {  // loopback group: the ranks are threads of this process
+      if (!c->loop) return fail(LASP_ERR_SHAPE, "handles NULL outside a loopback group");
+      std::unique_lock<std::mutex> g(c->loop->mu);
+      if (!c->loop->cv.wait_for(g, std::chrono::seconds(120), [&] { return c->loop->p2p.count(peer) != 0; }))
+        return fail(LASP_ERR_COMM, "P2P connect: loopback peer never set up");
+      *dst = c->loop->p2p[peer];
+      return LASP_OK;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + size_t(peer) * 64, 64);
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      char b[160];
+      std::snprintf(b, sizeof b, "cudaIpcOpenMemHandle(rank %d) on rank %d: %s", peer, c->rank, cudaGetErrorString(e));
+      return fail(LASP_ERR_COMM, b);
+    }
+    *dst = static_cast<char*>(ptr);
+    c->p2p_ipc = true;
+    return LASP_OK;
+  };
+  if (c->loop) c->loop->cv.notify_all();
+  lasp_status_t s;
+  if ((s = open(c->rank - 1, &c->p2p_prev)) != LASP_OK) return s;
+  if ((s = open(c->rank + 1, &c->p2p_next)) != LASP_OK) return s;
   return LASP_OK;
 }
 
 lasp_status_t lasp_ctx_destroy(lasp_ctx_t c) {
   if (!c) return LASP_OK;
   if (c->gather) cudaFree(c->gather);
+  if (c->p2p_ipc) {
+    if (c->p2p_prev) cudaIpcCloseMemHandle(c->p2p_prev);
+    if (c->p2p_next) cudaIpcCloseMemHandle(c->p2p_next);
+  }
+  if (c->p2p) {
+    if (c->loop) {
+      std::lock_guard<std::mutex> g(c->loop->mu);
+      c->loop->p2p.erase(c->rank);
+    }
+    cudaFree(c->p2p);
+  }
   if (c->comm) nccl().CommDestroy(c->comm);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_done) cudaEventDestroy(c->ev_done);

@@ -146,6 +146,21 @@ cudaError_t launch_fold_ranks(const Plan& p, const float* gathered, int64_t stri
                               float* out, cudaStream_t st);
 cudaError_t launch_combine(const Plan& p, const float* kv_in, const float* local, float* kv_out,
                            cudaStream_t st);
+// P2P exchange hop (kernels_simt.cu p2p_hop_kernel): flags and buffers as in the kernel's comment
+constexpr int kP2PCtas = 16;
+struct P2PHop {
+  const float* local;     // this rank's local state (L_r or G_r), n floats
+  float* in_priv;         // out: the received state (KV_in / dKV_in), n floats (workspace)
+  const float* my_recv;   // this rank's receive buffer for dir (written by the upstream rank)
+  uint64_t* my_flags;     // this rank's 8 flag words
+  float* peer_recv;       // the downstream rank's receive buffer for dir (peer memory), nullptr: no downstream
+  uint64_t* peer_flags;   // the downstream rank's flag words
+  uint64_t* up_flags;     // the upstream rank's flag words (ack), when has_up
+  int has_up;             // an upstream rank exists (else KV_in = 0)
+  int dir;                // 0 forward, 1 backward
+  int64_t n;
+};
+cudaError_t launch_p2p_hop(const Plan& p, const P2PHop& h, cudaStream_t st);
 
 // Segment-prefix fold (F2 / B2, same arithmetic as prefix_kernel) run by a core launch before its main
 // loop: the 256 state + epilogue threads of each CTA claim chunks of elements (gbar[0]) and fold them;

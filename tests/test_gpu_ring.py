@@ -109,9 +109,10 @@ def test_ring_cache_tag_checks_rank(ring):
 
 
 # ---- world > 1 on one GPU: the same lasp_fwd / lasp_bwd code with the in-process loopback transport ----
-def _run_loopback(p, world, n_global, dtype, group, exchange="ring", bounds=None):
+def _run_loopback(p, world, n_global, dtype, group, exchange="ring", bounds=None, steps=1):
     """Each rank is a thread with its own CUDA stream and ring context; returns the gathered outputs.
-    ``bounds``: per-rank token ranges (default: equal shares C = N/T)."""
+    ``bounds``: per-rank token ranges (default: equal shares C = N/T). ``steps``: fwd + bwd repeated (the P2P
+    exchange's epoch flags and acks advance every step); the outputs of every step must be identical."""
     import threading
     import paper_2404_02882_b200 as lasp
     C = n_global // world
@@ -123,14 +124,26 @@ def _run_loopback(p, world, n_global, dtype, group, exchange="ring", bounds=None
         ring = None
         try:
             torch.cuda.set_device(0)
-            ring = lasp.Ring.loopback(r, world, group).set_exchange(exchange)
+            ring = lasp.Ring.loopback(r, world, group)
+            if exchange == "p2p":
+                kk = p["k"]
+                ring.enable_p2p(kk.shape[0] * kk.shape[2] * kk.shape[3] ** 2)
+            else:
+                ring.set_exchange(exchange)
             stream = torch.cuda.Stream()
             with torch.cuda.stream(stream):
                 sl = slice(*bounds[r])
                 q, k, v, do = (torch.from_numpy(np.ascontiguousarray(p[x][:, sl])).cuda().to(dtype)
                                for x in ("q", "k", "v", "do"))
-                o, cache = ring.fwd(q, k, v, p["lam"])
-                dq, dk, dv = ring.bwd(q, k, v, p["lam"], do, cache)
+                first = None
+                for _ in range(steps):
+                    o, cache = ring.fwd(q, k, v, p["lam"])
+                    dq, dk, dv = ring.bwd(q, k, v, p["lam"], do, cache)
+                    if first is None:
+                        first = [t.clone() for t in (o, dq, dk, dv)]
+                    else:
+                        for a_, b_ in zip(first, (o, dq, dk, dv)):
+                            assert torch.equal(a_, b_), "a later step differs from the first"
             stream.synchronize()
             B, Cr, H, D = k.shape   # states are per kv-head
             seg = lasp.segment_len(lasp.api._shape(q, k))
@@ -159,14 +172,15 @@ def _run_loopback(p, world, n_global, dtype, group, exchange="ring", bounds=None
     return [np.concatenate([out[r][i] for r in range(world)], axis=1) for i in range(4)], [o[4] for o in out]
 
 
-@pytest.mark.parametrize("exchange", ["ring", "allgather"])
+@pytest.mark.parametrize("exchange", ["ring", "allgather", "p2p"])
 @pytest.mark.parametrize("world", [2, 3, 4])
 def test_loopback_ring_bf16_matches_oracle(oracle_mod, world, exchange):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     N = 768 * world
     p = synth.problem(40 + world, 1, N, 4, 64, dtype="bf16")
-    got, _ = _run_loopback(p, world, N, torch.bfloat16, f"bf16-w{world}-{exchange}", exchange)
+    got, _ = _run_loopback(p, world, N, torch.bfloat16, f"bf16-w{world}-{exchange}", exchange,
+                           steps=3 if exchange == "p2p" else 1)
     refs = [oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])] + \
         list(oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"]))
     for x, r in zip(got, refs):
@@ -269,3 +283,54 @@ def test_ring_fused_fold_matches_separate_kernel(tmp_path):
         res[off] = np.load(dst)
     for key in res["0"].files:
         assert np.array_equal(res["0"][key], res["1"][key]), key
+
+
+# ---- the P2P exchange across PROCESSES (CUDA IPC peer buffers; two processes share GPU 0) -----------------
+def _p2p_proc(rank, world, port, N, errq):
+    try:
+        import torch.distributed as dist
+        import paper_2404_02882_b200 as lasp
+        import oracle
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        p = synth.problem(77, 1, N, 4, 64, dtype="bf16")
+        C = N // world
+        sl = slice(rank * C, (rank + 1) * C)
+        q, k, v, do = (torch.from_numpy(np.ascontiguousarray(p[x][:, sl])).cuda().to(torch.bfloat16)
+                       for x in ("q", "k", "v", "do"))
+        ring = lasp.Ring.p2p_only(1 * 4 * 64 * 64)
+        refs = [oracle.fwd(p["q"], p["k"], p["v"], p["lam"])] + list(oracle.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"]))
+        for step in range(3):
+            o, cache = ring.fwd(q, k, v, p["lam"])
+            dq, dk, dv = ring.bwd(q, k, v, p["lam"], do, cache)
+            torch.cuda.synchronize()
+            for x, r in zip((o, dq, dk, dv), refs):
+                err = oracle.normwise_err(x.float().cpu().numpy(), r[:, sl])
+                assert err <= 2e-2, (rank, step, err)
+        dist.barrier()
+        ring.close()
+        dist.destroy_process_group()
+    except BaseException as e:  # noqa: BLE001
+        errq.put(f"rank {rank}: {type(e).__name__}: {e}")
+
+
+def test_p2p_exchange_two_processes_one_gpu():
+    """lasp_fwd / lasp_bwd with the P2P exchange between two PROCESSES sharing GPU 0 through CUDA IPC handles
+    (the code path multi-GPU ranks take; NCCL refuses two ranks on one device, the P2P transport does not):
+    three steps (epoch flags and acks advancing) against the oracle on each rank's shard."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    ctx = mp.get_context("spawn")
+    errq = ctx.Queue()
+    procs = [ctx.Process(target=_p2p_proc, args=(r, 2, port, 2048, errq)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=600)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, errs
+    assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
