@@ -441,13 +441,24 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
     o, dq = torch.empty_like(q), torch.empty_like(q)
     dk, dv = torch.empty_like(k), torch.empty_like(v)
     cache, ws = lasp.alloc_cache(q, k), lasp.alloc_workspace(q, k)
+    p2p_skipped = None
     # N > 1: time the paper's ring and the all-gather exchange (NEXT-2) in the same run; `value` is the ring
     if T > 1:
         exchanges = {"all": ["ring", "allgather", "p2p"], "both": ["ring", "allgather"]}.get(args.exchange,
                                                                                             [args.exchange])
         ring = make_ring()
         if "p2p" in exchanges:  # the ring with each hop one kernel over peer memory (CUDA IPC / NVLink)
-            ring.enable_p2p(B * Hk * D * D)
+            ok, p2p_note = 1.0, "a peer rank failed to set up"
+            try:
+                ring.enable_p2p(B * Hk * D * D)
+            except Exception as e:  # noqa: BLE001 - e.g. no CUDA IPC between these processes: reported, not fatal
+                ok = 0.0
+                p2p_note = f"{type(e).__name__}: {e}"
+            ok = -(comm.max(-ok, rank) if loopback else comm.max(-ok))  # every rank must have connected
+            if ok < 1.0:
+                exchanges = [x for x in exchanges if x != "p2p"]
+                ring.set_exchange("ring")
+                p2p_skipped = p2p_note
     else:
         exchanges, ring = ["none"], None
 
@@ -721,6 +732,8 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
             "path": path, "cpu_baseline": cpu, "layer": layer, "gla": gla}
     if T > 1:
         line["exchanges"] = ex_report
+        if p2p_skipped:
+            line["exchanges_skipped"] = {"p2p": p2p_skipped}
     else:
         line["parity_max_err"] = ex_report[main_ex]["parity_max_err"]
     if loopback:
