@@ -184,22 +184,25 @@ def cpu_baseline(H, D, C, desc):
 
 # ----------------------------------------------------------------------------------------------------
 class TorchComm:
-    """Barrier / max-over-ranks for one process per GPU (torch.distributed over NCCL)."""
+    """Barrier / max-over-ranks for one process per GPU (torch.distributed over NCCL; gloo with --transport p2p)."""
 
-    def __init__(self, world, dev):
-        self.world, self.dev = world, dev
+    def __init__(self, world, dev, gloo=False):
+        self.world, self.dev, self.gloo = world, dev, gloo
 
     def barrier(self):
         if self.world > 1:
             import torch.distributed as dist
-            dist.barrier(device_ids=[self.dev.index])
+            if self.gloo:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[self.dev.index])
 
     def max(self, x):
         if self.world == 1:
             return float(x)
         import torch
         import torch.distributed as dist
-        t = torch.tensor([float(x)], dtype=torch.float64, device=self.dev)
+        t = torch.tensor([float(x)], dtype=torch.float64, device="cpu" if self.gloo else self.dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -401,7 +404,7 @@ def cpu_info():
     return os.cpu_count() or 1, model
 
 
-def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
+def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False, shared_device=False):
     """One rank's measurement (returns the JSON line on rank 0, None elsewhere)."""
     import ctypes
 
@@ -427,7 +430,7 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
     def sync():
         # loopback ranks are threads sharing one device: a device-wide synchronize from one rank's thread would also
         # wait for the other ranks' streams, which the P2P exchange's device-side waits make mutually dependent
-        if loopback:
+        if loopback or shared_device:
             stream.synchronize()
         else:
             torch.cuda.synchronize(dev)
@@ -447,7 +450,7 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False):
         exchanges = {"all": ["ring", "allgather", "p2p"], "both": ["ring", "allgather"]}.get(args.exchange,
                                                                                             [args.exchange])
         ring = make_ring()
-        if "p2p" in exchanges:  # the ring with each hop one kernel over peer memory (CUDA IPC / NVLink)
+        if "p2p" in exchanges and not getattr(ring, "_p2p", False):  # the ring, each hop one kernel over peer memory
             ok, p2p_note = 1.0, "a peer rank failed to set up"
             try:
                 ring.enable_p2p(B * Hk * D * D)
@@ -778,16 +781,35 @@ def run_lasp(args):
     world, rank, local = dist_env()
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    p2p_only = args.transport == "p2p"
+    # --transport p2p: no NCCL (gloo for the host-side barriers, the P2P exchange over CUDA IPC), so several ranks
+    # may share one GPU (local rank modulo the visible devices): the multi-process path on a one-GPU lease
+    local_dev = local % torch.cuda.device_count() if p2p_only else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if p2p_only:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     import paper_2404_02882_b200 as lasp
     T = args.sp_size or world
     group = None
     if 1 < T < world:
         group = lasp.sp_group(T)
-    line = rank_bench(args, rank, world, dev, TorchComm(world, dev), lambda: lasp.Ring(dev, group=group))
+    if p2p_only:
+        H_, D_ = CONFIGS[args.config][:2]
+        n_state = (args.kv_heads or H_) * D_ * D_
+        args.exchange = "p2p"
+        make_ring = lambda: lasp.Ring.p2p_only(n_state, dev, group=group)  # noqa: E731
+    else:
+        make_ring = lambda: lasp.Ring(dev, group=group)  # noqa: E731
+    line = rank_bench(args, rank, world, dev, TorchComm(world, dev, gloo=p2p_only), make_ring,
+                      shared_device=p2p_only and world > torch.cuda.device_count())
+    if line is not None and p2p_only:
+        line["transport"] = "p2p-only ctx (no NCCL; CUDA IPC), " + (
+            f"{world} processes sharing {torch.cuda.device_count()} GPU(s): checks the multi-process path, not a "
+            "scaling number" if world > torch.cuda.device_count() else "one process per GPU")
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -820,6 +842,9 @@ def main():
                     help="grouped-query attention: key/value heads (default: the config's heads, i.e. multi-head)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-layer", action="store_true", help="skip the NEXT-3 whole-layer line")
+    ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
+                    help="N > 1 ring context: NCCL (default) or a P2P-only context without NCCL (CUDA IPC; ranks may "
+                         "share a GPU)")
     ap.add_argument("--no-gla", action="store_true", help="skip the NEXT-4 generalised-decay line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
