@@ -1081,7 +1081,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           ++nku;
         }
         mbar_wait(&bar->full[s], (JJ / ST) & 1);
-#ifdef LASP_EXPERIMENT_NOSTATE
+#if defined(LASP_EXPERIMENT_NOSTATE) || defined(LASP_EXPERIMENT_NOUC)
         if (false)
 #endif
 #pragma unroll
@@ -1099,7 +1099,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         // of block J - NSB are done)
         const int sb = int(J % L::NSB);
         mbar_wait(&bar->st_empty[sb], ((J / L::NSB) & 1) ^ 1);
-#ifdef LASP_EXPERIMENT_NOSTATE  // timing experiment only: no state math
+#if defined(LASP_EXPERIMENT_NOSTATE) || defined(LASP_EXPERIMENT_NOCOPY)  // timing experiments only
         if (false)
 #endif
         if constexpr (SPLIT) {
@@ -1142,7 +1142,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         if (g == 0) LASP_TRACE(6, J);
         tc_fence_after();
         const uint32_t td = tmem + ((q4 * 32) << 16) + L::T_DS;
-#ifdef LASP_EXPERIMENT_NOSTATE
+#if defined(LASP_EXPERIMENT_NOSTATE) || defined(LASP_EXPERIMENT_NOUPD)
         if (false)
 #endif
         if constexpr (SPLIT) {
