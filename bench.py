@@ -447,10 +447,10 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False, shared_d
     p2p_skipped = None
     # N > 1: time the paper's ring and the all-gather exchange (NEXT-2) in the same run; `value` is the ring
     if T > 1:
-        exchanges = {"all": ["ring", "allgather", "p2p"], "both": ["ring", "allgather"]}.get(args.exchange,
+        exchanges = {"all": ["ring", "allgather", "p2p", "p2p_allgather"], "both": ["ring", "allgather"]}.get(args.exchange,
                                                                                             [args.exchange])
         ring = make_ring()
-        if "p2p" in exchanges and not getattr(ring, "_p2p", False):  # the ring, each hop one kernel over peer memory
+        if any(x.startswith("p2p") for x in exchanges) and not getattr(ring, "_p2p", False):  # peer-memory exchanges
             ok, p2p_note = 1.0, "a peer rank failed to set up"
             try:
                 ring.enable_p2p(B * Hk * D * D)
@@ -459,7 +459,7 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False, shared_d
                 p2p_note = f"{type(e).__name__}: {e}"
             ok = -(comm.max(-ok, rank) if loopback else comm.max(-ok))  # every rank must have connected
             if ok < 1.0:
-                exchanges = [x for x in exchanges if x != "p2p"]
+                exchanges = [x for x in exchanges if not x.startswith("p2p")]
                 ring.set_exchange("ring")
                 p2p_skipped = p2p_note
     else:
@@ -739,7 +739,7 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False, shared_d
     if T > 1:
         line["exchanges"] = ex_report
         if p2p_skipped:
-            line["exchanges_skipped"] = {"p2p": p2p_skipped}
+            line["exchanges_skipped"] = {"p2p, p2p_allgather": p2p_skipped}
     else:
         line["parity_max_err"] = ex_report[main_ex]["parity_max_err"]
     if loopback:
@@ -803,7 +803,8 @@ def run_lasp(args):
     if p2p_only:
         H_, D_ = CONFIGS[args.config][:2]
         n_state = (args.kv_heads or H_) * D_ * D_
-        args.exchange = "p2p"
+        if args.exchange not in ("p2p", "p2p_allgather"):
+            args.exchange = "p2p"
         make_ring = lambda: lasp.Ring.p2p_only(n_state, dev, group=group)  # noqa: E731
     else:
         make_ring = lambda: lasp.Ring(dev, group=group)  # noqa: E731
@@ -833,7 +834,7 @@ def main():
     ap.add_argument("--sp-size", type=int, default=0,
                     help="sequence-parallel size T (default: all ranks in one ring); G = N/T data-parallel groups "
                          "(Alg. 1 data-sequence hybrid, NEXT-1)")
-    ap.add_argument("--exchange", choices=["all", "both", "ring", "allgather", "p2p"], default="all",
+    ap.add_argument("--exchange", choices=["all", "both", "ring", "allgather", "p2p", "p2p_allgather"], default="all",
                     help="state exchange at N > 1: the paper's ring over NCCL, one all-gather (NEXT-2), the ring with "
                          "fused P2P hop kernels (p2p), ring + allgather (both), or all three (default: each timed in "
                          "the same run; `value` is the NCCL ring's, every one is reported under `exchanges`)")

@@ -205,9 +205,15 @@ lasp_status_t lasp_ctx_create_loopback(int rank, int world, const char* group, i
 #define LASP_EXCHANGE_RING 0
 #define LASP_EXCHANGE_ALLGATHER 1
 #define LASP_EXCHANGE_P2P 2
+/*   LASP_EXCHANGE_P2P_ALLGATHER: the all-gather exchange as ONE kernel per direction over peer memory: each rank
+ *     stores its local state (and n_local) into its slot of every downstream rank's block, publishes a data flag
+ *     there, waits for the flags of every upstream rank and folds what arrived (the same fold as
+ *     LASP_EXCHANGE_ALLGATHER); acks and epochs as LASP_EXCHANGE_P2P. One step instead of T - 1 dependent hops,
+ *     no NCCL. Same setup (lasp_ctx_p2p_setup / _connect; world <= 64). */
+#define LASP_EXCHANGE_P2P_ALLGATHER 3
 lasp_status_t lasp_ctx_set_exchange(lasp_ctx_t ctx, int exchange);
 
-/* A ring ctx without NCCL whose only exchange is LASP_EXCHANGE_P2P (peer buffers through CUDA IPC): rank r of
+/* A ring ctx without NCCL whose only exchanges are the P2P ones (peer buffers through CUDA IPC): rank r of
  * world ranks on `device` (several processes may share one GPU). Destroy with lasp_ctx_destroy. */
 lasp_status_t lasp_ctx_create_p2p(int rank, int world, int device, lasp_ctx_t* out);
 /* Collective P2P setup, step 1 (every rank): allocate this rank's flag / receive block for states of up to
@@ -215,7 +221,7 @@ lasp_status_t lasp_ctx_create_p2p(int rank, int world, int device, lasp_ctx_t* o
  * (64 bytes) to `handle`. The caller gathers the world's handles in rank order (e.g. torch.distributed
  * all_gather_object). LASP_ERR_STATE if already set up. */
 lasp_status_t lasp_ctx_p2p_setup(lasp_ctx_t ctx, size_t max_state_elems, uint8_t handle[64]);
-/* Step 2: open the blocks of ranks r - 1 and r + 1 from `handles` (world x 64 bytes, rank order), or, on a
+/* Step 2: open the blocks of the other ranks from `handles` (world x 64 bytes, rank order), or, on a
  * loopback ctx, handles = NULL: take them from the loopback group (waits up to 120 s for the peers' setup).
  * LASP_ERR_COMM if a handle cannot be opened. */
 lasp_status_t lasp_ctx_p2p_connect(lasp_ctx_t ctx, const uint8_t* handles);

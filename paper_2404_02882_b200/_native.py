@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("LASP_LIB") or os.path.join(HERE, "liblasp.so")  # LAS
 HEADER = os.path.join(os.path.dirname(HERE), "include", "lasp.h")
 
 LASP_BF16, LASP_FP32 = 0, 1
-LASP_EXCHANGE_RING, LASP_EXCHANGE_ALLGATHER, LASP_EXCHANGE_P2P = 0, 1, 2
+LASP_EXCHANGE_RING, LASP_EXCHANGE_ALLGATHER, LASP_EXCHANGE_P2P, LASP_EXCHANGE_P2P_ALLGATHER = 0, 1, 2, 3
 STATUS = {0: "LASP_OK", 1: "LASP_ERR_SHAPE", 2: "LASP_ERR_DOMAIN", 3: "LASP_ERR_PARTITION", 4: "LASP_ERR_STATE",
           5: "LASP_ERR_COMM", 6: "LASP_ERR_CUDA", 7: "LASP_ERR_UNSUPPORTED"}
 

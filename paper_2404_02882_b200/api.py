@@ -250,10 +250,11 @@ class Ring:
 
     def set_exchange(self, exchange: str) -> "Ring":
         """'ring' (the paper's T-1 hops, default), 'allgather' (one all-gather of the local states plus a
-        local fold) or 'p2p' (the ring with each hop one kernel over peer memory; needs
-        enable_p2p first)."""
+        local fold), 'p2p' (the ring with each hop one kernel over peer memory) or
+        'p2p_allgather' (the all-gather as one kernel per direction over peer memory); the P2P ones need enable_p2p
+        first."""
         mode = {"ring": N.LASP_EXCHANGE_RING, "allgather": N.LASP_EXCHANGE_ALLGATHER,
-                "p2p": N.LASP_EXCHANGE_P2P}[exchange]
+                "p2p": N.LASP_EXCHANGE_P2P, "p2p_allgather": N.LASP_EXCHANGE_P2P_ALLGATHER}[exchange]
         N.check(N.lib().lasp_ctx_set_exchange(self._ctx, mode))
         return self
 

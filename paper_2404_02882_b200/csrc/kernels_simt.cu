@@ -466,6 +466,82 @@ __global__ void p2p_hop_kernel(Plan p, P2PHop h) {
   }
 }
 
+// ---- P2P all-gather exchange (LASP_EXCHANGE_P2P_ALLGATHER): ONE kernel per direction and rank ---------------
+// Forward on rank r: store this rank's local state L_r (and its n_local) into slot r of every later rank's gather
+// block (peer memory), publish a data flag there; wait for the data flags of every earlier rank in this rank's
+// block and fold what arrived, KV_in(r) = sum_{i<r} lam^(C_{i+1} + ... + C_{r-1}) L_i (cur = lam^(C_i) cur + L_i
+// in rank order, the ring's combine applied rank by rank); acknowledge each earlier rank. Backward mirrors it
+// (to the earlier ranks, from the later ones). A sender overwrites a slot only after that receiver acknowledged the
+// previous epoch. Gather-block words: data [dir][src] at dir 64 + src, ack [dir][dst] at 128 + dir 64 + dst,
+// epoch [dir] at 256 + dir, CTA-done counters at 258 + dir (send) / 260 + dir (fold); slots follow the 4 KB flags.
+__device__ __forceinline__ uint64_t* gflag(char* base, int w) { return reinterpret_cast<uint64_t*>(base) + w; }
+__device__ __forceinline__ float* gslot(const P2PGather& g, char* base, int dir, int src) {
+  return reinterpret_cast<float*>(base + kP2PFlagBytes + (size_t(dir) * g.world + src) * g.slot_bytes);
+}
+
+__global__ void p2p_gather_kernel(Plan p, P2PGather g) {
+  pdl_wait();  // no early trigger (see p2p_hop_kernel)
+  const int dir = g.dir, r = g.rank, T = g.world;
+  const int dlo = dir == 0 ? r + 1 : 0, dhi = dir == 0 ? T : r;      // downstream ranks [dlo, dhi)
+  const int ulo = dir == 0 ? 0 : r + 1, uhi = dir == 0 ? r : T;      // upstream ranks [ulo, uhi)
+  char* mine = g.bases[r];
+  __shared__ uint64_t e_s;
+  if (threadIdx.x == 0) {
+    const uint64_t e = *reinterpret_cast<volatile uint64_t*>(gflag(mine, 256 + dir)) + 1;
+    for (int j = dlo; j < dhi; ++j) spin_until_ge(gflag(mine, 128 + dir * 64 + j), e - 1);
+    e_s = e;
+  }
+  __syncthreads();
+  const uint64_t e = e_s;
+  // send: this rank's local state into slot r of every downstream rank
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < g.n; idx += int64_t(gridDim.x) * blockDim.x) {
+    const float v = g.local[idx];
+    for (int j = dlo; j < dhi; ++j) gslot(g, g.bases[j], dir, r)[idx] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int j = dlo; j < dhi; ++j) *reinterpret_cast<int64_t*>(gslot(g, g.bases[j], dir, r) + g.n) = p.C;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long done = atomicAdd(reinterpret_cast<unsigned long long*>(gflag(mine, 258 + dir)), 1ull) + 1ull;
+    if (done == gridDim.x) {
+      __threadfence_system();
+      for (int j = dlo; j < dhi; ++j) st_release_sys(gflag(g.bases[j], dir * 64 + r), e);
+      *gflag(mine, 258 + dir) = 0;
+    }
+    for (int i = ulo; i < uhi; ++i) spin_until_ge(gflag(mine, dir * 64 + i), e);
+  }
+  __syncthreads();
+  // fold what the upstream ranks sent, in rank order along the direction
+  const int64_t DD = p.D * p.D;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < g.n; idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t hd = (idx / DD) % p.Hk;
+    float cur = 0.f;
+    for (int t = 0; t < uhi - ulo; ++t) {
+      const int i = dir == 0 ? ulo + t : uhi - 1 - t;
+      const float* sl = gslot(g, mine, dir, i);
+      const int64_t Ci = __ldcg(reinterpret_cast<const long long*>(sl + g.n));
+      cur = fmaf(powk(p.lam[hd], double(Ci)), cur, __ldcg(sl + idx));
+    }
+    g.in_priv[idx] = cur;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long done = atomicAdd(reinterpret_cast<unsigned long long*>(gflag(mine, 260 + dir)), 1ull) + 1ull;
+    if (done == gridDim.x) {
+      __threadfence_system();
+      for (int i = ulo; i < uhi; ++i) st_release_sys(gflag(g.bases[i], 128 + dir * 64 + r), e);
+      *gflag(mine, 260 + dir) = 0;
+      st_release_sys(gflag(mine, 256 + dir), e);
+    }
+  }
+}
+
+cudaError_t launch_p2p_gather(const Plan& p, const P2PGather& g, cudaStream_t st) {
+  return launch_k(p2p_gather_kernel, dim3(kP2PCtas), dim3(256), 0, st, p, g);
+}
+
 cudaError_t launch_p2p_hop(const Plan& p, const P2PHop& h, cudaStream_t st) {
   return launch_k(p2p_hop_kernel, dim3(kP2PCtas), dim3(256), 0, st, p, h);
 }

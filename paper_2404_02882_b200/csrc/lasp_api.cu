@@ -576,6 +576,7 @@ struct lasp_ctx {
   size_t p2p_elems = 0;
   char* p2p_prev = nullptr;
   char* p2p_next = nullptr;
+  std::vector<char*> p2p_peers;  // every rank's block (this rank's own at [rank]); the all-gather needs them all
   bool p2p_ipc = false;  // the peer pointers are opened IPC handles (closed on destroy)
 };
 
@@ -665,6 +666,29 @@ lasp_status_t exchange_allgather(lasp_ctx* c, const Plan& p, const float* local,
 // P2P exchange (LASP_EXCHANGE_P2P): the ring hop as one kernel that receives (flag wait on this rank's buffer),
 // combines and stores the result into the downstream rank's buffer over peer memory (kernels_simt.cu).
 size_t p2p_off_recv(const lasp_ctx* c, int dir) { return 256 + size_t(dir) * align256(c->p2p_elems * 4); }
+// the all-gather part of a rank's block follows the ring part: 4 KB of flags, then [2 directions][world] slots
+size_t p2p_off_gather(size_t elems) { return 256 + 2 * align256(elems * 4); }
+size_t p2p_slot_bytes(size_t elems) { return align256((elems + 64) * 4); }
+size_t p2p_block_bytes(size_t elems, int world) {
+  return p2p_off_gather(elems) + kP2PFlagBytes + 2 * size_t(world) * p2p_slot_bytes(elems);
+}
+lasp_status_t p2p_gather(lasp_ctx* c, const Plan& p, const float* local, float* in, bool backward, cudaStream_t st) {
+  const size_t n = state_elems(p);
+  if (!c->p2p || int(c->p2p_peers.size()) != c->world)
+    return fail(LASP_ERR_COMM, "P2P all-gather: lasp_ctx_p2p_setup / lasp_ctx_p2p_connect not done");
+  if (n > c->p2p_elems) return fail(LASP_ERR_SHAPE, "P2P exchange: state larger than the setup's max_state_elems");
+  P2PGather g{};
+  g.local = local;
+  g.in_priv = in;
+  for (int k = 0; k < c->world; ++k) g.bases[k] = c->p2p_peers[k] + p2p_off_gather(c->p2p_elems);
+  g.slot_bytes = p2p_slot_bytes(c->p2p_elems);
+  g.rank = c->rank;
+  g.world = c->world;
+  g.dir = backward ? 1 : 0;
+  g.n = int64_t(n);
+  LASP_CUDA(staged(backward ? "p2p_gather_bwd" : "p2p_gather_fwd", st, [&] { return launch_p2p_gather(p, g, st); }));
+  return LASP_OK;
+}
 lasp_status_t p2p_hop(lasp_ctx* c, const Plan& p, const float* local, float* in, bool backward, cudaStream_t st) {
   const size_t n = state_elems(p);
   if (!c->p2p || (c->world > 1 && !c->p2p_prev && !c->p2p_next))
@@ -706,6 +730,8 @@ lasp_status_t fwd_body(lasp_ctx* c, const Plan& p, const void* q, const void* k,
   ProfSpan hop("exchange_fwd", st);
   if (c->exchange == LASP_EXCHANGE_P2P) {
     if ((s = p2p_hop(c, p, w.local, w.in, false, st)) != LASP_OK) return s;
+  } else if (c->exchange == LASP_EXCHANGE_P2P_ALLGATHER) {
+    if ((s = p2p_gather(c, p, w.local, w.in, false, st)) != LASP_OK) return s;
   } else if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
     if ((s = exchange_allgather(c, p, w.local, w.in, false, st)) != LASP_OK) return s;
   } else {
@@ -763,6 +789,8 @@ lasp_status_t bwd_body(lasp_ctx* c, const Plan& p, const void* q, const void* k,
   const bool hop_pending = c->world > 1;  // a receive, send or all-gather runs on the comm stream under dQ
   if (c->exchange == LASP_EXCHANGE_P2P) {
     if ((s = p2p_hop(c, p, w.local, w.in, true, c->comm_stream)) != LASP_OK) return s;
+  } else if (c->exchange == LASP_EXCHANGE_P2P_ALLGATHER) {
+    if ((s = p2p_gather(c, p, w.local, w.in, true, c->comm_stream)) != LASP_OK) return s;
   } else if (c->exchange == LASP_EXCHANGE_ALLGATHER && c->world > 1) {
     if ((s = exchange_allgather(c, p, w.local, w.in, true, c->comm_stream)) != LASP_OK) return s;
   } else if (from >= 0) {
@@ -898,7 +926,7 @@ lasp_status_t gla_check(const GlaPlan& g, std::initializer_list<const void*> seq
 // message for the next rank: KV_out = Diag(prod_t g_t) KV_in + L_rank; dKV_out = G'_rank + Diag(...) dKV_in),
 // send, then the per-token passes.
 lasp_status_t gla_hop_in(lasp_ctx* c, const GlaPlan& g, float* in, bool backward, cudaStream_t st) {
-  if (c->exchange == LASP_EXCHANGE_P2P || (!c->comm && !c->loop))
+  if (c->exchange == LASP_EXCHANGE_P2P || c->exchange == LASP_EXCHANGE_P2P_ALLGATHER || (!c->comm && !c->loop))
     return fail(LASP_ERR_UNSUPPORTED, "generalised decay: the ring exchange only (the P2P hop applies a scalar decay)");
   int from = -1, to = -1;
   lasp_ring_peers(c->rank, c->world, backward ? 1 : 0, &from, &to);
@@ -1116,10 +1144,12 @@ lasp_status_t lasp_ctx_create_loopback(int rank, int world, const char* group, i
 
 lasp_status_t lasp_ctx_set_exchange(lasp_ctx_t c, int exchange) {
   if (!c) return fail(LASP_ERR_SHAPE, "ctx is NULL");
-  if (exchange != LASP_EXCHANGE_RING && exchange != LASP_EXCHANGE_ALLGATHER && exchange != LASP_EXCHANGE_P2P)
-    return fail(LASP_ERR_DOMAIN, "exchange must be LASP_EXCHANGE_RING, _ALLGATHER or _P2P");
-  if (exchange != LASP_EXCHANGE_P2P && !c->comm && !c->loop)
-    return fail(LASP_ERR_COMM, "a P2P-only ctx (lasp_ctx_create_p2p) supports only LASP_EXCHANGE_P2P");
+  if (exchange != LASP_EXCHANGE_RING && exchange != LASP_EXCHANGE_ALLGATHER && exchange != LASP_EXCHANGE_P2P &&
+      exchange != LASP_EXCHANGE_P2P_ALLGATHER)
+    return fail(LASP_ERR_DOMAIN, "exchange must be LASP_EXCHANGE_RING, _ALLGATHER, _P2P or _P2P_ALLGATHER");
+  const bool p2p_mode = exchange == LASP_EXCHANGE_P2P || exchange == LASP_EXCHANGE_P2P_ALLGATHER;
+  if (!p2p_mode && !c->comm && !c->loop)
+    return fail(LASP_ERR_COMM, "a P2P-only ctx (lasp_ctx_create_p2p) supports only the P2P exchanges");
   c->exchange = exchange;
   return LASP_OK;
 }
@@ -1143,10 +1173,13 @@ lasp_status_t lasp_ctx_p2p_setup(lasp_ctx_t c, size_t max_state_elems, uint8_t h
   if (!c || !handle || max_state_elems == 0) return fail(LASP_ERR_SHAPE, "NULL ctx / handle or zero size");
   if (c->p2p) return fail(LASP_ERR_STATE, "P2P exchange already set up on this ctx");
   LASP_CUDA(cudaSetDevice(c->device));
+  if (c->world > kP2PMaxWorld) return fail(LASP_ERR_UNSUPPORTED, "P2P exchange: world > 64");
   c->p2p_elems = max_state_elems;
-  const size_t bytes = 256 + 2 * align256(max_state_elems * 4);
+  const size_t bytes = p2p_block_bytes(max_state_elems, c->world);
   LASP_CUDA(cudaMalloc(&c->p2p, bytes));
-  LASP_CUDA(cudaMemset(c->p2p, 0, 256));  // epochs, acks and counters start at 0 on every rank
+  // epochs, acks and counters start at 0 on every rank (ring flags and the all-gather's flag page)
+  LASP_CUDA(cudaMemset(c->p2p, 0, 256));
+  LASP_CUDA(cudaMemset(c->p2p + p2p_off_gather(max_state_elems), 0, kP2PFlagBytes));
   cudaIpcMemHandle_t h;
   static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
   LASP_CUDA(cudaIpcGetMemHandle(&h, c->p2p));
@@ -1189,18 +1222,25 @@ lasp_status_t lasp_ctx_p2p_connect(lasp_ctx_t c, const uint8_t* handles) {
   };
   if (c->loop) c->loop->cv.notify_all();
   lasp_status_t s;
-  if ((s = open(c->rank - 1, &c->p2p_prev)) != LASP_OK) return s;
-  if ((s = open(c->rank + 1, &c->p2p_next)) != LASP_OK) return s;
+  c->p2p_peers.assign(size_t(c->world), nullptr);
+  for (int k = 0; k < c->world; ++k) {
+    if (k == c->rank) {
+      c->p2p_peers[size_t(k)] = c->p2p;
+    } else if ((s = open(k, &c->p2p_peers[size_t(k)])) != LASP_OK) {
+      return s;
+    }
+  }
+  c->p2p_prev = c->rank > 0 ? c->p2p_peers[size_t(c->rank - 1)] : nullptr;
+  c->p2p_next = c->rank + 1 < c->world ? c->p2p_peers[size_t(c->rank + 1)] : nullptr;
   return LASP_OK;
 }
 
 lasp_status_t lasp_ctx_destroy(lasp_ctx_t c) {
   if (!c) return LASP_OK;
   if (c->gather) cudaFree(c->gather);
-  if (c->p2p_ipc) {
-    if (c->p2p_prev) cudaIpcCloseMemHandle(c->p2p_prev);
-    if (c->p2p_next) cudaIpcCloseMemHandle(c->p2p_next);
-  }
+  if (c->p2p_ipc)
+    for (int k = 0; k < int(c->p2p_peers.size()); ++k)
+      if (k != c->rank && c->p2p_peers[size_t(k)]) cudaIpcCloseMemHandle(c->p2p_peers[size_t(k)]);
   if (c->p2p) {
     if (c->loop) {
       std::lock_guard<std::mutex> g(c->loop->mu);

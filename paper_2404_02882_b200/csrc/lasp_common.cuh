@@ -161,6 +161,18 @@ struct P2PHop {
   int64_t n;
 };
 cudaError_t launch_p2p_hop(const Plan& p, const P2PHop& h, cudaStream_t st);
+// P2P all-gather exchange (kernels_simt.cu p2p_gather_kernel): bases[k] = rank k's gather block (peer memory)
+constexpr int kP2PMaxWorld = 64;
+constexpr size_t kP2PFlagBytes = 4096;
+struct P2PGather {
+  const float* local;            // this rank's local state, n floats
+  float* in_priv;                // out: KV_in / dKV_in folded from the gathered states
+  char* bases[kP2PMaxWorld];
+  size_t slot_bytes;             // per (direction, source rank): n floats + the source's n_local (int64)
+  int rank, world, dir;
+  int64_t n;
+};
+cudaError_t launch_p2p_gather(const Plan& p, const P2PGather& g, cudaStream_t st);
 
 // Segment-prefix fold (F2 / B2, same arithmetic as prefix_kernel) run by a core launch before its main
 // loop: the 256 state + epilogue threads of each CTA claim chunks of elements (gbar[0]) and fold them;

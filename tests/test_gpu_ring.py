@@ -125,9 +125,9 @@ def _run_loopback(p, world, n_global, dtype, group, exchange="ring", bounds=None
         try:
             torch.cuda.set_device(0)
             ring = lasp.Ring.loopback(r, world, group)
-            if exchange == "p2p":
+            if exchange.startswith("p2p"):
                 kk = p["k"]
-                ring.enable_p2p(kk.shape[0] * kk.shape[2] * kk.shape[3] ** 2)
+                ring.enable_p2p(kk.shape[0] * kk.shape[2] * kk.shape[3] ** 2).set_exchange(exchange)
             else:
                 ring.set_exchange(exchange)
             stream = torch.cuda.Stream()
@@ -172,7 +172,7 @@ def _run_loopback(p, world, n_global, dtype, group, exchange="ring", bounds=None
     return [np.concatenate([out[r][i] for r in range(world)], axis=1) for i in range(4)], [o[4] for o in out]
 
 
-@pytest.mark.parametrize("exchange", ["ring", "allgather", "p2p"])
+@pytest.mark.parametrize("exchange", ["ring", "allgather", "p2p", "p2p_allgather"])
 @pytest.mark.parametrize("world", [2, 3, 4])
 def test_loopback_ring_bf16_matches_oracle(oracle_mod, world, exchange):
     if not torch.cuda.is_available():
@@ -180,7 +180,7 @@ def test_loopback_ring_bf16_matches_oracle(oracle_mod, world, exchange):
     N = 768 * world
     p = synth.problem(40 + world, 1, N, 4, 64, dtype="bf16")
     got, _ = _run_loopback(p, world, N, torch.bfloat16, f"bf16-w{world}-{exchange}", exchange,
-                           steps=3 if exchange == "p2p" else 1)
+                           steps=3 if exchange.startswith("p2p") else 1)
     refs = [oracle_mod.fwd(p["q"], p["k"], p["v"], p["lam"])] + \
         list(oracle_mod.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"]))
     for x, r in zip(got, refs):
@@ -286,7 +286,7 @@ def test_ring_fused_fold_matches_separate_kernel(tmp_path):
 
 
 # ---- the P2P exchange across PROCESSES (CUDA IPC peer buffers; two processes share GPU 0) -----------------
-def _p2p_proc(rank, world, port, N, errq):
+def _p2p_proc(rank, world, port, N, errq, exchange="p2p"):
     try:
         import torch.distributed as dist
         import paper_2404_02882_b200 as lasp
@@ -298,7 +298,7 @@ def _p2p_proc(rank, world, port, N, errq):
         sl = slice(rank * C, (rank + 1) * C)
         q, k, v, do = (torch.from_numpy(np.ascontiguousarray(p[x][:, sl])).cuda().to(torch.bfloat16)
                        for x in ("q", "k", "v", "do"))
-        ring = lasp.Ring.p2p_only(1 * 4 * 64 * 64)
+        ring = lasp.Ring.p2p_only(1 * 4 * 64 * 64).set_exchange(exchange)
         refs = [oracle.fwd(p["q"], p["k"], p["v"], p["lam"])] + list(oracle.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"]))
         for step in range(3):
             o, cache = ring.fwd(q, k, v, p["lam"])
@@ -314,17 +314,18 @@ def _p2p_proc(rank, world, port, N, errq):
         errq.put(f"rank {rank}: {type(e).__name__}: {e}")
 
 
-def test_p2p_exchange_two_processes_one_gpu():
-    """lasp_fwd / lasp_bwd with the P2P exchange between two PROCESSES sharing GPU 0 through CUDA IPC handles
-    (the code path multi-GPU ranks take; NCCL refuses two ranks on one device, the P2P transport does not):
-    three steps (epoch flags and acks advancing) against the oracle on each rank's shard."""
+@pytest.mark.parametrize("exchange,world", [("p2p", 2), ("p2p_allgather", 3)])
+def test_p2p_exchange_processes_one_gpu(exchange, world):
+    """lasp_fwd / lasp_bwd with a P2P exchange (ring hops, or the one-step all-gather) between PROCESSES sharing
+    GPU 0 through CUDA IPC handles (the code path multi-GPU ranks take; NCCL refuses two ranks on one device, the
+    P2P transport does not): three steps (epoch flags and acks advancing) against the oracle on each rank's shard."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
     s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
     ctx = mp.get_context("spawn")
     errq = ctx.Queue()
-    procs = [ctx.Process(target=_p2p_proc, args=(r, 2, port, 2048, errq)) for r in range(2)]
+    procs = [ctx.Process(target=_p2p_proc, args=(r, world, port, 1024 * world, errq, exchange)) for r in range(world)]
     for pr in procs:
         pr.start()
     for pr in procs:
