@@ -388,16 +388,10 @@ cudaError_t launch_norm_apply(const Plan& p, void* y, const NormArgs& n, cudaStr
 // prefix fold; ctrl[3..15]: work-claim counters of the persistent kernels).
 __global__ void tag_kernel(CacheTag t, uint64_t* __restrict__ hdr, unsigned check_mask, unsigned* __restrict__ ctrl) {
   pdl_wait();
+  entry_duty(t, hdr, check_mask, ctrl);
+  // trigger only after the control block is zeroed: the next kernel's CTAs claim work items from it as they start
+  __threadfence();
   pdl_trigger();
-  const int i = threadIdx.x;
-  bool bad = false;
-  if (check_mask == 0u) {
-    if (i < kTagWords) hdr[i] = t.w[i];
-  } else {
-    bad = i < kTagWords && ((check_mask >> i) & 1u) && hdr[i] != t.w[i];
-  }
-  const unsigned bits = __ballot_sync(0xffffffffu, bad);
-  if (i < 16) ctrl[i] = i == 2 ? bits : 0u;
 }
 
 cudaError_t launch_tag(const CacheTag& t, uint64_t* hdr, unsigned check_mask, unsigned* ctrl, cudaStream_t st) {

@@ -233,6 +233,8 @@ struct SegParams {
   CUtensorMap my2;
   const float* rnorm;    // [B][C][H]
   __nv_bfloat16* dout;   // [B][C][H][D]
+  EntryDuty entry;       // the call's entry duty (has_entry: this launch replaces tag_kernel)
+  int has_entry;
 };
 
 // debug timeline: event ev (0..15) of block J (< 64) of CTA 0 -> trace[ev * 64 + J] = clock64()
@@ -295,6 +297,9 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
 
   if (warp == 0) {
     if (elect_one()) {
+      // first kernel of the call: nothing is read before all earlier work on the stream is complete (the
+      // inputs may come from a kernel that triggered its dependents early)
+      if (prm.has_entry) pdl_wait();
       uint32_t J = 0;
       for (uint32_t k = 0;; ++k) {
         const int64_t w = q_claim(*iq, k, prm.claim);
@@ -426,6 +431,13 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
     const bool valid = D == 128 || lane < 16;
     const int row = D == 128 ? int(q4 * 32 + lane) : int(q4 * 16 + lane);
     pdl_wait();
+    if (prm.has_entry && blockIdx.x == 0) {
+      // the call's entry duty before this CTA lets the next kernel launch: its CTAs claim items from the
+      // control block as they start
+      if (warp == 8) entry_duty(prm.entry.tag, prm.entry.hdr, prm.entry.check_mask, prm.entry.ctrl);
+      __threadfence();
+      named_bar_sync(3, 128);
+    }
     pdl_trigger();
     for (uint32_t k = 0;; ++k) {
       const int64_t w = q_fetch_warp(*iq, k);
@@ -1304,9 +1316,13 @@ unsigned persistent_grid(const Plan& p, int per_sm = 1) {
 
 template <int D, Dir DIR, bool NORM>
 cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, cudaStream_t st,
-                       unsigned* claim, const NormBwdArgs* nb) {
+                       unsigned* claim, const NormBwdArgs* nb, const EntryDuty* entry) {
   SegParams prm;
   std::memset(&prm, 0, sizeof prm);
+  if (entry) {
+    prm.entry = *entry;
+    prm.has_entry = 1;
+  }
   if (NORM) {
     if (nb == nullptr || DIR != Dir::REV) return cudaErrorInvalidValue;
     cudaError_t e2 = make_seq_map(&prm.my2, nb->y, p, p.H);
@@ -1314,7 +1330,7 @@ cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, 
     prm.rnorm = nb->rnorm;
     prm.dout = static_cast<__nv_bfloat16*>(nb->dout);
   }
-  prm.claim = static_items() ? nullptr : claim;
+  prm.claim = static_items() || entry ? nullptr : claim;  // (the entry duty zeroes the counters only now)
   // F1 reads k, v (Hk heads); B1 reads q, do (H heads), summing the G query heads of each state head
   prm.sub = DIR == Dir::FWD ? 1 : int(p.G);
   const int64_t heads = DIR == Dir::FWD ? p.Hk : p.H;
@@ -1474,20 +1490,20 @@ bool tc_supported(const Plan& p) {
 }
 
 cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st,
-                                unsigned* r, const NormBwdArgs* nb) {
+                                unsigned* r, const NormBwdArgs* nb, const EntryDuty* e) {
   if (r == nullptr) return cudaErrorInvalidValue;  // the work-claim counter is required
   if (nb != nullptr) {
     if (dir != Dir::REV) return cudaErrorInvalidValue;
-    if (p.D == 64) return launch_seg<64, Dir::REV, true>(p, x, y, out, st, r, nb);
-    if (p.D == 128) return launch_seg<128, Dir::REV, true>(p, x, y, out, st, r, nb);
+    if (p.D == 64) return launch_seg<64, Dir::REV, true>(p, x, y, out, st, r, nb, e);
+    if (p.D == 128) return launch_seg<128, Dir::REV, true>(p, x, y, out, st, r, nb, e);
     return cudaErrorNotSupported;
   }
   if (p.D == 64)
-    return dir == Dir::FWD ? launch_seg<64, Dir::FWD, false>(p, x, y, out, st, r, nullptr)
-                           : launch_seg<64, Dir::REV, false>(p, x, y, out, st, r, nullptr);
+    return dir == Dir::FWD ? launch_seg<64, Dir::FWD, false>(p, x, y, out, st, r, nullptr, e)
+                           : launch_seg<64, Dir::REV, false>(p, x, y, out, st, r, nullptr, e);
   if (p.D == 128)
-    return dir == Dir::FWD ? launch_seg<128, Dir::FWD, false>(p, x, y, out, st, r, nullptr)
-                           : launch_seg<128, Dir::REV, false>(p, x, y, out, st, r, nullptr);
+    return dir == Dir::FWD ? launch_seg<128, Dir::FWD, false>(p, x, y, out, st, r, nullptr, e)
+                           : launch_seg<128, Dir::REV, false>(p, x, y, out, st, r, nullptr, e);
   return cudaErrorNotSupported;
 }
 

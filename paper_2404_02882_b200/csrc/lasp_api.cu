@@ -293,6 +293,25 @@ cudaError_t entry_tag(const Plan& p, const void* cache, const Workspace& w, int 
   });
 }
 
+// The first kernel of a call: on the tensor-core path with tokens, the segment-state launch carries the entry duty
+// (one kernel boundary less per call; LASP_SEPARATE_ENTRY=1 keeps tag_kernel); otherwise tag_kernel runs it.
+bool entry_in_seg_state(const Plan& p) {
+  static const bool sep = [] {
+    const char* s = std::getenv("LASP_SEPARATE_ENTRY");
+    return s && *s && *s != '0';
+  }();
+  return !sep && p.C > 0 && tc_supported(p);
+}
+EntryDuty make_entry(const Plan& p, const void* cache, const Workspace& w, int rank, int world, bool check,
+                     bool check_rank) {
+  EntryDuty e{};
+  e.tag = make_tag(p, rank, world);
+  e.hdr = cache_tag_ptr(p, cache);
+  e.check_mask = check ? tag_mask(check_rank) : 0u;
+  e.ctrl = w.gbar;
+  return e;
+}
+
 // a profiled span that is not one launch (the ring hop / state exchange: receive ... send on one stream,
 // including the wait for the upstream rank): events recorded only while profiling is enabled
 struct ProfSpan {
@@ -314,12 +333,13 @@ struct ProfSpan {
 
 // ---- stage dispatch: tcgen05 for covered bf16 shapes, CUDA cores otherwise ---------------------
 cudaError_t seg_state(const Plan& p, Dir dir, const void* x, const void* y, float* out, cudaStream_t st,
-                      unsigned* claim, const NormBwdArgs* nb = nullptr) {
+                      unsigned* claim, const NormBwdArgs* nb = nullptr, const EntryDuty* entry = nullptr) {
   const bool tc = tc_supported(p);
-  if (nb && !tc) return cudaErrorNotSupported;
+  if ((nb || entry) && !tc) return cudaErrorNotSupported;
   return staged(dir == Dir::FWD ? (tc ? "seg_state_fwd_tc" : "seg_state_fwd_simt")
                                 : (tc ? (nb ? "seg_state_rev_norm_tc" : "seg_state_rev_tc") : "seg_state_rev_simt"), st, [&] {
-    return tc ? launch_seg_state_tc(p, dir, x, y, out, st, claim, nb) : launch_seg_state_simt(p, dir, x, y, out, st);
+    return tc ? launch_seg_state_tc(p, dir, x, y, out, st, claim, nb, entry)
+              : launch_seg_state_simt(p, dir, x, y, out, st);
   });
 }
 
@@ -719,8 +739,13 @@ lasp_status_t fwd_body(lasp_ctx* c, const Plan& p, const void* q, const void* k,
   Workspace w = carve(p, workspace);
   lasp_status_t s;
   unsigned* gbar = p.C > 0 && fused_fold(p) ? w.gbar : nullptr;
-  LASP_CUDA(entry_tag(p, cache, w, c ? c->rank : -1, c ? c->world : -1, false, false, st));   // cache tag
-  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, w.claim(0)));                  // F1
+  if (entry_in_seg_state(p)) {  // F1, with the call's entry duty (cache tag, control block)
+    const EntryDuty e = make_entry(p, cache, w, c ? c->rank : -1, c ? c->world : -1, false, false);
+    LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, w.claim(0), nullptr, &e));
+  } else {
+    LASP_CUDA(entry_tag(p, cache, w, c ? c->rank : -1, c ? c->world : -1, false, false, st));   // cache tag
+    if (p.C > 0) LASP_CUDA(seg_state(p, Dir::FWD, k, v, w.seg, st, w.claim(0)));                // F1
+  }
   if (c == nullptr)
     return fwd_tail(p, q, k, v, kv_in, o, kv_out, cache, w.seg, gbar, w.claim(1), st, norm);  // F2 + F3
   const size_t n = state_elems(p);
@@ -760,13 +785,16 @@ lasp_status_t bwd_body(lasp_ctx* c, const Plan& p, const void* q, const void* k,
   const float* P = static_cast<const float*>(cache);
   const bool fuse = p.C > 0 && fused_fold(p);
   const void* g = nb ? nb->dout : d_o;  // the dO the B3 passes read
-  LASP_CUDA(entry_tag(p, cache, w, c ? c->rank : -1, c ? c->world : -1, true, c != nullptr, st));  // tag check
+  // B1 carries the call's entry duty (tag check, control block) on the tensor-core path, else tag_kernel
+  const bool entry_b1 = entry_in_seg_state(p);
+  const EntryDuty e = make_entry(p, cache, w, c ? c->rank : -1, c ? c->world : -1, true, c != nullptr);
+  if (!entry_b1) LASP_CUDA(entry_tag(p, cache, w, c ? c->rank : -1, c ? c->world : -1, true, c != nullptr, st));
   if (c == nullptr) {
     if (p.C == 0) {
       LASP_CUDA(prefix(p, Dir::REV, dkv_in, nullptr, nullptr, dkv_out, st));
       return LASP_OK;
     }
-    LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, w.claim(0), nb));                      // B1
+    LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, w.claim(0), nb, entry_b1 ? &e : nullptr));  // B1
     const PrefixFold fold{dkv_in, w.seg, w.seg, dkv_out, w.gbar, int(Dir::REV)};
     if (!fuse) LASP_CUDA(prefix(p, Dir::REV, dkv_in, w.seg, w.seg, dkv_out, st));          // B2 (in place)
     // B3: dQ (needs only the cache), dV and dK in one launch (with B2 folded in when fused)
@@ -778,7 +806,7 @@ lasp_status_t bwd_body(lasp_ctx* c, const Plan& p, const void* q, const void* k,
     return LASP_OK;
   }
   const size_t n = state_elems(p);
-  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, w.claim(0), nb));         // B1
+  if (p.C > 0) LASP_CUDA(seg_state(p, Dir::REV, q, d_o, w.seg, st, w.claim(0), nb, entry_b1 ? &e : nullptr));  // B1
   LASP_CUDA(prefix(p, Dir::REV, nullptr, p.C > 0 ? w.seg : nullptr, nullptr, w.local, st));
   // B2 ring hop on the comm stream: Recv dKV_in from r+1 (Alg. 3), combine, Send to r-1
   LASP_CUDA(cudaEventRecord(c->ev_ready, st));

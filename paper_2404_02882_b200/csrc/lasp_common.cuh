@@ -116,6 +116,26 @@ constexpr uint64_t kTagMagicValue = 0x4c41535043414348ull;  // "LASPCACH"
 // check_mask == 0: write the tag, else compare the masked words; the mismatch bits go to ctrl[2] (the
 // call's status word) and the other 15 words of the call's control block (counters) are zeroed
 cudaError_t launch_tag(const CacheTag& t, uint64_t* hdr, unsigned check_mask, unsigned* ctrl, cudaStream_t st);
+// The entry duty of a call, run by one warp after griddepcontrol.wait (tag_kernel, or the first CTA of the call's
+// first segment-state launch): write (check_mask == 0) or compare the cache tag and reset the call's 16-word
+// control block (fold counters, status word = the tag mismatch bits, work-claim counters).
+__device__ __forceinline__ void entry_duty(const CacheTag& t, uint64_t* hdr, unsigned check_mask, unsigned* ctrl) {
+  const int i = int(threadIdx.x & 31);
+  bool bad = false;
+  if (check_mask == 0u) {
+    if (i < kTagWords) hdr[i] = t.w[i];
+  } else {
+    bad = i < kTagWords && ((check_mask >> i) & 1u) && hdr[i] != t.w[i];
+  }
+  const unsigned bits = __ballot_sync(0xffffffffu, bad);
+  if (i < 16) ctrl[i] = i == 2 ? bits : 0u;
+}
+struct EntryDuty {       // passed to the first launch of a call instead of a separate tag_kernel launch
+  CacheTag tag;
+  uint64_t* hdr;
+  unsigned check_mask;
+  unsigned* ctrl;
+};
 // true (on the device) when the call's entry kernel found a mismatching cache tag
 __device__ __forceinline__ bool tag_poisoned(const unsigned* status) { return status != nullptr && __ldcg(status) != 0u; }
 
@@ -200,8 +220,12 @@ struct NormBwdArgs {
   void* dout;          // [B][C][H][D] bf16, written
 };
 // claim: the launch's work-claim counter (a workspace word zeroed by the call's entry kernel)
+// entry != nullptr: this launch is the call's first kernel and also runs the entry duty (no tag_kernel): its
+// producer waits for all earlier work before loading, items are assigned statically (the claim counters are only
+// zeroed by the duty), and CTA 0 triggers the next kernel only after the control block is reset
 cudaError_t launch_seg_state_tc(const Plan& p, Dir dir, const void* x, const void* y, float* out,
-                                cudaStream_t st, unsigned* claim, const NormBwdArgs* norm_bwd = nullptr);
+                                cudaStream_t st, unsigned* claim, const NormBwdArgs* norm_bwd = nullptr,
+                                const EntryDuty* entry = nullptr);
 // Norm(.) of Eq. 2 (NEXT-3, reading N1: per-head RMS normalization) fused into the forward core's epilogue
 constexpr float kNormEps = 1e-6f;  // reading N1
 struct NormArgs {
