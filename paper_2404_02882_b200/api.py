@@ -471,6 +471,36 @@ def lasp_attention(q, k, v, lam, ring=None):
     return LaspAttention.apply(q, k, v, lam, ring)
 
 
+class GlaAttention(torch.autograd.Function):
+    """O = generalised-decay LASP(Q, K, V; log_g) (NEXT-4, the GLA / GateLoop row) with gradients for q, k, v and
+    the log decay; the state cache is saved for backward. ``ring`` None runs the single-rank path."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, log_g, ring=None):
+        q, k, v, log_g = q.contiguous(), k.contiguous(), v.contiguous(), log_g.contiguous()
+        if ring is None:
+            o, _, cache = gla_fwd_local(q, k, v, log_g, kv_out=False)
+        else:
+            o, cache = ring.gla_fwd(q, k, v, log_g)
+        ctx.save_for_backward(q, k, v, log_g, cache)
+        ctx.ring = ring
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, log_g, cache = ctx.saved_tensors
+        do = do.contiguous()
+        if ctx.ring is None:
+            dq, dk, dv, dlg, _ = gla_bwd_local(q, k, v, log_g, do, cache, dkv_out=False)
+        else:
+            dq, dk, dv, dlg = ctx.ring.gla_bwd(q, k, v, log_g, do, cache)
+        return dq, dk, dv, dlg, None
+
+
+def gla_attention(q, k, v, log_g, ring=None):
+    return GlaAttention.apply(q, k, v, log_g, ring)
+
+
 # ---- NEXT-3: the layer around the path (include/lasp.h lasp_layer_fwd / lasp_layer_bwd) ----------------------
 def layer_workspace_bytes(shape: N.lasp_shape_t) -> int:
     return int(N.lib().lasp_layer_workspace_bytes(ctypes.byref(shape)))

@@ -173,3 +173,14 @@ def test_gla_rejects_bf16_and_grouped_queries(L):
     q = torch.zeros(1, 64, 2, 64, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(ValueError):
         L.gla_fwd_local(q, q, q, q)
+
+
+def test_gla_autograd_function(L, oracle_mod):
+    """gla_attention as a torch.autograd.Function: O and the gradients of q, k, v and the log decay against the
+    oracle through a scalar loss sum(O * dO)."""
+    t = synth.gla_problem(31, 1, 700, 2, 64)
+    q, k, v, lg = (dev(t[x]).requires_grad_() for x in ("q", "k", "v", "lg"))
+    o = L.gla_attention(q, k, v, lg)
+    (o * dev(t["do"])).sum().backward()
+    got = [o.detach().cpu().numpy()] + [x.grad.cpu().numpy() for x in (q, k, v, lg)]
+    check(oracle_mod, t, got)

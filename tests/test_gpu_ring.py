@@ -335,3 +335,54 @@ def test_p2p_exchange_processes_one_gpu(exchange, world):
         errs.append(errq.get())
     assert not errs, errs
     assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
+
+
+def _p2p_hybrid_proc(rank, world, sp, port, C, errq):
+    try:
+        import torch.distributed as dist
+        import paper_2404_02882_b200 as lasp
+        import oracle
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        grp = lasp.sp_group(sp)
+        gid, grank, _ = lasp.topology(rank, world, sp)
+        p = synth.problem(90 + gid, 1, C * sp, 4, 64, dtype="bf16")   # each group its own sequence (Alg. 1)
+        sl = slice(grank * C, (grank + 1) * C)
+        q, k, v, do = (torch.from_numpy(np.ascontiguousarray(p[x][:, sl])).cuda().to(torch.bfloat16)
+                       for x in ("q", "k", "v", "do"))
+        ring = lasp.Ring.p2p_only(4 * 64 * 64, group=grp).set_exchange("p2p_allgather" if gid else "p2p")
+        refs = [oracle.fwd(p["q"], p["k"], p["v"], p["lam"])] + list(oracle.bwd(p["q"], p["k"], p["v"], p["lam"], p["do"]))
+        for step in range(2):
+            o, cache = ring.fwd(q, k, v, p["lam"])
+            dq, dk, dv = ring.bwd(q, k, v, p["lam"], do, cache)
+            torch.cuda.synchronize()
+            for x, r in zip((o, dq, dk, dv), refs):
+                err = oracle.normwise_err(x.float().cpu().numpy(), r[:, sl])
+                assert err <= 2e-2, (rank, step, err)
+        dist.barrier()
+        ring.close()
+        dist.destroy_process_group()
+    except BaseException as e:  # noqa: BLE001
+        errq.put(f"rank {rank}: {type(e).__name__}: {e}")
+
+
+def test_p2p_hybrid_groups_processes_one_gpu():
+    """Data-sequence hybrid (Alg. 1, NEXT-1) with the P2P exchanges: 4 processes on GPU 0, two sequence-parallel
+    groups of 2 (group 0 the P2P ring, group 1 the P2P all-gather), each with its own sequence; every rank's shard
+    against the oracle on its group's sequence, two steps."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    ctx = mp.get_context("spawn")
+    errq = ctx.Queue()
+    procs = [ctx.Process(target=_p2p_hybrid_proc, args=(r, 4, 2, port, 768, errq)) for r in range(4)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=600)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, errs
+    assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
