@@ -475,6 +475,13 @@ def rank_bench(args, rank, world, dev, comm, make_ring, loopback=False, shared_d
                 ring.bwd(q, k, v, lam, do, cache, dq=dq, dk=dk, dv=dv, workspace=ws)
         return step
 
+    if loopback and exchanges and exchanges[0].startswith("p2p"):
+        # thread-ranks share one context: load every kernel over the host transport first, since a first launch
+        # (lazy module loading) synchronizes the context and must not meet a peer's spinning hop kernel
+        ring.set_exchange("ring")
+        step_fn("ring")()
+        sync()
+
     # L2 flush between timed steps: READ a 256 MiB buffer (> 126 MB L2), so L2 holds clean lines and no
     # write-back of the flush lands inside the next step (a write-based flush would)
     flush = torch.ones(64 << 20, dtype=torch.int32, device=dev)

@@ -200,7 +200,9 @@ lasp_status_t lasp_ctx_create_loopback(int rank, int world, const char* group, i
  *     graph-captured and replayed. Needs lasp_ctx_p2p_setup + lasp_ctx_p2p_connect; scalar-decay path only.
  *     The waits are on the device: with several ranks on ONE device (a loopback ctx, or processes sharing a
  *     GPU) no rank may block in a device-wide synchronize before the other ranks have submitted their calls
- *     (synchronize the rank's own stream instead); across GPUs the ranks are independent.
+ *     (synchronize the rank's own stream instead), and no rank may launch a kernel for the first time in the
+ *     process while a peer's hop kernel waits (lazy module loading synchronizes the context): run one step
+ *     over another exchange first, or set CUDA_MODULE_LOADING=EAGER; across GPUs the ranks are independent.
  * LASP_ERR_DOMAIN for any other value; LASP_ERR_COMM for RING / ALLGATHER on a P2P-only ctx. */
 #define LASP_EXCHANGE_RING 0
 #define LASP_EXCHANGE_ALLGATHER 1

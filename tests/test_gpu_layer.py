@@ -123,3 +123,54 @@ def test_layer_unrounded_gap_is_norm_conditioning(L, oracle_mod):
           "kappa there", kappa[worst])
     assert np.all(err <= bound), (err[worst], bound[worst])
     assert err.max() > 2e-2  # the gap the bf16-points oracle removes is real at this shape
+
+
+@pytest.mark.parametrize("exchange", ["ring", "p2p"])
+def test_layer_over_loopback_ring(L, oracle_mod, exchange):
+    """The NEXT-3 layer across a 2-rank ring (lasp_layer_fwd / lasp_layer_bwd with a loopback ctx; the ring over the
+    in-process transport, or the P2P ring exchange): each rank projects its chunk, the state crosses the ring,
+    Norm runs per token. The concatenated Y, dX and the sum over ranks of the weight gradients match the single-sequence oracle chain (reading N2)."""
+    import threading
+    B, N, H, D, T = 1, 1536, 4, 64, 2
+    t = synth.layer_problem(44, B, N, H, H, D, H * D)
+    C = N // T
+    res, errs = [None] * T, []
+
+    def rank(r):
+        ring = None
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                ring = L.Ring.loopback(r, T, f"layer-{exchange}")
+                x = dev(t["x"][:, r * C:(r + 1) * C])
+                wq, wk, wv = (dev(t[n]) for n in ("w_q", "w_k", "w_v"))
+                dy = dev(t["dy"][:, r * C:(r + 1) * C])
+                if exchange == "p2p":
+                    # one step over the host transport first: a kernel's first launch (lazy module loading)
+                    # synchronizes the context, which must not happen while the peer's hop kernel spins on
+                    # this GPU (include/lasp.h, LASP_EXCHANGE_P2P)
+                    L.layer_bwd(x, wq, wk, wv, t["lam"], L.layer_fwd(x, wq, wk, wv, t["lam"], H, ring), dy, ring)
+                    s.synchronize()
+                    ring.enable_p2p(B * H * D * D)
+                fw = L.layer_fwd(x, wq, wk, wv, t["lam"], H, ring)
+                g = L.layer_bwd(x, wq, wk, wv, t["lam"], fw, dy, ring)
+            s.synchronize()
+            res[r] = (fw["y"].float().cpu().numpy(), g["dx"].float().cpu().numpy(),
+                      [g[n].cpu().numpy() for n in ("dw_q", "dw_k", "dw_v")])
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+    ths = [threading.Thread(target=rank, args=(r,)) for r in range(T)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert not errs, errs
+    ref = oracle_mod.layer_fwd(t["x"], t["w_q"], t["w_k"], t["w_v"], t["lam"], H, H, bf16_points=True)
+    rdx, rdwq, rdwk, rdwv = oracle_mod.layer_bwd(t["x"], t["w_q"], t["w_k"], t["w_v"], t["lam"], ref, t["dy"])[:4]
+    y = np.concatenate([res[r][0] for r in range(T)], 1)
+    dx = np.concatenate([res[r][1] for r in range(T)], 1)
+    assert per_head(y, ref["y"]) <= TOL
+    assert rel(dx, rdx) <= TOL_GRAD
+    for i, rw in enumerate((rdwq, rdwk, rdwv)):
+        assert rel(sum(res[r][2][i] for r in range(T)), rw) <= TOL_GRAD

@@ -125,16 +125,21 @@ def _run_loopback(p, world, n_global, dtype, group, exchange="ring", bounds=None
         try:
             torch.cuda.set_device(0)
             ring = lasp.Ring.loopback(r, world, group)
-            if exchange.startswith("p2p"):
-                kk = p["k"]
-                ring.enable_p2p(kk.shape[0] * kk.shape[2] * kk.shape[3] ** 2).set_exchange(exchange)
-            else:
-                ring.set_exchange(exchange)
             stream = torch.cuda.Stream()
             with torch.cuda.stream(stream):
                 sl = slice(*bounds[r])
                 q, k, v, do = (torch.from_numpy(np.ascontiguousarray(p[x][:, sl])).cuda().to(dtype)
                                for x in ("q", "k", "v", "do"))
+                if exchange.startswith("p2p"):
+                    # warm-up over the host transport: no kernel may load lazily (a context synchronize) while a
+                    # peer's hop kernel spins on this GPU (include/lasp.h, LASP_EXCHANGE_P2P)
+                    o, cache = ring.fwd(q, k, v, p["lam"])
+                    ring.bwd(q, k, v, p["lam"], do, cache)
+                    stream.synchronize()
+                    kk = p["k"]
+                    ring.enable_p2p(kk.shape[0] * kk.shape[2] * kk.shape[3] ** 2).set_exchange(exchange)
+                else:
+                    ring.set_exchange(exchange)
                 first = None
                 for _ in range(steps):
                     o, cache = ring.fwd(q, k, v, p["lam"])
