@@ -92,7 +92,12 @@ __global__ void __launch_bounds__(kThreads) seg_state_simt_kernel(Plan p, const 
 // ---------------------------------------------------------------------------------------------
 // prefix: per element, cur = init; for p: prefix[p] = cur; cur = lam^len_p cur + seg[p]; final = cur
 // (Alg. 2 P:171 / Alg. 3 P:648 applied between segments). `prefix` may alias `seg_states`.
-__global__ void __launch_bounds__(64) prefix_kernel(Plan p, Dir dir, const float* __restrict__ init,
+// U: segment loads in flight per thread, the smallest of {8, 16, 24, 40} that covers nseg (chosen by the host),
+// D and DIR compile-time so the segment stride is an immediate offset (one base address per thread instead of
+// one 64-bit address per load): TNL-1B's 24 segments took ~170-255 registers per thread with runtime strides,
+// which left part of the launch to a second wave
+template <int U, int D, Dir DIR>
+__global__ void __launch_bounds__(64) prefix_kernel(Plan p, const float* __restrict__ init,
                                                     const float* seg_states, float* prefix,
                                                     float* __restrict__ final_out) {
   pdl_wait();
@@ -100,7 +105,8 @@ __global__ void __launch_bounds__(64) prefix_kernel(Plan p, Dir dir, const float
   // One thread per 4 consecutive state elements (float4); all (up to U) segment loads of a batch are
   // issued before the serial fold (nseg <= U: one L2 round trip). `prefix` may alias `seg_states`: a
   // thread loads every segment of a batch before it stores any of them.
-  const int64_t DD = p.D * p.D;
+  constexpr int64_t DD = int64_t(D) * D;
+  constexpr int64_t step = DIR == Dir::FWD ? DD : -DD;  // floats between consecutive folded segments
   const int64_t idx4 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over B*H*D*D/4
   if (idx4 * 4 >= p.B * p.Hk * DD) return;
   const int64_t bh = (idx4 * 4) / DD, e = (idx4 * 4) % DD, h = bh % p.Hk;
@@ -111,22 +117,21 @@ __global__ void __launch_bounds__(64) prefix_kernel(Plan p, Dir dir, const float
   const float dec_full = exp2f(float(p.seg_len) * l2);
   const float dec_last = exp2f(float(last_len > 0 ? last_len : 0) * l2);
   float4 cur = init ? *reinterpret_cast<const float4*>(init + idx4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-  const float* src = seg_states ? seg_states + bh * p.nseg * DD + e : nullptr;
-  float* dst = prefix ? prefix + bh * p.nseg * DD + e : nullptr;
-  constexpr int U = 40;
-  for (int64_t s0 = 0; s0 < p.nseg; s0 += U) {
+  // first folded segment: 0 (FWD) or nseg - 1 (REV, folds from the rank end)
+  const int64_t first = (bh * p.nseg + (DIR == Dir::FWD ? 0 : p.nseg - 1)) * DD + e;
+  const float* src = seg_states ? seg_states + first : nullptr;
+  float* dst = prefix ? prefix + first : nullptr;
+  for (int64_t s0 = 0; s0 < p.nseg; s0 += U, src = src ? src + U * step : src, dst = dst ? dst + U * step : dst) {
+    const int nb = int(p.nseg - s0);  // segments left
     float4 v[U];
 #pragma unroll
-    for (int t = 0; t < U; ++t) {
-      const int64_t sg = dir == Dir::FWD ? s0 + t : p.nseg - 1 - (s0 + t);  // REV folds from the rank end
-      v[t] = (src && s0 + t < p.nseg) ? __ldcg(reinterpret_cast<const float4*>(src + sg * DD))
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    for (int t = 0; t < U; ++t)
+      v[t] = (src && t < nb) ? __ldcg(reinterpret_cast<const float4*>(src + t * step)) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int t = 0; t < U; ++t) {
-      const int64_t sg = dir == Dir::FWD ? s0 + t : p.nseg - 1 - (s0 + t);
-      if (s0 + t < p.nseg) {
-        if (dst) *reinterpret_cast<float4*>(dst + sg * DD) = cur;
+      if (t < nb) {
+        if (dst) *reinterpret_cast<float4*>(dst + t * step) = cur;
+        const int64_t sg = DIR == Dir::FWD ? s0 + t : p.nseg - 1 - (s0 + t);
         const float dcy = (sg == p.nseg - 1) ? dec_last : dec_full;
         cur.x = fmaf(dcy, cur.x, v[t].x); cur.y = fmaf(dcy, cur.y, v[t].y);
         cur.z = fmaf(dcy, cur.z, v[t].z); cur.w = fmaf(dcy, cur.w, v[t].w);
@@ -299,8 +304,24 @@ cudaError_t launch_prefix(const Plan& p, Dir dir, const float* init, const float
                           float* final_out, cudaStream_t st) {
   const int64_t n = p.B * p.Hk * p.D * p.D / 4;  // D*D is a multiple of 4
   const int threads = 64;
-  return launch_k(prefix_kernel, dim3((unsigned)((n + threads - 1) / threads)), dim3(threads), 0, st, p, dir, init,
-                  seg_states, prefix_out, final_out);
+  const dim3 grid((unsigned)((n + threads - 1) / threads));
+  auto go = [&](auto kern) { return launch_k(kern, grid, dim3(threads), 0, st, p, init, seg_states, prefix_out, final_out); };
+  auto by_u = [&](auto d_tag, auto dir_tag) {
+    constexpr int D = decltype(d_tag)::value;
+    constexpr Dir R = decltype(dir_tag)::value;
+    if (p.nseg <= 8) return go(prefix_kernel<8, D, R>);
+    if (p.nseg <= 16) return go(prefix_kernel<16, D, R>);
+    if (p.nseg <= 24) return go(prefix_kernel<24, D, R>);
+    return go(prefix_kernel<40, D, R>);
+  };
+  auto by_dir = [&](auto d_tag) {
+    return dir == Dir::FWD ? by_u(d_tag, std::integral_constant<Dir, Dir::FWD>{})
+                           : by_u(d_tag, std::integral_constant<Dir, Dir::REV>{});
+  };
+  if (p.D == 32) return by_dir(std::integral_constant<int, 32>{});
+  if (p.D == 64) return by_dir(std::integral_constant<int, 64>{});
+  if (p.D == 128) return by_dir(std::integral_constant<int, 128>{});
+  return cudaErrorInvalidValue;
 }
 
 // All-gather exchange: fold the gathered per-rank local states of ranks

@@ -203,7 +203,19 @@ template <int D, bool NORM = false>
 struct SegLayout {
   static constexpr int NBOX = D / 64;
   static constexpr uint32_t TILE = NBOX * BOX;
-  static constexpr int NT = NORM ? 3 : 2;  // tiles per stage
+  // VS = 2 (experiment, LASP_SEG_VSPLIT; head_dim 128 without the fused Norm backward): an item is one 64-wide
+  // value slice of a segment's state, so the persistent grid gets twice the items (TNL-1B: 384 segment items are
+  // 2.6 per SM) with 4 x 48 KB stages. Measured: F1 59.7 -> 74 us at TNL-1B, 347 -> 604 us at TNL-7B (the X tile
+  // is fetched and row-scaled once per slice), so whole segments stay the default.
+#ifdef LASP_SEG_VSPLIT
+  static constexpr int VS = (D == 128 && !NORM) ? 2 : 1;
+#else
+  static constexpr int VS = 1;
+#endif
+  static constexpr int NBOXY = NBOX / VS;            // 64-wide boxes of the Y tile
+  static constexpr int DN = D / VS;                  // state columns per item (UMMA N)
+  static constexpr uint32_t TILEY = NBOXY * BOX;
+  static constexpr uint32_t STG_BYTES = TILE + TILEY + (NORM ? TILE : 0);
 #ifndef LASP_SEG_STAGES64
 #define LASP_SEG_STAGES64 2  // 2 x 2 beat 3 x 2, 4 x 1 and 6 x 1 (stages x CTAs/SM) by ~1 % (round 1 sweep)
 #define LASP_SEG_CTAS64 2
@@ -211,14 +223,15 @@ struct SegLayout {
 #ifndef LASP_SEG_STAGES128
 #define LASP_SEG_STAGES128 3  // 3 x 64 KB stages, 1 CTA/SM: seg F 61.4 -> 58.0 us at TNL-1B
 #endif
-  static constexpr int STAGES = NORM ? 2 : D == 64 ? LASP_SEG_STAGES64 : LASP_SEG_STAGES128;
+  static constexpr int STAGES = NORM ? 2 : D == 64 ? LASP_SEG_STAGES64 : VS > 1 ? 4 : LASP_SEG_STAGES128;
   static constexpr int CTAS_PER_SM = D == 64 ? LASP_SEG_CTAS64 : 1;  // 2 x (96 KB smem, 128 TMEM columns) per SM
-  static constexpr uint32_t X(int s) { return uint32_t(s) * NT * TILE; }
-  static constexpr uint32_t Y(int s) { return uint32_t(s) * NT * TILE + TILE; }
-  static constexpr uint32_t Y2(int s) { return uint32_t(s) * NT * TILE + 2 * TILE; }
-  static constexpr uint32_t BARS = STAGES * NT * TILE;
+  static constexpr uint32_t X(int s) { return uint32_t(s) * STG_BYTES; }
+  static constexpr uint32_t Y(int s) { return uint32_t(s) * STG_BYTES + TILE; }
+  static constexpr uint32_t Y2(int s) { return uint32_t(s) * STG_BYTES + TILE + TILEY; }
+  static constexpr uint32_t BARS = STAGES * STG_BYTES;
   static constexpr uint32_t BYTES = BARS + 512 + 1024;  // barriers + item queue + tmem slot + alignment slack
-  static constexpr uint32_t TCOLS = 2 * D;             // two accumulators
+  static constexpr uint32_t TCOLS = 2 * DN < 32 ? 32 : 2 * DN;  // two accumulators
+  static_assert(BYTES <= 232448, "shared memory budget");
 };
 
 struct SegParams {
@@ -272,7 +285,8 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
   const uint32_t sbase = smem_u32(sm);
 
   const Plan& p = prm.p;
-  const int64_t W = p.B * p.Hk * p.nseg;
+  constexpr int VS = L::VS;
+  const int64_t W = p.B * p.Hk * p.nseg * VS;
   const int sub = prm.sub;
   const uint32_t warp = warp_id(), lane = lane_id();
 
@@ -304,18 +318,20 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
       for (uint32_t k = 0;; ++k) {
         const int64_t w = q_claim(*iq, k, prm.claim);
         if (w >= W) break;
-        const Item it = get_item(p, DIR, w);
+        const Item it = get_item(p, DIR, w / VS);
+        [[maybe_unused]] const int vs = int(w % VS);  // value slice of the item (head_dim 128)
         for (int jj = 0; jj < it.nblk * sub; ++jj, ++J) {  // block j = jj / sub, summed head u = jj % sub
           const int s = J % ST;
           mbar_wait(&empty[s], ((J / ST) & 1) ^ 1);
           LASP_TRACE(0, J);
-          mbar_expect_tx(&full[s], L::NT * L::TILE);
+          mbar_expect_tx(&full[s], L::STG_BYTES);
           const int t0 = int(block_row(DIR, it, jj / sub));
           const int hh = int(it.h) * sub + jj % sub;
 #pragma unroll
           for (int x = 0; x < L::NBOX; ++x) {
             tma_load_4d(sm + L::X(s) + x * BOX, &prm.mx, &full[s], x * 64, hh, t0, int(it.b));
-            tma_load_4d(sm + L::Y(s) + x * BOX, &prm.my, &full[s], x * 64, hh, t0, int(it.b));
+            if (x < L::NBOXY)
+              tma_load_4d(sm + L::Y(s) + x * BOX, &prm.my, &full[s], (vs * L::NBOXY + x) * 64, hh, t0, int(it.b));
             if (NORM) tma_load_4d(sm + L::Y2(s) + x * BOX, &prm.my2, &full[s], x * 64, hh, t0, int(it.b));
           }
         }
@@ -323,14 +339,15 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
     }
   } else if (warp == 1) {
     if (elect_one()) {
-      constexpr uint32_t idesc = idesc_bf16(D, D, 1, 1);
+      constexpr uint32_t idesc = idesc_bf16(D, L::DN, 1, 1);
       uint32_t J = 0;
       for (uint32_t k = 0;; ++k) {
         const int64_t w = q_fetch(*iq, k);
         q_release(*iq, k);
         if (w >= W) break;
-        const Item it = get_item(p, DIR, w);
-        const uint32_t acc = tmem + (k & 1) * D;
+        const Item it = get_item(p, DIR, w / VS);
+        [[maybe_unused]] const int vs = int(w % VS);  // value slice of the item (head_dim 128)
+        const uint32_t acc = tmem + (k & 1) * L::DN;
         mbar_wait(&acc_empty[k & 1], ((k >> 1) & 1) ^ 1);
         tc_fence_after();
         for (int jj = 0; jj < it.nblk * sub; ++jj, ++J) {
@@ -357,7 +374,8 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
     for (uint32_t k = 0;; ++k) {
       const int64_t w = q_fetch_warp(*iq, k);
       if (w >= W) break;
-      const Item it = get_item(p, DIR, w);
+      const Item it = get_item(p, DIR, w / VS);
+        [[maybe_unused]] const int vs = int(w % VS);  // value slice of the item (head_dim 128)
       const float l2 = p.l2lam[it.h];
       for (int jj = 0; jj < it.nblk * sub; ++jj, ++J) {
         const int s = J % ST;
@@ -442,17 +460,18 @@ __global__ void __launch_bounds__(384, 2) seg_state_tc_kernel(const __grid_const
     for (uint32_t k = 0;; ++k) {
       const int64_t w = q_fetch_warp(*iq, k);
       if (w >= W) break;
-      const Item it = get_item(p, DIR, w);
+      const Item it = get_item(p, DIR, w / VS);
+        [[maybe_unused]] const int vs = int(w % VS);  // value slice of the item (head_dim 128)
       mbar_wait(&acc_full[k & 1], (k >> 1) & 1);
       tc_fence_after();
-      float* o = prm.out + ((it.b * p.Hk + it.h) * p.nseg + it.seg) * D * D + int64_t(row) * D;
-      const uint32_t ta = tmem + ((q4 * 32) << 16) + (k & 1) * D;
+      float* o = prm.out + ((it.b * p.Hk + it.h) * p.nseg + it.seg) * D * D + int64_t(row) * D + vs * L::DN;
+      const uint32_t ta = tmem + ((q4 * 32) << 16) + (k & 1) * L::DN;
 #pragma unroll
-      for (int c = 0; c < D / 16; ++c) {
+      for (int c = 0; c < L::DN / 16; ++c) {
         float v[16];
         tmem_ld16(ta + c * 16, v);
         tmem_ld_wait();
-        if (c == D / 16 - 1) {
+        if (c == L::DN / 16 - 1) {
           tc_fence_before();
           mbar_arrive(&acc_empty[k & 1]);
         }
@@ -494,8 +513,8 @@ struct CoreLayout {
   static constexpr uint32_t SLO(int b) { return SBF(b) + DK * 128; }
   static constexpr uint32_t OST = KU + TC + NSB * DK * 256;  // [128][64] bf16 output staging
   static constexpr uint32_t STG = OST + TC;                  // [D][D] fp32 segment prefix state (TMA, SW128)
-  static constexpr uint32_t BARS = STG + (HAS_STG ? 4 * D * D : 0);  // barriers (256 B) + mask factors (512 B)
-  static constexpr uint32_t BYTES = BARS + 256 + 512 + 1024;
+  static constexpr uint32_t BARS = STG + (HAS_STG ? 4 * D * D : 0);  // barriers and item queue (768 B)
+  static constexpr uint32_t BYTES = BARS + 768 + 1024;
   // TMEM columns (P, bf16, overwrites the first 64 columns of its S buffer: FA4-style TS MMA)
   static constexpr uint32_t T_S0 = 0, T_S1 = 128, T_OI = 256, T_OX = 320, T_DS = 384;
   static_assert(BYTES <= 232448, "shared memory budget");
@@ -540,6 +559,7 @@ struct CoreParams {
   float norm_eps;
   int seg_desc;               // 1: items in descending segment order (the segment-state launch before this one
                               // ascended, so its last-read tiles are still in L2)
+  int short_last;             // with seg_desc: order nseg - 2, ..., 0, nseg - 1 (the last segment is ragged)
   int late_inputs;            // 1: an input tensor is written by the preceding kernel (fused Norm
                               // backward): the producer waits for it before the first load
 };
@@ -618,7 +638,10 @@ __device__ __noinline__ CItem get_citem(const CoreParams& prm, int64_t w) {
   const uint32_t wu = uint32_t(w);
   const uint32_t sg = prm.div_per.div(wu);
   const uint32_t rem = wu - sg * prm.per;
-  it.seg = prm.seg_desc ? int32_t(p.nseg - 1 - sg) : int32_t(sg);
+  // descending order; with short_last the ragged (shorter) last segment goes last instead of first, so the
+  // launch's final claims are the short items (a smaller tail)
+  it.seg = !prm.seg_desc ? int32_t(sg) : prm.short_last ? int32_t(sg + 1 < uint32_t(p.nseg) ? p.nseg - 2 - sg : p.nseg - 1)
+                                                        : int32_t(p.nseg - 1 - sg);
   if constexpr (!GQ) {  // multi-head: every pass has B * H * NV items per segment row (round-1 decode)
     const uint32_t nbh = uint32_t(p.B * p.H) * uint32_t(NV), nh = uint32_t(p.H);
     uint32_t bhv;
@@ -683,13 +706,14 @@ __device__ __forceinline__ int64_t cblock_row(const CItem& it, int j) {
 }
 struct CoreBars {
   uint64_t full[3], empty[3], s_full[2], s_empty[2];
-  uint64_t p_full[2], ku_full, ku_empty, ds_full, ds_empty, st_full[2], st_empty[2], o_full, o_empty;
+  uint64_t fullc[3];  // ring slot: full = a, b tiles landed; fullc = c tile landed
+  uint64_t p_full[2][4], ku_full, ku_empty, ds_full, ds_empty, st_full[2], st_empty[2], o_full, o_empty;
   uint64_t stg_full, stg_empty;
   ItemQueue iq;
   uint32_t tmem_slot;
   uint32_t fold_chunk;  // fused prefix fold: chunk claimed by this CTA's fold threads
 };
-static_assert(sizeof(CoreBars) <= 256, "CoreBars must fit its 256-byte slot");
+static_assert(sizeof(CoreBars) <= 768, "CoreBars must fit its 768-byte slot");
 constexpr int kFoldChunk = 256;  // float2 elements per claimed fold chunk (one per fold thread)
 __device__ __forceinline__ unsigned fold_chunks(const Plan& p) {
   return unsigned((p.B * p.Hk * p.D * p.D / 2 + kFoldChunk - 1) / kFoldChunk);
@@ -720,9 +744,10 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
     for (int x = 0; x < prm.npass; ++x) tma_prefetch(&prm.mout[x]);
     tma_prefetch(&prm.mst[0]); tma_prefetch(&prm.mst[1]);
     mbar_init(&bar->stg_full, 1); mbar_init(&bar->stg_empty, 128);
-    for (int s = 0; s < ST; ++s) { mbar_init(&bar->full[s], 1); mbar_init(&bar->empty[s], 2); }
+    for (int s = 0; s < ST; ++s) { mbar_init(&bar->full[s], 1); mbar_init(&bar->fullc[s], 1); mbar_init(&bar->empty[s], 2); }
     for (int s = 0; s < 2; ++s) { mbar_init(&bar->s_full[s], 1); mbar_init(&bar->s_empty[s], 1); }
-    mbar_init(&bar->p_full[0], 128); mbar_init(&bar->p_full[1], 128);
+    for (int b2 = 0; b2 < 2; ++b2)
+      for (int c = 0; c < 4; ++c) mbar_init(&bar->p_full[b2][c], 128);
     mbar_init(&bar->ku_full, 128); mbar_init(&bar->ku_empty, 1);
     mbar_init(&bar->ds_full, 1); mbar_init(&bar->ds_empty, 128);
     for (int b2 = 0; b2 < L::NSB; ++b2) { mbar_init(&bar->st_full[b2], 128); mbar_init(&bar->st_empty[b2], 1); }
@@ -793,6 +818,16 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           }
         };
         if (waited) load_stg();
+#ifndef LASP_NO_STATE_PREFETCH
+        if constexpr (!L::HAS_STG) {
+          // head_dim 128: the state warps read the item's prefix state with plain loads when the item starts;
+          // pull it into L2 now, ~one ring depth ahead (a state written by the preceding kernel has usually left
+          // L2 by the time the late items read it: the item-start load was ~3-5k cycles on the critical path)
+          if (k > 0)
+            l2_prefetch_bulk(prm.stp[ps.state] + ((int64_t(it.b) * p.Hk + it.sh) * p.nseg + it.seg) * D * D,
+                             uint32_t(D * D * 4));
+        }
+#endif
         const CUtensorMap* ma = &prm.min[ps.a];
         const CUtensorMap* mb = &prm.min[ps.b];
         const CUtensorMap* mc = &prm.min[ps.c];
@@ -808,7 +843,16 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           const int s = J % ST;
           mbar_wait(&bar->empty[s], ((J / ST) & 1) ^ 1);
           LASP_TRACE(0, J);
+#ifdef LASP_FULL_WHOLE  // A/B experiment: one barrier for the whole stage
           mbar_expect_tx(&bar->full[s], L::STAGE);
+          uint64_t* fc = &bar->full[s];
+#else
+          // a, b (S, O_inter, dS) and c (u . c, P c) on separate barriers, a and b issued first: S starts
+          // before the c tile has landed
+          mbar_expect_tx(&bar->full[s], 2 * L::TA);
+          mbar_expect_tx(&bar->fullc[s], L::TC);
+          uint64_t* fc = &bar->fullc[s];
+#endif
           const int j = GQ ? jj / isub : jj;
           const int t0 = int(cblock_row(it, j)), hb = it.bh0 + (jj - j * isub);
 #pragma unroll
@@ -816,7 +860,10 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             tma_load_4d(sm + L::A(s) + x * BOX, ma, &bar->full[s], x * 64, int(it.h), t0, int(it.b));
             tma_load_4d(sm + L::B_(s) + x * BOX, mb, &bar->full[s], x * 64, hb, t0, int(it.b));
           }
-          tma_load_4d(sm + L::C_(s), mc, &bar->full[s], it.v * 64, hb, t0, int(it.b));
+          tma_load_4d(sm + L::C_(s), mc, fc, it.v * 64, hb, t0, int(it.b));
+#ifdef LASP_FULL_WHOLE
+          mbar_arrive(&bar->fullc[s]);
+#endif
         }
         if (!waited) {  // first item shorter than the ring
           pdl_wait();
@@ -856,6 +903,8 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
             mbar_wait(&bar->s_empty[J & 1], ((J >> 1) & 1) ^ 1);
             tc_fence_after();
             const uint32_t dt = tmem + ((J & 1) ? L::T_S1 : L::T_S0);
+            // (one N = 128 product: two N = 64 halves on separate barriers, so that the mask could start one half
+            // earlier, measured TNL-1B fused bwd 325 -> 334 us -- each half re-reads the a tile from shared memory)
 #pragma unroll
             for (int kk = 0; kk < L::DK / 16; ++kk)
               mma_bf16(dt, desc_k(sbase + L::A(s) + koff(kk)), desc_k(sbase + L::B_(s) + koff(kk)), id_qk, kk != 0);
@@ -864,6 +913,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           } else if (warp == 3) {
             // dS = sum_u b_u^T (u . c_u), only for blocks that are not the last of their segment
             if (j + 1 < nblk) {
+              mbar_wait(&bar->full[s], (J / ST) & 1);  // b (the u . c hand-off implies only the c tile)
               mbar_wait(&bar->ku_full, nku & 1);
               if (u == 0) mbar_wait(&bar->ds_empty, (kd & 1) ^ 1);
               tc_fence_after();
@@ -901,13 +951,29 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
                          id_x, 1);
               mma_commit(&bar->st_empty[sb]);  // the state copy is free once the inter MMAs have read it
             }
-            mbar_wait(&bar->p_full[J & 1], (J >> 1) & 1);
+            const uint32_t pt = tmem + ((J & 1) ? L::T_S1 : L::T_S0);  // P in TMEM (2 bf16 / column)
+            mbar_wait(&bar->fullc[s], (J / ST) & 1);  // the c tile
+#ifdef LASP_P_WHOLE  // A/B experiment: wait for the whole P before the first K step
+            for (int c4 = 0; c4 < 4; ++c4) mbar_wait(&bar->p_full[J & 1][c4], (J >> 1) & 1);
             LASP_TRACE(11, J);
             tc_fence_after();
-            const uint32_t pt = tmem + ((J & 1) ? L::T_S1 : L::T_S0);  // P in TMEM (2 bf16 / column)
 #pragma unroll
             for (int kk = 0; kk < BT / 16; ++kk)
               mma_bf16_ts(tmem + L::T_OI, pt + kk * 8, desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv, (kk | u) != 0);
+#else
+            // P c in four K steps of 32 tokens, each issued as soon as the mask warps have written that chunk of
+            // P (the light row quadrants finish their chunks early; only the last K step waits for the
+            // quadrant with the most live chunks), so P c ends ~one K step after the mask instead of four
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              mbar_wait(&bar->p_full[J & 1][c4], (J >> 1) & 1);
+              if (c4 == 0) LASP_TRACE(11, J);
+              tc_fence_after();
+#pragma unroll
+              for (int kk = 2 * c4; kk < 2 * c4 + 2; ++kk)
+                mma_bf16_ts(tmem + L::T_OI, pt + kk * 8, desc_mn(sbase + L::C_(s) + kk * 2048, BOX), id_pv, (kk | u) != 0);
+            }
+#endif
             if (u + 1 == sub) {
               mma_commit(&bar->o_full);
               ++Jb;
@@ -988,15 +1054,23 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
 #pragma unroll
             for (int q = 0; q < 16; ++q) pk[q] = pack_bf16(v[2 * q], v[2 * q + 1]);
           }
-          // P chunk -> TMEM columns [16 c4, 16 c4 + 16) of the same buffer (already consumed S columns)
+          // P chunk -> TMEM columns [16 c4, 16 c4 + 16) of the same buffer (already consumed S columns); the
+          // chunk is published on its own barrier (the P c MMA's K step c4 waits for it)
           tmem_st16(ts + c4 * 16, pk);
           if (lane == 0 && q4 == 3) LASP_TRACE2(c4 * 3 + 2, J);
+#ifndef LASP_P_WHOLE
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&bar->p_full[sb][c4]);  // per buffer: mask(J+1) may finish before out(J) is issued
+#endif
         }
         if (lane == 0 && q4 == 3) LASP_TRACE(14, J);
+#if defined(LASP_P_WHOLE) || defined(LASP_EXPERIMENT_NOMASK)
         tmem_st_wait();
         if (lane == 0 && q4 == 3) LASP_TRACE(15, J);
         tc_fence_before();
-        mbar_arrive(&bar->p_full[sb]);  // per-buffer: mask(J+1) may finish before out(J) is issued
+        for (int c4 = 0; c4 < 4; ++c4) mbar_arrive(&bar->p_full[sb][c4]);
+#endif
         if (lane == 0 && q4 == 3) LASP_TRACE(5, J);
       }
     }
@@ -1069,6 +1143,9 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         if (prm.fold.gbar == nullptr) load([](auto* ptr) { return __ldg(ptr); });
         else load([](auto* ptr) { return *ptr; });
       }
+    };
+    // after the loads are issued (the first block's u . c scaling runs while they are in flight)
+    auto finish_state = [&]() {
       if (tag_poisoned(prm.status)) {  // the call's cache tag did not match: every output becomes NaN
 #pragma unroll
         for (int e = 0; e < NS; ++e) S[e] = __int_as_float(0x7fc00000);
@@ -1080,7 +1157,11 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       if (w >= W) break;
       const CItem it = get_citem<L::NV, GQ>(prm, w);
       const CorePass& ps = prm.pass[it.pass];
+      if (g == 0) LASP_TRACE2(12, J);  // item fetched
       load_state(k, it, ps.trans != 0, ps.state);
+#ifdef LASP_STATE_FINISH_EARLY  // A/B experiment: the round-2 order (state complete before the first u . c)
+      finish_state();
+#endif
       const float l2 = p.l2lam[it.sh];
       const uint32_t u2 = bf16x2_splat(exp2f(float(it.dir == Dir::FWD ? (BT - 1 - g) : (g + 1)) * l2));
       const float decay = exp2f(float(BT) * l2);
@@ -1092,7 +1173,11 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
           mbar_wait(&bar->ku_empty, (nku & 1) ^ 1);
           ++nku;
         }
+#ifdef LASP_FULL_WHOLE
         mbar_wait(&bar->full[s], (JJ / ST) & 1);
+#else
+        mbar_wait(&bar->fullc[s], (JJ / ST) & 1);  // the c tile
+#endif
 #if defined(LASP_EXPERIMENT_NOSTATE) || defined(LASP_EXPERIMENT_NOUC)
         if (false)
 #endif
@@ -1106,6 +1191,10 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
       };
       const int sub = GQ ? it.sub : 1;
       if (it.nblk > 1) scale_ku(Js);
+#ifndef LASP_STATE_FINISH_EARLY
+      finish_state();
+#endif
+      if (g == 0) LASP_TRACE(13, J);   // prefix state in registers
       for (int j = 0;; ++j, ++J) {
         // bf16 hi/lo copy of the state entering block J into buffer J % NSB (free once the output MMAs
         // of block J - NSB are done)
@@ -1308,11 +1397,6 @@ int sm_count() {
   return n;
 }
 
-unsigned persistent_grid(const Plan& p, int per_sm = 1) {
-  const int64_t W = p.B * p.Hk * p.nseg;
-  const int64_t g = W < int64_t(sm_count()) * per_sm ? W : int64_t(sm_count()) * per_sm;
-  return unsigned(g > 0 ? g : 1);
-}
 
 template <int D, Dir DIR, bool NORM>
 cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, cudaStream_t st,
@@ -1343,7 +1427,9 @@ cudaError_t launch_seg(const Plan& p, const void* x, const void* y, float* out, 
   auto kern = seg_state_tc_kernel<D, DIR, NORM>;
   const int smem = int(SegLayout<D, NORM>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
-  return launch_k(kern, dim3(persistent_grid(p, SegLayout<D, NORM>::CTAS_PER_SM)), dim3(384), smem, st, prm);
+  using SL = SegLayout<D, NORM>;
+  const int64_t W = p.B * p.Hk * p.nseg * SL::VS, slots = int64_t(sm_count()) * SL::CTAS_PER_SM;
+  return launch_k(kern, dim3(unsigned(W < slots ? W : slots)), dim3(384), smem, st, prm);
 }
 
 template <int D>
@@ -1433,6 +1519,12 @@ cudaError_t launch_core_multi(const Plan& p, int npass, const SeqArgs* a, const 
     return e && *e ? std::atoi(e) : 1;
   }();
   prm.seg_desc = seg_desc;
+  // the ragged last segment's items are claimed last (tail of the persistent launch); LASP_SHORT_LAST=0: first
+  static const int short_last = [] {
+    const char* e = std::getenv("LASP_SHORT_LAST");
+    return e && *e ? std::atoi(e) : 1;
+  }();
+  prm.short_last = short_last && p.nseg > 1 && p.C % p.seg_len != 0;
   const int smem = int(CoreLayout<D>::BYTES);
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
   const int64_t W = p.nseg * int64_t(off);

@@ -22,7 +22,7 @@ buf = buf[:2 * 16 * 64]
 tt = buf.cpu().numpy().reshape(2, 16, 64).astype(np.int64)
 t = tt[0]
 base = t[t > 0].min()
-names = ["tma_issue", "qk_iss", "ds_iss", "out_iss", "mask_beg", "mask_end", "ds_ready", "sbf_next", "o_full", "store", "g_full", "g_pfull", "g_oempty", "-", "st_iss", "st_done"]
+names = ["tma_issue", "qk_iss", "ds_iss", "out_iss", "mask_beg", "mask_end", "ds_ready", "sbf_next", "o_full", "store", "g_full", "g_pfull", "g_oempty", "st_loaded", "st_iss", "st_done"]
 print("J   " + " ".join(f"{n:>9s}" for n in names))
 for J in range(int(sys.argv[1]) if len(sys.argv) > 1 else 30):
     print(f"{J:3d} " + " ".join(f"{(t[e, J] - base) if t[e, J] else -1:9d}" for e in range(len(names))))
@@ -32,3 +32,7 @@ for J in range(int(sys.argv[1]) if len(sys.argv) > 1 else 30):
     if t[4, J] == 0:
         break
     print(f"{J:3d} " + " ".join(f"{(tt[1, e, J] - t[4, J]) if tt[1, e, J] else -1:6d}" for e in range(12)))
+print("state warps: item fetched (absolute, cycles)")
+for J in range(int(sys.argv[1]) if len(sys.argv) > 1 else 30):
+    if tt[1, 12, J]:
+        print(f"{J:3d} {tt[1, 12, J] - base:9d}")
