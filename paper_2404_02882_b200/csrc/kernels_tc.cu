@@ -1011,6 +1011,8 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         if (lane == 0 && q4 == 3) LASP_TRACE(4, J);
         tc_fence_after();
         const uint32_t ts = tmem + ((q4 * 32) << 16) + (sb ? L::T_S1 : L::T_S0);
+        // (software-pipelining the TMEM loads over half chunks -- next half loaded while the current one is
+        // scaled -- measured TNL-0.4B fused bwd 121.3 -> 132 us: more spills, interleaved TMEM traffic; dropped)
 #ifdef LASP_EXPERIMENT_NOMASK  // timing experiment only (tools/cmp_variants.sh): P = garbage
         if (false)
 #endif
