@@ -212,6 +212,16 @@ def test_state_error_on_reused_cache_address(L):
     assert e.value.name == "LASP_ERR_STATE"
 
 
+@pytest.mark.parametrize("D", [64, 128])
+def test_many_segments_parity(L, oracle_mod, monkeypatch, D):
+    """52 segments of 128 tokens (ragged tail): the prefix fold runs in two load batches of at most 40 segments
+    (fused fold and prefix kernel alike), against the fp64 oracle."""
+    monkeypatch.setenv("LASP_SEG_LEN", "128")
+    p = synth.problem(13 + D, 1, 51 * 128 + 40, 2, D, dtype="bf16")
+    res = run_sim_ring(L, p, 1, torch.bfloat16, 51 * 128 + 40)
+    check_against_oracle(oracle_mod, p, res, BF16_TOL)
+
+
 def test_ragged_multi_segment_rev_store_deterministic(L, oracle_mod, monkeypatch):
     """with several segments and a ragged rank length, the REV passes' ragged block starts inside
     the previous segment; only the segment's own rows may be stored (else two CTAs race on those rows with
@@ -449,9 +459,17 @@ import sys, numpy as np, torch
 sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
 import synth, paper_2404_02882_b200 as L
 out = {{}}
-# (B, H, D, C): small states; and B*H*D*D/2 = 65536 float2 = 256 fold chunks for at most 148 CTAs (2 rounds)
-for B, H, D, C in ((2, 3, 64, 3 * 1024 + 384), (2, 3, 128, 2 * 1024 + 256), (2, 16, 64, 4096 + 640)):
-    p = synth.problem(77 + D + H, B, C, H, D, dtype="bf16")
+import os
+# (B, H, D, C, forced segment length): small states; B*H*D*D/2 = 65536 float2 = 256 fold chunks for at most 148 CTAs
+# (2 rounds); and segment counts on both sides of the prefix kernel's load batches (U = 8 / 16 / 24 / 40: 13, 21 and
+# 52 segments, the last folded in two batches of at most 40)
+for B, H, D, C, seg in ((2, 3, 64, 3 * 1024 + 384, 0), (2, 3, 128, 2 * 1024 + 256, 0), (2, 16, 64, 4096 + 640, 0),
+                        (1, 2, 64, 13 * 128, 128), (1, 2, 128, 20 * 128 + 10, 128), (1, 2, 64, 51 * 128 + 40, 128)):
+    if seg:
+        os.environ["LASP_SEG_LEN"] = str(seg)
+    else:
+        os.environ.pop("LASP_SEG_LEN", None)
+    p = synth.problem(77 + D + H + seg, B, C, H, D, dtype="bf16")
     q, k, v, do = (torch.from_numpy(np.ascontiguousarray(p[x])).cuda().to(torch.bfloat16) for x in ("q", "k", "v", "do"))
     g = torch.Generator().manual_seed(D)
     kv_in = torch.randn(B, H, D, D, generator=g).cuda()
@@ -459,7 +477,7 @@ for B, H, D, C in ((2, 3, 64, 3 * 1024 + 384), (2, 3, 128, 2 * 1024 + 256), (2, 
     o, kv_out, cache = L.fwd_local(q, k, v, p["lam"], kv_in)
     dq, dk, dv, dkv_out = L.bwd_local(q, k, v, p["lam"], do, cache, dkv_in)
     for n, t in zip(("o", "kv_out", "dq", "dk", "dv", "dkv_out"), (o, kv_out, dq, dk, dv, dkv_out)):
-        out[f"{{n}}{{D}}_{{H}}"] = t.float().cpu().numpy()
+        out[f"{{n}}{{D}}_{{H}}_{{C}}"] = t.float().cpu().numpy()
 np.savez({dst!r}, **out)
 """
 
