@@ -1179,6 +1179,11 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         mbar_arrive(&bar->ku_full);
       };
       const int sub = GQ ? it.sub : 1;
+#ifndef LASP_KU_EARLY
+      const bool ku_late = !SPLIT && prm.npass == 1;
+#else  // A/B experiment: the next block's u . c before its state copy in every launch
+      constexpr bool ku_late = false;
+#endif
       if (it.nblk > 1) scale_ku(Js);
 #ifndef LASP_STATE_FINISH_EARLY
       finish_state();
@@ -1222,6 +1227,11 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         fence_async_smem();
         mbar_arrive(&bar->st_full[sb]);
         if (g == 0) LASP_TRACE(7, J);
+        // head_dim-128 forward (one pass): u . c of this block (after the first; not for the last block: no dS)
+        // only now -- done before the copy above, it made the copy wait for this block's c tile, which the copy
+        // does not need (forward core 130 -> 125 us at TNL-1B); in the backward the dS chain wants u . c early
+        // (fused bwd 324 -> 346 us with the late order), so there it stays at the end of the previous block
+        if (ku_late && j > 0 && j + 1 < it.nblk) scale_ku(Js);
         if (j + 1 == it.nblk) {  // no state leaves the last block of a segment
           Js += sub;
           break;
@@ -1255,7 +1265,7 @@ __global__ void __launch_bounds__(512, 1) core_tc_kernel(const __grid_constant__
         mbar_arrive(&bar->ds_empty);
         ++kd;
         Js += sub;
-        if (j + 2 < it.nblk) scale_ku(Js);
+        if (!ku_late && j + 2 < it.nblk) scale_ku(Js);
       }
       ++J;  // the break skipped the increment of the last block
     }
