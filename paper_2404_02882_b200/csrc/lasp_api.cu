@@ -73,6 +73,15 @@ int64_t choose_seg_len(int64_t B, int64_t C, int64_t H, int64_t D) {
   if (C <= 0) return q;
   const int64_t nb = (C + q - 1) / q;
   const int64_t nv = D >= 128 ? D / 64 : 1;  // value slices per item (tensor-core core kernel)
+  // head_dim 128 with enough work: segments of 28 blocks (3584 tokens), if the forward launch still gets at least
+  // two items per SM. Same-box sweeps (profiles/r4q_*, r4p_*): TNL-1B 58.5 -> 59.9 M tokens/s (10 segments instead
+  // of 24: the ragged last segment's short items, claimed last, fill the final wave of the long ones), TNL-7B
+  // 30.0 -> 30.9 M (37 instead of 12: the 86-block items left the last wave's SMs idle); 22- and 19-block segments
+  // lost at TNL-1B (56.0), so the block count is a measured value, not a model. LASP_LONG_SEG_BLOCKS=0: off.
+  if (nv > 1) {
+    const int64_t lb = env_i64("LASP_LONG_SEG_BLOCKS", 28);
+    if (lb > 0 && B * H * nv * ((nb + lb - 1) / lb) >= 2 * 148) return lb * q;
+  }
   const int64_t target = env_i64("LASP_TARGET_CTAS", (nv > 1 ? 5 : 4) * 148);
   int64_t nseg_t = (target + B * H * nv - 1) / (B * H * nv);
   if (nseg_t < 1) nseg_t = 1;
