@@ -454,6 +454,28 @@ def test_random_shapes_long_sweep(L, oracle_mod, case):
     check_against_oracle(oracle_mod, p, res, FP32_TOL if dtype == "fp32" else BF16_TOL)
 
 
+_PLAN = int(__import__("os").environ.get("LASP_PLAN_SWEEP", "0"))
+
+
+@pytest.mark.parametrize("case", range(_PLAN))
+def test_random_shapes_long_segment_plan(L, oracle_mod, case):
+    """Opt-in (LASP_PLAN_SWEEP=<count>): head_dim-128 shapes large enough for the 28-block segment plan (B*H*2*nseg
+    >= 296), random lengths with ragged last segments, against the fp64 oracle."""
+    rng = np.random.default_rng(11000 + case)
+    B = int(rng.integers(1, 3))
+    H = int(rng.choice([8, 12, 16, 24]))
+    nb_min = -(-296 // (2 * B * H)) * 28  # blocks for enough 28-block segments
+    C = int(rng.integers(max(nb_min - 27, 1) * 128, max(nb_min, 160) * 128 + 1))
+    lam = rng.uniform(0.3, 1.0, H).astype(np.float32)
+    p = synth.problem(12000 + case, B, C, H, 128, dtype="bf16")
+    p["lam"] = lam
+    shape = L.api._shape(torch.empty((B, C, H, 128), dtype=torch.bfloat16, device="meta"))
+    seg = L.segment_len(shape)
+    res = run_sim_ring(L, p, 1, torch.bfloat16, C)
+    check_against_oracle(oracle_mod, p, res, BF16_TOL)
+    print(f"case {case}: B={B} H={H} C={C} seg_len={seg}")
+
+
 _FOLD_SCRIPT = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
